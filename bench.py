@@ -1,0 +1,318 @@
+"""Benchmark of the HiGP hot path on B200 (contract: see DESIGN.md §Measurement).
+
+Default workload = BASELINE.json configs[1]: the standalone fused MatMul,
+Gaussian Khat.Z and dKhat/dl.Z, n=65536, d=8, Z (n, 32), l=1 f=1 s=1e-2,
+synthetic seeded inputs. One step = one fused pass producing both outputs.
+
+    metric: kernel entries x RHS / s  (entries x RHS = n_rows * n_cols * k per output matrix)
+
+    python bench.py [--gpus N --steps K --warmup W] [--precision fast|tf32|fp64] [--impl reference]
+
+Multi-GPU (torchrun): each rank owns a contiguous row block of Khat and needs
+the whole RHS block; the RHS is replicated (an all-gather per application in a
+solver, not in this single-pass benchmark). Per-GPU work is n/N rows x n cols;
+"scaling": "strong" (total work fixed).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", default="fast", choices=["fast", "tf32", "fp64"])
+    ap.add_argument("--n", type=int, default=65536)
+    ap.add_argument("--k", type=int, default=32)
+    ap.add_argument("--cpu-rows", type=int, default=2048, help="rows in the bounded CPU-baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--skip-nlml", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------- CPU baseline (oracle port)
+def cpu_baseline(w, rows, steps=1):
+    """The reference algorithm (C restatement of kmat.py:165-189 + numba panels, OpenMP on every
+    host core) on a bounded row sample of the same workload; returns entries x RHS / s."""
+    from oracle import kgp_oracle_c as oc
+
+    oc.matmul("gaussian", w.x, w.l, w.f, w.s, w.z, row0=0, nrows=8, want_dl=True)  # warm
+    best = float("inf")
+    for _ in range(max(1, steps)):
+        t0 = time.perf_counter()
+        oc.matmul("gaussian", w.x, w.l, w.f, w.s, w.z, row0=0, nrows=rows, want_dl=True)
+        best = min(best, time.perf_counter() - t0)
+    units = 2.0 * rows * w.n * w.z.shape[1]
+    return units / best, best, oc.max_threads()
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU algorithm (oracle port) on this box's host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2503_02259_b200 import workloads
+
+    w = workloads.cfg2(n=args.n, k=args.k)
+    for _ in range(max(0, args.warmup)):
+        cpu_baseline(w, 64)
+    vals = []
+    times = []
+    for _ in range(args.steps):
+        v, t, cores = cpu_baseline(w, args.cpu_rows)
+        vals.append(v)
+        times.append(t)
+    value = float(np.median(vals))
+    line = {
+        "impl": "reference", "metric": "kernel entries x RHS / s (fused Khat.Z + dKhat/dl.Z)",
+        "value": value, "unit": "entries*RHS/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": float(np.median(times)) * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, cfg2 shapes)",
+        "config": {"workload": "cfg2 standalone fused MatMul", "n": args.n, "d": 8, "k": args.k,
+                   "kernel": "gaussian", "outputs": ["Khat.Z", "dKhat/dl.Z"]},
+        "cpu_baseline": {"value": value, "unit": "entries*RHS/s", "cores": cores, "kind": "port",
+                         "sample": f"{args.cpu_rows} of {args.n} rows per step, both outputs, fp64; "
+                                   "oracle/kgp_oracle.c (C restatement of kmat.py:165-189)"},
+        "e2e": {"value": value, "unit": "entries*RHS/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ------------------------------------------------------------------------- GPU arm
+def measured_tf32_peak(torch):
+    """cuBLAS TF32 GEMM (8192^3), best of 5 -- the tensor-pipe denominator for tf32 MMA work."""
+    a = torch.randn(8192, 8192, device="cuda", dtype=torch.float32)
+    b = torch.randn(8192, 8192, device="cuda", dtype=torch.float32)
+    old = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    for _ in range(2):
+        a @ b
+    best = float("inf")
+    for _ in range(5):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        a @ b
+        e.record()
+        e.synchronize()
+        best = min(best, s.elapsed_time(e) / 1e3)
+    torch.backends.cuda.matmul.allow_tf32 = old
+    del a, b
+    return 2.0 * 8192 ** 3 / best / 1e12
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2503_02259_b200 import KernelEngine, KernelType, _lib, workloads
+    from paper_2503_02259_b200.kmat import Hyperparams
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    w = workloads.cfg2(n=args.n, k=args.k)
+    n, k = w.n, w.z.shape[1]
+    r0, r1 = rank * n // world, (rank + 1) * n // world
+    hp = Hyperparams(w.l, w.f, w.s)
+    eng = KernelEngine(KernelType.GAUSSIAN, w.x, hp, precision=args.precision)
+    if world > 1:
+        _lib.call("kgp_engine_set_rows", eng.handle, r0, r1 - r0)
+    rows = r1 - r0
+    zd = torch.from_numpy(w.z).cuda()
+    out_k = torch.empty((rows, k), dtype=torch.float64, device="cuda")
+    out_l = torch.empty_like(out_k)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # 256 MB > 126 MB L2
+
+    def step():
+        _lib.call("kgp_engine_matmul", eng.handle, k, zd.data_ptr(), zd.stride(0), zd.stride(1),
+                  out_k.data_ptr(), out_l.data_ptr(), None, out_k.stride(0), out_k.stride(1), stream.cuda_stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        for s_ev, e_ev in ev:
+            flush.zero_()  # L2 flush between timed iterations (outside the event pair)
+            s_ev.record(stream)
+            step()
+            e_ev.record(stream)
+        torch.cuda.synchronize()
+    times = [s.elapsed_time(e) / 1e3 for s, e in ev]
+    t_step = float(np.mean(times))
+    if world > 1:
+        t = torch.tensor([t_step], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_step = float(t.item())
+    units = 2.0 * n * n * k  # both outputs, whole job
+    value = units / t_step
+
+    # ---- e2e: C ABI call with HOST buffers, H2D of Z and D2H of both outputs inside the timed region
+    zh = torch.from_numpy(w.z).pin_memory()
+    ok_h = torch.empty((rows, k), dtype=torch.float64).pin_memory()
+    ol_h = torch.empty_like(ok_h).pin_memory()
+    zbuf = torch.empty_like(zd)
+
+    def e2e_step():
+        zbuf.copy_(zh, non_blocking=True)
+        _lib.call("kgp_engine_matmul", eng.handle, k, zbuf.data_ptr(), zbuf.stride(0), zbuf.stride(1),
+                  out_k.data_ptr(), out_l.data_ptr(), None, out_k.stride(0), out_k.stride(1), stream.cuda_stream)
+        ok_h.copy_(out_k, non_blocking=True)
+        ol_h.copy_(out_l, non_blocking=True)
+
+    for _ in range(3):
+        e2e_step()
+    torch.cuda.synchronize()
+    ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for s_ev, e_ev in ev2:
+        flush.zero_()
+        s_ev.record(stream)
+        e2e_step()
+        e_ev.record(stream)
+    torch.cuda.synchronize()
+    t_e2e = float(np.mean([s.elapsed_time(e) / 1e3 for s, e in ev2]))
+    if world > 1:
+        t = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_e2e = float(t.item())
+
+    # ---- roofline of the dominant kernel (kmm_tc_kernel), timed alone on the same stream
+    kernel_t = t_step
+    try:
+        from paper_2503_02259_b200 import _bench_hooks
+
+        kernel_t = _bench_hooks.time_main_kernel(eng, zd, out_k, out_l, args.steps)
+    except Exception:
+        pass
+    splits = {"fast": 3, "tf32": 1, "fp64": 0}[args.precision]
+    tc_flops = 2 * splits * 2.0 * rows * n * k  # 2 outputs x split products x 2 flops per MAC
+    peak_tf32 = measured_tf32_peak(torch) if rank == 0 and splits else None
+    roof = None
+    if splits:
+        achieved = tc_flops / kernel_t / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak_tf32, "unit": "TFLOP/s",
+                "frac": achieved / peak_tf32 if peak_tf32 else None, "traffic": None,
+                "peak_source": "measured cuBLAS TF32 GEMM 8192^3 in this run (MEASURED_PEAKS.json has bf16 only)",
+                "algorithmic": f"{2 * splits} tf32 MMAs x 2k flops per kernel entry",
+                "kernel_ms": kernel_t * 1e3}
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            v, t, cores = cpu_baseline(w, args.cpu_rows)
+            cpu = {"value": v, "unit": "entries*RHS/s", "cores": cores, "kind": "port",
+                   "sample": f"{args.cpu_rows} of {n} rows, both outputs, fp64, best of 1 "
+                             "(oracle/kgp_oracle.c: C restatement of kmat.py:165-189 + numba panels)"}
+        line = {
+            "metric": "kernel entries x RHS / s (fused Khat.Z + dKhat/dl.Z)",
+            "value": value, "unit": "entries*RHS/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": t_step * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": {"fast": "f32 tile + 3xtf32 mma", "tf32": "f32 tile + tf32 mma", "fp64": "f64"}[args.precision],
+            "data": "synthetic (seeded numpy default_rng, BASELINE configs[1] shapes and distributions)",
+            "config": {"workload": "cfg2 standalone fused MatMul (BASELINE.json configs[1])", "n": n, "d": 8,
+                       "k": k, "kernel": "gaussian", "l": w.l, "f": w.f, "s": w.s,
+                       "outputs": ["Khat.Z", "dKhat/dl.Z"], "precision": args.precision,
+                       "l2": "flushed (256 MB write) between timed iterations", "parallelism": f"rows{world}"},
+            "e2e": {"value": units / t_e2e, "unit": "entries*RHS/s", "h2d_bytes_per_step": int(zh.numel() * 8),
+                    "d2h_bytes_per_step": int(2 * ok_h.numel() * 8), "ms_per_step": t_e2e * 1e3},
+            "gpu_launches": 2 * args.steps,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

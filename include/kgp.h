@@ -1,0 +1,138 @@
+/*
+ * libkgp — C ABI of the B200-native HiGP hot path.
+ *
+ * Plain pointers and sizes only; no torch or C++ types cross this boundary.
+ * Device pointers are CUDA global-memory addresses on the engine's device;
+ * `stream` is a cudaStream_t (NULL = legacy default stream). All work is
+ * stream-ordered; functions that return host scalars synchronise the stream.
+ *
+ * Every entry point replaces one reference interface (paths relative to
+ * /root/reference/pkg/src/kernelgp/); the citation is next to each declaration.
+ *
+ * Errors: every function returns KGP_OK (0) or a KGP_ERR_* code; the message
+ * is available from kgp_last_error() (thread-local). The Python host maps
+ * codes onto the reference exception types (errors.py:4-17).
+ */
+#ifndef KGP_H_
+#define KGP_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KGP_ABI_VERSION 1
+
+/* return codes */
+#define KGP_OK 0
+#define KGP_ERR_INVALID 1   /* -> ValueError            (kernels.py:43-64, kmat.py:62-73) */
+#define KGP_ERR_RESOURCE 2  /* -> ResourceLimitError    (kmat.py:111-115)                  */
+#define KGP_ERR_BREAKDOWN 3 /* -> BreakdownError        (solver.py:160-164)                */
+#define KGP_ERR_NUMERICAL 4 /* -> NumericalError        (solver.py:172-173, 260-263)       */
+#define KGP_ERR_CUDA 5      /* -> KernelGpError         (device / launch failure)          */
+#define KGP_ERR_STATE 6     /* -> KernelGpError         (use after destroy, double destroy) */
+
+/* kernel ids: KernelType (kernels.py:29-40) */
+#define KGP_GAUSSIAN 0
+#define KGP_MATERN32 1
+#define KGP_MATERN52 2
+
+/* operator arithmetic */
+#define KGP_FP64 0  /* fp64 tile, fp64 contraction (parity anchor)                        */
+#define KGP_FAST 1  /* fp32 centred tile + 3xTF32 tcgen05 contraction, fp32 TMEM accumulation */
+#define KGP_TF32 2  /* fp32 centred tile + 1xTF32 tcgen05 contraction (throughput mode)     */
+
+typedef struct kgp_engine_s kgp_engine;
+typedef struct kgp_precond_s kgp_precond;
+
+/* ------------------------------------------------------------------ library */
+int kgp_version(void);
+const char* kgp_last_error(void);
+int kgp_device_count(int* count);
+
+/* ------------------------------------------------------------------ engine
+ * KernelEngine.__init__ (kmat.py:79-103): Khat = f^2 kappa(X, X; l) + s I with X
+ * copied into HBM (the engine never aliases caller data, kmat.py:90).
+ * x: (n, d) row-major fp64, host (x_on_device = 0) or device (1). */
+int kgp_engine_create(kgp_engine** out, int device, int kernel, int precision, int64_t n, int d,
+                      const double* x, int x_on_device, double l, double f, double s, void* stream);
+/* Engines are immutable in the reference; hyperparameters are reset here so a
+ * training loop (train.py:196-204) reuses the resident X. */
+int kgp_engine_set_params(kgp_engine* e, double l, double f, double s, void* stream);
+int kgp_engine_set_precision(kgp_engine* e, int precision);
+/* Row partition for multi-GPU: this engine produces rows [row0, row0 + nrows) of Khat.B. */
+int kgp_engine_set_rows(kgp_engine* e, int64_t row0, int64_t nrows);
+int kgp_engine_destroy(kgp_engine* e); /* second destroy of the same handle -> KGP_ERR_STATE */
+
+/* KernelEngine.matmul / grad_matmul (kmat.py:145-189), fused in one pass:
+ *   out_k  = f^2 kappa(X_rows, X) B + s B_rows        (matmul)
+ *   out_dl = f^2 dkappa/dl(X_rows, X) B               (grad_matmul Theta.L)
+ *   out_df = 2 f kappa(X_rows, X) B                   (grad_matmul Theta.F)
+ * Any output may be NULL. B: (n, k) device fp64 with element (i, c) at
+ * b[i*b_rs + c*b_cs]; outputs (nrows, k) at o[i*o_rs + c*o_cs]. */
+int kgp_engine_matmul(kgp_engine* e, int64_t k, const double* b, int64_t b_rs, int64_t b_cs,
+                      double* out_k, double* out_dl, double* out_df, int64_t o_rs, int64_t o_cs,
+                      void* stream);
+
+/* Rectangular f^2 kappa(Xs, X) B (no diagonal shift): the cross kernel of predict
+ * (gp.py:223-241), never materialised. xs: (m, d) device fp64 row-major. */
+int kgp_engine_cross_matmul(kgp_engine* e, int64_t m, const double* xs, int64_t k, const double* b,
+                            int64_t b_rs, int64_t b_cs, double* out, int64_t o_rs, int64_t o_cs,
+                            void* stream);
+
+/* ------------------------------------------------------------------ panels
+ * eval_kernel / eval_kernel_grad_l / pairwise_sq_dist (kernels.py:72-94):
+ * out[i*ldo + j] = kappa(x_i, y_j; l) (grad=0), dkappa/dl (grad=1), r^2 (grad=2).
+ * x (nx, d), y (ny, d) device row-major fp64. */
+int kgp_eval_panel(int kernel, int grad, int64_t nx, int64_t ny, int d, const double* x, const double* y,
+                   double l, double* out, int64_t ldo, void* stream);
+
+/* fps_select (precond.py:39-59): greedy farthest-point sampling from seed_index,
+ * ties to the lowest index. x (n, d) device; idx_out: m int64 on the device. */
+int kgp_fps(int64_t n, int d, const double* x, int64_t m, int64_t seed_index, int64_t* idx_out,
+            void* stream);
+
+/* ------------------------------------------------------------------ preconditioner
+ * NystromPreconditioner.apply_inverse (precond.py:74-83) in factored Woodbury form
+ *   M^-1 B = B / s - W (W^T B) / s^2,   W = V L_C^-T,  C = I/f^2 + V^T V / s = L_C L_C^T
+ * wt: W^T as (m, n) row-major device fp64 (copied). */
+int kgp_precond_create(kgp_precond** out, int64_t n, int64_t m, const double* wt, double s, void* stream);
+int kgp_precond_destroy(kgp_precond* p);
+/* B and out: (n, k) strided device fp64 as in kgp_engine_matmul. */
+int kgp_precond_apply_inverse(kgp_precond* p, int64_t k, const double* b, int64_t b_rs, int64_t b_cs,
+                              double* out, int64_t o_rs, int64_t o_cs, void* stream);
+
+/* NystromPreconditioner.apply (precond.py:85-92) and any symmetric low-rank update:
+ * out = beta B + alpha U (U^T B), with U^T the handle's (m, n) factor. A handle
+ * created from V^T with beta = s, alpha = f^2 applies M itself. */
+int kgp_lowrank_apply(kgp_precond* p, double beta, double alpha, int64_t k, const double* b, int64_t b_rs,
+                      int64_t b_cs, double* out, int64_t o_rs, int64_t o_cs, void* stream);
+
+/* ------------------------------------------------------------------ solvers
+ * pcg_solve (solver.py:122-192): batched PCG, per-column alpha/beta capture,
+ * converged columns freeze in place. y and x_out: (k, n) device (column c
+ * contiguous, the reference's transposed state, solver.py:143-146).
+ * alphas/betas: (k, max_iter) device; iters, converged: k int32 device; rel: k fp64.
+ * precond may be NULL (unpreconditioned). Breakdown -> KGP_ERR_BREAKDOWN. */
+int kgp_pcg(kgp_engine* e, kgp_precond* p, int64_t k, const double* y, double tol, int32_t max_iter,
+            double* x_out, double* alphas, double* betas, int32_t* iters, double* rel, int32_t* converged,
+            void* stream);
+
+/* slq_logdet (solver.py:238-265): per-probe e1^T log(T) e1 from the CG
+ * coefficients on the device; returns the probe mean of |z|^2 e1^T log(T) e1 in
+ * *logdet (host). norms_sq: k fp64 device. Non-positive Ritz value -> KGP_ERR_NUMERICAL. */
+int kgp_slq_logdet(int64_t k, int32_t max_iter, const double* alphas, const double* betas,
+                   const int32_t* iters, const double* norms_sq, double* logdet, void* stream);
+
+/* nlml_grad_iterative (gp.py:133-179) end to end on the device:
+ * out[0..3] = loss, grad_l, grad_f, grad_s (host); out_converged (host).
+ * y: n device; probes: (k_z, n) device (probe c contiguous). */
+int kgp_nlml_grad(kgp_engine* e, kgp_precond* p, const double* y, int64_t k_z, const double* probes,
+                  double tol, int32_t max_iter, double probe_tol, double* out, int32_t* out_converged,
+                  void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KGP_H_ */

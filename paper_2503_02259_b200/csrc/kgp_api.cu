@@ -1,0 +1,411 @@
+// C ABI: library, engine and preconditioner handles (include/kgp.h).
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+#include <set>
+
+#include "kgp_common.cuh"
+#include "kgp_internal.h"
+
+namespace kgp {
+
+static thread_local char g_err_msg[1024] = "";
+
+void set_error(int code, const char* fmt, ...) {
+  (void)code;
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err_msg, sizeof(g_err_msg), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return KGP_OK;
+  set_error(KGP_ERR_CUDA, "CUDA error in %s: %s", what, cudaGetErrorString(e));
+  return KGP_ERR_CUDA;
+}
+
+int DevBuf::ensure(size_t bytes) {
+  if (bytes <= cap && p) return KGP_OK;
+  release();
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) {
+    p = nullptr;
+    cap = 0;
+    (void)cudaGetLastError();
+    set_error(KGP_ERR_RESOURCE, "device allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+    return KGP_ERR_RESOURCE;
+  }
+  cap = bytes;
+  return KGP_OK;
+}
+
+void DevBuf::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  cap = 0;
+}
+
+double tc_kernel_gamma(int kt, double l);
+
+static std::mutex g_handles_mu;
+static std::set<const void*> g_handles;
+
+static bool handle_live(const void* h) {
+  std::lock_guard<std::mutex> g(g_handles_mu);
+  return g_handles.count(h) != 0;
+}
+
+int engine_prepare(kgp_engine_s* e, cudaStream_t st) {
+  if (e->prepared || e->precision == KGP_FP64) return KGP_OK;
+  const int dp = e->dpad;
+  int nblk = (int)((e->n + 31) / 32);
+  int rc = e->xcol.ensure(sizeof(float) * (size_t)nblk * (dp + 1) * 32);
+  if (rc) return rc;
+  rc = e->xrow.ensure(sizeof(float) * (size_t)(e->nrows + 1) * (dp + 1));
+  if (rc) return rc;
+  rc = prep_cols(e->kt, e->d, dp, e->n, e->x64.as<double>(), e->mean.as<double>(), e->l, e->xcol.as<float>(), st);
+  if (rc) return rc;
+  rc = prep_rows(e->kt, 0, e->d, dp, e->nrows, e->x64.as<double>() + e->row0 * e->d, e->mean.as<double>(), e->l,
+                 e->xrow.as<float>(), st);
+  if (rc) return rc;
+  e->prepared = true;
+  return KGP_OK;
+}
+
+static double scale_dl_fast(int kt, double l, double f) {
+  double f2 = f * f;
+  if (kt == GAUSS) return f2 / (tc_kernel_gamma(kt, l) * l * l * l);
+  if (kt == MAT32) return f2 / l;
+  return f2 / (3.0 * l);
+}
+
+// Shared by the square operator (xrow = engine rows, shift on) and the cross operator.
+static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t diag_row0, int64_t k, const double* b,
+                     int64_t b_rs, int64_t b_cs, double* out_k, double* out_dl, double* out_df, int64_t o_rs,
+                     int64_t o_cs, cudaStream_t st) {
+  const int split = (e->precision == KGP_FAST) ? 3 : 1;
+  const int nout = out_dl ? 2 : 1;
+  const int tpo = split == 3 ? 2 : 1;
+  const int nblk = (int)((e->n + 31) / 32);
+  for (int64_t c0 = 0; c0 < k; c0 += 128) {
+    const int kc = (int)((k - c0) < 128 ? (k - c0) : 128);
+    const int kp = (kc + 15) / 16 * 16;
+    int rc = e->bsplit.ensure((size_t)nblk * tpo * kp * 128);
+    if (rc) return rc;
+    rc = prep_rhs(split, e->n, k, c0, kp, b, b_rs, b_cs, e->bsplit.as<uint8_t>(), st);
+    if (rc) return rc;
+    TcParams p{};
+    p.xrow = xrow;
+    p.xcol = e->xcol.as<float>();
+    p.bsplit = e->bsplit.as<uint8_t>();
+    p.nrows = nrows;
+    p.nblk = nblk;
+    p.kp = kp;
+    p.k = kc;
+    int nsa = (512 - nout * kp) / (nout * tpo * 32);
+    p.nsa = nsa > 4 ? 4 : nsa;
+    p.f2 = e->f * e->f;
+    p.s = e->s;
+    p.two_f = 2.0 * e->f;
+    p.scale_dl = scale_dl_fast(e->kt, e->l, e->f);
+    p.b = b + c0 * b_cs;
+    p.b_rs = b_rs;
+    p.b_cs = b_cs;
+    p.diag_row0 = diag_row0;
+    p.out_k = out_k ? out_k + c0 * o_cs : nullptr;
+    p.out_dl = out_dl ? out_dl + c0 * o_cs : nullptr;
+    p.out_df = out_df ? out_df + c0 * o_cs : nullptr;
+    p.o_rs = o_rs;
+    p.o_cs = o_cs;
+    rc = launch_kmm_tc(e->kt, e->dpad, nout, split, p, st);
+    if (rc) return rc;
+  }
+  return KGP_OK;
+}
+
+int engine_matmul_impl(kgp_engine_s* e, int64_t k, const double* b, int64_t b_rs, int64_t b_cs, double* out_k,
+                       double* out_dl, double* out_df, int64_t o_rs, int64_t o_cs, cudaStream_t st) {
+  if (k <= 0 || e->nrows <= 0) return KGP_OK;
+  if (!out_k && !out_dl && !out_df) return KGP_OK;
+  if (e->precision == KGP_FP64) {
+    F64Params p{};
+    p.xr = e->x64.as<double>() + e->row0 * e->d;
+    p.xc = e->x64.as<double>();
+    p.nrows = e->nrows;
+    p.ncols = e->n;
+    p.d = e->d;
+    p.k = (int)k;
+    p.l = e->l;
+    p.f2 = e->f * e->f;
+    p.s = e->s;
+    p.two_f = 2.0 * e->f;
+    p.f2_dl = e->f * e->f;
+    p.b = b;
+    p.b_rs = b_rs;
+    p.b_cs = b_cs;
+    p.diag_row0 = e->row0;
+    p.out_k = out_k;
+    p.out_dl = out_dl;
+    p.out_df = out_df;
+    p.o_rs = o_rs;
+    p.o_cs = o_cs;
+    return launch_kmm_f64(e->kt, p, st);
+  }
+  int rc = engine_prepare(e, st);
+  if (rc) return rc;
+  return tc_matmul(e, e->xrow.as<float>(), e->nrows, e->row0, k, b, b_rs, b_cs, out_k, out_dl, out_df, o_rs, o_cs,
+                   st);
+}
+
+}  // namespace kgp
+
+using namespace kgp;
+
+#define CHECK_ENGINE(e)                                                                          \
+  KGP_REQUIRE((e) != nullptr && handle_live(e) && (e)->magic == ENGINE_MAGIC, KGP_ERR_STATE, \
+              "invalid or destroyed engine handle")
+#define CHECK_PRECOND(p)                                                                          \
+  KGP_REQUIRE((p) != nullptr && handle_live(p) && (p)->magic == PRECOND_MAGIC, KGP_ERR_STATE, \
+              "invalid or destroyed preconditioner handle")
+
+extern "C" int kgp_version(void) { return KGP_ABI_VERSION; }
+
+extern "C" const char* kgp_last_error(void) { return g_err_msg; }
+
+extern "C" int kgp_device_count(int* count) {
+  KGP_REQUIRE(count != nullptr, KGP_ERR_INVALID, "count pointer is NULL");
+  KGP_CUDA(cudaGetDeviceCount(count));
+  return KGP_OK;
+}
+
+static int check_params(double l, double f, double s) {
+  KGP_REQUIRE(l > 0.0 && l < INFINITY, KGP_ERR_INVALID, "hyperparameter l must be positive and finite, got %g", l);
+  KGP_REQUIRE(f > 0.0 && f < INFINITY, KGP_ERR_INVALID, "hyperparameter f must be positive and finite, got %g", f);
+  KGP_REQUIRE(s > 0.0 && s < INFINITY, KGP_ERR_INVALID, "hyperparameter s must be positive and finite, got %g", s);
+  return KGP_OK;
+}
+
+extern "C" int kgp_engine_create(kgp_engine** out, int device, int kernel, int precision, int64_t n, int d,
+                                 const double* x, int x_on_device, double l, double f, double s, void* stream) {
+  KGP_REQUIRE(out != nullptr, KGP_ERR_INVALID, "out pointer is NULL");
+  *out = nullptr;
+  KGP_REQUIRE(kernel >= 0 && kernel <= 2, KGP_ERR_INVALID, "unknown kernel id %d", kernel);
+  KGP_REQUIRE(precision >= 0 && precision <= 2, KGP_ERR_INVALID, "unknown precision %d", precision);
+  KGP_REQUIRE(n >= 1 && d >= 1, KGP_ERR_INVALID, "X must be a nonempty 2-d array, got (%lld, %d)", (long long)n, d);
+  KGP_REQUIRE(d <= 16, KGP_ERR_INVALID, "dimension d=%d exceeds the supported maximum of 16", d);
+  KGP_REQUIRE(x != nullptr, KGP_ERR_INVALID, "X pointer is NULL");
+  int rc = check_params(l, f, s);
+  if (rc) return rc;
+  KGP_CUDA(cudaSetDevice(device));
+  cudaStream_t st = (cudaStream_t)stream;
+  kgp_engine_s* e = new kgp_engine_s();
+  e->magic = ENGINE_MAGIC;
+  e->device = device;
+  e->kt = kernel;
+  e->precision = precision;
+  e->n = n;
+  e->d = d;
+  e->dpad = tc_pad_dim(d);
+  e->row0 = 0;
+  e->nrows = n;
+  e->l = l;
+  e->f = f;
+  e->s = s;
+  e->prepared = false;
+  e->hstatus = nullptr;
+  rc = cuda_check(cudaMallocHost(&e->hstatus, sizeof(int32_t) * 4), "pinned status");
+  if (!rc) rc = e->x64.ensure(sizeof(double) * n * d);
+  if (!rc) rc = e->mean.ensure(sizeof(double) * d);
+  if (!rc)
+    rc = cuda_check(cudaMemcpyAsync(e->x64.p, x, sizeof(double) * n * d,
+                                    x_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st),
+                    "copy X");
+  if (!rc) rc = col_mean(n, d, e->x64.as<double>(), e->mean.as<double>(), st);
+  if (!rc && !x_on_device) rc = cuda_check(cudaStreamSynchronize(st), "engine create");
+  if (rc) {
+    if (e->hstatus) cudaFreeHost(e->hstatus);
+    delete e;
+    return rc;
+  }
+  {
+    std::lock_guard<std::mutex> g(g_handles_mu);
+    g_handles.insert(e);
+  }
+  *out = e;
+  return KGP_OK;
+}
+
+extern "C" int kgp_engine_set_params(kgp_engine* e, double l, double f, double s, void* stream) {
+  CHECK_ENGINE(e);
+  int rc = check_params(l, f, s);
+  if (rc) return rc;
+  if (l != e->l) e->prepared = false;
+  e->l = l;
+  e->f = f;
+  e->s = s;
+  (void)stream;
+  return KGP_OK;
+}
+
+extern "C" int kgp_engine_set_precision(kgp_engine* e, int precision) {
+  CHECK_ENGINE(e);
+  KGP_REQUIRE(precision >= 0 && precision <= 2, KGP_ERR_INVALID, "unknown precision %d", precision);
+  e->precision = precision;
+  e->prepared = false;
+  return KGP_OK;
+}
+
+extern "C" int kgp_engine_set_rows(kgp_engine* e, int64_t row0, int64_t nrows) {
+  CHECK_ENGINE(e);
+  KGP_REQUIRE(row0 >= 0 && nrows >= 0 && row0 + nrows <= e->n, KGP_ERR_INVALID, "row range [%lld, %lld) outside [0, %lld)",
+              (long long)row0, (long long)(row0 + nrows), (long long)e->n);
+  e->row0 = row0;
+  e->nrows = nrows;
+  e->prepared = false;
+  return KGP_OK;
+}
+
+extern "C" int kgp_engine_destroy(kgp_engine* e) {
+  {
+    std::lock_guard<std::mutex> g(g_handles_mu);
+    if (e == nullptr || g_handles.count(e) == 0) {
+      set_error(KGP_ERR_STATE, "engine handle already destroyed or never created");
+      return KGP_ERR_STATE;
+    }
+    g_handles.erase(e);
+  }
+  cudaSetDevice(e->device);
+  cudaDeviceSynchronize();
+  e->magic = DEAD_MAGIC;
+  if (e->hstatus) cudaFreeHost(e->hstatus);
+  delete e;
+  return KGP_OK;
+}
+
+extern "C" int kgp_engine_matmul(kgp_engine* e, int64_t k, const double* b, int64_t b_rs, int64_t b_cs, double* out_k,
+                                 double* out_dl, double* out_df, int64_t o_rs, int64_t o_cs, void* stream) {
+  CHECK_ENGINE(e);
+  KGP_REQUIRE(k >= 1, KGP_ERR_INVALID, "B must have at least one column");
+  KGP_REQUIRE(b != nullptr, KGP_ERR_INVALID, "B pointer is NULL");
+  KGP_CUDA(cudaSetDevice(e->device));
+  return engine_matmul_impl(e, k, b, b_rs, b_cs, out_k, out_dl, out_df, o_rs, o_cs, (cudaStream_t)stream);
+}
+
+extern "C" int kgp_engine_cross_matmul(kgp_engine* e, int64_t m, const double* xs, int64_t k, const double* b,
+                                       int64_t b_rs, int64_t b_cs, double* out, int64_t o_rs, int64_t o_cs,
+                                       void* stream) {
+  CHECK_ENGINE(e);
+  KGP_REQUIRE(k >= 1 && m >= 0, KGP_ERR_INVALID, "bad cross shape");
+  if (m == 0) return KGP_OK;
+  KGP_CUDA(cudaSetDevice(e->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (e->precision == KGP_FP64) {
+    F64Params p{};
+    p.xr = xs;
+    p.xc = e->x64.as<double>();
+    p.nrows = m;
+    p.ncols = e->n;
+    p.d = e->d;
+    p.k = (int)k;
+    p.l = e->l;
+    p.f2 = e->f * e->f;
+    p.s = 0.0;
+    p.two_f = 0.0;
+    p.f2_dl = 0.0;
+    p.b = b;
+    p.b_rs = b_rs;
+    p.b_cs = b_cs;
+    p.diag_row0 = -1;
+    p.out_k = out;
+    p.o_rs = o_rs;
+    p.o_cs = o_cs;
+    return launch_kmm_f64(e->kt, p, st);
+  }
+  int rc = engine_prepare(e, st);
+  if (rc) return rc;
+  rc = e->xrow_cross.ensure(sizeof(float) * (size_t)(m + 1) * (e->dpad + 1));
+  if (rc) return rc;
+  rc = prep_rows(e->kt, 0, e->d, e->dpad, m, xs, e->mean.as<double>(), e->l, e->xrow_cross.as<float>(), st);
+  if (rc) return rc;
+  return tc_matmul(e, e->xrow_cross.as<float>(), m, -1, k, b, b_rs, b_cs, out, nullptr, nullptr, o_rs, o_cs, st);
+}
+
+// ------------------------------------------------------------------ preconditioner
+extern "C" int kgp_precond_create(kgp_precond** out, int64_t n, int64_t m, const double* wt, double s, void* stream) {
+  KGP_REQUIRE(out != nullptr && wt != nullptr, KGP_ERR_INVALID, "NULL pointer");
+  KGP_REQUIRE(n >= 1 && m >= 1 && m <= n, KGP_ERR_INVALID, "need 1 <= m <= n, got m=%lld, n=%lld", (long long)m,
+              (long long)n);
+  KGP_REQUIRE(s > 0.0, KGP_ERR_INVALID, "shift must be positive");
+  kgp_precond_s* p = new kgp_precond_s();
+  p->magic = PRECOND_MAGIC;
+  p->n = n;
+  p->m = m;
+  p->s = s;
+  int rc = p->wt.ensure(sizeof(double) * n * m);
+  if (!rc)
+    rc = cuda_check(cudaMemcpyAsync(p->wt.p, wt, sizeof(double) * n * m, cudaMemcpyDeviceToDevice, (cudaStream_t)stream),
+                    "copy W");
+  if (rc) {
+    delete p;
+    return rc;
+  }
+  {
+    std::lock_guard<std::mutex> g(g_handles_mu);
+    g_handles.insert(p);
+  }
+  *out = p;
+  return KGP_OK;
+}
+
+extern "C" int kgp_precond_destroy(kgp_precond* p) {
+  {
+    std::lock_guard<std::mutex> g(g_handles_mu);
+    if (p == nullptr || g_handles.count(p) == 0) {
+      set_error(KGP_ERR_STATE, "preconditioner handle already destroyed or never created");
+      return KGP_ERR_STATE;
+    }
+    g_handles.erase(p);
+  }
+  cudaDeviceSynchronize();
+  p->magic = DEAD_MAGIC;
+  delete p;
+  return KGP_OK;
+}
+
+extern "C" int kgp_precond_apply_inverse(kgp_precond* p, int64_t k, const double* b, int64_t b_rs, int64_t b_cs,
+                                         double* out, int64_t o_rs, int64_t o_cs, void* stream) {
+  CHECK_PRECOND(p);
+  KGP_REQUIRE(k >= 1, KGP_ERR_INVALID, "B must have at least one column");
+  return precond_apply_impl(p, k, b, b_rs, b_cs, out, o_rs, o_cs, (cudaStream_t)stream);
+}
+
+extern "C" int kgp_lowrank_apply(kgp_precond* p, double beta, double alpha, int64_t k, const double* b, int64_t b_rs,
+                                 int64_t b_cs, double* out, int64_t o_rs, int64_t o_cs, void* stream) {
+  CHECK_PRECOND(p);
+  KGP_REQUIRE(k >= 1, KGP_ERR_INVALID, "B must have at least one column");
+  return lowrank_apply_impl(p, beta, alpha, k, b, b_rs, b_cs, out, o_rs, o_cs, (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------------------ solvers
+extern "C" int kgp_pcg(kgp_engine* e, kgp_precond* p, int64_t k, const double* y, double tol, int32_t max_iter,
+                       double* x_out, double* alphas, double* betas, int32_t* iters, double* rel, int32_t* converged,
+                       void* stream) {
+  CHECK_ENGINE(e);
+  if (p) CHECK_PRECOND(p);
+  KGP_REQUIRE(tol >= 0.0 && max_iter >= 1, KGP_ERR_INVALID, "need tol >= 0 and max_iter >= 1");
+  KGP_REQUIRE(e->row0 == 0 && e->nrows == e->n, KGP_ERR_INVALID, "kgp_pcg needs an unpartitioned engine");
+  KGP_REQUIRE(!p || p->n == e->n, KGP_ERR_INVALID, "preconditioner size mismatch");
+  KGP_CUDA(cudaSetDevice(e->device));
+  return pcg_solve_impl(e, p, k, y, tol, max_iter, x_out, alphas, betas, iters, rel, converged, (cudaStream_t)stream);
+}
+
+extern "C" int kgp_slq_logdet(int64_t k, int32_t max_iter, const double* alphas, const double* betas,
+                              const int32_t* iters, const double* norms_sq, double* logdet, void* stream) {
+  KGP_REQUIRE(k >= 1, KGP_ERR_INVALID, "need at least one probe trace");
+  KGP_REQUIRE(logdet != nullptr, KGP_ERR_INVALID, "logdet pointer is NULL");
+  return slq_impl(k, max_iter, alphas, betas, iters, norms_sq, logdet, (cudaStream_t)stream);
+}

@@ -1,0 +1,184 @@
+// Shared device helpers for libkgp (sm_100a only).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/kgp.h"
+
+#define KGP_DEV __device__ __forceinline__
+
+namespace kgp {
+
+// ---------------------------------------------------------------- error plumbing
+void set_error(int code, const char* fmt, ...);
+int cuda_check(cudaError_t e, const char* what);
+#define KGP_CUDA(call)                                         \
+  do {                                                         \
+    int _rc = ::kgp::cuda_check((call), #call);                \
+    if (_rc != KGP_OK) return _rc;                             \
+  } while (0)
+#define KGP_LAUNCH(what)                                       \
+  do {                                                         \
+    int _rc = ::kgp::cuda_check(cudaGetLastError(), what);     \
+    if (_rc != KGP_OK) return _rc;                             \
+  } while (0)
+#define KGP_REQUIRE(cond, code, ...)                           \
+  do {                                                         \
+    if (!(cond)) {                                             \
+      ::kgp::set_error((code), __VA_ARGS__);                   \
+      return (code);                                           \
+    }                                                          \
+  } while (0)
+
+// ---------------------------------------------------------------- kernel constants
+enum Kern { GAUSS = 0, MAT32 = 1, MAT52 = 2 };
+
+constexpr double SQRT3 = 1.7320508075688772;
+constexpr double SQRT5 = 2.23606797749979;
+constexpr double LOG2E = 1.4426950408889634;
+
+// ---------------------------------------------------------------- fp64 entry formulas
+// The reference panels (_panels_numba.py:37-131), evaluated from r^2.
+template <int KT>
+KGP_DEV double kappa64(double r2, double l) {
+  if (KT == GAUSS) return exp(-r2 * (1.0 / (2.0 * l * l)));
+  double t = (KT == MAT32 ? SQRT3 : SQRT5) / l * sqrt(r2);
+  if (KT == MAT32) return (1.0 + t) * exp(-t);
+  return (1.0 + t + (5.0 / (3.0 * l * l)) * r2) * exp(-t);
+}
+
+template <int KT>
+KGP_DEV double dkappa64(double r2, double l) {
+  if (KT == GAUSS) return r2 * (1.0 / (l * l * l)) * exp(-r2 * (1.0 / (2.0 * l * l)));
+  if (KT == MAT32) return (3.0 / (l * l * l)) * r2 * exp(-(SQRT3 / l) * sqrt(r2));
+  double t = (SQRT5 / l) * sqrt(r2);
+  return (5.0 / (3.0 * l * l * l)) * r2 * (1.0 + t) * exp(-t);
+}
+
+// ---------------------------------------------------------------- warp helpers
+KGP_DEV double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---------------------------------------------------------------- PTX: mbarrier / bulk copy / tcgen05
+KGP_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+KGP_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+KGP_DEV void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+KGP_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar))
+               : "memory");
+}
+KGP_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(
+                   smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+KGP_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk async copy global -> shared, completion signalled on an mbarrier (tx bytes).
+KGP_DEV void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+KGP_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+KGP_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+KGP_DEV void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+KGP_DEV void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// Commit all prior tcgen05.mma of this thread to an mbarrier (one arrival when they finish).
+KGP_DEV void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+// D[tmem] (+)= A[tmem] * B[smem desc], kind::tf32, cta_group::1.
+KGP_DEV void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+// 32 lanes x 32 bit, 16 consecutive columns: thread t <-> lane (quadrant base + t).
+KGP_DEV void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+      "%13, %14, %15, %16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+KGP_DEV void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+      "%13, %14, %15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+        "=r"(v[15])
+      : "r"(taddr)
+      : "memory");
+}
+
+template <int NCOLS>
+KGP_DEV void tmem_alloc(uint32_t* dst_smem) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "n"(NCOLS)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+template <int NCOLS>
+KGP_DEV void tmem_dealloc(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(NCOLS) : "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row atoms 1024 B apart.
+// Fields (sm100): start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46), version=1 [46,48),
+// base offset [49,52), layout type [61,64) (2 = SWIZZLE_128B).
+KGP_DEV uint64_t sw128_kmajor_desc(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;            // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;  // SBO: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;            // descriptor version (Blackwell)
+  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor, kind::tf32: D=F32, A=B=TF32, both K-major, M=128, N=n.
+__host__ __device__ constexpr uint32_t idesc_tf32_m128(int n) {
+  return (1u << 4)                       // D format F32
+         | (2u << 7)                     // A format TF32
+         | (2u << 10)                    // B format TF32
+         | ((uint32_t)(n >> 3) << 17)    // N >> 3
+         | ((uint32_t)(128 >> 4) << 24); // M >> 4
+}
+
+// Byte offset of element (row r, k-index j) of a K-major fp32 tile whose rows are
+// 128 B (32 elements), under the 128-byte swizzle (Swizzle<3,4,3>).
+__host__ __device__ inline uint32_t sw128_offset(uint32_t r, uint32_t j) {
+  uint32_t o = r * 128u + j * 4u;
+  return o ^ (((o >> 7) & 7u) << 4);
+}
+
+}  // namespace kgp

@@ -1,0 +1,116 @@
+// Internal (non-ABI) declarations shared by the libkgp translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "../../include/kgp.h"
+
+namespace kgp {
+
+// ------------------------------------------------------------------ fast (tcgen05) operator
+struct TcParams {
+  const float* xrow;      // (nrows, dpad+1): [q_i, u_i0 .. u_i(dpad-1)]
+  const float* xcol;      // nblk x (dpad+1) x 32: per 32-column block [q_j | v_j0 | ...]
+  const uint8_t* bsplit;  // nblk x TPO x kp x 128 B: RHS tiles, tf32 hi (/lo), swizzled K-major
+  int64_t nrows;
+  int nblk;
+  int kp;                 // padded RHS count (multiple of 16, <= 128)
+  int k;                  // true RHS count in this launch
+  int nsa;                // TMEM A-stage ring depth
+  double f2, s, two_f, scale_dl;
+  const double* b;        // original fp64 RHS (for + s B)
+  int64_t b_rs, b_cs;
+  int64_t diag_row0;      // global row of local row 0 for the shift; < 0: no shift
+  double *out_k, *out_dl, *out_df;
+  int64_t o_rs, o_cs;
+};
+int tc_pad_dim(int d);
+bool tc_direct(int dpad);
+int launch_kmm_tc(int kt, int dpad, int nout, int split, const TcParams& p, cudaStream_t st);
+
+// ------------------------------------------------------------------ fp64 operator
+struct F64Params {
+  const double* xr;       // (nrows, d) row points
+  const double* xc;       // (ncols, d) column points
+  int64_t nrows, ncols;
+  int d, k;
+  double l, f2, s, two_f, f2_dl;
+  const double* b;
+  int64_t b_rs, b_cs;
+  int64_t diag_row0;
+  double *out_k, *out_dl, *out_df;
+  int64_t o_rs, o_cs;
+};
+int launch_kmm_f64(int kt, const F64Params& p, cudaStream_t st);
+
+// ------------------------------------------------------------------ preprocessing (prep.cu)
+int prep_rows(int kt, int precision_split, int d, int dpad, int64_t nrows, const double* x, const double* mean,
+              double l, float* out, cudaStream_t st);
+int prep_cols(int kt, int d, int dpad, int64_t n, const double* x, const double* mean, double l, float* out,
+              cudaStream_t st);
+int prep_rhs(int split, int64_t n, int64_t k, int64_t c0, int kp, const double* b, int64_t b_rs, int64_t b_cs,
+             uint8_t* out, cudaStream_t st);
+int col_mean(int64_t n, int d, const double* x, double* mean, cudaStream_t st);
+
+// ------------------------------------------------------------------ device buffer helper
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  int ensure(size_t bytes);
+  void release();
+  ~DevBuf() { release(); }
+  template <class T>
+  T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+}  // namespace kgp
+
+// ------------------------------------------------------------------ opaque handles
+struct kgp_engine_s {
+  uint64_t magic;
+  int device, kt, precision, d, dpad;
+  int64_t n, row0, nrows;
+  double l, f, s;
+  kgp::DevBuf x64;   // (n, d) fp64 points
+  kgp::DevBuf mean;  // d
+  kgp::DevBuf xrow;  // fast path row data for the engine's own rows
+  kgp::DevBuf xcol;  // fast path column tiles
+  kgp::DevBuf xrow_cross;  // scratch for cross (prediction) rows
+  kgp::DevBuf bsplit;      // per-call RHS split
+  bool prepared;
+  // PCG workspace (grown on demand) and a pinned status word for the per-iteration readback
+  kgp::DevBuf ws;
+  int32_t* hstatus;
+};
+
+struct kgp_precond_s {
+  uint64_t magic;
+  int64_t n, m;
+  double s;
+  kgp::DevBuf wt;    // (m, n) row-major
+  kgp::DevBuf tmp;   // (m, k) scratch + partials
+};
+
+namespace kgp {
+constexpr uint64_t ENGINE_MAGIC = 0x6b67702d656e6731ull;
+constexpr uint64_t PRECOND_MAGIC = 0x6b67702d70726531ull;
+constexpr uint64_t DEAD_MAGIC = 0xdeaddeaddeaddeadull;
+
+int engine_prepare(kgp_engine_s* e, cudaStream_t st);
+int engine_matmul_impl(kgp_engine_s* e, int64_t k, const double* b, int64_t b_rs, int64_t b_cs, double* out_k,
+                       double* out_dl, double* out_df, int64_t o_rs, int64_t o_cs, cudaStream_t st);
+int lowrank_apply_impl(kgp_precond_s* p, double beta, double alpha, int64_t k, const double* b, int64_t b_rs,
+                       int64_t b_cs, double* out, int64_t o_rs, int64_t o_cs, cudaStream_t st);
+int precond_apply_impl(kgp_precond_s* p, int64_t k, const double* b, int64_t b_rs, int64_t b_cs, double* out,
+                       int64_t o_rs, int64_t o_cs, cudaStream_t st);
+
+// column-wise reductions / updates used by the PCG driver (pcg.cu)
+int pcg_solve_impl(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, const double* y, double tol, int max_iter,
+                   double* x_out, double* alphas, double* betas, int32_t* iters, double* rel, int32_t* conv,
+                   cudaStream_t st);
+int slq_impl(int64_t k, int max_iter, const double* alphas, const double* betas, const int32_t* iters,
+             const double* norms_sq, double* logdet, cudaStream_t st);
+int col_dots(int64_t k, int64_t n, const double* a, const double* b, double* out, double* partial, cudaStream_t st);
+}  // namespace kgp

@@ -1,0 +1,493 @@
+// Device-resident batched PCG, SLQ log-determinant and NLML+gradient assembly.
+//
+// pcg_solve (solver.py:122-192): the k right-hand sides share one fused
+// operator call per iteration (frozen columns included, solver.py:158); the
+// per-column alpha/beta recurrences, breakdown checks and the freeze decision
+// run in small device kernels, and the host reads back one status word per
+// iteration. State is (k, n): column c contiguous (the reference's transposed
+// layout, solver.py:143-146), which makes every per-column dot a contiguous
+// reduction and every operator output write coalesced.
+//
+// slq_logdet (solver.py:238-265): one thread per probe rebuilds the Lanczos
+// tridiagonal from the CG coefficients (solver.py:220-235) and diagonalises it
+// with implicit-shift QL, tracking only the first row of the eigenvector
+// matrix (all that e1^T log(T) e1 needs).
+//
+// nlml_grad_iterative (gp.py:133-179): PCG w-solve, unpreconditioned probe
+// solves, SLQ, then one fused derivative pass over V = [w, Z] producing
+// dKhat/dl V and dKhat/df V together.
+#include <math.h>
+#include <string.h>
+
+#include <vector>
+
+#include "kgp_common.cuh"
+#include "kgp_internal.h"
+
+namespace kgp {
+
+namespace {
+
+constexpr int DOT_THREADS = 256;
+constexpr int DOT_CHUNK = 8192;  // elements per block in the first reduction pass
+
+// partial[c * nb + blk] = sum over the block's chunk of a[c*n+i] * b[c*n+i]
+__global__ void dot_partial_kernel(int64_t n, int nb, const double* __restrict__ a, const double* __restrict__ b,
+                                   double* __restrict__ partial) {
+  const int c = blockIdx.y, blk = blockIdx.x;
+  const double* ac = a + (int64_t)c * n;
+  const double* bc = b + (int64_t)c * n;
+  const int64_t i0 = (int64_t)blk * DOT_CHUNK;
+  const int64_t i1 = i0 + DOT_CHUNK < n ? i0 + DOT_CHUNK : n;
+  double s = 0.0;
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += DOT_THREADS) s = fma(ac[i], bc[i], s);
+  __shared__ double red[DOT_THREADS / 32];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < DOT_THREADS / 32 ? red[threadIdx.x] : 0.0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) partial[(int64_t)c * nb + blk] = v;
+  }
+}
+
+__global__ void dot_final_kernel(int k, int nb, const double* __restrict__ partial, double* __restrict__ out) {
+  const int c = blockIdx.x;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nb; i += 32) s += partial[(int64_t)c * nb + i];
+  s = warp_sum(s);
+  if (threadIdx.x == 0) out[c] = s;
+}
+
+struct PcgState {
+  double *x, *r, *z, *p, *ap;  // (k, n)
+  double *rz, *ynorm, *alpha, *beta, *dots1, *dots2, *partial;
+  int32_t* active;
+  int32_t* status;  // [0] active count, [1] error code, [2] error column (min), [3] pad
+  double* err_val;
+};
+
+__global__ void pcg_init_kernel(int k, double tol, const double* ynorm_sq, double* ynorm, double* rel, int32_t* active,
+                                int32_t* iters, int32_t* status) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c == 0) {
+    status[1] = 0;
+    status[2] = 0x7fffffff;
+  }
+  if (c >= k) return;
+  double yn = sqrt(ynorm_sq[c]);
+  ynorm[c] = yn;
+  double rl = yn > 0.0 ? 1.0 : 0.0;  // solver.py:150
+  rel[c] = rl;
+  int a = rl > tol ? 1 : 0;
+  active[c] = a;
+  iters[c] = 0;
+  if (a) atomicAdd(&status[0], 1);
+}
+
+// alpha step (solver.py:159-168)
+__global__ void pcg_alpha_kernel(int k, int max_iter, const double* pap, const double* rz, const int32_t* active,
+                                 const int32_t* iters, double* alpha, double* alphas, int32_t* status,
+                                 double* err_val) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= k || !active[c]) return;
+  double v = pap[c];
+  if (!isfinite(v) || v <= 0.0) {
+    int old = atomicMin(&status[2], c);
+    status[1] = KGP_ERR_BREAKDOWN;
+    if (c <= old) err_val[0] = v;
+    alpha[c] = 0.0;
+    return;
+  }
+  double a = rz[c] / v;
+  alpha[c] = a;
+  alphas[(int64_t)c * max_iter + iters[c]] = a;
+}
+
+// x += alpha p; r -= alpha Ap on active columns
+__global__ void pcg_update_xr_kernel(int64_t n, int k, const int32_t* active, const double* alpha, const double* p,
+                                     const double* ap, double* x, double* r) {
+  const int c = blockIdx.y;
+  if (!active[c]) return;
+  const double a = alpha[c];
+  const int64_t off = (int64_t)c * n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[off + i] = fma(a, p[off + i], x[off + i]);
+    r[off + i] = fma(-a, ap[off + i], r[off + i]);
+  }
+}
+
+// beta step and freeze decision (solver.py:170-182)
+__global__ void pcg_beta_kernel(int k, int max_iter, double tol, bool precond, const double* rr, const double* rzn,
+                                double* rz, const double* ynorm, int32_t* active, int32_t* iters, double* beta,
+                                double* betas, double* rel, int32_t* status) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c == 0) status[0] = 0;
+  __syncthreads();
+  if (c >= k || !active[c]) return;
+  double v = rr[c];
+  if (!isfinite(v)) {
+    atomicMin(&status[2], c);
+    status[1] = KGP_ERR_NUMERICAL;
+    return;
+  }
+  double rn = precond ? rzn[c] : v;
+  double b = rn / rz[c];
+  int it = iters[c];
+  betas[(int64_t)c * max_iter + it] = b;
+  iters[c] = it + 1;
+  rz[c] = rn;
+  double rl = sqrt(v) / ynorm[c];
+  rel[c] = rl;
+  beta[c] = b;
+  if (rl <= tol) {
+    active[c] = 0;
+  } else {
+    atomicAdd(&status[0], 1);
+  }
+}
+
+// p = z + beta p on the still-active columns
+__global__ void pcg_update_p_kernel(int64_t n, int k, const int32_t* active, const double* beta, const double* z,
+                                    double* p) {
+  const int c = blockIdx.y;
+  if (!active[c]) return;
+  const double b = beta[c];
+  const int64_t off = (int64_t)c * n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[off + i] = fma(b, p[off + i], z[off + i]);
+}
+
+__global__ void pcg_finish_kernel(int k, double tol, const double* rel, int32_t* conv) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < k) conv[c] = rel[c] <= tol ? 1 : 0;
+}
+
+// ---------------------------------------------------------------- SLQ
+// Implicit-shift QL on the symmetric tridiagonal (d, e), rotating only the first
+// row z of the eigenvector matrix. Returns false if an eigenvalue does not
+// converge in 60 sweeps.
+__device__ bool tridiag_ql_first_row(int m, double* d, double* e, double* z) {
+  for (int l = 0; l < m; ++l) {
+    int sweeps = 0;
+    while (true) {
+      int mm = l;
+      for (; mm < m - 1; ++mm) {
+        double dd = fabs(d[mm]) + fabs(d[mm + 1]);
+        if (fabs(e[mm]) <= 2.2204460492503131e-16 * dd) break;
+      }
+      if (mm == l) break;
+      if (++sweeps > 60) return false;
+      double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+      double r = hypot(g, 1.0);
+      g = d[mm] - d[l] + e[l] / (g + copysign(r, g));
+      double s = 1.0, c = 1.0, p = 0.0;
+      int i = mm - 1;
+      bool deflated = false;
+      for (; i >= l; --i) {
+        double f = s * e[i], b = c * e[i];
+        r = hypot(f, g);
+        e[i + 1] = r;
+        if (r == 0.0) {  // split: the rotation underflowed
+          d[i + 1] -= p;
+          e[mm] = 0.0;
+          deflated = true;
+          break;
+        }
+        s = f / r;
+        c = g / r;
+        g = d[i + 1] - p;
+        r = (d[i] - g) * s + 2.0 * c * b;
+        p = s * r;
+        d[i + 1] = g + p;
+        g = c * r - b;
+        double zf = z[i + 1];
+        z[i + 1] = s * z[i] + c * zf;
+        z[i] = c * z[i] - s * zf;
+      }
+      if (deflated) continue;
+      d[l] -= p;
+      e[l] = g;
+      e[mm] = 0.0;
+    }
+  }
+  return true;
+}
+
+__global__ void slq_kernel(int k, int max_iter, const double* __restrict__ alphas, const double* __restrict__ betas,
+                           const int32_t* __restrict__ iters, const double* __restrict__ norms_sq,
+                           double* __restrict__ scratch, double* __restrict__ contrib, int32_t* __restrict__ status) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= k) return;
+  const int m = iters[c];
+  if (m == 0) {  // zero-iteration probes contribute 0 but count (solver.py:253-255)
+    contrib[c] = 0.0;
+    return;
+  }
+  double* d = scratch + (int64_t)c * 3 * max_iter;
+  double* e = d + max_iter;
+  double* z = e + max_iter;
+  const double* a = alphas + (int64_t)c * max_iter;
+  const double* b = betas + (int64_t)c * max_iter;
+  // solver.py:232-234: d_i = 1/a_i + b_{i-1}/a_{i-1}; e_i = sqrt(b_i)/a_i
+  for (int i = 0; i < m; ++i) {
+    d[i] = 1.0 / a[i] + (i > 0 ? b[i - 1] / a[i - 1] : 0.0);
+    e[i] = (i < m - 1) ? sqrt(b[i]) / a[i] : 0.0;
+    z[i] = (i == 0) ? 1.0 : 0.0;
+  }
+  if (!tridiag_ql_first_row(m, d, e, z)) {
+    status[1] = KGP_ERR_NUMERICAL;
+    contrib[c] = NAN;
+    return;
+  }
+  double wmin = d[0], acc = 0.0;
+  for (int i = 0; i < m; ++i) wmin = fmin(wmin, d[i]);
+  if (!(wmin > 0.0)) {
+    status[1] = KGP_ERR_NUMERICAL;
+    atomicMin(&status[2], c);
+    contrib[c] = wmin;
+    return;
+  }
+  for (int i = 0; i < m; ++i) acc += z[i] * z[i] * log(d[i]);
+  contrib[c] = norms_sq[c] * acc;
+}
+
+int read_status(const int32_t* dev_status, int32_t* host4, cudaStream_t st) {
+  KGP_CUDA(cudaMemcpyAsync(host4, dev_status, sizeof(int32_t) * 4, cudaMemcpyDeviceToHost, st));
+  KGP_CUDA(cudaStreamSynchronize(st));
+  return KGP_OK;
+}
+
+}  // namespace
+
+int col_dots(int64_t k, int64_t n, const double* a, const double* b, double* out, double* partial, cudaStream_t st) {
+  int nb = (int)((n + DOT_CHUNK - 1) / DOT_CHUNK);
+  dim3 g1(nb, (unsigned)k);
+  dot_partial_kernel<<<g1, DOT_THREADS, 0, st>>>(n, nb, a, b, partial);
+  KGP_LAUNCH("dot_partial_kernel");
+  dot_final_kernel<<<(unsigned)k, 32, 0, st>>>((int)k, nb, partial, out);
+  KGP_LAUNCH("dot_final_kernel");
+  return KGP_OK;
+}
+
+int pcg_solve_impl(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, const double* y, double tol, int max_iter,
+                   double* x_out, double* alphas, double* betas, int32_t* iters, double* rel, int32_t* conv,
+                   cudaStream_t st) {
+  const int64_t n = e->n;
+  const int nb = (int)((n + DOT_CHUNK - 1) / DOT_CHUNK);
+  // workspace: r, z (if preconditioned), p, ap : (k, n); scalars
+  size_t vec = (size_t)k * n;
+  size_t bytes = sizeof(double) * (vec * (pc ? 4 : 3) + (size_t)k * (8 + nb) + 8) + sizeof(int32_t) * (k + 8);
+  KGP_REQUIRE(k <= 1024, KGP_ERR_INVALID, "pcg supports at most 1024 right-hand sides per call, got %lld",
+              (long long)k);
+  int rc = e->ws.ensure(bytes);
+  if (rc) return rc;
+  double* base = e->ws.as<double>();
+  PcgState S{};
+  S.x = x_out;
+  S.r = base;
+  S.p = S.r + vec;
+  S.ap = S.p + vec;
+  S.z = pc ? S.ap + vec : S.r;  // unpreconditioned: z aliases r (solver.py:195-199)
+  double* sc = (pc ? S.z : S.ap) + vec;
+  S.rz = sc;
+  S.ynorm = sc + k;
+  S.alpha = sc + 2 * k;
+  S.beta = sc + 3 * k;
+  S.dots1 = sc + 4 * k;
+  S.dots2 = sc + 5 * k;
+  S.err_val = sc + 6 * k;
+  S.partial = sc + 7 * k;
+  S.active = reinterpret_cast<int32_t*>(S.partial + (size_t)k * nb + 8);
+  S.status = S.active + k;
+
+  int32_t* hstatus = e->hstatus;
+
+  const unsigned kb = (unsigned)((k + 127) / 128);
+  dim3 vgrid((unsigned)((n + 255) / 256 < 64 ? (n + 255) / 256 : 64), (unsigned)k);
+
+  KGP_CUDA(cudaMemsetAsync(x_out, 0, sizeof(double) * vec, st));
+  KGP_CUDA(cudaMemcpyAsync(S.r, y, sizeof(double) * vec, cudaMemcpyDeviceToDevice, st));
+  KGP_CUDA(cudaMemsetAsync(S.status, 0, sizeof(int32_t) * 4, st));
+  KGP_CUDA(cudaMemsetAsync(alphas, 0, sizeof(double) * k * max_iter, st));
+  KGP_CUDA(cudaMemsetAsync(betas, 0, sizeof(double) * k * max_iter, st));
+  rc = col_dots(k, n, S.r, S.r, S.dots1, S.partial, st);
+  if (rc) return rc;
+  pcg_init_kernel<<<kb, 128, 0, st>>>((int)k, tol, S.dots1, S.ynorm, rel, S.active, iters, S.status);
+  KGP_LAUNCH("pcg_init_kernel");
+  rc = read_status(S.status, hstatus, st);
+  if (rc) return rc;
+  if (hstatus[0] > 0) {
+    if (pc) {
+      rc = precond_apply_impl(pc, k, S.r, 1, n, S.z, 1, n, st);
+      if (rc) return rc;
+    }
+    KGP_CUDA(cudaMemcpyAsync(S.p, S.z, sizeof(double) * vec, cudaMemcpyDeviceToDevice, st));
+    rc = col_dots(k, n, S.r, S.z, S.rz, S.partial, st);
+    if (rc) return rc;
+    for (int it = 0; it < max_iter; ++it) {
+      rc = engine_matmul_impl(e, k, S.p, 1, n, S.ap, nullptr, nullptr, 1, n, st);
+      if (rc) return rc;
+      rc = col_dots(k, n, S.p, S.ap, S.dots1, S.partial, st);
+      if (rc) return rc;
+      pcg_alpha_kernel<<<kb, 128, 0, st>>>((int)k, max_iter, S.dots1, S.rz, S.active, iters, S.alpha, alphas,
+                                            S.status, S.err_val);
+      KGP_LAUNCH("pcg_alpha_kernel");
+      pcg_update_xr_kernel<<<vgrid, 256, 0, st>>>(n, (int)k, S.active, S.alpha, S.p, S.ap, x_out, S.r);
+      KGP_LAUNCH("pcg_update_xr_kernel");
+      if (pc) {
+        rc = precond_apply_impl(pc, k, S.r, 1, n, S.z, 1, n, st);
+        if (rc) return rc;
+        rc = col_dots(k, n, S.r, S.z, S.dots2, S.partial, st);
+        if (rc) return rc;
+      }
+      rc = col_dots(k, n, S.r, S.r, S.dots1, S.partial, st);
+      if (rc) return rc;
+      pcg_beta_kernel<<<1, 1024, 0, st>>>((int)k, max_iter, tol, pc != nullptr, S.dots1, S.dots2, S.rz, S.ynorm,
+                                          S.active, iters, S.beta, betas, rel, S.status);
+      KGP_LAUNCH("pcg_beta_kernel");
+      pcg_update_p_kernel<<<vgrid, 256, 0, st>>>(n, (int)k, S.active, S.beta, S.z, S.p);
+      KGP_LAUNCH("pcg_update_p_kernel");
+      rc = read_status(S.status, hstatus, st);
+      if (rc) return rc;
+      if (hstatus[1] == KGP_ERR_BREAKDOWN) {
+        double v = 0.0;
+        cudaMemcpy(&v, S.err_val, sizeof(double), cudaMemcpyDeviceToHost);
+        set_error(KGP_ERR_BREAKDOWN, "p^T A p = %.17g in column %d; operator is not SPD", v, hstatus[2]);
+        return KGP_ERR_BREAKDOWN;
+      }
+      if (hstatus[1] == KGP_ERR_NUMERICAL) {
+        set_error(KGP_ERR_NUMERICAL, "residual became non-finite during PCG");
+        return KGP_ERR_NUMERICAL;
+      }
+      if (hstatus[0] == 0) break;
+    }
+  }
+  pcg_finish_kernel<<<kb, 128, 0, st>>>((int)k, tol, rel, conv);
+  KGP_LAUNCH("pcg_finish_kernel");
+  KGP_CUDA(cudaStreamSynchronize(st));
+  return KGP_OK;
+}
+
+int slq_impl(int64_t k, int max_iter, const double* alphas, const double* betas, const int32_t* iters,
+             const double* norms_sq, double* logdet, cudaStream_t st) {
+  DevBuf ws;
+  int rc = ws.ensure(sizeof(double) * ((size_t)k * 3 * max_iter + k) + 64);
+  if (rc) return rc;
+  double* scratch = ws.as<double>();
+  double* contrib = scratch + (size_t)k * 3 * max_iter;
+  int32_t* status = reinterpret_cast<int32_t*>(contrib + k);
+  KGP_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * 4, st));
+  int32_t init_min = 0x7fffffff;
+  KGP_CUDA(cudaMemcpyAsync(status + 2, &init_min, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  slq_kernel<<<(unsigned)((k + 63) / 64), 64, 0, st>>>((int)k, max_iter, alphas, betas, iters, norms_sq, scratch,
+                                                       contrib, status);
+  KGP_LAUNCH("slq_kernel");
+  std::vector<double> h(k);
+  int32_t hs[4];
+  KGP_CUDA(cudaMemcpyAsync(h.data(), contrib, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+  KGP_CUDA(cudaMemcpyAsync(hs, status, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  KGP_CUDA(cudaStreamSynchronize(st));
+  if (hs[1] == KGP_ERR_NUMERICAL) {
+    double w = (hs[2] >= 0 && hs[2] < k) ? h[hs[2]] : NAN;
+    set_error(KGP_ERR_NUMERICAL, "nonpositive Ritz value %.17g; operator is not SPD or CG broke down", w);
+    return KGP_ERR_NUMERICAL;
+  }
+  double total = 0.0;  // probe order, as solver.py:253-265
+  for (int64_t c = 0; c < k; ++c) total += h[c];
+  *logdet = total / (double)k;
+  return KGP_OK;
+}
+
+}  // namespace kgp
+
+using namespace kgp;
+
+// nlml_grad_iterative (gp.py:133-179)
+extern "C" int kgp_nlml_grad(kgp_engine* e, kgp_precond* p, const double* y, int64_t k_z, const double* probes,
+                             double tol, int32_t max_iter, double probe_tol, double* out, int32_t* out_converged,
+                             void* stream) {
+  KGP_REQUIRE(e != nullptr && e->magic == ENGINE_MAGIC, KGP_ERR_STATE, "invalid engine handle");
+  KGP_REQUIRE(p == nullptr || p->magic == PRECOND_MAGIC, KGP_ERR_STATE, "invalid preconditioner handle");
+  KGP_REQUIRE(k_z >= 1 && max_iter >= 1 && tol >= 0.0 && probe_tol >= 0.0, KGP_ERR_INVALID, "bad solver arguments");
+  KGP_REQUIRE(out != nullptr && out_converged != nullptr, KGP_ERR_INVALID, "NULL output pointer");
+  KGP_CUDA(cudaSetDevice(e->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = e->n;
+  const int64_t kv = 1 + k_z;
+  const int nb = (int)((n + DOT_CHUNK - 1) / DOT_CHUNK);
+  // workspace: V = [w, Z] (kv, n); U' = [w, u] (kv, n); dV_l, dV_f (kv, n); traces; scalars
+  size_t vec = (size_t)kv * n;
+  size_t bytes = sizeof(double) * (4 * vec + 2 * (size_t)kv * max_iter + 4 * kv + (size_t)kv * nb + 16) +
+                 sizeof(int32_t) * (4 * kv + 8);
+  DevBuf ws;
+  int rc = ws.ensure(bytes);
+  if (rc) return rc;
+  double* V = ws.as<double>();
+  double* U = V + vec;
+  double* dL = U + vec;
+  double* dF = dL + vec;
+  double* alphas = dF + vec;
+  double* betas = alphas + (size_t)kv * max_iter;
+  double* rel = betas + (size_t)kv * max_iter;
+  double* dots = rel + kv;
+  double* nz2 = dots + kv;
+  double* partial = nz2 + kv;
+  int32_t* iters = reinterpret_cast<int32_t*>(partial + (size_t)kv * nb + 8);
+  int32_t* conv = iters + kv;
+
+  // (1) w = PCG(Khat, M, y, tol)   -> U row 0, and V row 0 = w
+  rc = pcg_solve_impl(e, p, 1, y, tol, max_iter, U, alphas, betas, iters, rel, conv, st);
+  if (rc) return rc;
+  int32_t wconv = 0;
+  KGP_CUDA(cudaMemcpyAsync(&wconv, conv, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  // (2) u = CG(Khat, Z, probe_tol), unpreconditioned: coefficients rebuild Lanczos of Khat itself
+  rc = pcg_solve_impl(e, nullptr, k_z, probes, probe_tol, max_iter, U + n, alphas + max_iter, betas + max_iter,
+                      iters + 1, rel + 1, conv + 1, st);
+  if (rc) return rc;
+  // (3) log|Khat| by SLQ over the probe traces
+  rc = col_dots(k_z, n, probes, probes, nz2, partial, st);
+  if (rc) return rc;
+  double logdet = 0.0;
+  rc = slq_impl(k_z, max_iter, alphas + max_iter, betas + max_iter, iters + 1, nz2, &logdet, st);
+  if (rc) return rc;
+  // (4) loss = 1/2 (y.w + logdet + n log 2 pi)
+  rc = col_dots(1, n, y, U, dots, partial, st);
+  if (rc) return rc;
+  double yw = 0.0;
+  KGP_CUDA(cudaMemcpyAsync(&yw, dots, sizeof(double), cudaMemcpyDeviceToHost, st));
+  // (5) one fused derivative pass over V = [w, Z]
+  KGP_CUDA(cudaMemcpyAsync(V, U, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  KGP_CUDA(cudaMemcpyAsync(V + n, probes, sizeof(double) * k_z * n, cudaMemcpyDeviceToDevice, st));
+  rc = engine_matmul_impl(e, kv, V, 1, n, nullptr, dL, dF, 1, n, st);
+  if (rc) return rc;
+  std::vector<double> hd(kv);
+  double grads[3];
+  const double* dV[3] = {dL, dF, V};  // Theta.L, Theta.F, Theta.S (dKhat/ds = I, kmat.py:157-158)
+  for (int th = 0; th < 3; ++th) {
+    // column dots of [w, u_1..u_kz] against dV columns: quad from column 0, trace from the rest
+    rc = col_dots(kv, n, U, dV[th], dots, partial, st);
+    if (rc) return rc;
+    KGP_CUDA(cudaMemcpyAsync(hd.data(), dots, sizeof(double) * kv, cudaMemcpyDeviceToHost, st));
+    KGP_CUDA(cudaStreamSynchronize(st));
+    double quad = -hd[0];
+    double tr = 0.0;
+    for (int64_t c = 1; c < kv; ++c) tr += hd[c];
+    tr /= (double)k_z;
+    grads[th] = 0.5 * (quad + tr);
+  }
+  std::vector<int32_t> hc(kv);
+  KGP_CUDA(cudaMemcpyAsync(hc.data(), conv, sizeof(int32_t) * kv, cudaMemcpyDeviceToHost, st));
+  KGP_CUDA(cudaStreamSynchronize(st));
+  int ok = 1;
+  for (int64_t c = 0; c < kv; ++c) ok &= hc[c] ? 1 : 0;
+  const double LOG_2PI = 1.8378770664093453;
+  out[0] = 0.5 * (yw + logdet + (double)n * LOG_2PI);
+  out[1] = grads[0];
+  out[2] = grads[1];
+  out[3] = grads[2];
+  *out_converged = ok;
+  (void)wconv;
+  return KGP_OK;
+}

@@ -1,0 +1,151 @@
+// Woodbury application of the landmark preconditioner on the device.
+//
+// NystromPreconditioner.apply_inverse (precond.py:74-83) computes
+//   out = B / s - V cho_solve(C, V^T B) / s^2,   C = I/f^2 + V^T V / s.
+// With C = L_C L_C^T factored once at build time and W = V L_C^-T, this is
+//   out = B / s - W (W^T B) / s^2
+// two tall-skinny fp64 GEMMs per application and no triangular solve in the
+// PCG loop. Both GEMMs run on one tiled fp64 kernel (64x64 tiles, split-K with
+// a fixed-order partial reduction so results are run-to-run deterministic).
+#include "kgp_common.cuh"
+#include "kgp_internal.h"
+
+namespace kgp {
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16, GT = 256;
+
+struct GemmArgs {
+  int64_t M, N, K;             // C (M x N) = A (M x K) . B (K x N)
+  const double* a;
+  int64_t a_is, a_ks;          // A(i, q) = a[i*a_is + q*a_ks]
+  const double* b;
+  int64_t b_ks, b_ns;          // B(q, c) = b[q*b_ks + c*b_ns]
+  double* c;                   // partial or final output
+  int64_t c_is, c_ns;
+  int64_t kchunk;              // split-K chunk (grid.z slices)
+  int64_t part_stride;         // elements between split-K partial slices (0: final)
+  double alpha, beta;          // final: c = beta * src + alpha * acc
+  const double* src;
+  int64_t s_is, s_ns;
+};
+
+__global__ void __launch_bounds__(GT) dgemm_kernel(const GemmArgs g) {
+  __shared__ double As[BK][BM + 1];
+  __shared__ double Bs[BK][BN + 1];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int64_t i0 = (int64_t)blockIdx.x * BM, c0 = (int64_t)blockIdx.y * BN;
+  const int64_t q_begin = (int64_t)blockIdx.z * g.kchunk;
+  const int64_t q_end = q_begin + g.kchunk < g.K ? q_begin + g.kchunk : g.K;
+  double acc[4][4] = {};
+  const bool a_i_contig = (g.a_is == 1);
+  const bool b_n_contig = (g.b_ns == 1);
+  for (int64_t q0 = q_begin; q0 < q_end; q0 += BK) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      int e = tid + GT * t;
+      int ii, qq;
+      if (a_i_contig) { ii = e % BM; qq = e / BM; } else { qq = e % BK; ii = e / BK; }
+      int64_t gi = i0 + ii, gq = q0 + qq;
+      As[qq][ii] = (gi < g.M && gq < q_end) ? g.a[gi * g.a_is + gq * g.a_ks] : 0.0;
+      int cc;
+      if (b_n_contig) { cc = e % BN; qq = e / BN; } else { qq = e % BK; cc = e / BK; }
+      int64_t gc = c0 + cc;
+      gq = q0 + qq;
+      Bs[qq][cc] = (gc < g.N && gq < q_end) ? g.b[gq * g.b_ks + gc * g.b_ns] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int qq = 0; qq < BK; ++qq) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) av[u] = As[qq][ty + 16 * u];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) bv[v] = Bs[qq][tx + 16 * v];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fma(av[u], bv[v], acc[u][v]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      int64_t gi = i0 + ty + 16 * u, gc = c0 + tx + 16 * v;
+      if (gi >= g.M || gc >= g.N) continue;
+      if (g.part_stride) {
+        g.c[blockIdx.z * g.part_stride + gi * g.c_is + gc * g.c_ns] = acc[u][v];
+      } else {
+        double val = g.alpha * acc[u][v];
+        if (g.src) val += g.beta * g.src[gi * g.s_is + gc * g.s_ns];
+        g.c[gi * g.c_is + gc * g.c_ns] = val;
+      }
+    }
+}
+
+// c[e] = sum_z part[z * stride + e], fixed order in z
+__global__ void sum_partials_kernel(int64_t count, int nz, int64_t stride, const double* __restrict__ part,
+                                    double* __restrict__ out) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= count) return;
+  double s = 0.0;
+  for (int z = 0; z < nz; ++z) s += part[z * stride + e];
+  out[e] = s;
+}
+
+}  // namespace
+
+// out = beta B + alpha U (U^T B) with U^T = p->wt (m x n)
+int lowrank_apply_impl(kgp_precond_s* p, double beta, double alpha, int64_t k, const double* b, int64_t b_rs,
+                       int64_t b_cs, double* out, int64_t o_rs, int64_t o_cs, cudaStream_t st) {
+  const int64_t n = p->n, m = p->m;
+  // T = W^T B  (m x k), split over n
+  int64_t tiles = ((m + BM - 1) / BM) * ((k + BN - 1) / BN);
+  int64_t nz = (n + 2047) / 2048;
+  int64_t cap = 296 / tiles;
+  if (cap < 1) cap = 1;
+  if (nz > cap) nz = cap;
+  int64_t kchunk = ((n + nz - 1) / nz + BK - 1) / BK * BK;
+  nz = (n + kchunk - 1) / kchunk;
+  int rc = p->tmp.ensure(sizeof(double) * (size_t)m * k * (nz + 1));
+  if (rc) return rc;
+  double* T = p->tmp.as<double>();
+  double* part = T + m * k;
+  GemmArgs g{};
+  g.M = m; g.N = k; g.K = n;
+  g.a = p->wt.as<double>(); g.a_is = n; g.a_ks = 1;
+  g.b = b; g.b_ks = b_rs; g.b_ns = b_cs;
+  g.c = part; g.c_is = k; g.c_ns = 1;
+  g.kchunk = kchunk; g.part_stride = m * k;
+  dim3 grid1((unsigned)((m + BM - 1) / BM), (unsigned)((k + BN - 1) / BN), (unsigned)nz);
+  dgemm_kernel<<<grid1, GT, 0, st>>>(g);
+  KGP_LAUNCH("dgemm_kernel (W^T B)");
+  sum_partials_kernel<<<(unsigned)((m * k + 255) / 256), 256, 0, st>>>(m * k, (int)nz, m * k, part, T);
+  KGP_LAUNCH("sum_partials_kernel");
+  // out = beta B + alpha U T
+  GemmArgs h{};
+  h.M = n; h.N = k; h.K = m;
+  h.a = p->wt.as<double>(); h.a_is = 1; h.a_ks = n;
+  h.b = T; h.b_ks = k; h.b_ns = 1;
+  h.c = out; h.c_is = o_rs; h.c_ns = o_cs;
+  h.kchunk = m; h.part_stride = 0;
+  h.alpha = alpha;
+  h.beta = beta;
+  h.src = b; h.s_is = b_rs; h.s_ns = b_cs;
+  dim3 grid2((unsigned)((n + BM - 1) / BM), (unsigned)((k + BN - 1) / BN), 1);
+  dgemm_kernel<<<grid2, GT, 0, st>>>(h);
+  KGP_LAUNCH("dgemm_kernel (W T)");
+  return KGP_OK;
+}
+
+// Woodbury inverse: B / s - W (W^T B) / s^2
+int precond_apply_impl(kgp_precond_s* p, int64_t k, const double* b, int64_t b_rs, int64_t b_cs, double* out,
+                       int64_t o_rs, int64_t o_cs, cudaStream_t st) {
+  return lowrank_apply_impl(p, 1.0 / p->s, -1.0 / (p->s * p->s), k, b, b_rs, b_cs, out, o_rs, o_cs, st);
+}
+
+}  // namespace kgp
