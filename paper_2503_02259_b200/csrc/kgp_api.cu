@@ -1,6 +1,7 @@
 // C ABI: library, engine and preconditioner handles (include/kgp.h).
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <mutex>
@@ -51,6 +52,16 @@ void DevBuf::release() {
 
 double tc_kernel_gamma(int kt, double l);
 
+// blocks (x32 columns) accumulated in TMEM before promotion; env KGP_TC_FLUSH overrides
+static int tc_flush_blocks() {
+  static int v = [] {
+    const char* s = getenv("KGP_TC_FLUSH");
+    int f = s ? atoi(s) : 8;
+    return f < 1 ? 1 : f;
+  }();
+  return v;
+}
+
 static std::mutex g_handles_mu;
 static std::set<const void*> g_handles;
 
@@ -91,8 +102,9 @@ static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t 
   const int nout = out_dl ? 2 : 1;
   const int tpo = split == 3 ? 2 : 1;
   const int nblk = (int)((e->n + 31) / 32);
-  for (int64_t c0 = 0; c0 < k; c0 += 128) {
-    const int kc = (int)((k - c0) < 128 ? (k - c0) : 128);
+  const int kmax = tc_max_kp(nout, split);
+  for (int64_t c0 = 0; c0 < k; c0 += kmax) {
+    const int kc = (int)((k - c0) < kmax ? (k - c0) : kmax);
     const int kp = (kc + 15) / 16 * 16;
     int rc = e->bsplit.ensure((size_t)nblk * tpo * kp * 128);
     if (rc) return rc;
@@ -106,8 +118,9 @@ static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t 
     p.nblk = nblk;
     p.kp = kp;
     p.k = kc;
-    int nsa = (512 - nout * kp) / (nout * tpo * 32);
+    int nsa = (512 - 2 * nout * kp) / (nout * tpo * 32);
     p.nsa = nsa > 4 ? 4 : nsa;
+    p.flush = tc_flush_blocks();
     p.f2 = e->f * e->f;
     p.s = e->s;
     p.two_f = 2.0 * e->f;

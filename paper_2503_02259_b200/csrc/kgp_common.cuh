@@ -98,6 +98,20 @@ KGP_DEV void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, uint
       : "memory");
 }
 
+// One lane of a converged warp (elect.sync): the single issuing thread for
+// tcgen05.mma / bulk copies, without a divergent `lane == 0` region that would
+// force the compiler to waterfall the (warp-uniform) operands into uniform registers.
+KGP_DEV bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .b32 rx;\n\t.reg .pred px;\n\t"
+      "elect.sync rx|px, %1;\n\t"
+      "@px mov.s32 %0, 1;\n\t}"
+      : "+r"(pred)
+      : "r"(0xFFFFFFFFu));
+  return pred != 0;
+}
+
 KGP_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 KGP_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 KGP_DEV void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
@@ -128,6 +142,14 @@ KGP_DEV void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
       "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
       "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
       : "memory");
+}
+// 16 lanes x 256 bit, twice along columns (16 columns): thread t holds lanes {t/4, t/4+8}
+// (relative to the address lane) and columns {2(t%4), 2(t%4)+1} (+8 for the second half):
+// v[0..1] = (t/4, c..c+1), v[2..3] = (t/4+8, c..c+1), v[4..5] = (t/4, c+8..c+9), v[6..7] = (t/4+8, c+8..c+9).
+KGP_DEV void tmem_st_16x256b_x2(uint32_t taddr, const uint32_t (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.16x256b.x2.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+               "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
 }
 KGP_DEV void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
   asm volatile(

@@ -19,6 +19,7 @@ struct TcParams {
   int kp;                 // padded RHS count (multiple of 16, <= 128)
   int k;                  // true RHS count in this launch
   int nsa;                // TMEM A-stage ring depth
+  int flush;              // blocks per TMEM accumulation segment before promotion to fp32 smem
   double f2, s, two_f, scale_dl;
   const double* b;        // original fp64 RHS (for + s B)
   int64_t b_rs, b_cs;
@@ -27,6 +28,7 @@ struct TcParams {
   int64_t o_rs, o_cs;
 };
 int tc_pad_dim(int d);
+int tc_max_kp(int nout, int split);
 bool tc_direct(int dpad);
 int launch_kmm_tc(int kt, int dpad, int nout, int split, const TcParams& p, cudaStream_t st);
 

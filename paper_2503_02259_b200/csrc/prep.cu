@@ -59,14 +59,18 @@ __global__ void prep_cols_kernel(int kt, int d, int dpad, bool direct, int64_t n
   if (j >= (int64_t)nblk * 32) return;
   const int64_t t = j >> 5;
   const int jj = (int)(j & 31);
+  // position inside the block: the tile kernel's thread (h, g) reads columns
+  // (16h + 2g, +1, +8, +9) as one float4 at 16h + 4g
+  const int hh = jj >> 4, cc = jj & 15;
+  const int pos = 16 * hh + 4 * ((cc & 7) >> 1) + (cc & 1) + 2 * (cc >> 3);
   float* o = out + t * (int64_t)(dpad + 1) * 32;
   double sg = sqrt(gamma), nrm = 0.0;
   for (int k = 0; k < dpad; ++k) {
     double c = (j < n && k < d) ? x[j * d + k] - mean[k] : 0.0;
     nrm += c * c;
-    o[(1 + k) * 32 + jj] = direct ? (float)(sg * c) : (float)c;
+    o[(1 + k) * 32 + pos] = direct ? (float)(sg * c) : (float)c;
   }
-  o[jj] = (direct || j >= n) ? 0.0f : (float)(gamma * nrm);
+  o[pos] = (direct || j >= n) ? 0.0f : (float)(gamma * nrm);
 }
 
 __device__ inline uint32_t tf32_rna_bits(float v) {

@@ -57,6 +57,7 @@ class _LowRank:
     """Owns one libkgp low-rank handle (U^T on the device)."""
 
     def __init__(self, ut, s):
+        ut = ut.contiguous()  # torch.linalg returns column-major factors; libkgp wants (m, n) row-major
         self.h = ctypes.c_void_p()
         call("kgp_precond_create", ctypes.byref(self.h), ut.shape[1], ut.shape[0], ut.data_ptr(), float(s),
              _device.stream_ptr())
