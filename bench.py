@@ -173,6 +173,58 @@ def measured_tf32_peak(torch):
     return 2.0 * 8192 ** 3 / best / 1e12
 
 
+def nlml_metric(cpu: bool):
+    """Secondary metric: NLML+gradient evaluations/s at BASELINE configs[0] (n=4096, Gaussian,
+    16 probes, rank 256) with its fixed recipe (PCG 50 iterations, 20 Lanczos steps), fp64
+    operator. Each eval includes the H2D copy of y and the probes; the preconditioner build is
+    timed separately (the reference's 1.41 s likewise excludes its 0.19 s build)."""
+    import torch
+
+    from paper_2503_02259_b200 import gp, precond, workloads
+    from paper_2503_02259_b200.kmat import Hyperparams, KernelEngine
+    from paper_2503_02259_b200.kernels import KernelType
+
+    w = workloads.cfg1()
+    probes = gp.ProbeSet.generate(w.n, w.k_z, w.probe_seed)
+    eng = KernelEngine(KernelType.GAUSSIAN, w.x, Hyperparams(w.l, w.f, w.s), precision="fp64")
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    pre = precond.build(eng, w.rank)
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t0
+
+    def ev():
+        return gp.nlml_grad_iterative(eng, w.y, pre, probes, tol=0.0, max_iter=50, probe_tol=0.0,
+                                      probe_max_iter=20)
+
+    for _ in range(2):
+        ev()
+    torch.cuda.synchronize()
+    reps = 10
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        lg = ev()
+    torch.cuda.synchronize()
+    t_eval = (time.perf_counter() - t0) / reps
+    out = {"workload": "cfg1 fixed recipe (BASELINE.json configs[0]): n=4096 d=3 Gaussian, 16 probes, "
+                       "rank 256, PCG 50 + SLQ 20, fp64 operator",
+           "evals_per_s": 1.0 / t_eval, "ms_per_eval": t_eval * 1e3, "precond_build_ms": t_build * 1e3,
+           "loss": lg.loss, "timer": "wall clock around synchronous calls (each eval ends in a D2H read)"}
+    if cpu:
+        from oracle import kgp_oracle as orc
+
+        ny = orc.Nystrom("gaussian", w.x, w.l, w.f, w.s, w.rank)
+        t0 = time.perf_counter()
+        ref = orc.nlml_grad("gaussian", w.x, w.y, w.l, w.f, w.s, probes.vectors, ny, tol=0.0, max_iter=50,
+                            probe_tol=0.0, dense=True, probe_max_iter=20)
+        t_cpu = time.perf_counter() - t0
+        out["cpu_baseline"] = {"evals_per_s": 1.0 / t_cpu, "kind": "port", "cores": os.cpu_count(),
+                               "sample": "one full eval, oracle/kgp_oracle.py dense path (the reference's "
+                                         "default auto->DENSE mode at n <= 20000), numpy BLAS threads"}
+        out["loss_rel_diff_vs_cpu"] = abs(lg.loss - ref[0]) / abs(ref[0])
+    return out
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -300,6 +352,8 @@ def run_gpu(args):
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
         }
+        if not args.skip_nlml and world == 1:
+            line["nlml"] = nlml_metric(cpu=not args.no_cpu_baseline)
         print(json.dumps(line))
     if world > 1:
         dist.barrier()

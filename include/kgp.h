@@ -127,10 +127,12 @@ int kgp_slq_logdet(int64_t k, int32_t max_iter, const double* alphas, const doub
 
 /* nlml_grad_iterative (gp.py:133-179) end to end on the device:
  * out[0..3] = loss, grad_l, grad_f, grad_s (host); out_converged (host).
- * y: n device; probes: (k_z, n) device (probe c contiguous). */
+ * y: n device; probes: (k_z, n) device (probe c contiguous). probe_max_iter caps the
+ * probe CG / Lanczos length separately (<= 0: max_iter, the reference's single knob);
+ * with tol = probe_tol = 0 this is BASELINE configs[0]'s fixed recipe (PCG 50, SLQ 20). */
 int kgp_nlml_grad(kgp_engine* e, kgp_precond* p, const double* y, int64_t k_z, const double* probes,
-                  double tol, int32_t max_iter, double probe_tol, double* out, int32_t* out_converged,
-                  void* stream);
+                  double tol, int32_t max_iter, double probe_tol, int32_t probe_max_iter, double* out,
+                  int32_t* out_converged, void* stream);
 
 #ifdef __cplusplus
 }

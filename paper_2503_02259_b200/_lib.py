@@ -62,7 +62,7 @@ _SIGNATURES = {
     "kgp_lowrank_apply": [c_vp, c_dbl, c_dbl, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_vp],
     "kgp_pcg": [c_vp, c_vp, c_i64, c_vp, c_dbl, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
     "kgp_slq_logdet": [c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, _P(c_dbl), c_vp],
-    "kgp_nlml_grad": [c_vp, c_vp, c_vp, c_i64, c_vp, c_dbl, c_i32, c_dbl, _P(c_dbl), _P(c_i32), c_vp],
+    "kgp_nlml_grad": [c_vp, c_vp, c_vp, c_i64, c_vp, c_dbl, c_i32, c_dbl, c_i32, _P(c_dbl), _P(c_i32), c_vp],
 }
 
 EXPORTED = tuple(_SIGNATURES) + ("kgp_last_error",)

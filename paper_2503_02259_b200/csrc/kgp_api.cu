@@ -166,7 +166,7 @@ int engine_matmul_impl(kgp_engine_s* e, int64_t k, const double* b, int64_t b_rs
     p.out_df = out_df;
     p.o_rs = o_rs;
     p.o_cs = o_cs;
-    return launch_kmm_f64(e->kt, p, st);
+    return launch_kmm_f64(e->kt, p, e->f64part, st);
   }
   int rc = engine_prepare(e, st);
   if (rc) return rc;
@@ -336,7 +336,7 @@ extern "C" int kgp_engine_cross_matmul(kgp_engine* e, int64_t m, const double* x
     p.out_k = out;
     p.o_rs = o_rs;
     p.o_cs = o_cs;
-    return launch_kmm_f64(e->kt, p, st);
+    return launch_kmm_f64(e->kt, p, e->f64part, st);
   }
   int rc = engine_prepare(e, st);
   if (rc) return rc;

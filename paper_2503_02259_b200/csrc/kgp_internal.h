@@ -44,8 +44,12 @@ struct F64Params {
   int64_t diag_row0;
   double *out_k, *out_dl, *out_df;
   int64_t o_rs, o_cs;
+  int64_t jchunk;          // columns per grid.z split (set by launch_kmm_f64)
+  double* part;            // split partials (set by launch_kmm_f64)
+  int64_t part_stride;
 };
-int launch_kmm_f64(int kt, const F64Params& p, cudaStream_t st);
+struct DevBuf;
+int launch_kmm_f64(int kt, const F64Params& p, DevBuf& ws, cudaStream_t st);
 
 // ------------------------------------------------------------------ preprocessing (prep.cu)
 int prep_rows(int kt, int precision_split, int d, int dpad, int64_t nrows, const double* x, const double* mean,
@@ -81,6 +85,7 @@ struct kgp_engine_s {
   kgp::DevBuf xcol;  // fast path column tiles
   kgp::DevBuf xrow_cross;  // scratch for cross (prediction) rows
   kgp::DevBuf bsplit;      // per-call RHS split
+  kgp::DevBuf f64part;     // fp64 operator column-split partials
   bool prepared;
   // PCG workspace (grown on demand) and a pinned status word for the per-iteration readback
   kgp::DevBuf ws;

@@ -406,8 +406,8 @@ using namespace kgp;
 
 // nlml_grad_iterative (gp.py:133-179)
 extern "C" int kgp_nlml_grad(kgp_engine* e, kgp_precond* p, const double* y, int64_t k_z, const double* probes,
-                             double tol, int32_t max_iter, double probe_tol, double* out, int32_t* out_converged,
-                             void* stream) {
+                             double tol, int32_t max_iter, double probe_tol, int32_t probe_max_iter, double* out,
+                             int32_t* out_converged, void* stream) {
   KGP_REQUIRE(e != nullptr && e->magic == ENGINE_MAGIC, KGP_ERR_STATE, "invalid engine handle");
   KGP_REQUIRE(p == nullptr || p->magic == PRECOND_MAGIC, KGP_ERR_STATE, "invalid preconditioner handle");
   KGP_REQUIRE(k_z >= 1 && max_iter >= 1 && tol >= 0.0 && probe_tol >= 0.0, KGP_ERR_INVALID, "bad solver arguments");
@@ -417,9 +417,11 @@ extern "C" int kgp_nlml_grad(kgp_engine* e, kgp_precond* p, const double* y, int
   const int64_t n = e->n;
   const int64_t kv = 1 + k_z;
   const int nb = (int)((n + DOT_CHUNK - 1) / DOT_CHUNK);
+  const int32_t pmax = probe_max_iter > 0 ? probe_max_iter : max_iter;
+  const int32_t wide = pmax > max_iter ? pmax : max_iter;  // per-column stride of the coefficient arrays
   // workspace: V = [w, Z] (kv, n); U' = [w, u] (kv, n); dV_l, dV_f (kv, n); traces; scalars
   size_t vec = (size_t)kv * n;
-  size_t bytes = sizeof(double) * (4 * vec + 2 * (size_t)kv * max_iter + 4 * kv + (size_t)kv * nb + 16) +
+  size_t bytes = sizeof(double) * (4 * vec + 2 * (size_t)kv * wide + 4 * kv + (size_t)kv * nb + 16) +
                  sizeof(int32_t) * (4 * kv + 8);
   DevBuf ws;
   int rc = ws.ensure(bytes);
@@ -429,8 +431,8 @@ extern "C" int kgp_nlml_grad(kgp_engine* e, kgp_precond* p, const double* y, int
   double* dL = U + vec;
   double* dF = dL + vec;
   double* alphas = dF + vec;
-  double* betas = alphas + (size_t)kv * max_iter;
-  double* rel = betas + (size_t)kv * max_iter;
+  double* betas = alphas + (size_t)kv * wide;
+  double* rel = betas + (size_t)kv * wide;
   double* dots = rel + kv;
   double* nz2 = dots + kv;
   double* partial = nz2 + kv;
@@ -443,14 +445,14 @@ extern "C" int kgp_nlml_grad(kgp_engine* e, kgp_precond* p, const double* y, int
   int32_t wconv = 0;
   KGP_CUDA(cudaMemcpyAsync(&wconv, conv, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   // (2) u = CG(Khat, Z, probe_tol), unpreconditioned: coefficients rebuild Lanczos of Khat itself
-  rc = pcg_solve_impl(e, nullptr, k_z, probes, probe_tol, max_iter, U + n, alphas + max_iter, betas + max_iter,
+  rc = pcg_solve_impl(e, nullptr, k_z, probes, probe_tol, pmax, U + n, alphas + max_iter, betas + max_iter,
                       iters + 1, rel + 1, conv + 1, st);
   if (rc) return rc;
   // (3) log|Khat| by SLQ over the probe traces
   rc = col_dots(k_z, n, probes, probes, nz2, partial, st);
   if (rc) return rc;
   double logdet = 0.0;
-  rc = slq_impl(k_z, max_iter, alphas + max_iter, betas + max_iter, iters + 1, nz2, &logdet, st);
+  rc = slq_impl(k_z, pmax, alphas + max_iter, betas + max_iter, iters + 1, nz2, &logdet, st);
   if (rc) return rc;
   // (4) loss = 1/2 (y.w + logdet + n log 2 pi)
   rc = col_dots(1, n, y, U, dots, partial, st);

@@ -153,8 +153,12 @@ def _generic_iterative(engine, y, preconditioner, probes, tol, max_iter, probe_t
 
 
 def nlml_grad_iterative(engine, y, preconditioner, probes: ProbeSet, tol: float = solver.DEFAULT_TOL,
-                        max_iter: int = solver.DEFAULT_MAX_ITER, probe_tol: float | None = None) -> LossGrad:
-    """Matrix-free loss and gradient from one probe set (gp.py:133-179)."""
+                        max_iter: int = solver.DEFAULT_MAX_ITER, probe_tol: float | None = None, *,
+                        probe_max_iter: int | None = None) -> LossGrad:
+    """Matrix-free loss and gradient from one probe set (gp.py:133-179).
+
+    ``probe_max_iter`` (keyword-only extension) caps the probe CG / Lanczos length
+    separately from the w-solve; None keeps the reference's single ``max_iter``."""
     n = engine.n
     y = _check_y(y, n)
     if probes.vectors.shape[0] != n:
@@ -164,6 +168,8 @@ def nlml_grad_iterative(engine, y, preconditioner, probes: ProbeSet, tol: float 
     ours = isinstance(engine, KernelEngine)
     pre_ok = preconditioner is None or isinstance(preconditioner, precond_mod.NystromPreconditioner)
     if not (ours and pre_ok):
+        if probe_max_iter is not None:
+            raise ValueError("probe_max_iter needs this package's KernelEngine")
         return _generic_iterative(engine, y, preconditioner, probes, tol, max_iter, probe_tol)
     torch = _device.torch()
     dev = _device.device()
@@ -172,7 +178,8 @@ def nlml_grad_iterative(engine, y, preconditioner, probes: ProbeSet, tol: float 
     out = (ctypes.c_double * 4)()
     conv = ctypes.c_int32()
     call("kgp_nlml_grad", engine.handle, None if preconditioner is None else preconditioner.handle,
-         yd.data_ptr(), probes.k_z, zt.data_ptr(), float(tol), int(max_iter), float(probe_tol), out,
+         yd.data_ptr(), probes.k_z, zt.data_ptr(), float(tol), int(max_iter), float(probe_tol),
+         int(probe_max_iter or 0), out,
          ctypes.byref(conv), _device.stream_ptr())
     return LossGrad(out[0], out[1], out[2], out[3], converged=bool(conv.value))
 

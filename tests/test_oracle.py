@@ -109,3 +109,20 @@ def test_cfg1_generator_checksum():
     w = workloads.cfg1()
     z = np.random.default_rng(w.probe_seed).standard_normal((w.n, w.k_z))
     np.testing.assert_allclose([np.sum(w.x ** 2), np.sum(w.y ** 2), np.sum(z ** 2)], g["checksum"], rtol=1e-14)
+
+
+def test_fixed_recipe_logdet():
+    """configs[0]'s fixed recipe (PCG 50 + 20-step probe CG + SLQ) through the oracle, DENSE like
+    the reference run that made the fixture; fixed-step SLQ is chaotic under rounding changes
+    (reference DENSE vs ON_THE_FLY: 1.5e-6), hence the 1e-5 bar."""
+    g = golden("nlml.npz")
+    l, f, s = g["hp"]
+    ny = orc.Nystrom("gaussian", g["x"], l, f, s, int(g["rank"]))
+    khat = orc.khat_dense("gaussian", g["x"], l, f, s)
+    _, al, be, _, _ = orc.pcg(lambda b: khat @ b, None, g["probes"], 0.0, 20)
+    ld = orc.slq_logdet(al, be, np.einsum("ij,ij->j", g["probes"], g["probes"]))
+    assert abs(ld - g["fixed_logdet"]) <= 1e-5 * abs(g["fixed_logdet"])
+    w, *_ = orc.pcg(lambda b: khat @ b, ny.apply_inverse, g["y"], 0.0, 50)
+    assert rel_max(w, g["fixed_w"]) <= 1e-8
+    res = orc.nlml_grad("gaussian", g["x"], g["y"], l, f, s, g["probes"], ny, tol=1e-10, max_iter=3000, dense=True)
+    assert np.all(np.abs(np.array(res[:4]) - g["iter_tight"][:4]) <= 1e-9 * np.abs(g["iter_tight"][:4]))
