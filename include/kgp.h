@@ -109,6 +109,14 @@ int kgp_precond_apply_inverse(kgp_precond* p, int64_t k, const double* b, int64_
 int kgp_lowrank_apply(kgp_precond* p, double beta, double alpha, int64_t k, const double* b, int64_t b_rs,
                       int64_t b_cs, double* out, int64_t o_rs, int64_t o_cs, void* stream);
 
+/* The two halves of kgp_lowrank_apply, for a row-partitioned factor (multi-GPU):
+ * project: t_out = U^T B, (m, k) row-major device (the caller all-reduces it across ranks);
+ * expand:  out = beta B + alpha U t. The handle then holds only this rank's rows of U. */
+int kgp_lowrank_project(kgp_precond* p, int64_t k, const double* b, int64_t b_rs, int64_t b_cs, double* t_out,
+                        void* stream);
+int kgp_lowrank_expand(kgp_precond* p, double beta, double alpha, int64_t k, const double* b, int64_t b_rs,
+                       int64_t b_cs, const double* t, double* out, int64_t o_rs, int64_t o_cs, void* stream);
+
 /* ------------------------------------------------------------------ solvers
  * pcg_solve (solver.py:122-192): batched PCG, per-column alpha/beta capture,
  * converged columns freeze in place. y and x_out: (k, n) device (column c

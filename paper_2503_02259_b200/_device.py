@@ -47,6 +47,8 @@ def to_device(a, dtype=None):
     if isinstance(a, t.Tensor):
         return a.to(device=dev, dtype=dtype or t.float64).contiguous()
     arr = np.ascontiguousarray(a, dtype=np.float64 if dtype is None else None)
+    if not arr.flags.writeable:  # e.g. the engine's read-only X copy; torch wants writable memory
+        arr = arr.copy()
     return t.from_numpy(arr).to(dev, non_blocking=False)
 
 

@@ -60,6 +60,8 @@ _SIGNATURES = {
     "kgp_precond_destroy": [c_vp],
     "kgp_precond_apply_inverse": [c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_vp],
     "kgp_lowrank_apply": [c_vp, c_dbl, c_dbl, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_vp],
+    "kgp_lowrank_project": [c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_vp],
+    "kgp_lowrank_expand": [c_vp, c_dbl, c_dbl, c_i64, c_vp, c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp],
     "kgp_pcg": [c_vp, c_vp, c_i64, c_vp, c_dbl, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
     "kgp_slq_logdet": [c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, _P(c_dbl), c_vp],
     "kgp_nlml_grad": [c_vp, c_vp, c_vp, c_i64, c_vp, c_dbl, c_i32, c_dbl, c_i32, _P(c_dbl), _P(c_i32), c_vp],

@@ -403,6 +403,21 @@ extern "C" int kgp_lowrank_apply(kgp_precond* p, double beta, double alpha, int6
   return lowrank_apply_impl(p, beta, alpha, k, b, b_rs, b_cs, out, o_rs, o_cs, (cudaStream_t)stream);
 }
 
+extern "C" int kgp_lowrank_project(kgp_precond* p, int64_t k, const double* b, int64_t b_rs, int64_t b_cs,
+                                   double* t_out, void* stream) {
+  CHECK_PRECOND(p);
+  KGP_REQUIRE(k >= 1 && t_out != nullptr, KGP_ERR_INVALID, "bad projection arguments");
+  return lowrank_project_impl(p, k, b, b_rs, b_cs, t_out, (cudaStream_t)stream);
+}
+
+extern "C" int kgp_lowrank_expand(kgp_precond* p, double beta, double alpha, int64_t k, const double* b, int64_t b_rs,
+                                  int64_t b_cs, const double* t, double* out, int64_t o_rs, int64_t o_cs,
+                                  void* stream) {
+  CHECK_PRECOND(p);
+  KGP_REQUIRE(k >= 1 && t != nullptr, KGP_ERR_INVALID, "bad expansion arguments");
+  return lowrank_expand_impl(p, beta, alpha, k, b, b_rs, b_cs, t, out, o_rs, o_cs, (cudaStream_t)stream);
+}
+
 // ------------------------------------------------------------------ solvers
 extern "C" int kgp_pcg(kgp_engine* e, kgp_precond* p, int64_t k, const double* y, double tol, int32_t max_iter,
                        double* x_out, double* alphas, double* betas, int32_t* iters, double* rel, int32_t* converged,

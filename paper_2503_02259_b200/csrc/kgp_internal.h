@@ -97,7 +97,8 @@ struct kgp_precond_s {
   int64_t n, m;
   double s;
   kgp::DevBuf wt;    // (m, n) row-major
-  kgp::DevBuf tmp;   // (m, k) scratch + partials
+  kgp::DevBuf tmp;   // split-K partials
+  kgp::DevBuf tproj; // (m, k) projection U^T B
 };
 
 namespace kgp {
@@ -108,6 +109,10 @@ constexpr uint64_t DEAD_MAGIC = 0xdeaddeaddeaddeadull;
 int engine_prepare(kgp_engine_s* e, cudaStream_t st);
 int engine_matmul_impl(kgp_engine_s* e, int64_t k, const double* b, int64_t b_rs, int64_t b_cs, double* out_k,
                        double* out_dl, double* out_df, int64_t o_rs, int64_t o_cs, cudaStream_t st);
+int lowrank_project_impl(kgp_precond_s* p, int64_t k, const double* b, int64_t b_rs, int64_t b_cs, double* T,
+                         cudaStream_t st);
+int lowrank_expand_impl(kgp_precond_s* p, double beta, double alpha, int64_t k, const double* b, int64_t b_rs,
+                        int64_t b_cs, const double* T, double* out, int64_t o_rs, int64_t o_cs, cudaStream_t st);
 int lowrank_apply_impl(kgp_precond_s* p, double beta, double alpha, int64_t k, const double* b, int64_t b_rs,
                        int64_t b_cs, double* out, int64_t o_rs, int64_t o_cs, cudaStream_t st);
 int precond_apply_impl(kgp_precond_s* p, int64_t k, const double* b, int64_t b_rs, int64_t b_cs, double* out,

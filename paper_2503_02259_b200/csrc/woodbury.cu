@@ -99,11 +99,10 @@ __global__ void sum_partials_kernel(int64_t count, int nz, int64_t stride, const
 
 }  // namespace
 
-// out = beta B + alpha U (U^T B) with U^T = p->wt (m x n)
-int lowrank_apply_impl(kgp_precond_s* p, double beta, double alpha, int64_t k, const double* b, int64_t b_rs,
-                       int64_t b_cs, double* out, int64_t o_rs, int64_t o_cs, cudaStream_t st) {
+// T = U^T B (m x k, row-major), U^T = p->wt (m x n); split over n with fixed-order partials
+int lowrank_project_impl(kgp_precond_s* p, int64_t k, const double* b, int64_t b_rs, int64_t b_cs, double* T,
+                         cudaStream_t st) {
   const int64_t n = p->n, m = p->m;
-  // T = W^T B  (m x k), split over n
   int64_t tiles = ((m + BM - 1) / BM) * ((k + BN - 1) / BN);
   int64_t nz = (n + 2047) / 2048;
   int64_t cap = 296 / tiles;
@@ -111,10 +110,9 @@ int lowrank_apply_impl(kgp_precond_s* p, double beta, double alpha, int64_t k, c
   if (nz > cap) nz = cap;
   int64_t kchunk = ((n + nz - 1) / nz + BK - 1) / BK * BK;
   nz = (n + kchunk - 1) / kchunk;
-  int rc = p->tmp.ensure(sizeof(double) * (size_t)m * k * (nz + 1));
+  int rc = p->tmp.ensure(sizeof(double) * (size_t)m * k * nz);
   if (rc) return rc;
-  double* T = p->tmp.as<double>();
-  double* part = T + m * k;
+  double* part = p->tmp.as<double>();
   GemmArgs g{};
   g.M = m; g.N = k; g.K = n;
   g.a = p->wt.as<double>(); g.a_is = n; g.a_ks = 1;
@@ -123,10 +121,16 @@ int lowrank_apply_impl(kgp_precond_s* p, double beta, double alpha, int64_t k, c
   g.kchunk = kchunk; g.part_stride = m * k;
   dim3 grid1((unsigned)((m + BM - 1) / BM), (unsigned)((k + BN - 1) / BN), (unsigned)nz);
   dgemm_kernel<<<grid1, GT, 0, st>>>(g);
-  KGP_LAUNCH("dgemm_kernel (W^T B)");
+  KGP_LAUNCH("dgemm_kernel (U^T B)");
   sum_partials_kernel<<<(unsigned)((m * k + 255) / 256), 256, 0, st>>>(m * k, (int)nz, m * k, part, T);
   KGP_LAUNCH("sum_partials_kernel");
-  // out = beta B + alpha U T
+  return KGP_OK;
+}
+
+// out = beta B + alpha U T
+int lowrank_expand_impl(kgp_precond_s* p, double beta, double alpha, int64_t k, const double* b, int64_t b_rs,
+                        int64_t b_cs, const double* T, double* out, int64_t o_rs, int64_t o_cs, cudaStream_t st) {
+  const int64_t n = p->n, m = p->m;
   GemmArgs h{};
   h.M = n; h.N = k; h.K = m;
   h.a = p->wt.as<double>(); h.a_is = 1; h.a_ks = n;
@@ -138,8 +142,18 @@ int lowrank_apply_impl(kgp_precond_s* p, double beta, double alpha, int64_t k, c
   h.src = b; h.s_is = b_rs; h.s_ns = b_cs;
   dim3 grid2((unsigned)((n + BM - 1) / BM), (unsigned)((k + BN - 1) / BN), 1);
   dgemm_kernel<<<grid2, GT, 0, st>>>(h);
-  KGP_LAUNCH("dgemm_kernel (W T)");
+  KGP_LAUNCH("dgemm_kernel (U T)");
   return KGP_OK;
+}
+
+// out = beta B + alpha U (U^T B)
+int lowrank_apply_impl(kgp_precond_s* p, double beta, double alpha, int64_t k, const double* b, int64_t b_rs,
+                       int64_t b_cs, double* out, int64_t o_rs, int64_t o_cs, cudaStream_t st) {
+  int rc = p->tproj.ensure(sizeof(double) * (size_t)p->m * k);
+  if (rc) return rc;
+  rc = lowrank_project_impl(p, k, b, b_rs, b_cs, p->tproj.as<double>(), st);
+  if (rc) return rc;
+  return lowrank_expand_impl(p, beta, alpha, k, b, b_rs, b_cs, p->tproj.as<double>(), out, o_rs, o_cs, st);
 }
 
 // Woodbury inverse: B / s - W (W^T B) / s^2

@@ -1,0 +1,264 @@
+"""Row-partitioned multi-GPU PCG / NLML+gradient.
+
+One process per GPU. X is replicated (n*d*8 bytes); every n-vector -- the PCG
+state, y, the probes -- is split into contiguous row blocks, rank g owning rows
+I_g. One operator application is
+
+    P_full = all_gather(P_g)                (NCCL over NVLink; k x n fp64)
+    (K^ P)_g = K^[I_g, :] . P_full          (libkgp fused kernel, rows I_g only)
+
+and the per-column PCG scalars (p.Ap, r.r, r.z) are all-reduced (2k doubles per
+iteration), so alpha/beta -- and therefore every freeze decision and the Lanczos
+coefficients that feed SLQ -- are bitwise identical on all ranks. The Woodbury
+preconditioner keeps W row-sharded too: W_g^T R_g is all-reduced (m x k) before
+the local expansion. SLQ is replicated (scalars only). Gradient: local partial
+dots, one all-reduce of 3(1+k_z) values.
+
+The recurrences are the reference's (solver.py:143-192, gp.py:133-179). They run
+over a small "local ops" interface so the host-side logic is exercised on the
+CPU with gloo (tests/test_dist.py injects an oracle-backed implementation);
+``CudaRowOps`` is the GPU implementation (libkgp).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from paper_2503_02259_b200.errors import BreakdownError, NumericalError
+
+LOG_2PI = math.log(2.0 * math.pi)
+
+
+def row_range(n: int, world: int, rank: int):
+    """Balanced contiguous row block of `rank`."""
+    return rank * n // world, (rank + 1) * n // world
+
+
+class Comm:
+    """The two collectives the solver needs, over torch.distributed (nccl or gloo)."""
+
+    def __init__(self, n: int, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.n = n
+        self.ranges = [row_range(n, self.world, r) for r in range(self.world)]
+        self.maxloc = max(r1 - r0 for r0, r1 in self.ranges)
+        self.nccl = dist.get_backend(group) == "nccl"
+
+    def allgather_rows(self, x_loc):
+        """(k, n_loc) on every rank -> (k, n) full, rows in rank order."""
+        torch = __import__("torch")
+        k, nloc = x_loc.shape
+        if self.world == 1:
+            return x_loc
+        pad = torch.zeros((k, self.maxloc), dtype=x_loc.dtype, device=x_loc.device)
+        pad[:, :nloc] = x_loc
+        if self.nccl:
+            buf = torch.empty((self.world, k, self.maxloc), dtype=x_loc.dtype, device=x_loc.device)
+            self.dist.all_gather_into_tensor(buf, pad, group=self.group)
+            parts = [buf[r] for r in range(self.world)]
+        else:
+            parts = [torch.empty_like(pad) for _ in range(self.world)]
+            self.dist.all_gather(parts, pad, group=self.group)
+        return torch.cat([parts[r][:, :r1 - r0] for r, (r0, r1) in enumerate(self.ranges)], dim=1)
+
+    def allreduce(self, t):
+        if self.world > 1:
+            self.dist.all_reduce(t, group=self.group)
+        return t
+
+
+@dataclass
+class DistSolve:
+    x: object          # (k, n_loc) local rows of the solution
+    alphas: object     # (k, max_iter), identical on all ranks
+    betas: object
+    iters: np.ndarray  # (k,)
+    rel: np.ndarray
+    converged: np.ndarray
+
+
+def dist_pcg(ops, comm: Comm, y_loc, tol: float, max_iter: int, precondition: bool, shift: float = 1.0):
+    """Batched PCG over row-sharded state (solver.py:122-192). y_loc: (k, n_loc)."""
+    torch = __import__("torch")
+    if tol < 0 or max_iter < 1:
+        raise ValueError("need tol >= 0 and max_iter >= 1")
+    k = y_loc.shape[0]
+    dev, f64 = y_loc.device, torch.float64
+
+    def dots(a, b):
+        return comm.allreduce((a * b).sum(dim=1)).cpu().numpy()
+
+    def minv(r):
+        if not precondition:
+            return r
+        t = comm.allreduce(ops.project(r))
+        return ops.expand(r, t, 1.0 / shift, -1.0 / (shift * shift))
+
+    x = torch.zeros_like(y_loc)
+    r = y_loc.clone()
+    ynorm = np.sqrt(dots(r, r))
+    rel = np.where(ynorm > 0, 1.0, 0.0)
+    active = rel > tol
+    alphas = torch.zeros((k, max_iter), dtype=f64, device=dev)
+    betas = torch.zeros((k, max_iter), dtype=f64, device=dev)
+    iters = np.zeros(k, dtype=np.int64)
+    if active.any():
+        z = minv(r)
+        p = z.clone()
+        rz = dots(r, z)
+        for _ in range(max_iter):
+            ap = ops.matmul_rows(comm.allgather_rows(p))
+            pap = dots(p, ap)
+            act = np.flatnonzero(active)
+            bad = [j for j in act if not np.isfinite(pap[j]) or pap[j] <= 0.0]
+            if bad:
+                raise BreakdownError(f"p^T A p = {pap[bad[0]]} in column {bad[0]}; operator is not SPD")
+            alpha = np.zeros(k)
+            alpha[act] = rz[act] / pap[act]
+            at = torch.from_numpy(alpha).to(dev)[:, None]
+            x += at * p
+            r -= at * ap
+            idx = torch.from_numpy(act).to(dev)
+            alphas[idx, torch.from_numpy(iters[act]).to(dev)] = torch.from_numpy(alpha[act]).to(dev)
+            z = minv(r)
+            rr = dots(r, r)
+            rzn = rr if not precondition else dots(r, z)
+            if not np.all(np.isfinite(rr[act])):
+                raise NumericalError("residual became non-finite during PCG")
+            beta = np.zeros(k)
+            beta[act] = rzn[act] / rz[act]
+            betas[idx, torch.from_numpy(iters[act]).to(dev)] = torch.from_numpy(beta[act]).to(dev)
+            iters[act] += 1
+            rz[act] = rzn[act]
+            rel[act] = np.sqrt(rr[act]) / ynorm[act]
+            active[act] = rel[act] > tol
+            keep = np.flatnonzero(active)
+            if keep.size == 0:
+                break
+            kt = torch.from_numpy(keep).to(dev)
+            p[kt] = z[kt] + torch.from_numpy(beta[keep]).to(dev)[:, None] * p[kt]
+    return DistSolve(x, alphas, betas, iters, rel, rel <= tol)
+
+
+def dist_nlml_grad(ops, comm: Comm, y_loc, probes_loc, norms_sq, tol, max_iter, probe_tol=None,
+                   precondition=True, shift=1.0, probe_max_iter=None):
+    """nlml_grad_iterative (gp.py:133-179) over row-sharded vectors.
+
+    y_loc: (n_loc,), probes_loc: (k_z, n_loc) local rows; norms_sq: (k_z,) full |z|^2.
+    Returns (loss, grad_l, grad_f, grad_s, converged), identical on every rank."""
+    torch = __import__("torch")
+    probe_tol = tol if probe_tol is None else probe_tol
+    probe_max_iter = max_iter if probe_max_iter is None else probe_max_iter
+    kz = probes_loc.shape[0]
+    ws = dist_pcg(ops, comm, y_loc[None, :], tol, max_iter, precondition, shift)
+    us = dist_pcg(ops, comm, probes_loc, probe_tol, probe_max_iter, False, shift)
+    logdet = ops.slq(us.alphas, us.betas, us.iters, norms_sq)
+    w = ws.x[0]
+    yw = float(comm.allreduce((y_loc * w).sum()[None])[0])
+    loss = 0.5 * (yw + logdet + comm.n * LOG_2PI)
+    v_loc = torch.cat([w[None, :], probes_loc], dim=0)
+    u_loc = torch.cat([w[None, :], us.x], dim=0)
+    dl, df = ops.grads_rows(comm.allgather_rows(v_loc))
+    part = torch.stack([(u_loc * dl).sum(dim=1), (u_loc * df).sum(dim=1), (u_loc * v_loc).sum(dim=1)])
+    part = comm.allreduce(part).cpu().numpy()
+    grads = [0.5 * (-part[t, 0] + part[t, 1:].sum() / kz) for t in range(3)]
+    ok = bool(ws.converged.all() and us.converged.all())
+    return loss, grads[0], grads[1], grads[2], ok
+
+
+class CudaRowOps:
+    """GPU local ops: this rank's rows of the fused operator and of the Woodbury factor."""
+
+    def __init__(self, engine, r0: int, r1: int, precond_wt=None):
+        from paper_2503_02259_b200 import _device
+        from paper_2503_02259_b200._lib import PRECISIONS, call
+        from paper_2503_02259_b200.kmat import KernelEngine
+
+        self._device, self._call = _device, call
+        self.r0, self.r1 = r0, r1
+        # a private engine handle restricted to rows [r0, r1)
+        self.engine = KernelEngine(engine.kt, engine.x, engine.params, precision=engine.precision)
+        call("kgp_engine_set_rows", self.engine.handle, r0, r1 - r0)
+        self.pre = None
+        if precond_wt is not None:
+            from paper_2503_02259_b200.precond import _LowRank
+
+            self.pre = _LowRank(precond_wt[:, r0:r1], engine.params.s)
+            self.m = precond_wt.shape[0]
+
+    def _out(self, k):
+        torch = self._device.torch()
+        return torch.empty((k, self.r1 - self.r0), dtype=torch.float64, device=self._device.device())
+
+    def matmul_rows(self, p_full):
+        k, n = p_full.shape
+        out = self._out(k)
+        self._call("kgp_engine_matmul", self.engine.handle, k, p_full.data_ptr(), 1, n, out.data_ptr(), None, None,
+                   1, out.shape[1], self._device.stream_ptr())
+        return out
+
+    def grads_rows(self, v_full):
+        k, n = v_full.shape
+        dl, df = self._out(k), self._out(k)
+        self._call("kgp_engine_matmul", self.engine.handle, k, v_full.data_ptr(), 1, n, None, dl.data_ptr(),
+                   df.data_ptr(), 1, dl.shape[1], self._device.stream_ptr())
+        return dl, df
+
+    def project(self, r_loc):
+        torch = self._device.torch()
+        k, nloc = r_loc.shape
+        t = torch.empty((self.m, k), dtype=torch.float64, device=r_loc.device)
+        self._call("kgp_lowrank_project", self.pre.h, k, r_loc.data_ptr(), 1, nloc, t.data_ptr(),
+                   self._device.stream_ptr())
+        return t
+
+    def expand(self, r_loc, t, beta, alpha):
+        k, nloc = r_loc.shape
+        out = self._out(k)
+        self._call("kgp_lowrank_expand", self.pre.h, beta, alpha, k, r_loc.data_ptr(), 1, nloc, t.contiguous().data_ptr(),
+                   out.data_ptr(), 1, nloc, self._device.stream_ptr())
+        return out
+
+    def slq(self, alphas, betas, iters, norms_sq):
+        from paper_2503_02259_b200 import solver
+
+        torch = self._device.torch()
+        dev = alphas.device
+        return solver.slq_logdet_device(alphas.contiguous(), betas.contiguous(),
+                                        torch.from_numpy(np.asarray(iters, dtype=np.int32)).to(dev),
+                                        torch.from_numpy(np.asarray(norms_sq, dtype=np.float64)).to(dev))
+
+
+def build_precond_factor(engine, m):
+    """Replicated device build (every rank runs the same deterministic FPS + factorisation);
+    returns W^T (m, n) so each rank can keep its own columns of it."""
+    from paper_2503_02259_b200 import precond
+
+    torch = __import__("torch")
+    xd = engine.x_device()
+    p = engine.params
+    idx = precond.fps_device(xd, m, 0)
+    xm = xd.index_select(0, idx)
+    from paper_2503_02259_b200.kernels import device_panel
+
+    kmm = device_panel(engine._kid, 0, xm, xm, p.l)
+    kmm.diagonal().add_(precond.RIDGE_SCALE * float(torch.trace(kmm)) / m)
+    low, info = torch.linalg.cholesky_ex(kmm)
+    if int(info):
+        raise BreakdownError("landmark factorization failed; increase the noise term s or reduce the rank m")
+    vt = torch.linalg.solve_triangular(low, device_panel(engine._kid, 0, xm, xd, p.l), upper=False)
+    cap = (vt @ vt.T) / p.s
+    cap.diagonal().add_(1.0 / (p.f * p.f))
+    lc, info = torch.linalg.cholesky_ex(cap)
+    if int(info):
+        raise BreakdownError("landmark factorization failed; increase the noise term s or reduce the rank m")
+    return torch.linalg.solve_triangular(lc, vt, upper=False).contiguous()

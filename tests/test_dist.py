@@ -1,0 +1,120 @@
+"""World-size-2 gloo test of the row-partitioned solver logic on the CPU.
+
+Each rank owns a contiguous row block; the local operator rows, Woodbury halves and SLQ
+come from the CPU oracle (the GPU implementation is dist.CudaRowOps). The distributed
+PCG and NLML+gradient must reproduce the single-process oracle on the same inputs.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+from scipy.linalg import cho_solve
+
+from oracle import kgp_oracle as orc
+from paper_2503_02259_b200 import dist as kdist
+
+KT, L, F, S = "matern52", 0.7, 1.2, 0.05
+
+
+def _problem(n=240, seed=8):
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(-1, 1, (n, 2))
+    y = np.sin(3 * x[:, 0]) + 0.1 * rng.standard_normal(n)
+    z = rng.standard_normal((n, 5))
+    return x, y, z
+
+
+class OracleRowOps:
+    def __init__(self, x, r0, r1, ny):
+        self.x, self.r0, self.r1, self.ny = x, r0, r1, ny
+        self.rows = np.arange(r0, r1)
+
+    def matmul_rows(self, p_full):
+        out = orc.khat_matmul(KT, self.x, L, F, S, p_full.numpy().T, rows=self.rows)
+        return torch.from_numpy(np.ascontiguousarray(out.T))
+
+    def grads_rows(self, v_full):
+        b = v_full.numpy().T
+        dl = orc.khat_matmul(KT, self.x, L, F, S, b, theta="l", rows=self.rows)
+        df = orc.khat_matmul(KT, self.x, L, F, S, b, theta="f", rows=self.rows)
+        return torch.from_numpy(np.ascontiguousarray(dl.T)), torch.from_numpy(np.ascontiguousarray(df.T))
+
+    def project(self, r_loc):
+        return torch.from_numpy(self.ny.v[self.r0:self.r1].T @ r_loc.numpy().T)
+
+    def expand(self, r_loc, t, beta, alpha):
+        y = cho_solve(self.ny.cap, t.numpy())
+        out = beta * r_loc.numpy().T + alpha * (self.ny.v[self.r0:self.r1] @ y)
+        return torch.from_numpy(np.ascontiguousarray(out.T))
+
+    def slq(self, alphas, betas, iters, norms_sq):
+        a = [alphas[j, :it].numpy() for j, it in enumerate(iters)]
+        b = [betas[j, :it].numpy() for j, it in enumerate(iters)]
+        return orc.slq_logdet(a, b, norms_sq)
+
+
+def _worker(rank, world, port, errfile):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        x, y, z = _problem()
+        n = len(y)
+        ny = orc.Nystrom(KT, x, L, F, S, 30)
+        comm = kdist.Comm(n)
+        r0, r1 = kdist.row_range(n, world, rank)
+        ops = OracleRowOps(x, r0, r1, ny)
+
+        def op(b):
+            return orc.khat_matmul(KT, x, L, F, S, b)
+
+        # batched PCG, preconditioned and not, against the single-process oracle
+        for pre, tol in ((True, 1e-10), (False, 1e-8)):
+            res = kdist.dist_pcg(ops, comm, torch.from_numpy(np.ascontiguousarray(z.T[:, r0:r1])), tol, 500,
+                                 pre, shift=S)
+            sol, al, be, rel, conv = orc.pcg(op, ny.apply_inverse if pre else None, z, tol, 500)
+            full = comm.allgather_rows(res.x).numpy().T
+            assert np.max(np.abs(full - sol)) <= 1e-6 * np.max(np.abs(sol)), "solution"
+            assert np.all(np.abs(res.iters - np.array([len(a) for a in al])) <= 3), (res.iters, [len(a) for a in al])
+            for j in range(z.shape[1]):
+                m = min(6, len(al[j]))
+                np.testing.assert_allclose(res.alphas[j, :m].numpy(), al[j][:m], rtol=1e-9)
+            assert list(res.converged) == list(conv)
+        # NLML + gradient in tolerance mode
+        got = kdist.dist_nlml_grad(ops, comm, torch.from_numpy(y[r0:r1].copy()),
+                                   torch.from_numpy(np.ascontiguousarray(z.T[:, r0:r1])),
+                                   np.einsum("ij,ij->j", z, z), 1e-10, 3000, precondition=True, shift=S)
+        ref = orc.nlml_grad(KT, x, y, L, F, S, z, ny, tol=1e-10, max_iter=3000)
+        assert np.all(np.abs(np.array(got[:4]) - np.array(ref[:4])) <= 1e-8 * np.abs(np.array(ref[:4]))), (got, ref)
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as exc:  # surface the failure to the parent
+        with open(errfile, "a") as fh:
+            fh.write(f"rank {rank}: {type(exc).__name__}: {exc}\n")
+        raise
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world", [2])
+def test_row_partitioned_pcg_and_nlml_gloo(tmp_path, world):
+    errfile = str(tmp_path / "err.txt")
+    mp.spawn(_worker, args=(world, _free_port(), errfile), nprocs=world, join=True)
+    assert not os.path.exists(errfile), open(errfile).read()
+
+
+def test_row_ranges_cover_and_balance():
+    for n, w in ((10, 3), (65536, 8), (7, 8)):
+        rs = [kdist.row_range(n, w, r) for r in range(w)]
+        assert rs[0][0] == 0 and rs[-1][1] == n
+        assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+        sizes = [b - a for a, b in rs]
+        assert max(sizes) - min(sizes) <= 1

@@ -356,3 +356,58 @@ def test_fixed_recipe_matches_reference(pkg):
     rel = np.abs(got - np.array(ref[:4])) / np.abs(np.array(ref[:4]))
     assert np.all(rel <= bars), (got, ref, rel)
     assert not lg.converged  # tol = 0: the solves stop on the iteration caps by construction
+
+
+def _dist_gpu_worker(rank, world, port, errfile):
+    import os
+
+    import torch
+    import torch.distributed as tdist
+
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        # gloo: the collectives run on the host, so two ranks may share one GPU safely
+        tdist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        import paper_2503_02259_b200 as kgp
+        from paper_2503_02259_b200 import dist as kdist
+        from paper_2503_02259_b200 import gp, precond
+
+        g = golden("nlml.npz")
+        l, f, s = g["hp"]
+        n = g["x"].shape[0]
+        e = kgp.KernelEngine(kgp.KernelType.GAUSSIAN, g["x"], kgp.Hyperparams(l, f, s))
+        wt = kdist.build_precond_factor(e, int(g["rank"]))
+        r0, r1 = kdist.row_range(n, world, rank)
+        ops = kdist.CudaRowOps(e, r0, r1, wt)
+        comm = kdist.Comm(n)
+        y = torch.from_numpy(g["y"][r0:r1].copy()).cuda()
+        z = torch.from_numpy(np.ascontiguousarray(g["probes"].T[:, r0:r1])).cuda()
+        got = kdist.dist_nlml_grad(ops, comm, y, z, np.einsum("ij,ij->j", g["probes"], g["probes"]), 1e-10, 3000,
+                                   precondition=True, shift=s)
+        ref = g["iter_tight"][:4]
+        assert np.all(np.abs(np.array(got[:4]) - ref) <= 1e-6 * np.abs(ref)), (got, ref)
+        single = gp.nlml_grad_iterative(e, g["y"], precond.build(e, int(g["rank"])), gp.ProbeSet(g["probes"]),
+                                        tol=1e-10, max_iter=3000)
+        assert abs(got[0] - single.loss) <= 1e-9 * abs(single.loss)
+        tdist.barrier()
+        tdist.destroy_process_group()
+    except Exception as exc:
+        with open(errfile, "a") as fh:
+            fh.write(f"rank {rank}: {type(exc).__name__}: {exc}\n")
+        raise
+
+
+def test_row_partitioned_nlml_on_device(pkg, tmp_path):
+    """dist.CudaRowOps (libkgp row-block operator + sharded Woodbury) with 2 ranks on one GPU."""
+    import os
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    errfile = str(tmp_path / "err.txt")
+    mp.spawn(_dist_gpu_worker, args=(2, port, errfile), nprocs=2, join=True)
+    assert not os.path.exists(errfile), open(errfile).read()
