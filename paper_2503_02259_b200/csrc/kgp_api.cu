@@ -52,6 +52,11 @@ void DevBuf::release() {
 
 double tc_kernel_gamma(int kt, double l);
 
+static int tc_env_int(const char* name, int dflt) {
+  const char* s = getenv(name);
+  return s ? atoi(s) : dflt;
+}
+
 // blocks (x32 columns) accumulated in TMEM before promotion; env KGP_TC_FLUSH overrides
 static int tc_flush_blocks() {
   static int v = [] {
@@ -74,7 +79,7 @@ int engine_prepare(kgp_engine_s* e, cudaStream_t st) {
   if (e->prepared || e->precision == KGP_FP64) return KGP_OK;
   const int dp = e->dpad;
   int nblk = (int)((e->n + 31) / 32);
-  int rc = e->xcol.ensure(sizeof(float) * (size_t)nblk * (dp + 1) * 32);
+  int rc = e->xcol.ensure((size_t)nblk * tc_col_block_bytes(dp));
   if (rc) return rc;
   rc = e->xrow.ensure(sizeof(float) * (size_t)(e->nrows + 1) * (dp + 1));
   if (rc) return rc;
@@ -102,7 +107,7 @@ static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t 
   const int nout = out_dl ? 2 : 1;
   const int tpo = split == 3 ? 2 : 1;
   const int nblk = (int)((e->n + 31) / 32);
-  const int kmax = tc_max_kp(nout, split);
+  const int kmax = tc_max_kp(e->dpad, nout, split);
   for (int64_t c0 = 0; c0 < k; c0 += kmax) {
     const int kc = (int)((k - c0) < kmax ? (k - c0) : kmax);
     const int kp = (kc + 15) / 16 * 16;
@@ -118,9 +123,9 @@ static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t 
     p.nblk = nblk;
     p.kp = kp;
     p.k = kc;
-    int nsa = (512 - 2 * nout * kp) / (nout * tpo * 32);
-    p.nsa = nsa > 4 ? 4 : nsa;
+    p.nsa = tc_nsa(e->dpad, nout, split, kp);
     p.flush = tc_flush_blocks();
+    p.defer = tc_env_int("KGP_TC_DEFER", 1);
     p.f2 = e->f * e->f;
     p.s = e->s;
     p.two_f = 2.0 * e->f;

@@ -19,7 +19,9 @@ struct TcParams {
   int kp;                 // padded RHS count (multiple of 16, <= 128)
   int k;                  // true RHS count in this launch
   int nsa;                // TMEM A-stage ring depth
+  int nsb;                // shared-memory ring depth (set at launch)
   int flush;              // blocks per TMEM accumulation segment before promotion to fp32 smem
+  int defer;              // compute warps release a block's A stage one block late (hides tcgen05.st latency)
   double f2, s, two_f, scale_dl;
   const double* b;        // original fp64 RHS (for + s B)
   int64_t b_rs, b_cs;
@@ -28,7 +30,9 @@ struct TcParams {
   int64_t o_rs, o_cs;
 };
 int tc_pad_dim(int d);
-int tc_max_kp(int nout, int split);
+int tc_max_kp(int dpad, int nout, int split);
+int tc_nsa(int dpad, int nout, int split, int kp);
+int tc_col_block_bytes(int dpad);
 bool tc_direct(int dpad);
 int launch_kmm_tc(int kt, int dpad, int nout, int split, const TcParams& p, cudaStream_t st);
 

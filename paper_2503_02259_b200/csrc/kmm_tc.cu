@@ -7,22 +7,27 @@
 //
 // The kernel matrix is never stored. One CTA owns 128 rows (the TMEM lanes) and
 // streams the columns in blocks of 32 (one 128-byte swizzle atom of tf32):
-//   * warp 8 (producer) bulk-copies each block's RHS tiles -- pre-split into tf32
-//     hi/lo and already in the UMMA K-major 128B-swizzled layout -- and the
-//     block's column-point data into a 4-stage shared-memory ring;
-//   * warps 0-7 (compute) evaluate the 128x32 tile in registers: fp32 centred
-//     coordinates, packed FFMA2 distances, MUFU ex2/sqrt transforms; each thread
-//     owns a 4-row x 4-column patch so one broadcast LDS.128 of column data feeds
-//     16 FMAs. The tile, split into tf32 hi/lo, goes straight to TMEM
-//     (tcgen05.st 16x256b): the A operand of the MMA;
-//   * warp 9 issues tcgen05.mma kind::tf32 (A in TMEM, B in shared memory,
-//     D in TMEM): hi*hi + hi*lo + lo*hi per output and K=8 chunk for 3xTF32;
-//   * warps 10-13 (drain) promote the TMEM accumulators every `flush` blocks into
-//     fp32 shared-memory sums (two accumulator buffers ping-pong, so the MMA never
-//     waits). The tensor core's fp32 accumulation truncates; unpromoted it drifts
-//     linearly in n (measured 4.6e-4 at n=65536), promoted it stays near 1e-6.
-// The drain warps then apply f^2, 2f, s*B and the derivative scale in fp64 and
-// write the outputs.
+//   * warp 8 (producer) bulk-copies each block's operands into a 4-stage SMEM
+//     ring: the RHS tiles, pre-split into tf32 hi/lo and already in the UMMA
+//     K-major 128B-swizzled layout, plus the block's column-point data;
+//   * DISTANCE (d > 4): the scaled squared distance t2 = gamma r^2 is itself an
+//     MMA: with U'_i = [-2 gamma c_i, q_i, 1] and V'_j = [c_j, 1, q_j]
+//     (q = gamma |c|^2, c centred), t2 = U' V'^T exactly, a K = d+2 (padded to
+//     16) 3xTF32 product into TMEM -- 6 small MMAs per block instead of d FFMA
+//     per entry on the FP32 pipe. (d <= 4 keeps direct differences on the FP32
+//     pipe: cheaper there and exact for near-coincident points.);
+//   * warps 0-7 (compute) read t2 from TMEM (tcgen05.ld 16x256b), apply the
+//     kernel transform (MUFU ex2/sqrt), split into tf32 hi/lo and store the tile
+//     back to TMEM (tcgen05.st 16x256b): the A operand of the contraction;
+//   * warp 9 issues the contraction tcgen05.mma (kind::tf32, cta_group::1) from
+//     one elected lane of a converged warp: hi*hi + hi*lo + lo*hi per output and
+//     K=8 chunk (3xTF32); warp 10 issues the distance MMAs independently, as soon
+//     as a block's V' lands, so they never queue behind a blocking wait;
+//   * warps 11-14 (drain) promote the TMEM accumulators every `flush` blocks into
+//     fp32 shared-memory sums (two accumulator buffers ping-pong). The tensor
+//     core's fp32 accumulation truncates: unpromoted it drifts linearly in n
+//     (measured 4.6e-4 at n = 65536); promoted it stays near 2e-6.
+// The drain warps finally apply f^2, 2f, s*B and the derivative scale in fp64.
 #include <cuda.h>
 
 #include "kgp_common.cuh"
@@ -33,10 +38,13 @@ namespace kgp {
 namespace {
 
 constexpr int NCW = 8;                    // compute warps (2 per TMEM lane quadrant)
-constexpr int WPROD = NCW, WMMA = NCW + 1;
-constexpr int NTHREADS = (NCW + 6) * 32;  // + producer, MMA, 4 drain warps = 448
-constexpr int NSB = 4;                    // shared-memory ring depth (RHS + column data)
+constexpr int WPROD = NCW, WMMA = NCW + 1, WDIST = NCW + 2;
+constexpr int NTHREADS = (NCW + 7) * 32;  // + producer, contraction MMA, distance MMA, 4 drain = 480
+constexpr int MAXNSB = 8;                 // shared-memory ring depth: runtime p.nsb in {4, 8}
 constexpr int BJ = 32;                    // columns per block
+constexpr int ND = 2;                     // distance accumulator buffers in TMEM (one per warp set)
+constexpr int NSET = 2;                   // compute warp sets: set e handles blocks t = e (mod 2)
+constexpr int WPS = NCW / NSET;           // warps per set = one per TMEM lane quadrant
 
 KGP_DEV float ex2f(float x) {
   float y;
@@ -82,71 +90,98 @@ KGP_DEV void transform2(float2 t2, float2& kv, float2& gv) {
   }
 }
 
-// register order of tcgen05.st 16x256b.x2 for one thread: rows (r, r+8) x column pairs (c, c+8)
-KGP_DEV void pack8(uint32_t (&w)[8], float2 r0c0, float2 r1c0, float2 r0c1, float2 r1c1) {
-  w[0] = __float_as_uint(r0c0.x); w[1] = __float_as_uint(r0c0.y);
-  w[2] = __float_as_uint(r1c0.x); w[3] = __float_as_uint(r1c0.y);
-  w[4] = __float_as_uint(r0c1.x); w[5] = __float_as_uint(r0c1.y);
-  w[6] = __float_as_uint(r1c1.x); w[7] = __float_as_uint(r1c1.y);
-}
-
-template <int SPLIT>
-KGP_DEV void store_tile(uint32_t taddr, const float2 (&v)[2][2]) {
-  uint32_t w[8];
-  if (SPLIT == 3) {
-    pack8(w, hi2(v[0][0]), hi2(v[1][0]), hi2(v[0][1]), hi2(v[1][1]));
-    tmem_st_16x256b_x2(taddr, w);
-    pack8(w, lo2(v[0][0]), lo2(v[1][0]), lo2(v[0][1]), lo2(v[1][1]));
-    tmem_st_16x256b_x2(taddr + 32, w);
-  } else {
-    pack8(w, v[0][0], v[1][0], v[0][1], v[1][1]);
-    tmem_st_16x256b_x2(taddr, w);
+// register order of tcgen05 16x256b.x4 for one thread: for column group m (columns
+// c + 8m, c = 2(t%4)): (row r: 2 regs), (row r+8: 2 regs)
+KGP_DEV void pack16(uint32_t (&w)[16], const float2 (&v)[2][4], int mode) {
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    float2 a = v[0][m], b = v[1][m];
+    if (mode == 1) { a = hi2(a); b = hi2(b); }
+    if (mode == 2) { a = lo2(a); b = lo2(b); }
+    w[4 * m] = __float_as_uint(a.x); w[4 * m + 1] = __float_as_uint(a.y);
+    w[4 * m + 2] = __float_as_uint(b.x); w[4 * m + 3] = __float_as_uint(b.y);
   }
 }
 
-template <int KT, int D, bool DIRECT, int NOUT, int SPLIT>
+template <int SPLIT>
+KGP_DEV void store_tile(uint32_t taddr, const float2 (&v)[2][4]) {
+  uint32_t w[16];
+  if (SPLIT == 3) {
+    pack16(w, v, 1);
+    tmem_st_16x256b_x4(taddr, w);
+    pack16(w, v, 2);
+    tmem_st_16x256b_x4(taddr + 32, w);
+  } else {
+    pack16(w, v, 0);
+    tmem_st_16x256b_x4(taddr, w);
+  }
+}
+
+template <int D>
+struct Geo {
+  static constexpr bool DMMA = (D > 4);                      // distance on the tensor core
+  static constexpr int KD = ((D + 2) + 7) / 8 * 8;           // augmented K of the distance MMA
+  static constexpr uint32_t VBYTES = DMMA ? 2u * BJ * KD * 4u : (uint32_t)(D + 1) * BJ * 4u;  // per block
+  static constexpr uint32_t UBYTES = 0u;  // U' lives in TMEM
+};
+
+template <int KT, int D, int NOUT, int SPLIT>
 __global__ void __launch_bounds__(NTHREADS, 1) kmm_tc_kernel(const TcParams p) {
+  using G = Geo<D>;
+  constexpr bool DMMA = G::DMMA;
+  constexpr int KD = G::KD;
+  constexpr int KDS = (KD + 15) / 16 * 16;  // TMEM column stride of U' hi -> lo
   constexpr int TPO = (SPLIT == 3) ? 2 : 1;  // TMEM tiles per output (hi, lo)
   constexpr int ATILES = NOUT * TPO;
-  constexpr int XFL = (D + 1) * BJ;          // floats of column data per block
-  constexpr uint32_t XBYTES = XFL * 4;
+  constexpr uint32_t VBYTES = G::VBYTES;
   constexpr bool NEED_G = (NOUT == 2);
 
   extern __shared__ __align__(1024) uint8_t smem[];
   const int KP = p.kp;
+  const int NSB = p.nsb;                           // 4 or 8
+  const int nsb_log = (NSB == 8) ? 3 : 2;
   const int NACC = NOUT * KP;                      // accumulator columns per buffer
   const uint32_t BBYTES = (uint32_t)(TPO * KP * 128);
   uint8_t* sB = smem;                              // NSB x BBYTES, 1024-aligned
-  float* sX = reinterpret_cast<float*>(smem + NSB * BBYTES);  // NSB x XFL
-  float* sAcc = sX + NSB * XFL;                    // NACC x 128 fp32, column-major
+  uint8_t* sV = smem + NSB * BBYTES;               // NSB x VBYTES (column data / V' tiles)
+  uint8_t* sU = sV + NSB * VBYTES;                 // U' hi/lo (DMMA)
+  float* sAcc = reinterpret_cast<float*>(sU + G::UBYTES);  // NACC x 128 fp32, column-major
   uint64_t* bars = reinterpret_cast<uint64_t*>(sAcc + NACC * 128);
   uint64_t* full = bars;
-  uint64_t* empty = bars + NSB;
-  uint64_t* afull = bars + 2 * NSB;
-  uint64_t* aempty = bars + 2 * NSB + 4;
-  uint64_t* accfull = bars + 2 * NSB + 8;
-  uint64_t* accempty = bars + 2 * NSB + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NSB + 12);
+  uint64_t* empty = bars + MAXNSB;
+  uint64_t* afull = bars + 2 * MAXNSB;
+  uint64_t* aempty = bars + 2 * MAXNSB + 4;
+  uint64_t* accfull = bars + 2 * MAXNSB + 8;
+  uint64_t* accempty = bars + 2 * MAXNSB + 10;
+  uint64_t* dfull = bars + 2 * MAXNSB + 12;
+  uint64_t* dempty = bars + 2 * MAXNSB + 12 + ND;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * MAXNSB + 12 + 2 * ND);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int NSA = p.nsa;
-  const int abase = 2 * NACC;  // A stages follow the two accumulator buffers
+  const int dbase = 2 * NACC;                      // distance buffers follow the accumulators
+  const int ucol = dbase + (DMMA ? ND * BJ : 0);   // then U' hi | lo (KD columns each)
+  const int abase = ucol + (DMMA ? 2 * KDS : 0);   // then the A stages
   const int nblk = p.nblk;
   const int flush = p.flush;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSB; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1 + NCW);
+      mbar_init(&empty[s], DMMA ? 2 : 1 + WPS);  // DMMA: released by both MMA warps' commits
     }
     for (int a = 0; a < NSA; ++a) {
-      mbar_init(&afull[a], NCW);
+      mbar_init(&afull[a], WPS);
       mbar_init(&aempty[a], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&accfull[b], 1);
       mbar_init(&accempty[b], 4);
+    }
+    for (int b = 0; b < ND; ++b) {
+      mbar_init(&dfull[b], 1);
+      mbar_init(&dempty[b], WPS);
     }
     fence_barrier_init();
   }
@@ -155,6 +190,34 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmm_tc_kernel(const TcParams p) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  if (DMMA && warp < 4) {
+    // U'_r = [-2 gamma c_r (D), q_r, 1, 0 ...] as tf32 hi / lo in TMEM (A operand of the
+    // distance MMA): warp w writes lanes 32w..32w+31 (thread = row), KD columns each
+    const int r = threadIdx.x;
+    const int64_t gr = (int64_t)blockIdx.x * 128 + r;
+    const bool ok = gr < p.nrows;
+    const float* xr = p.xrow + (ok ? gr : 0) * (D + 1);
+    const uint32_t uaddr = tbase + ((uint32_t)(warp * 32) << 16) + ucol;
+#pragma unroll
+    for (int k0 = 0; k0 < KD; k0 += 16) {
+      uint32_t hv[16], lv[16];
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) {
+        const int k = k0 + kk;
+        float v = 0.f;
+        if (ok && k < KD) v = (k < D) ? xr[1 + k] : (k == D ? xr[0] : (k == D + 1 ? 1.0f : 0.0f));
+        const float hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+        hv[kk] = __float_as_uint(hi);
+        lv[kk] = __float_as_uint(v - hi);
+      }
+      tmem_st16(uaddr + k0, hv);
+      tmem_st16(uaddr + KDS + k0, lv);
+    }
+    tc_wait_st();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
 
   if (warp == WPROD) {
     // ------------------------------------------------------------ producer (converged warp, one elected issuer)
@@ -163,15 +226,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmm_tc_kernel(const TcParams p) {
     for (int t = 0; t < nblk; ++t) {
       mbar_wait(&empty[s], ph ^ 1);
       if (elect_one()) {
-        mbar_arrive_expect_tx(&full[s], BBYTES + XBYTES);
+        mbar_arrive_expect_tx(&full[s], BBYTES + VBYTES);
         bulk_g2s(sB + s * BBYTES, p.bsplit + (size_t)t * BBYTES, BBYTES, &full[s]);
-        bulk_g2s(sX + s * XFL, p.xcol + (size_t)t * XFL, XBYTES, &full[s]);
+        bulk_g2s(sV + s * VBYTES, reinterpret_cast<const uint8_t*>(p.xcol) + (size_t)t * VBYTES, VBYTES, &full[s]);
       }
       __syncwarp();
       if (++s == NSB) { s = 0; ph ^= 1; }
     }
   } else if (warp == WMMA) {
-    // ------------------------------------------------------------ MMA issuer (converged warp, one elected issuer)
+    // ------------------------------------------------------------ contraction MMA issuer (converged warp)
     const uint32_t idesc = idesc_tf32_m128(KP);
     int s = 0, a = 0, pos = 0, ab = 0;
     uint32_t ph_s = 0, ph_a = 0, ph_acc = 0;
@@ -214,100 +277,127 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmm_tc_kernel(const TcParams p) {
       if (++s == NSB) { s = 0; ph_s ^= 1; }
       if (++a == NSA) { a = 0; ph_a ^= 1; }
     }
+  } else if (warp == WDIST) {
+    // ------------------------------------------------------------ distance MMA issuer (DMMA only)
+    if (DMMA) {
+      const uint32_t idesc_d = idesc_tf32_m128(BJ);
+      const uint32_t vlo_off = (uint32_t)BJ * KD * 4u;
+      int s = 0, db = 0;
+      uint32_t ph_s = 0, ph_d = 0;
+      for (int t = 0; t < nblk; ++t) {
+        mbar_wait(&full[s], ph_s);
+        mbar_wait(&dempty[db], ph_d ^ 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t va = smem_u32(sV + s * VBYTES);
+          const uint32_t dd = tbase + dbase + db * BJ;
+#pragma unroll
+          for (int kk = 0; kk < KD / 8; ++kk) {
+            // one K=8 step = two 16-byte chunks; chunk stride (LBO) = rows * 16 B
+            const uint32_t uh = tbase + ucol + 8 * kk, ul = uh + KDS;  // U' hi / lo in TMEM
+            const uint64_t vh = interleave_kmajor_desc(va + kk * 2 * BJ * 16, BJ * 16, 128);
+            const uint64_t vl = interleave_kmajor_desc(va + vlo_off + kk * 2 * BJ * 16, BJ * 16, 128);
+            mma_tf32_ts(dd, uh, vh, idesc_d, kk > 0 ? 1u : 0u);
+            mma_tf32_ts(dd, uh, vl, idesc_d, 1u);
+            mma_tf32_ts(dd, ul, vh, idesc_d, 1u);
+          }
+          tc_commit(&dfull[db]);
+          tc_commit(&empty[s]);  // this stage's V' has been read
+        }
+        __syncwarp();
+        if (++s == NSB) { s = 0; ph_s ^= 1; }
+        if (++db == ND) { db = 0; ph_d ^= 1; }
+      }
+    }
   } else if (warp < NCW) {
     // ------------------------------------------------------------ compute warps
-    const int qd = warp & 3;  // TMEM lane quadrant
-    const int h = warp >> 2;  // columns [16h, 16h+16) of each block
+    // Two sets of four warps (one per TMEM lane quadrant) take alternate blocks, so
+    // one set's TMEM/barrier latencies overlap the other set's transform work.
+    const int qd = warp & 3;    // TMEM lane quadrant
+    const int set = warp >> 2;  // blocks t = set (mod 2)
     const int g = lane & 3;
-    // rows owned by this thread: 32 qd + lane/4 + {0, 8, 16, 24}
-    float qi[4], u[4][D];
+    // rows owned by this thread: 32 qd + lane/4 + {0, 8, 16, 24}; columns 2g + {0,1} + 8m, m < 4
+    float u[4][DMMA ? 1 : D];
+    if (!DMMA) {
 #pragma unroll
-    for (int rr = 0; rr < 4; ++rr) {
-      const int64_t r = (int64_t)blockIdx.x * 128 + qd * 32 + (lane >> 2) + 8 * rr;
-      const bool ok = r < p.nrows;
-      const float* xr = p.xrow + (ok ? r : 0) * (D + 1);
-      qi[rr] = ok ? xr[0] : 0.f;
+      for (int rr = 0; rr < 4; ++rr) {
+        const int64_t r = (int64_t)blockIdx.x * 128 + qd * 32 + (lane >> 2) + 8 * rr;
+        const bool ok = r < p.nrows;
+        const float* xr = p.xrow + (ok ? r : 0) * (D + 1);
 #pragma unroll
-      for (int k = 0; k < D; ++k) u[rr][k] = ok ? xr[1 + k] : 0.f;
+        for (int k = 0; k < (DMMA ? 1 : D); ++k) u[rr][k] = ok ? xr[1 + k] : 0.f;
+      }
     }
     const uint32_t lane_base = tbase + ((uint32_t)(qd * 32) << 16);
-    int s = 0, a = 0, prev_a = -1;
-    uint32_t ph_s = 0, ph_a = 0;
-    for (int t = 0; t < nblk; ++t) {
-      mbar_wait(&full[s], ph_s);
-      // this thread's columns, permuted by prep_cols: (c, c+1, c+8, c+9), c = 16h + 2g
-      const float* xs = sX + s * XFL + 16 * h + 4 * g;
-      float2 acc[4][2];  // [row][column pair]
-      if (DIRECT) {
+    const int nsa_log = (NSA == 4) ? 2 : 1;
+    for (int t = set; t < nblk; t += NSET) {
+      const int s = t & (NSB - 1), a = t & (NSA - 1), db = t & (ND - 1);
+      const uint32_t ph_s = (t >> nsb_log) & 1, ph_a = (t >> nsa_log) & 1, ph_d = (t / ND) & 1;
+      float2 acc[4][4];  // [row][column pair m]: rows lane/4 + 8 rr, columns 2g + 8m + {0,1}
+      if (DMMA) {
+        mbar_wait(&dfull[db], ph_d);
+        tc_fence_after();
+        const uint32_t dcol = lane_base + dbase + db * BJ;
 #pragma unroll
-        for (int rr = 0; rr < 4; ++rr) acc[rr][0] = acc[rr][1] = make_float2(0.f, 0.f);
+        for (int half = 0; half < 2; ++half) {
+          uint32_t v[16];
+          tmem_ld_16x256b_x4(dcol + ((uint32_t)(16 * half) << 16), v);
+          tc_wait_ld_tied(v);
 #pragma unroll
-        for (int k = 0; k < D; ++k) {
-          const float4 v = *reinterpret_cast<const float4*>(xs + (k + 1) * BJ);
-          const float2 v0 = make_float2(v.x, v.y), v1 = make_float2(v.z, v.w);
-#pragma unroll
-          for (int rr = 0; rr < 4; ++rr) {
-            const float2 uk = make_float2(u[rr][k], u[rr][k]);
-            const float2 d0 = fsub2(v0, uk);
-            const float2 d1 = fsub2(v1, uk);
-            acc[rr][0] = __ffma2_rn(d0, d0, acc[rr][0]);
-            acc[rr][1] = __ffma2_rn(d1, d1, acc[rr][1]);
+          for (int m = 0; m < 4; ++m) {
+            acc[2 * half][m] = make_float2(__uint_as_float(v[4 * m]), __uint_as_float(v[4 * m + 1]));
+            acc[2 * half + 1][m] = make_float2(__uint_as_float(v[4 * m + 2]), __uint_as_float(v[4 * m + 3]));
           }
         }
-      } else {
-        const float4 qv = *reinterpret_cast<const float4*>(xs);
-#pragma unroll
-        for (int rr = 0; rr < 4; ++rr) {
-          const float2 qq = make_float2(qi[rr], qi[rr]);
-          acc[rr][0] = __fadd2_rn(make_float2(qv.x, qv.y), qq);
-          acc[rr][1] = __fadd2_rn(make_float2(qv.z, qv.w), qq);
-        }
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-          const float4 v = *reinterpret_cast<const float4*>(xs + (k + 1) * BJ);
-          const float2 v0 = make_float2(v.x, v.y), v1 = make_float2(v.z, v.w);
-#pragma unroll
-          for (int rr = 0; rr < 4; ++rr) {
-            const float2 uk = make_float2(u[rr][k], u[rr][k]);
-            acc[rr][0] = __ffma2_rn(uk, v0, acc[rr][0]);
-            acc[rr][1] = __ffma2_rn(uk, v1, acc[rr][1]);
-          }
-        }
-      }
-      // column data consumed: release the ring slot
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      // hand the previous block's A stage to the MMA (its stores were issued one block ago)
-      if (prev_a >= 0) {
-        tc_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&afull[prev_a]);
+        if (lane == 0) mbar_arrive(&dempty[db]);
+      } else {
+        mbar_wait(&full[s], ph_s);
+        // this thread's 8 columns, permuted by prep_cols into two float4 at 8g
+        const float* xs = reinterpret_cast<const float*>(sV + s * VBYTES) + 8 * g;
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+          for (int m = 0; m < 4; ++m) acc[rr][m] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < (DMMA ? 1 : D); ++k) {
+          const float4 va = *reinterpret_cast<const float4*>(xs + (k + 1) * BJ);
+          const float4 vb = *reinterpret_cast<const float4*>(xs + (k + 1) * BJ + 4);
+          const float2 vv[4] = {make_float2(va.x, va.y), make_float2(va.z, va.w), make_float2(vb.x, vb.y),
+                                make_float2(vb.z, vb.w)};
+#pragma unroll
+          for (int rr = 0; rr < 4; ++rr) {
+            const float2 uk = make_float2(u[rr][k], u[rr][k]);
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+              const float2 dd = fsub2(vv[m], uk);
+              acc[rr][m] = __ffma2_rn(dd, dd, acc[rr][m]);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
       }
       mbar_wait(&aempty[a], ph_a ^ 1);
       tc_fence_after();
-      const uint32_t tcol = lane_base + abase + a * ATILES * 32 + 16 * h;
+      const uint32_t tcol = lane_base + abase + a * ATILES * 32;
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         // 16-lane group `half`: this thread's rows lane/4 (+16 half) and lane/4 + 8
-        float2 kv[2][2], gv[2][2];
+        float2 kv[2][4], gv[2][4];
 #pragma unroll
         for (int q = 0; q < 2; ++q)
 #pragma unroll
-          for (int cp = 0; cp < 2; ++cp) transform2<KT, NEED_G>(acc[2 * half + q][cp], kv[q][cp], gv[q][cp]);
+          for (int m = 0; m < 4; ++m) transform2<KT, NEED_G>(acc[2 * half + q][m], kv[q][m], gv[q][m]);
         const uint32_t taddr = tcol + ((uint32_t)(16 * half) << 16);
         store_tile<SPLIT>(taddr, kv);
         if (NEED_G) store_tile<SPLIT>(taddr + TPO * 32, gv);
       }
-      prev_a = a;
-      if (++s == NSB) { s = 0; ph_s ^= 1; }
-      if (++a == NSA) { a = 0; ph_a ^= 1; }
-    }
-    if (prev_a >= 0) {
       tc_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&afull[prev_a]);
+      if (lane == 0) mbar_arrive(&afull[a]);
     }
   } else {
     // ------------------------------------------------------------ drain + epilogue warps
@@ -361,16 +451,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmm_tc_kernel(const TcParams p) {
   }
 }
 
-template <int KT, int D, bool DIRECT, int NOUT, int SPLIT>
-int launch_one(const TcParams& p, cudaStream_t st) {
-  auto kern = kmm_tc_kernel<KT, D, DIRECT, NOUT, SPLIT>;
+template <int KT, int D, int NOUT, int SPLIT>
+int launch_one(const TcParams& p_in, cudaStream_t st) {
+  auto kern = kmm_tc_kernel<KT, D, NOUT, SPLIT>;
   const int TPO = (SPLIT == 3) ? 2 : 1;
-  size_t smem = NSB * (size_t)(TPO * p.kp * 128) + NSB * (size_t)((D + 1) * BJ * 4) +
-                (size_t)NOUT * p.kp * 128 * 4 + 256;
-  KGP_REQUIRE(smem <= 225 * 1024, KGP_ERR_INVALID, "fast operator tile config needs %zu B of shared memory", smem);
+  TcParams p = p_in;
+  const size_t stage = (size_t)(TPO * p.kp * 128) + Geo<D>::VBYTES;
+  const size_t fixed = Geo<D>::UBYTES + (size_t)NOUT * p.kp * 128 * 4 + 512;
+  const size_t limit = 225 * 1024;
+  p.nsb = (fixed + 8 * stage <= limit) ? 8 : 4;  // deeper prefetch when shared memory allows
+  const size_t smem = fixed + p.nsb * stage;
+  KGP_REQUIRE(smem <= limit, KGP_ERR_INVALID, "fast operator tile config needs %zu B of shared memory", smem);
   static bool configured = false;  // one attribute call per instantiation
   if (!configured) {
-    KGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 225 * 1024));
+    KGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)limit));
     configured = true;
   }
   dim3 grid((unsigned)((p.nrows + 127) / 128));
@@ -379,19 +473,19 @@ int launch_one(const TcParams& p, cudaStream_t st) {
   return KGP_OK;
 }
 
-template <int KT, int D, bool DIRECT>
+template <int KT, int D>
 int launch_kt_d(const TcParams& p, int nout, int split, cudaStream_t st) {
-  if (nout == 1) return split == 3 ? launch_one<KT, D, DIRECT, 1, 3>(p, st) : launch_one<KT, D, DIRECT, 1, 1>(p, st);
-  return split == 3 ? launch_one<KT, D, DIRECT, 2, 3>(p, st) : launch_one<KT, D, DIRECT, 2, 1>(p, st);
+  if (nout == 1) return split == 3 ? launch_one<KT, D, 1, 3>(p, st) : launch_one<KT, D, 1, 1>(p, st);
+  return split == 3 ? launch_one<KT, D, 2, 3>(p, st) : launch_one<KT, D, 2, 1>(p, st);
 }
 
 template <int KT>
 int launch_kt(const TcParams& p, int dpad, int nout, int split, cudaStream_t st) {
   switch (dpad) {
-    case 2: return launch_kt_d<KT, 2, true>(p, nout, split, st);
-    case 4: return launch_kt_d<KT, 4, true>(p, nout, split, st);
-    case 8: return launch_kt_d<KT, 8, false>(p, nout, split, st);
-    case 16: return launch_kt_d<KT, 16, false>(p, nout, split, st);
+    case 2: return launch_kt_d<KT, 2>(p, nout, split, st);
+    case 4: return launch_kt_d<KT, 4>(p, nout, split, st);
+    case 8: return launch_kt_d<KT, 8>(p, nout, split, st);
+    case 16: return launch_kt_d<KT, 16>(p, nout, split, st);
   }
   set_error(KGP_ERR_INVALID, "fast path supports d <= 16");
   return KGP_ERR_INVALID;
@@ -402,12 +496,31 @@ int launch_kt(const TcParams& p, int dpad, int nout, int split, cudaStream_t st)
 int tc_pad_dim(int d) { return d <= 2 ? 2 : d <= 4 ? 4 : d <= 8 ? 8 : 16; }
 bool tc_direct(int dpad) { return dpad <= 4; }
 
-int tc_max_kp(int nout, int split) {
-  // TMEM: two accumulator buffers (2 * nout * kp columns) + at least two A stages
+int tc_col_block_bytes(int dpad) {
+  if (dpad <= 4) return (dpad + 1) * BJ * 4;
+  const int kd = ((dpad + 2) + 7) / 8 * 8;
+  return 2 * BJ * kd * 4;
+}
+
+static int tc_fixed_cols(int dpad) {
+  if (tc_direct(dpad)) return 0;
+  const int kd = ((dpad + 2) + 7) / 8 * 8;
+  return ND * BJ + 2 * ((kd + 15) / 16 * 16);  // distance buffers + U' hi/lo
+}
+
+int tc_max_kp(int dpad, int nout, int split) {
+  // TMEM: two accumulator buffers (2 nout kp) + distance buffers + U' + at least two A stages
   const int stage = nout * (split == 3 ? 2 : 1) * 32;
-  int kp = (512 - 2 * stage) / (2 * nout);
+  int kp = (512 - tc_fixed_cols(dpad) - 2 * stage) / (2 * nout);
   kp = kp / 16 * 16;
   return kp > 128 ? 128 : kp;
+}
+
+int tc_nsa(int dpad, int nout, int split, int kp) {
+  const int stage = nout * (split == 3 ? 2 : 1) * 32;
+  int nsa = (512 - tc_fixed_cols(dpad) - 2 * nout * kp) / stage;
+  // a power of two >= 2: the two compute warp sets step through the ring by 2
+  return nsa >= 4 ? 4 : 2;
 }
 
 int launch_kmm_tc(int kt, int dpad, int nout, int split, const TcParams& p, cudaStream_t st) {

@@ -59,18 +59,34 @@ __global__ void prep_cols_kernel(int kt, int d, int dpad, bool direct, int64_t n
   if (j >= (int64_t)nblk * 32) return;
   const int64_t t = j >> 5;
   const int jj = (int)(j & 31);
-  // position inside the block: the tile kernel's thread (h, g) reads columns
-  // (16h + 2g, +1, +8, +9) as one float4 at 16h + 4g
-  const int hh = jj >> 4, cc = jj & 15;
-  const int pos = 16 * hh + 4 * ((cc & 7) >> 1) + (cc & 1) + 2 * (cc >> 3);
-  float* o = out + t * (int64_t)(dpad + 1) * 32;
-  double sg = sqrt(gamma), nrm = 0.0;
+  double c[16], nrm = 0.0;
   for (int k = 0; k < dpad; ++k) {
-    double c = (j < n && k < d) ? x[j * d + k] - mean[k] : 0.0;
-    nrm += c * c;
-    o[(1 + k) * 32 + pos] = direct ? (float)(sg * c) : (float)c;
+    c[k] = (j < n && k < d) ? x[j * d + k] - mean[k] : 0.0;
+    nrm += c[k] * c[k];
   }
-  o[pos] = (direct || j >= n) ? 0.0f : (float)(gamma * nrm);
+  if (direct) {
+    // position inside the block: the tile kernel's thread g reads columns
+    // 2g + {0, 1} + 8m (m < 4) as two float4 at 8g
+    const int m = jj >> 3, cc = jj & 7;
+    const int pos = 8 * (cc >> 1) + 2 * m + (cc & 1);
+    float* o = out + t * (int64_t)(dpad + 1) * 32;
+    const double sg = sqrt(gamma);
+    for (int k = 0; k < dpad; ++k) o[(1 + k) * 32 + pos] = (float)(sg * c[k]);
+    o[pos] = 0.0f;
+    return;
+  }
+  // tensor-core distance: V'_j = [c_j (dpad), 1, q_j, 0 ...] as tf32 hi / lo tiles
+  // (K-major, no swizzle, 32 rows), block t at byte t * 2 * 32 * kd * 4
+  const int kd = ((dpad + 2) + 7) / 8 * 8;
+  uint8_t* base = reinterpret_cast<uint8_t*>(out) + t * (int64_t)(2 * 32 * kd * 4);
+  for (int k = 0; k < kd; ++k) {
+    float v = 0.0f;
+    if (j < n) v = (k < dpad) ? (float)c[k] : (k == dpad ? 1.0f : (k == dpad + 1 ? (float)(gamma * nrm) : 0.0f));
+    const float hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+    const uint32_t off = interleave_offset((uint32_t)jj, (uint32_t)k, 32);
+    *reinterpret_cast<float*>(base + off) = hi;
+    *reinterpret_cast<float*>(base + 32 * kd * 4 + off) = v - hi;
+  }
 }
 
 __device__ inline uint32_t tf32_rna_bits(float v) {
