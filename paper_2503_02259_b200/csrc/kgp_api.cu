@@ -124,8 +124,16 @@ static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t 
     p.kp = kp;
     p.k = kc;
     p.nsa = tc_nsa(e->dpad, nout, split, kp);
+    const int nsplit = tc_col_split(nrows, nblk);
+    p.nper = (nblk + nsplit - 1) / nsplit;
+    p.part = nullptr;
+    if (nsplit > 1) {
+      rc = e->tcpart.ensure(sizeof(float) * (size_t)nsplit * nrows * nout * kp);
+      if (rc) return rc;
+      p.part = e->tcpart.as<float>();
+    }
     p.flush = tc_flush_blocks();
-    p.defer = tc_env_int("KGP_TC_DEFER", 1);
+    p.debug = tc_env_int("KGP_TC_DEBUG", 0);
     p.f2 = e->f * e->f;
     p.s = e->s;
     p.two_f = 2.0 * e->f;

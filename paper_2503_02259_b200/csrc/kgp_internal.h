@@ -16,12 +16,14 @@ struct TcParams {
   const uint8_t* bsplit;  // nblk x TPO x kp x 128 B: RHS tiles, tf32 hi (/lo), swizzled K-major
   int64_t nrows;
   int nblk;
+  int nper;               // column blocks per CTA along grid.y (column split)
+  float* part;            // split partial sums (nsplit x nrows x nout*kp); nullptr: no split
   int kp;                 // padded RHS count (multiple of 16, <= 128)
   int k;                  // true RHS count in this launch
   int nsa;                // TMEM A-stage ring depth
   int nsb;                // shared-memory ring depth (set at launch)
   int flush;              // blocks per TMEM accumulation segment before promotion to fp32 smem
-  int defer;              // compute warps release a block's A stage one block late (hides tcgen05.st latency)
+  int debug;              // diagnostic bit flags (env KGP_TC_DEBUG): 1 no contraction MMA, 2 no distance MMA, 4 no transform
   double f2, s, two_f, scale_dl;
   const double* b;        // original fp64 RHS (for + s B)
   int64_t b_rs, b_cs;
@@ -31,6 +33,7 @@ struct TcParams {
 };
 int tc_pad_dim(int d);
 int tc_max_kp(int dpad, int nout, int split);
+int tc_col_split(int64_t nrows, int nblk);
 int tc_nsa(int dpad, int nout, int split, int kp);
 int tc_col_block_bytes(int dpad);
 bool tc_direct(int dpad);
@@ -90,6 +93,7 @@ struct kgp_engine_s {
   kgp::DevBuf xrow_cross;  // scratch for cross (prediction) rows
   kgp::DevBuf bsplit;      // per-call RHS split
   kgp::DevBuf f64part;     // fp64 operator column-split partials
+  kgp::DevBuf tcpart;      // fast operator column-split partials
   bool prepared;
   // PCG workspace (grown on demand) and a pinned status word for the per-iteration readback
   kgp::DevBuf ws;

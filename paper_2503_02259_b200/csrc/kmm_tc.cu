@@ -163,7 +163,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmm_tc_kernel(const TcParams p) {
   const int dbase = 2 * NACC;                      // distance buffers follow the accumulators
   const int ucol = dbase + (DMMA ? ND * BJ : 0);   // then U' hi | lo (KD columns each)
   const int abase = ucol + (DMMA ? 2 * KDS : 0);   // then the A stages
-  const int nblk = p.nblk;
+  // column split (grid.y): this CTA sweeps column blocks [t0, t0 + nblk)
+  const int t0 = blockIdx.y * p.nper;
+  const int nblk = (p.nblk - t0) < p.nper ? (p.nblk - t0) : p.nper;
   const int flush = p.flush;
 
   if (threadIdx.x == 0) {
@@ -227,8 +229,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmm_tc_kernel(const TcParams p) {
       mbar_wait(&empty[s], ph ^ 1);
       if (elect_one()) {
         mbar_arrive_expect_tx(&full[s], BBYTES + VBYTES);
-        bulk_g2s(sB + s * BBYTES, p.bsplit + (size_t)t * BBYTES, BBYTES, &full[s]);
-        bulk_g2s(sV + s * VBYTES, reinterpret_cast<const uint8_t*>(p.xcol) + (size_t)t * VBYTES, VBYTES, &full[s]);
+        bulk_g2s(sB + s * BBYTES, p.bsplit + (size_t)(t0 + t) * BBYTES, BBYTES, &full[s]);
+        bulk_g2s(sV + s * VBYTES, reinterpret_cast<const uint8_t*>(p.xcol) + (size_t)(t0 + t) * VBYTES, VBYTES, &full[s]);
       }
       __syncwarp();
       if (++s == NSB) { s = 0; ph ^= 1; }
@@ -249,7 +251,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmm_tc_kernel(const TcParams p) {
       const bool last = (pos + 1 == flush) || (t == nblk - 1);
       if (elect_one()) {
 #pragma unroll
-        for (int o = 0; o < NOUT; ++o) {
+        for (int o = 0; o < ((p.debug & 1) ? 0 : NOUT); ++o) {
           const uint32_t dt = tbase + ab * NACC + o * KP;
           const uint32_t ahi = tbase + abase + (a * ATILES + o * TPO) * 32;
 #pragma unroll
@@ -292,7 +294,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmm_tc_kernel(const TcParams p) {
           const uint32_t va = smem_u32(sV + s * VBYTES);
           const uint32_t dd = tbase + dbase + db * BJ;
 #pragma unroll
-          for (int kk = 0; kk < KD / 8; ++kk) {
+          for (int kk = 0; kk < ((p.debug & 2) ? 0 : KD / 8); ++kk) {
             // one K=8 step = two 16-byte chunks; chunk stride (LBO) = rows * 16 B
             const uint32_t uh = tbase + ucol + 8 * kk, ul = uh + KDS;  // U' hi / lo in TMEM
             const uint64_t vh = interleave_kmajor_desc(va + kk * 2 * BJ * 16, BJ * 16, 128);
@@ -389,7 +391,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmm_tc_kernel(const TcParams p) {
 #pragma unroll
         for (int q = 0; q < 2; ++q)
 #pragma unroll
-          for (int m = 0; m < 4; ++m) transform2<KT, NEED_G>(acc[2 * half + q][m], kv[q][m], gv[q][m]);
+          for (int m = 0; m < 4; ++m) {
+            if (p.debug & 4) {
+              kv[q][m] = gv[q][m] = acc[2 * half + q][m];
+            } else {
+              transform2<KT, NEED_G>(acc[2 * half + q][m], kv[q][m], gv[q][m]);
+            }
+          }
         const uint32_t taddr = tcol + ((uint32_t)(16 * half) << 16);
         store_tile<SPLIT>(taddr, kv);
         if (NEED_G) store_tile<SPLIT>(taddr + TPO * 32, gv);
@@ -427,9 +435,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmm_tc_kernel(const TcParams p) {
       if (ab == 1) ph ^= 1;
       ab ^= 1;
     }
-    // epilogue: fp64 scaling, + s B on the diagonal rows, strided writes
+    // epilogue: fp64 scaling, + s B on the diagonal rows, strided writes -- or, when the
+    // columns are split over grid.y, the raw fp32 partial sums for tc_reduce_kernel
     const int64_t r = (int64_t)blockIdx.x * 128 + row;
-    if (r < p.nrows) {
+    if (p.part != nullptr) {
+      if (r < p.nrows) {
+        float* dst = p.part + ((int64_t)blockIdx.y * p.nrows + r) * NACC;
+        for (int c = 0; c < NACC; ++c) dst[c] = sAcc[c * 128 + row];
+      }
+    } else if (r < p.nrows) {
       for (int c = 0; c < p.k; ++c) {
         const double ak = (double)sAcc[c * 128 + row];
         const int64_t o = r * p.o_rs + c * p.o_cs;
@@ -451,6 +465,28 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmm_tc_kernel(const TcParams p) {
   }
 }
 
+// sum the grid.y column-split partials in split order, then the epilogue of kmm_tc_kernel
+__global__ void tc_reduce_kernel(const TcParams p, int nsplit, int nacc) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= p.nrows * p.k) return;
+  const int64_t r = e / p.k;
+  const int c = (int)(e % p.k);
+  double ak = 0.0, ag = 0.0;
+  for (int z = 0; z < nsplit; ++z) {
+    const float* src = p.part + ((int64_t)z * p.nrows + r) * nacc;
+    ak += (double)src[c];
+    if (nacc > p.kp) ag += (double)src[p.kp + c];
+  }
+  const int64_t o = r * p.o_rs + c * p.o_cs;
+  if (p.out_k) {
+    double val = p.f2 * ak;
+    if (p.diag_row0 >= 0) val += p.s * p.b[(p.diag_row0 + r) * p.b_rs + c * p.b_cs];
+    p.out_k[o] = val;
+  }
+  if (p.out_df) p.out_df[o] = p.two_f * ak;
+  if (nacc > p.kp && p.out_dl) p.out_dl[o] = p.scale_dl * ag;
+}
+
 template <int KT, int D, int NOUT, int SPLIT>
 int launch_one(const TcParams& p_in, cudaStream_t st) {
   auto kern = kmm_tc_kernel<KT, D, NOUT, SPLIT>;
@@ -467,9 +503,15 @@ int launch_one(const TcParams& p_in, cudaStream_t st) {
     KGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)limit));
     configured = true;
   }
-  dim3 grid((unsigned)((p.nrows + 127) / 128));
+  const int nsplit = (p.nblk + p.nper - 1) / p.nper;
+  dim3 grid((unsigned)((p.nrows + 127) / 128), (unsigned)nsplit);
   kern<<<grid, NTHREADS, smem, st>>>(p);
   KGP_LAUNCH("kmm_tc_kernel");
+  if (nsplit > 1) {
+    const int64_t cnt = p.nrows * p.k;
+    tc_reduce_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(p, nsplit, NOUT * p.kp);
+    KGP_LAUNCH("tc_reduce_kernel");
+  }
   return KGP_OK;
 }
 
@@ -521,6 +563,25 @@ int tc_nsa(int dpad, int nout, int split, int kp) {
   int nsa = (512 - tc_fixed_cols(dpad) - 2 * nout * kp) / stage;
   // a power of two >= 2: the two compute warp sets step through the ring by 2
   return nsa >= 4 ? 4 : 2;
+}
+
+// Column split factor that fills the last wave of 148 SMs (1 CTA/SM): the smallest
+// S <= 8 reaching 95% wave efficiency with >= 16 column blocks per CTA.
+int tc_col_split(int64_t nrows, int nblk) {
+  const int64_t rb = (nrows + 127) / 128;
+  int best = 1;
+  double best_eff = 0.0;
+  for (int sp = 1; sp <= 8; ++sp) {
+    if (sp > 1 && nblk / sp < 16) break;
+    const int64_t units = rb * sp;
+    const double eff = (double)units / (double)(((units + 147) / 148) * 148);
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = sp;
+    }
+    if (eff >= 0.95) break;
+  }
+  return best;
 }
 
 int launch_kmm_tc(int kt, int dpad, int nout, int split, const TcParams& p, cudaStream_t st) {
