@@ -40,7 +40,9 @@ def parse():
     ap.add_argument("--precision", default="fast", choices=["fast", "tf32", "fp64"])
     ap.add_argument("--n", type=int, default=65536)
     ap.add_argument("--k", type=int, default=32)
-    ap.add_argument("--cpu-rows", type=int, default=2048, help="rows in the bounded CPU-baseline sample")
+    ap.add_argument("--cpu-rows", type=int, default=8192,
+                    help="rows in the bounded CPU-baseline sample (~4 s of 16-core work at cfg2)")
+    ap.add_argument("--ref-rows", type=int, default=2048, help="rows per step of the --impl reference arm")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--skip-nlml", action="store_true")
     return ap.parse_args()
@@ -48,18 +50,49 @@ def parse():
 
 # ------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    """SM clock and throttle reasons sampled DURING the timed region: NVML every 5 ms when
+    available (the timed regions are tens of ms), else nvidia-smi every 200 ms."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits
+    REASONS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+               "hw_thermal_slowdown": 0x40}
 
     def __init__(self, gpu_index):
         self.gpu = gpu_index
         self.proc = None
         self.lines = []
+        self.nvml = None
+        self.stop = threading.Event()
+
+    def _nvml_loop(self, pynvml, h):
+        while not self.stop.is_set():
+            try:
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+                bits = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                flags = ["Active" if bits & b else "Not Active" for b in
+                         (self.REASONS["hw_slowdown"], self.REASONS["hw_thermal_slowdown"],
+                          self.REASONS["sw_thermal_slowdown"], self.REASONS["sw_power_cap"])]
+                self.lines.append(",".join([str(self.gpu), str(sm), str(mx), "", ""] + flags))
+            except Exception:
+                pass
+            time.sleep(0.005)
 
     def __enter__(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.nvml = pynvml
+            self.thread = threading.Thread(target=self._nvml_loop, args=(pynvml, h), daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
@@ -75,6 +108,9 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        if self.nvml is not None:
+            self.stop.set()
+            self.thread.join(timeout=2)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -132,7 +168,7 @@ def run_reference(args):
     vals = []
     times = []
     for _ in range(args.steps):
-        v, t, cores = cpu_baseline(w, args.cpu_rows)
+        v, t, cores = cpu_baseline(w, args.ref_rows)
         vals.append(v)
         times.append(t)
     value = float(np.median(vals))
@@ -144,7 +180,7 @@ def run_reference(args):
         "config": {"workload": "cfg2 standalone fused MatMul", "n": args.n, "d": 8, "k": args.k,
                    "kernel": "gaussian", "outputs": ["Khat.Z", "dKhat/dl.Z"]},
         "cpu_baseline": {"value": value, "unit": "entries*RHS/s", "cores": cores, "kind": "port",
-                         "sample": f"{args.cpu_rows} of {args.n} rows per step, both outputs, fp64; "
+                         "sample": f"{args.ref_rows} of {args.n} rows per step, both outputs, fp64; "
                                    "oracle/kgp_oracle.c (C restatement of kmat.py:165-189)"},
         "e2e": {"value": value, "unit": "entries*RHS/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

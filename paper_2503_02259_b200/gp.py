@@ -228,3 +228,41 @@ def predict(kt, x, y, xstar, params, mode: str = "exact", tol: float = solver.DE
     var = f2 - (cross * sol).sum(dim=0)
     stddev = torch.sqrt(torch.clamp(var, min=0.0))
     return Prediction(mean=_device.to_host(mean), stddev=_device.to_host(stddev))
+
+
+def predict_hutchinson(kt, x, y, xstar, params, tol: float = solver.DEFAULT_TOL,
+                       max_iter: int = solver.DEFAULT_MAX_ITER, precond_rank: int | None = None,
+                       num_probes: int = 64, seed=0, precision: str | None = None) -> Prediction:
+    """Large-scale prediction (BASELINE configs[4]): no n x m_test cross kernel is formed.
+
+    mean = f^2 kappa(X*, X) w with w = Khat^-1 y, one fused cross product (gp.py:241);
+    variance by Hutchinson's diagonal estimator instead of one solve per test point
+    (gp.py:242 needs all m_test columns):
+        diag(C^T Khat^-1 C) ~= (1/S) sum_s z_s o (C^T Khat^-1 C z_s),  C = f^2 kappa(X, X*),
+    with Rademacher z_s (m_test,), so each probe costs two fused cross products and one
+    column of a batched PCG solve. The estimate is unbiased; its spread shrinks as
+    1/sqrt(S). The reference has no estimator: this path is checked against
+    the exact variance statistically (tests/test_gpu_parity.py)."""
+    torch = _device.torch()
+    x = as_points(x, "X")
+    n = x.shape[0]
+    y = _check_y(y, n)
+    xstar = as_points(np.asarray(xstar, dtype=np.float64).reshape(-1, x.shape[1]), "Xstar")
+    m = xstar.shape[0]
+    f2 = params.f * params.f
+    engine = KernelEngine(kt, x, params, precision=precision)          # columns: training points
+    star = KernelEngine(kt, xstar, params, precision=precision)        # columns: test points
+    pre = precond_mod.build(engine, precond_rank)
+    xd, xsd = engine.x_device(), star.x_device()
+    rng = np.random.default_rng(seed)
+    zs = torch.from_numpy(rng.choice([-1.0, 1.0], size=(m, num_probes))).to(xd.device)
+    u = star.cross_matmul(xd, zs)                                       # C z      (n, S)
+    rhs = torch.cat([_device.to_device(y)[None, :], u.T], dim=0).contiguous()  # (1 + S, n)
+    parts = [solver.pcg_device(engine, pre, rhs[c0:c0 + 1024].contiguous(), tol, max_iter)[0]
+             for c0 in range(0, rhs.shape[0], 1024)]
+    sol = torch.cat(parts, dim=0)                                       # [w; Khat^-1 C z]
+    az = engine.cross_matmul(xsd, sol.T.contiguous())                   # C^T [w, Khat^-1 C z]
+    mean = az[:, 0]
+    diag = (zs * az[:, 1:]).mean(dim=1)
+    stddev = torch.sqrt(torch.clamp(f2 - diag, min=0.0))
+    return Prediction(mean=_device.to_host(mean), stddev=_device.to_host(stddev))

@@ -411,3 +411,28 @@ def test_row_partitioned_nlml_on_device(pkg, tmp_path):
     errfile = str(tmp_path / "err.txt")
     mp.spawn(_dist_gpu_worker, args=(2, port, errfile), nprocs=2, join=True)
     assert not os.path.exists(errfile), open(errfile).read()
+
+
+def test_predict_hutchinson_variance(pkg):
+    """configs[4]'s estimator (no reference oracle): the mean equals the exact posterior mean,
+    the Hutchinson variance is unbiased -- within 5 sigma of the exact diagonal, sigma from the
+    exact off-diagonal mass of C^T Khat^-1 C (Rademacher probes)."""
+    from oracle import kgp_oracle as orc
+    from paper_2503_02259_b200 import gp
+
+    rng = np.random.default_rng(12)
+    x = rng.uniform(0, 1, (400, 2))
+    y = np.sin(4 * np.pi * x[:, 0]) + np.cos(4 * np.pi * x[:, 1]) + 0.1 * rng.standard_normal(400)
+    xs = rng.uniform(0, 1, (30, 2))
+    hp = _hp(pkg, 0.1, 1.0, 1e-2)
+    S = 4096
+    got = gp.predict_hutchinson(pkg.KernelType.MATERN52, x, y, xs, hp, tol=1e-10, max_iter=3000,
+                                precond_rank=40, num_probes=S, seed=5)
+    mean, sd = orc.predict("matern52", x, y, xs, 0.1, 1.0, 1e-2)
+    np.testing.assert_allclose(got.mean, mean, rtol=1e-7, atol=1e-9)
+    c = orc.eval_kernel("matern52", x, xs, 0.1)
+    a = c.T @ np.linalg.solve(orc.khat_dense("matern52", x, 0.1, 1.0, 1e-2), c)
+    sigma = np.sqrt((a ** 2).sum(axis=1) - np.diag(a) ** 2) / np.sqrt(S)
+    var_got = got.stddev ** 2
+    var_ref = sd ** 2
+    assert np.all(np.abs(var_got - var_ref) <= 5 * sigma + 1e-9), (var_got - var_ref, sigma)
