@@ -4,6 +4,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <atomic>
 #include <mutex>
 #include <set>
 
@@ -28,9 +29,14 @@ int cuda_check(cudaError_t e, const char* what) {
   return KGP_ERR_CUDA;
 }
 
+static std::atomic<uint64_t> g_graph_epoch{1};
+uint64_t graph_epoch() { return g_graph_epoch.load(); }
+void bump_graph_epoch() { g_graph_epoch.fetch_add(1); }
+
 int DevBuf::ensure(size_t bytes) {
   if (bytes <= cap && p) return KGP_OK;
   release();
+  bump_graph_epoch();
   if (bytes == 0) bytes = 16;
   cudaError_t e = cudaMalloc(&p, bytes);
   if (e != cudaSuccess) {
@@ -45,12 +51,25 @@ int DevBuf::ensure(size_t bytes) {
 }
 
 void DevBuf::release() {
-  if (p) cudaFree(p);
+  if (p) {
+    cudaFree(p);
+    bump_graph_epoch();
+  }
   p = nullptr;
   cap = 0;
 }
 
 double tc_kernel_gamma(int kt, double l);
+
+static void engine_free_host_state(kgp_engine_s* e) {
+  if (e->hstatus) cudaFreeHost(e->hstatus);
+  if (e->hist_host) cudaFreeHost(e->hist_host);
+  for (auto& g : e->gcache)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  for (auto& ev : e->events)
+    if (ev) cudaEventDestroy(ev);
+  if (e->cstream) cudaStreamDestroy(e->cstream);
+}
 
 static int tc_env_int(const char* name, int dflt) {
   const char* s = getenv(name);
@@ -244,6 +263,9 @@ extern "C" int kgp_engine_create(kgp_engine** out, int device, int kernel, int p
   e->prepared = false;
   e->hstatus = nullptr;
   rc = cuda_check(cudaMallocHost(&e->hstatus, sizeof(int32_t) * 4), "pinned status");
+  for (int i = 0; i < PCG_LOOKAHEAD && !rc; ++i)
+    rc = cuda_check(cudaEventCreateWithFlags(&e->events[i], cudaEventDisableTiming), "event create");
+  if (!rc) rc = cuda_check(cudaStreamCreateWithFlags(&e->cstream, cudaStreamNonBlocking), "stream create");
   if (!rc) rc = e->x64.ensure(sizeof(double) * n * d);
   if (!rc) rc = e->mean.ensure(sizeof(double) * d);
   if (!rc)
@@ -253,7 +275,7 @@ extern "C" int kgp_engine_create(kgp_engine** out, int device, int kernel, int p
   if (!rc) rc = col_mean(n, d, e->x64.as<double>(), e->mean.as<double>(), st);
   if (!rc && !x_on_device) rc = cuda_check(cudaStreamSynchronize(st), "engine create");
   if (rc) {
-    if (e->hstatus) cudaFreeHost(e->hstatus);
+    engine_free_host_state(e);
     delete e;
     return rc;
   }
@@ -270,6 +292,7 @@ extern "C" int kgp_engine_set_params(kgp_engine* e, double l, double f, double s
   int rc = check_params(l, f, s);
   if (rc) return rc;
   if (l != e->l) e->prepared = false;
+  if (l != e->l || f != e->f || s != e->s) bump_graph_epoch();
   e->l = l;
   e->f = f;
   e->s = s;
@@ -282,6 +305,7 @@ extern "C" int kgp_engine_set_precision(kgp_engine* e, int precision) {
   KGP_REQUIRE(precision >= 0 && precision <= 2, KGP_ERR_INVALID, "unknown precision %d", precision);
   e->precision = precision;
   e->prepared = false;
+  bump_graph_epoch();
   return KGP_OK;
 }
 
@@ -292,6 +316,7 @@ extern "C" int kgp_engine_set_rows(kgp_engine* e, int64_t row0, int64_t nrows) {
   e->row0 = row0;
   e->nrows = nrows;
   e->prepared = false;
+  bump_graph_epoch();
   return KGP_OK;
 }
 
@@ -307,7 +332,7 @@ extern "C" int kgp_engine_destroy(kgp_engine* e) {
   cudaSetDevice(e->device);
   cudaDeviceSynchronize();
   e->magic = DEAD_MAGIC;
-  if (e->hstatus) cudaFreeHost(e->hstatus);
+  engine_free_host_state(e);
   delete e;
   return KGP_OK;
 }

@@ -78,6 +78,22 @@ struct DevBuf {
   T* as() const { return reinterpret_cast<T*>(p); }
 };
 
+// Incremented whenever any device buffer is (re)allocated or freed, or an engine's
+// parameters change: captured CUDA graphs record the epoch they were built at and are
+// re-captured when it moved (their kernel arguments hold raw pointers and parameters).
+uint64_t graph_epoch();
+void bump_graph_epoch();
+
+struct PcgGraph {
+  cudaGraphExec_t exec = nullptr;
+  int64_t k = 0;
+  const void* pc = nullptr;
+  double tol = 0.0;
+  int max_iter = 0;
+  uint64_t epoch = 0;
+};
+constexpr int PCG_LOOKAHEAD = 6;
+
 }  // namespace kgp
 
 // ------------------------------------------------------------------ opaque handles
@@ -97,7 +113,16 @@ struct kgp_engine_s {
   bool prepared;
   // PCG workspace (grown on demand) and a pinned status word for the per-iteration readback
   kgp::DevBuf ws;
+  kgp::DevBuf ws_nlml;     // NLML+gradient workspace
   int32_t* hstatus;
+  // captured PCG iteration graphs and their polling state (pcg.cu)
+  kgp::PcgGraph gcache[4];
+  int gnext = 0;
+  int32_t* hist_host = nullptr;  // mapped pinned (active, error) per iteration
+  int32_t* hist_dev = nullptr;
+  int hist_cap = 0;
+  cudaEvent_t events[kgp::PCG_LOOKAHEAD] = {};
+  cudaStream_t cstream = nullptr;  // private stream used only for graph capture (the caller's may be legacy)
 };
 
 struct kgp_precond_s {

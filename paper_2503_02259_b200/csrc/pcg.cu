@@ -119,32 +119,44 @@ __global__ void pcg_update_xr_kernel(int64_t n, int k, const int32_t* active, co
 }
 
 // beta step and freeze decision (solver.py:170-182)
+// One block (k <= 1024). Also publishes (active count, error code) of this iteration to
+// hist[2 * it], a host-mapped array the driver polls a few iterations behind the device.
 __global__ void pcg_beta_kernel(int k, int max_iter, double tol, bool precond, const double* rr, const double* rzn,
                                 double* rz, const double* ynorm, int32_t* active, int32_t* iters, double* beta,
-                                double* betas, double* rel, int32_t* status) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
+                                double* betas, double* rel, int32_t* status, int32_t* it_counter,
+                                volatile int32_t* hist) {
+  int c = threadIdx.x;
   if (c == 0) status[0] = 0;
   __syncthreads();
-  if (c >= k || !active[c]) return;
-  double v = rr[c];
-  if (!isfinite(v)) {
-    atomicMin(&status[2], c);
-    status[1] = KGP_ERR_NUMERICAL;
-    return;
+  if (c < k && active[c]) {
+    double v = rr[c];
+    if (!isfinite(v)) {
+      atomicMin(&status[2], c);
+      status[1] = KGP_ERR_NUMERICAL;
+    } else {
+      double rn = precond ? rzn[c] : v;
+      double b = rn / rz[c];
+      int it = iters[c];
+      betas[(int64_t)c * max_iter + it] = b;
+      iters[c] = it + 1;
+      rz[c] = rn;
+      double rl = sqrt(v) / ynorm[c];
+      rel[c] = rl;
+      beta[c] = b;
+      if (rl <= tol) {
+        active[c] = 0;
+      } else {
+        atomicAdd(&status[0], 1);
+      }
+    }
   }
-  double rn = precond ? rzn[c] : v;
-  double b = rn / rz[c];
-  int it = iters[c];
-  betas[(int64_t)c * max_iter + it] = b;
-  iters[c] = it + 1;
-  rz[c] = rn;
-  double rl = sqrt(v) / ynorm[c];
-  rel[c] = rl;
-  beta[c] = b;
-  if (rl <= tol) {
-    active[c] = 0;
-  } else {
-    atomicAdd(&status[0], 1);
+  __syncthreads();
+  if (c == 0) {
+    __threadfence();
+    const int it = *it_counter;
+    hist[2 * it] = status[0];
+    hist[2 * it + 1] = status[1];
+    *it_counter = it + 1;
   }
 }
 
@@ -271,26 +283,138 @@ int col_dots(int64_t k, int64_t n, const double* a, const double* b, double* out
   return KGP_OK;
 }
 
+// Device PCG state lives in the engine's workspace (not in the caller's buffers) so one
+// captured CUDA graph of the iteration body can be replayed across calls. The body is
+// captured once per (k, preconditioner, tol, max_iter) and launched with a look-ahead of
+// kLookahead iterations: the host polls the per-iteration (active, error) history that
+// pcg_beta_kernel writes into mapped host memory instead of synchronising every
+// iteration. Iterations issued after convergence are no-ops (every update is masked by
+// the per-column active flag), so results equal the synchronous loop's.
+namespace {
+constexpr int kLookahead = PCG_LOOKAHEAD;
+
+struct PcgBuffers {
+  PcgState S;
+  double *x, *alphas, *betas, *rel;
+  int32_t *iters, *it_counter;
+};
+
+int enqueue_iteration(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, double tol, int max_iter, const PcgBuffers& B,
+                      cudaStream_t st) {
+  const int64_t n = e->n;
+  const PcgState& S = B.S;
+  const unsigned kb = (unsigned)((k + 127) / 128);
+  dim3 vgrid((unsigned)((n + 255) / 256 < 64 ? (n + 255) / 256 : 64), (unsigned)k);
+  int rc = engine_matmul_impl(e, k, S.p, 1, n, S.ap, nullptr, nullptr, 1, n, st);
+  if (rc) return rc;
+  rc = col_dots(k, n, S.p, S.ap, S.dots1, S.partial, st);
+  if (rc) return rc;
+  pcg_alpha_kernel<<<kb, 128, 0, st>>>((int)k, max_iter, S.dots1, S.rz, S.active, B.iters, S.alpha, B.alphas,
+                                        S.status, S.err_val);
+  KGP_LAUNCH("pcg_alpha_kernel");
+  pcg_update_xr_kernel<<<vgrid, 256, 0, st>>>(n, (int)k, S.active, S.alpha, S.p, S.ap, B.x, S.r);
+  KGP_LAUNCH("pcg_update_xr_kernel");
+  if (pc) {
+    rc = precond_apply_impl(pc, k, S.r, 1, n, S.z, 1, n, st);
+    if (rc) return rc;
+    rc = col_dots(k, n, S.r, S.z, S.dots2, S.partial, st);
+    if (rc) return rc;
+  }
+  rc = col_dots(k, n, S.r, S.r, S.dots1, S.partial, st);
+  if (rc) return rc;
+  pcg_beta_kernel<<<1, 1024, 0, st>>>((int)k, max_iter, tol, pc != nullptr, S.dots1, S.dots2, S.rz, S.ynorm,
+                                      S.active, B.iters, S.beta, B.betas, B.rel, S.status, B.it_counter,
+                                      e->hist_dev);
+  KGP_LAUNCH("pcg_beta_kernel");
+  pcg_update_p_kernel<<<vgrid, 256, 0, st>>>(n, (int)k, S.active, S.beta, S.z, S.p);
+  KGP_LAUNCH("pcg_update_p_kernel");
+  return KGP_OK;
+}
+
+// returns the graph for this configuration, capturing it on first use
+int pcg_graph(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, double tol, int max_iter, const PcgBuffers& B,
+              cudaStream_t st, cudaGraphExec_t* out) {
+  for (auto& g : e->gcache)
+    if (g.exec && g.k == k && g.pc == pc && g.tol == tol && g.max_iter == max_iter && g.epoch == graph_epoch()) {
+      *out = g.exec;
+      return KGP_OK;
+    }
+  // captured on the engine's private stream (the legacy default stream cannot be captured);
+  // nothing is executed during capture, so no ordering with the caller's stream is needed
+  (void)st;
+  cudaGraph_t graph = nullptr;
+  KGP_CUDA(cudaStreamBeginCapture(e->cstream, cudaStreamCaptureModeThreadLocal));
+  int rc = enqueue_iteration(e, pc, k, tol, max_iter, B, e->cstream);
+  cudaError_t ce = cudaStreamEndCapture(e->cstream, &graph);
+  if (rc) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  KGP_CUDA(ce);
+  cudaGraphExec_t exec = nullptr;
+  ce = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  KGP_CUDA(ce);
+  auto& slot = e->gcache[e->gnext];
+  e->gnext = (e->gnext + 1) % (int)(sizeof(e->gcache) / sizeof(e->gcache[0]));
+  if (slot.exec) cudaGraphExecDestroy(slot.exec);
+  slot.exec = exec;
+  slot.k = k;
+  slot.pc = pc;
+  slot.tol = tol;
+  slot.max_iter = max_iter;
+  slot.epoch = graph_epoch();
+  *out = exec;
+  return KGP_OK;
+}
+
+int status_error(const PcgState& S, int code, int32_t col) {
+  if (code == KGP_ERR_BREAKDOWN) {
+    double v = 0.0;
+    cudaMemcpy(&v, S.err_val, sizeof(double), cudaMemcpyDeviceToHost);
+    set_error(KGP_ERR_BREAKDOWN, "p^T A p = %.17g in column %d; operator is not SPD", v, col);
+    return KGP_ERR_BREAKDOWN;
+  }
+  set_error(KGP_ERR_NUMERICAL, "residual became non-finite during PCG");
+  return KGP_ERR_NUMERICAL;
+}
+}  // namespace
+
 int pcg_solve_impl(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, const double* y, double tol, int max_iter,
                    double* x_out, double* alphas, double* betas, int32_t* iters, double* rel, int32_t* conv,
                    cudaStream_t st) {
   const int64_t n = e->n;
   const int nb = (int)((n + DOT_CHUNK - 1) / DOT_CHUNK);
-  // workspace: r, z (if preconditioned), p, ap : (k, n); scalars
-  size_t vec = (size_t)k * n;
-  size_t bytes = sizeof(double) * (vec * (pc ? 4 : 3) + (size_t)k * (8 + nb) + 8) + sizeof(int32_t) * (k + 8);
   KGP_REQUIRE(k <= 1024, KGP_ERR_INVALID, "pcg supports at most 1024 right-hand sides per call, got %lld",
               (long long)k);
+  // engine-owned state: r, p, ap, [z], x : (k, n); coefficient arrays; scalars
+  const size_t vec = (size_t)k * n;
+  const size_t coef = (size_t)k * max_iter;
+  size_t bytes = sizeof(double) * (vec * (pc ? 5 : 4) + 2 * coef + (size_t)k * (9 + nb) + 8) +
+                 sizeof(int32_t) * (2 * k + 16);
   int rc = e->ws.ensure(bytes);
   if (rc) return rc;
+  if (e->hist_cap < max_iter + 1) {  // mapped host history: 2 ints per iteration
+    if (e->hist_host) cudaFreeHost(e->hist_host);
+    e->hist_host = nullptr;
+    KGP_CUDA(cudaHostAlloc(&e->hist_host, sizeof(int32_t) * 2 * (max_iter + 1), cudaHostAllocMapped));
+    KGP_CUDA(cudaHostGetDevicePointer((void**)&e->hist_dev, e->hist_host, 0));
+    e->hist_cap = max_iter + 1;
+    bump_graph_epoch();
+  }
   double* base = e->ws.as<double>();
-  PcgState S{};
-  S.x = x_out;
+  PcgBuffers B{};
+  PcgState& S = B.S;
   S.r = base;
   S.p = S.r + vec;
   S.ap = S.p + vec;
-  S.z = pc ? S.ap + vec : S.r;  // unpreconditioned: z aliases r (solver.py:195-199)
-  double* sc = (pc ? S.z : S.ap) + vec;
+  B.x = S.ap + vec;
+  S.x = B.x;
+  S.z = pc ? B.x + vec : S.r;  // unpreconditioned: z aliases r (solver.py:195-199)
+  double* sc = (pc ? S.z : B.x) + vec;
+  B.alphas = sc;
+  B.betas = sc + coef;
+  sc += 2 * coef;
   S.rz = sc;
   S.ynorm = sc + k;
   S.alpha = sc + 2 * k;
@@ -298,23 +422,24 @@ int pcg_solve_impl(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, const double* 
   S.dots1 = sc + 4 * k;
   S.dots2 = sc + 5 * k;
   S.err_val = sc + 6 * k;
-  S.partial = sc + 7 * k;
+  B.rel = sc + 7 * k;
+  S.partial = sc + 8 * k;
   S.active = reinterpret_cast<int32_t*>(S.partial + (size_t)k * nb + 8);
-  S.status = S.active + k;
+  S.status = S.active + k;  // 4 ints
+  B.iters = S.status + 4;
+  B.it_counter = B.iters + k;
 
   int32_t* hstatus = e->hstatus;
-
   const unsigned kb = (unsigned)((k + 127) / 128);
-  dim3 vgrid((unsigned)((n + 255) / 256 < 64 ? (n + 255) / 256 : 64), (unsigned)k);
 
-  KGP_CUDA(cudaMemsetAsync(x_out, 0, sizeof(double) * vec, st));
+  KGP_CUDA(cudaMemsetAsync(B.x, 0, sizeof(double) * vec, st));
   KGP_CUDA(cudaMemcpyAsync(S.r, y, sizeof(double) * vec, cudaMemcpyDeviceToDevice, st));
   KGP_CUDA(cudaMemsetAsync(S.status, 0, sizeof(int32_t) * 4, st));
-  KGP_CUDA(cudaMemsetAsync(alphas, 0, sizeof(double) * k * max_iter, st));
-  KGP_CUDA(cudaMemsetAsync(betas, 0, sizeof(double) * k * max_iter, st));
+  KGP_CUDA(cudaMemsetAsync(B.it_counter, 0, sizeof(int32_t), st));
+  KGP_CUDA(cudaMemsetAsync(B.alphas, 0, sizeof(double) * 2 * coef, st));
   rc = col_dots(k, n, S.r, S.r, S.dots1, S.partial, st);
   if (rc) return rc;
-  pcg_init_kernel<<<kb, 128, 0, st>>>((int)k, tol, S.dots1, S.ynorm, rel, S.active, iters, S.status);
+  pcg_init_kernel<<<kb, 128, 0, st>>>((int)k, tol, S.dots1, S.ynorm, B.rel, S.active, B.iters, S.status);
   KGP_LAUNCH("pcg_init_kernel");
   rc = read_status(S.status, hstatus, st);
   if (rc) return rc;
@@ -326,53 +451,57 @@ int pcg_solve_impl(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, const double* 
     KGP_CUDA(cudaMemcpyAsync(S.p, S.z, sizeof(double) * vec, cudaMemcpyDeviceToDevice, st));
     rc = col_dots(k, n, S.r, S.z, S.rz, S.partial, st);
     if (rc) return rc;
-    for (int it = 0; it < max_iter; ++it) {
-      rc = engine_matmul_impl(e, k, S.p, 1, n, S.ap, nullptr, nullptr, 1, n, st);
+    // iteration 0 uncaptured: it also performs every lazy allocation / first-launch setup
+    rc = enqueue_iteration(e, pc, k, tol, max_iter, B, st);
+    if (rc) return rc;
+    KGP_CUDA(cudaStreamSynchronize(st));
+    volatile int32_t* H = e->hist_host;
+    if (H[1]) return status_error(S, H[1], 0);
+    bool done = (H[0] == 0);
+    if (!done && max_iter > 1) {
+      cudaGraphExec_t exec = nullptr;
+      rc = pcg_graph(e, pc, k, tol, max_iter, B, st, &exec);
       if (rc) return rc;
-      rc = col_dots(k, n, S.p, S.ap, S.dots1, S.partial, st);
-      if (rc) return rc;
-      pcg_alpha_kernel<<<kb, 128, 0, st>>>((int)k, max_iter, S.dots1, S.rz, S.active, iters, S.alpha, alphas,
-                                            S.status, S.err_val);
-      KGP_LAUNCH("pcg_alpha_kernel");
-      pcg_update_xr_kernel<<<vgrid, 256, 0, st>>>(n, (int)k, S.active, S.alpha, S.p, S.ap, x_out, S.r);
-      KGP_LAUNCH("pcg_update_xr_kernel");
-      if (pc) {
-        rc = precond_apply_impl(pc, k, S.r, 1, n, S.z, 1, n, st);
-        if (rc) return rc;
-        rc = col_dots(k, n, S.r, S.z, S.dots2, S.partial, st);
-        if (rc) return rc;
+      int launched = 1, checked = 1;
+      while (launched < max_iter && !done) {
+        KGP_CUDA(cudaGraphLaunch(exec, st));
+        KGP_CUDA(cudaEventRecord(e->events[launched % kLookahead], st));
+        ++launched;
+        if (launched - checked >= kLookahead) {
+          KGP_CUDA(cudaEventSynchronize(e->events[checked % kLookahead]));
+          if (H[2 * checked + 1]) {
+            KGP_CUDA(cudaStreamSynchronize(st));
+            KGP_CUDA(cudaMemcpy(hstatus, S.status, sizeof(int32_t) * 4, cudaMemcpyDeviceToHost));
+            return status_error(S, H[2 * checked + 1], hstatus[2]);
+          }
+          done = (H[2 * checked] == 0);
+          ++checked;
+        }
       }
-      rc = col_dots(k, n, S.r, S.r, S.dots1, S.partial, st);
-      if (rc) return rc;
-      pcg_beta_kernel<<<1, 1024, 0, st>>>((int)k, max_iter, tol, pc != nullptr, S.dots1, S.dots2, S.rz, S.ynorm,
-                                          S.active, iters, S.beta, betas, rel, S.status);
-      KGP_LAUNCH("pcg_beta_kernel");
-      pcg_update_p_kernel<<<vgrid, 256, 0, st>>>(n, (int)k, S.active, S.beta, S.z, S.p);
-      KGP_LAUNCH("pcg_update_p_kernel");
-      rc = read_status(S.status, hstatus, st);
-      if (rc) return rc;
-      if (hstatus[1] == KGP_ERR_BREAKDOWN) {
-        double v = 0.0;
-        cudaMemcpy(&v, S.err_val, sizeof(double), cudaMemcpyDeviceToHost);
-        set_error(KGP_ERR_BREAKDOWN, "p^T A p = %.17g in column %d; operator is not SPD", v, hstatus[2]);
-        return KGP_ERR_BREAKDOWN;
+      KGP_CUDA(cudaStreamSynchronize(st));
+      for (; checked < launched; ++checked) {
+        if (H[2 * checked + 1]) {
+          KGP_CUDA(cudaMemcpy(hstatus, S.status, sizeof(int32_t) * 4, cudaMemcpyDeviceToHost));
+          return status_error(S, H[2 * checked + 1], hstatus[2]);
+        }
+        if (H[2 * checked] == 0) break;
       }
-      if (hstatus[1] == KGP_ERR_NUMERICAL) {
-        set_error(KGP_ERR_NUMERICAL, "residual became non-finite during PCG");
-        return KGP_ERR_NUMERICAL;
-      }
-      if (hstatus[0] == 0) break;
     }
   }
-  pcg_finish_kernel<<<kb, 128, 0, st>>>((int)k, tol, rel, conv);
+  pcg_finish_kernel<<<kb, 128, 0, st>>>((int)k, tol, B.rel, conv);
   KGP_LAUNCH("pcg_finish_kernel");
+  KGP_CUDA(cudaMemcpyAsync(x_out, B.x, sizeof(double) * vec, cudaMemcpyDeviceToDevice, st));
+  KGP_CUDA(cudaMemcpyAsync(alphas, B.alphas, sizeof(double) * coef, cudaMemcpyDeviceToDevice, st));
+  KGP_CUDA(cudaMemcpyAsync(betas, B.betas, sizeof(double) * coef, cudaMemcpyDeviceToDevice, st));
+  KGP_CUDA(cudaMemcpyAsync(iters, B.iters, sizeof(int32_t) * k, cudaMemcpyDeviceToDevice, st));
+  KGP_CUDA(cudaMemcpyAsync(rel, B.rel, sizeof(double) * k, cudaMemcpyDeviceToDevice, st));
   KGP_CUDA(cudaStreamSynchronize(st));
   return KGP_OK;
 }
 
 int slq_impl(int64_t k, int max_iter, const double* alphas, const double* betas, const int32_t* iters,
              const double* norms_sq, double* logdet, cudaStream_t st) {
-  DevBuf ws;
+  static thread_local DevBuf ws;  // persistent: cudaMalloc/cudaFree per call would serialise the device
   int rc = ws.ensure(sizeof(double) * ((size_t)k * 3 * max_iter + k) + 64);
   if (rc) return rc;
   double* scratch = ws.as<double>();
@@ -423,7 +552,7 @@ extern "C" int kgp_nlml_grad(kgp_engine* e, kgp_precond* p, const double* y, int
   size_t vec = (size_t)kv * n;
   size_t bytes = sizeof(double) * (4 * vec + 2 * (size_t)kv * wide + 4 * kv + (size_t)kv * nb + 16) +
                  sizeof(int32_t) * (4 * kv + 8);
-  DevBuf ws;
+  DevBuf& ws = e->ws_nlml;  // persistent per engine (a training loop reuses it every step)
   int rc = ws.ensure(bytes);
   if (rc) return rc;
   double* V = ws.as<double>();
