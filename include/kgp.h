@@ -142,6 +142,16 @@ int kgp_nlml_grad(kgp_engine* e, kgp_precond* p, const double* y, int64_t k_z, c
                   double tol, int32_t max_iter, double probe_tol, int32_t probe_max_iter, double* out,
                   int32_t* out_converged, void* stream);
 
+/* ------------------------------------------------------------------ instrumentation (bench.py; no reference counterpart)
+ * kgp_launch_count: kernels this library has launched in this process (graph replays
+ * counted per kernel node). kgp_engine_set_timing(e, 1) brackets every launch of the
+ * tensor-core operator kernel with CUDA events on its stream; kgp_engine_kernel_time
+ * synchronises, returns the summed kernel time (ms) and the bracketed launch count
+ * since the previous read, and resets them. */
+int64_t kgp_launch_count(void);
+int kgp_engine_set_timing(kgp_engine* e, int enable);
+int kgp_engine_kernel_time(kgp_engine* e, double* ms, int64_t* launches);
+
 #ifdef __cplusplus
 }
 #endif

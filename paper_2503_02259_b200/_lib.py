@@ -65,9 +65,11 @@ _SIGNATURES = {
     "kgp_pcg": [c_vp, c_vp, c_i64, c_vp, c_dbl, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
     "kgp_slq_logdet": [c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, _P(c_dbl), c_vp],
     "kgp_nlml_grad": [c_vp, c_vp, c_vp, c_i64, c_vp, c_dbl, c_i32, c_dbl, c_i32, _P(c_dbl), _P(c_i32), c_vp],
+    "kgp_engine_set_timing": [c_vp, ctypes.c_int],
+    "kgp_engine_kernel_time": [c_vp, _P(c_dbl), _P(c_i64)],
 }
 
-EXPORTED = tuple(_SIGNATURES) + ("kgp_last_error",)
+EXPORTED = tuple(_SIGNATURES) + ("kgp_last_error", "kgp_launch_count")
 
 
 def load():
@@ -88,8 +90,23 @@ def load():
                 fn.restype = ctypes.c_int
             lib.kgp_last_error.argtypes = []
             lib.kgp_last_error.restype = ctypes.c_char_p
+            lib.kgp_launch_count.argtypes = []
+            lib.kgp_launch_count.restype = ctypes.c_int64
             _lib = lib
     return _lib
+
+
+def launch_count() -> int:
+    """Kernels libkgp has launched in this process (graph replays counted per kernel node)."""
+    return int(load().kgp_launch_count())
+
+
+def kernel_time(handle) -> tuple:
+    """(total ms, launches) of the tensor-core operator kernel since the last read
+    (requires kgp_engine_set_timing(handle, 1))."""
+    ms, n = ctypes.c_double(), ctypes.c_int64()
+    call("kgp_engine_kernel_time", handle, ctypes.byref(ms), ctypes.byref(n))
+    return ms.value, n.value
 
 
 def last_error() -> str:

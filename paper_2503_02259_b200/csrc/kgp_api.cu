@@ -29,6 +29,9 @@ int cuda_check(cudaError_t e, const char* what) {
   return KGP_ERR_CUDA;
 }
 
+static std::atomic<int64_t> g_launches{0};
+void count_launches(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
 static std::atomic<uint64_t> g_graph_epoch{1};
 uint64_t graph_epoch() { return g_graph_epoch.load(); }
 void bump_graph_epoch() { g_graph_epoch.fetch_add(1); }
@@ -69,6 +72,7 @@ static void engine_free_host_state(kgp_engine_s* e) {
   for (auto& ev : e->events)
     if (ev) cudaEventDestroy(ev);
   if (e->cstream) cudaStreamDestroy(e->cstream);
+  for (auto ev : e->tev) cudaEventDestroy(ev);
 }
 
 static int tc_env_int(const char* name, int dflt) {
@@ -166,6 +170,18 @@ static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t 
     p.out_df = out_df ? out_df + c0 * o_cs : nullptr;
     p.o_rs = o_rs;
     p.o_cs = o_cs;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (e->timing && cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusNone) {
+      if (e->tev_used + 2 > e->tev.size()) {
+        for (int i = 0; i < 2; ++i) {
+          cudaEvent_t ev;
+          KGP_CUDA(cudaEventCreate(&ev));
+          e->tev.push_back(ev);
+        }
+      }
+      p.ev_start = e->tev[e->tev_used++];
+      p.ev_stop = e->tev[e->tev_used++];
+    }
     rc = launch_kmm_tc(e->kt, e->dpad, nout, split, p, st);
     if (rc) return rc;
   }
@@ -218,6 +234,31 @@ using namespace kgp;
               "invalid or destroyed preconditioner handle")
 
 extern "C" int kgp_version(void) { return KGP_ABI_VERSION; }
+
+extern "C" int64_t kgp_launch_count(void) { return g_launches.load(); }
+
+extern "C" int kgp_engine_set_timing(kgp_engine* e, int enable) {
+  CHECK_ENGINE(e);
+  e->timing = enable != 0;
+  e->tev_used = 0;
+  return KGP_OK;
+}
+
+extern "C" int kgp_engine_kernel_time(kgp_engine* e, double* ms, int64_t* launches) {
+  CHECK_ENGINE(e);
+  KGP_REQUIRE(ms != nullptr && launches != nullptr, KGP_ERR_INVALID, "output pointer is NULL");
+  double total = 0.0;
+  for (size_t i = 0; i + 1 < e->tev_used; i += 2) {
+    KGP_CUDA(cudaEventSynchronize(e->tev[i + 1]));
+    float t = 0.f;
+    KGP_CUDA(cudaEventElapsedTime(&t, e->tev[i], e->tev[i + 1]));
+    total += t;
+  }
+  *ms = total;
+  *launches = (int64_t)(e->tev_used / 2);
+  e->tev_used = 0;
+  return KGP_OK;
+}
 
 extern "C" const char* kgp_last_error(void) { return g_err_msg; }
 

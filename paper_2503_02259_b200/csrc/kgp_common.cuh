@@ -12,6 +12,7 @@ namespace kgp {
 // ---------------------------------------------------------------- error plumbing
 void set_error(int code, const char* fmt, ...);
 int cuda_check(cudaError_t e, const char* what);
+void count_launches(int64_t n);
 #define KGP_CUDA(call)                                         \
   do {                                                         \
     int _rc = ::kgp::cuda_check((call), #call);                \
@@ -19,6 +20,7 @@ int cuda_check(cudaError_t e, const char* what);
   } while (0)
 #define KGP_LAUNCH(what)                                       \
   do {                                                         \
+    ::kgp::count_launches(1);                                  \
     int _rc = ::kgp::cuda_check(cudaGetLastError(), what);     \
     if (_rc != KGP_OK) return _rc;                             \
   } while (0)

@@ -30,6 +30,7 @@ struct TcParams {
   int64_t diag_row0;      // global row of local row 0 for the shift; < 0: no shift
   double *out_k, *out_dl, *out_df;
   int64_t o_rs, o_cs;
+  cudaEvent_t ev_start, ev_stop;  // host side: optional timing bracket around the main kernel
 };
 int tc_pad_dim(int d);
 int tc_max_kp(int dpad, int nout, int split);
@@ -81,6 +82,7 @@ struct DevBuf {
 // Incremented whenever any device buffer is (re)allocated or freed, or an engine's
 // parameters change: captured CUDA graphs record the epoch they were built at and are
 // re-captured when it moved (their kernel arguments hold raw pointers and parameters).
+void count_launches(int64_t n);
 uint64_t graph_epoch();
 void bump_graph_epoch();
 
@@ -91,6 +93,7 @@ struct PcgGraph {
   double tol = 0.0;
   int max_iter = 0;
   uint64_t epoch = 0;
+  int64_t kernels = 0;  // kernel nodes per replay (launch accounting)
 };
 constexpr int PCG_LOOKAHEAD = 6;
 
@@ -123,6 +126,10 @@ struct kgp_engine_s {
   int hist_cap = 0;
   cudaEvent_t events[kgp::PCG_LOOKAHEAD] = {};
   cudaStream_t cstream = nullptr;  // private stream used only for graph capture (the caller's may be legacy)
+  // optional main-kernel timing (kgp_engine_set_timing)
+  bool timing = false;
+  std::vector<cudaEvent_t> tev;  // start/stop pairs
+  size_t tev_used = 0;
 };
 
 struct kgp_precond_s {

@@ -505,8 +505,10 @@ int launch_one(const TcParams& p_in, cudaStream_t st) {
   }
   const int nsplit = (p.nblk + p.nper - 1) / p.nper;
   dim3 grid((unsigned)((p.nrows + 127) / 128), (unsigned)nsplit);
+  if (p.ev_start) KGP_CUDA(cudaEventRecord(p.ev_start, st));
   kern<<<grid, NTHREADS, smem, st>>>(p);
   KGP_LAUNCH("kmm_tc_kernel");
+  if (p.ev_stop) KGP_CUDA(cudaEventRecord(p.ev_stop, st));
   if (nsplit > 1) {
     const int64_t cnt = p.nrows * p.k;
     tc_reduce_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(p, nsplit, NOUT * p.kp);

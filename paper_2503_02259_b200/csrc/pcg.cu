@@ -333,24 +333,36 @@ int enqueue_iteration(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, double tol,
 
 // returns the graph for this configuration, capturing it on first use
 int pcg_graph(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, double tol, int max_iter, const PcgBuffers& B,
-              cudaStream_t st, cudaGraphExec_t* out) {
+              cudaStream_t st, cudaGraphExec_t* out, int64_t* kernels) {
   for (auto& g : e->gcache)
     if (g.exec && g.k == k && g.pc == pc && g.tol == tol && g.max_iter == max_iter && g.epoch == graph_epoch()) {
       *out = g.exec;
+      *kernels = g.kernels;
       return KGP_OK;
     }
   // captured on the engine's private stream (the legacy default stream cannot be captured);
   // nothing is executed during capture, so no ordering with the caller's stream is needed
   (void)st;
   cudaGraph_t graph = nullptr;
+  const int64_t counted = kgp_launch_count();
   KGP_CUDA(cudaStreamBeginCapture(e->cstream, cudaStreamCaptureModeThreadLocal));
   int rc = enqueue_iteration(e, pc, k, tol, max_iter, B, e->cstream);
   cudaError_t ce = cudaStreamEndCapture(e->cstream, &graph);
+  count_launches(counted - kgp_launch_count());  // captured, not launched
   if (rc) {
     if (graph) cudaGraphDestroy(graph);
     return rc;
   }
   KGP_CUDA(ce);
+  size_t nodes = 0;
+  cudaGraphGetNodes(graph, nullptr, &nodes);
+  std::vector<cudaGraphNode_t> all(nodes);
+  int64_t nkern = 0;
+  if (nodes && cudaGraphGetNodes(graph, all.data(), &nodes) == cudaSuccess)
+    for (auto nd : all) {
+      cudaGraphNodeType t;
+      if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++nkern;
+    }
   cudaGraphExec_t exec = nullptr;
   ce = cudaGraphInstantiate(&exec, graph, 0);
   cudaGraphDestroy(graph);
@@ -364,7 +376,9 @@ int pcg_graph(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, double tol, int max
   slot.tol = tol;
   slot.max_iter = max_iter;
   slot.epoch = graph_epoch();
+  slot.kernels = nkern;
   *out = exec;
+  *kernels = slot.kernels;
   return KGP_OK;
 }
 
@@ -460,11 +474,13 @@ int pcg_solve_impl(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, const double* 
     bool done = (H[0] == 0);
     if (!done && max_iter > 1) {
       cudaGraphExec_t exec = nullptr;
-      rc = pcg_graph(e, pc, k, tol, max_iter, B, st, &exec);
+      int64_t gk = 0;
+      rc = pcg_graph(e, pc, k, tol, max_iter, B, st, &exec, &gk);
       if (rc) return rc;
       int launched = 1, checked = 1;
       while (launched < max_iter && !done) {
         KGP_CUDA(cudaGraphLaunch(exec, st));
+        count_launches(gk);
         KGP_CUDA(cudaEventRecord(e->events[launched % kLookahead], st));
         ++launched;
         if (launched - checked >= kLookahead) {

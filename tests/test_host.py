@@ -15,7 +15,7 @@ def test_library_loads_and_exports_every_header_symbol():
 
     lib = _lib.load()
     header = open(os.path.join(REPO, "include", "kgp.h")).read()
-    declared = set(re.findall(r"^\s*(?:int|const char\*)\s+(kgp_\w+)\s*\(", header, re.M))
+    declared = set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(kgp_\w+)\s*\(", header, re.M))
     assert declared, "no declarations parsed"
     for name in declared:
         assert hasattr(lib, name), name
