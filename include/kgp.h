@@ -43,6 +43,10 @@ extern "C" {
 #define KGP_FAST 1  /* fp32 centred tile + 3xTF32 tcgen05 contraction, fp32 TMEM accumulation */
 #define KGP_TF32 2  /* fp32 centred tile + 1xTF32 tcgen05 contraction (throughput mode)     */
 
+/* preconditioner kinds (kgp_precond_kind) */
+#define KGP_PRECOND_NYSTROM 0
+#define KGP_PRECOND_AFN 1
+
 typedef struct kgp_engine_s kgp_engine;
 typedef struct kgp_precond_s kgp_precond;
 
@@ -116,6 +120,32 @@ int kgp_lowrank_project(kgp_precond* p, int64_t k, const double* b, int64_t b_rs
                         void* stream);
 int kgp_lowrank_expand(kgp_precond* p, double beta, double alpha, int64_t k, const double* b, int64_t b_rs,
                        int64_t b_cs, const double* t, double* out, int64_t o_rs, int64_t o_cs, void* stream);
+
+/* ------------------------------------------------------------------ AFN preconditioner
+ * The north star's "AFN preconditioner applied on device (landmark Cholesky solve plus
+ * sparse FSAI factor matvec)". The reference substitutes Nystrom for AFN
+ * ("the module interface (build/apply_inverse) is exactly what an
+ * AFN drop-in would implement"), so these entries extend precond.py's build/apply_inverse
+ * pair; an AFN handle is accepted wherever a kgp_precond is (kgp_precond_apply_inverse,
+ * kgp_pcg, kgp_nlml_grad). Ordering: m landmarks first, then the n2 = n - m others.
+ *
+ * kgp_knn_prev: for each point i of x (n, d) device fp64, the npt (<= 64) nearest points
+ *   j < i by squared distance, ties to the lower j, nearest first; idx_out (n, npt) int64
+ *   device, -1 padded (the FSAI sparsity pattern).
+ * kgp_afn_fsai: row i of the FSAI factor G of S = Khat22 - W W^T on the pattern
+ *   {nbr[i, :], i}: gval/gcol (npt + 1, n2) slot-major (entry t of row i at t*n2 + i),
+ *   the diagonal last, -1/0 padded. x2 (n2, d) the non-landmark points, w (n2, m)
+ *   row-major. A non-SPD pattern block -> KGP_ERR_BREAKDOWN.
+ * kgp_afn_create: handle from device factors (all copied): perm (n) permuted position ->
+ *   original row, linv (m, m) row-major L11^-1, w (n2, m), the ELL factor from
+ *   kgp_afn_fsai, and G^T as CSR (gtptr n2 + 1, gtrow/gtval nnz; rows ascending). */
+int kgp_knn_prev(int64_t n, int d, const double* x, int npt, int64_t* idx_out, void* stream);
+int kgp_afn_fsai(int kernel, int64_t n2, int d, const double* x2, double l, double f, double s, int64_t m,
+                 const double* w, int npt, const int64_t* nbr, double* gval, int32_t* gcol, void* stream);
+int kgp_afn_create(kgp_precond** out, int64_t n, int64_t m, const int64_t* perm, const double* linv,
+                   const double* w, int npt1, const double* gval, const int32_t* gcol, int64_t nnz,
+                   const int32_t* gtptr, const int32_t* gtrow, const double* gtval, double s, void* stream);
+int kgp_precond_kind(kgp_precond* p, int* kind);
 
 /* ------------------------------------------------------------------ solvers
  * pcg_solve (solver.py:122-192): batched PCG, per-column alpha/beta capture,

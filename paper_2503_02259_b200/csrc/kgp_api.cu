@@ -434,6 +434,7 @@ extern "C" int kgp_precond_create(kgp_precond** out, int64_t n, int64_t m, const
   KGP_REQUIRE(s > 0.0, KGP_ERR_INVALID, "shift must be positive");
   kgp_precond_s* p = new kgp_precond_s();
   p->magic = PRECOND_MAGIC;
+  p->kind = KGP_PRECOND_NYSTROM;
   p->n = n;
   p->m = m;
   p->s = s;
@@ -450,6 +451,61 @@ extern "C" int kgp_precond_create(kgp_precond** out, int64_t n, int64_t m, const
     g_handles.insert(p);
   }
   *out = p;
+  return KGP_OK;
+}
+
+extern "C" int kgp_afn_create(kgp_precond** out, int64_t n, int64_t m, const int64_t* perm, const double* linv,
+                              const double* w, int npt1, const double* gval, const int32_t* gcol, int64_t nnz,
+                              const int32_t* gtptr, const int32_t* gtrow, const double* gtval, double s,
+                              void* stream) {
+  KGP_REQUIRE(out != nullptr && perm != nullptr && linv != nullptr && w != nullptr && gval != nullptr &&
+                  gcol != nullptr && gtptr != nullptr && gtrow != nullptr && gtval != nullptr,
+              KGP_ERR_INVALID, "NULL pointer");
+  KGP_REQUIRE(n >= 2 && m >= 1 && m < n && n - m < ((int64_t)1 << 31), KGP_ERR_INVALID,
+              "need 1 <= m < n, got m=%lld, n=%lld", (long long)m, (long long)n);
+  KGP_REQUIRE(npt1 >= 1 && nnz >= n - m && nnz <= (int64_t)npt1 * (n - m), KGP_ERR_INVALID,
+              "bad FSAI factor shape (npt1=%d, nnz=%lld)", npt1, (long long)nnz);
+  KGP_REQUIRE(s > 0.0, KGP_ERR_INVALID, "shift must be positive");
+  cudaStream_t st = (cudaStream_t)stream;
+  kgp_precond_s* p = new kgp_precond_s();
+  p->magic = PRECOND_MAGIC;
+  p->kind = KGP_PRECOND_AFN;
+  p->n = n;
+  p->m = m;
+  p->s = s;
+  p->n2 = n - m;
+  p->npt1 = npt1;
+  p->nnz = nnz;
+  const int64_t n2 = n - m;
+  struct Copy { DevBuf* dst; const void* src; size_t bytes; };
+  const Copy copies[] = {
+      {&p->perm, perm, sizeof(int64_t) * n},           {&p->linv, linv, sizeof(double) * m * m},
+      {&p->w, w, sizeof(double) * n2 * m},             {&p->gval, gval, sizeof(double) * npt1 * n2},
+      {&p->gcol, gcol, sizeof(int32_t) * npt1 * n2},   {&p->gtptr, gtptr, sizeof(int32_t) * (n2 + 1)},
+      {&p->gtrow, gtrow, sizeof(int32_t) * nnz},       {&p->gtval, gtval, sizeof(double) * nnz}};
+  int rc = KGP_OK;
+  for (const Copy& c : copies) {
+    rc = c.dst->ensure(c.bytes);
+    if (!rc) rc = cuda_check(cudaMemcpyAsync(c.dst->p, c.src, c.bytes, cudaMemcpyDeviceToDevice, st), "copy AFN factor");
+    if (rc) break;
+  }
+  if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "AFN create");
+  if (rc) {
+    delete p;
+    return rc;
+  }
+  {
+    std::lock_guard<std::mutex> g(g_handles_mu);
+    g_handles.insert(p);
+  }
+  *out = p;
+  return KGP_OK;
+}
+
+extern "C" int kgp_precond_kind(kgp_precond* p, int* kind) {
+  CHECK_PRECOND(p);
+  KGP_REQUIRE(kind != nullptr, KGP_ERR_INVALID, "NULL pointer");
+  *kind = p->kind;
   return KGP_OK;
 }
 
@@ -478,6 +534,7 @@ extern "C" int kgp_precond_apply_inverse(kgp_precond* p, int64_t k, const double
 extern "C" int kgp_lowrank_apply(kgp_precond* p, double beta, double alpha, int64_t k, const double* b, int64_t b_rs,
                                  int64_t b_cs, double* out, int64_t o_rs, int64_t o_cs, void* stream) {
   CHECK_PRECOND(p);
+  KGP_REQUIRE(p->kind == KGP_PRECOND_NYSTROM, KGP_ERR_INVALID, "low-rank operations need a Nystrom handle");
   KGP_REQUIRE(k >= 1, KGP_ERR_INVALID, "B must have at least one column");
   return lowrank_apply_impl(p, beta, alpha, k, b, b_rs, b_cs, out, o_rs, o_cs, (cudaStream_t)stream);
 }
@@ -485,6 +542,7 @@ extern "C" int kgp_lowrank_apply(kgp_precond* p, double beta, double alpha, int6
 extern "C" int kgp_lowrank_project(kgp_precond* p, int64_t k, const double* b, int64_t b_rs, int64_t b_cs,
                                    double* t_out, void* stream) {
   CHECK_PRECOND(p);
+  KGP_REQUIRE(p->kind == KGP_PRECOND_NYSTROM, KGP_ERR_INVALID, "low-rank operations need a Nystrom handle");
   KGP_REQUIRE(k >= 1 && t_out != nullptr, KGP_ERR_INVALID, "bad projection arguments");
   return lowrank_project_impl(p, k, b, b_rs, b_cs, t_out, (cudaStream_t)stream);
 }
@@ -493,6 +551,7 @@ extern "C" int kgp_lowrank_expand(kgp_precond* p, double beta, double alpha, int
                                   int64_t b_cs, const double* t, double* out, int64_t o_rs, int64_t o_cs,
                                   void* stream) {
   CHECK_PRECOND(p);
+  KGP_REQUIRE(p->kind == KGP_PRECOND_NYSTROM, KGP_ERR_INVALID, "low-rank operations need a Nystrom handle");
   KGP_REQUIRE(k >= 1 && t != nullptr, KGP_ERR_INVALID, "bad expansion arguments");
   return lowrank_expand_impl(p, beta, alpha, k, b, b_rs, b_cs, t, out, o_rs, o_cs, (cudaStream_t)stream);
 }

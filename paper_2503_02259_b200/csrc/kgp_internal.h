@@ -134,11 +134,24 @@ struct kgp_engine_s {
 
 struct kgp_precond_s {
   uint64_t magic;
-  int64_t n, m;
+  int kind;          // KGP_PRECOND_NYSTROM or KGP_PRECOND_AFN
+  int64_t n, m;      // m: rank (Nystrom) / landmark count (AFN)
   double s;
-  kgp::DevBuf wt;    // (m, n) row-major
+  kgp::DevBuf wt;    // Nystrom: (m, n) row-major
   kgp::DevBuf tmp;   // split-K partials
   kgp::DevBuf tproj; // (m, k) projection U^T B
+  // AFN (afn.cu): landmarks first, then the rest (n2 = n - m points)
+  int64_t n2 = 0, nnz = 0;
+  int npt1 = 0;       // FSAI row width (neighbours + the diagonal)
+  kgp::DevBuf perm;   // n int64: permuted position -> original row
+  kgp::DevBuf linv;   // (m, m) row-major L11^-1
+  kgp::DevBuf w;      // (n2, m) row-major K21 L11^-T
+  kgp::DevBuf gval;   // (npt1, n2) FSAI values, slot-major
+  kgp::DevBuf gcol;   // (npt1, n2) int32 columns (-1 padding)
+  kgp::DevBuf gtptr;  // n2 + 1 int32: CSR of G^T
+  kgp::DevBuf gtrow;  // nnz int32
+  kgp::DevBuf gtval;  // nnz
+  kgp::DevBuf work;   // apply workspace
 };
 
 namespace kgp {
@@ -157,6 +170,12 @@ int lowrank_apply_impl(kgp_precond_s* p, double beta, double alpha, int64_t k, c
                        int64_t b_cs, double* out, int64_t o_rs, int64_t o_cs, cudaStream_t st);
 int precond_apply_impl(kgp_precond_s* p, int64_t k, const double* b, int64_t b_rs, int64_t b_cs, double* out,
                        int64_t o_rs, int64_t o_cs, cudaStream_t st);
+int afn_apply_impl(kgp_precond_s* p, int64_t k, const double* b, int64_t b_rs, int64_t b_cs, double* out,
+                   int64_t o_rs, int64_t o_cs, cudaStream_t st);
+// C (M x N) = alpha A B + beta SRC with arbitrary strides (fp64, deterministic split-K)
+int gemm_f64(int64_t M, int64_t N, int64_t K, const double* a, int64_t a_is, int64_t a_ks, const double* b,
+             int64_t b_ks, int64_t b_ns, double* c, int64_t c_is, int64_t c_ns, double alpha, double beta,
+             const double* src, int64_t s_is, int64_t s_ns, DevBuf& tmp, cudaStream_t st);
 
 // column-wise reductions / updates used by the PCG driver (pcg.cu)
 int pcg_solve_impl(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, const double* y, double tol, int max_iter,

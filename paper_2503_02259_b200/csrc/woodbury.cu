@@ -97,7 +97,62 @@ __global__ void sum_partials_kernel(int64_t count, int nz, int64_t stride, const
   out[e] = s;
 }
 
+// c[i, j] = alpha * sum_z part[z][i, j] + beta * src[i, j], fixed order in z
+__global__ void finish_partials_kernel(int64_t M, int64_t N, int nz, const double* __restrict__ part, double alpha,
+                                       double beta, const double* __restrict__ src, int64_t s_is, int64_t s_ns,
+                                       double* __restrict__ c, int64_t c_is, int64_t c_ns) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= M * N) return;
+  const int64_t i = e / N, j = e % N;
+  double acc = 0.0;
+  for (int z = 0; z < nz; ++z) acc += part[(int64_t)z * M * N + e];
+  double v = alpha * acc;
+  if (src) v += beta * src[i * s_is + j * s_ns];
+  c[i * c_is + j * c_ns] = v;
+}
+
 }  // namespace
+
+int gemm_f64(int64_t M, int64_t N, int64_t K, const double* a, int64_t a_is, int64_t a_ks, const double* b,
+             int64_t b_ks, int64_t b_ns, double* c, int64_t c_is, int64_t c_ns, double alpha, double beta,
+             const double* src, int64_t s_is, int64_t s_ns, DevBuf& tmp, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return KGP_OK;
+  const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  int64_t nz = 1;
+  if (tiles < 148 && K > 4096) {  // too few output tiles to fill the SMs: split K, fixed-order reduction
+    nz = (K + 2047) / 2048;
+    int64_t cap = 296 / tiles;
+    if (cap < 1) cap = 1;
+    if (nz > cap) nz = cap;
+  }
+  GemmArgs g{};
+  g.M = M; g.N = N; g.K = K;
+  g.a = a; g.a_is = a_is; g.a_ks = a_ks;
+  g.b = b; g.b_ks = b_ks; g.b_ns = b_ns;
+  if (nz <= 1) {
+    g.c = c; g.c_is = c_is; g.c_ns = c_ns;
+    g.kchunk = K > 0 ? K : 1; g.part_stride = 0;
+    g.alpha = alpha; g.beta = beta;
+    g.src = src; g.s_is = s_is; g.s_ns = s_ns;
+    dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN), 1);
+    dgemm_kernel<<<grid, GT, 0, st>>>(g);
+    KGP_LAUNCH("dgemm_kernel");
+    return KGP_OK;
+  }
+  const int64_t kchunk = ((K + nz - 1) / nz + BK - 1) / BK * BK;
+  nz = (K + kchunk - 1) / kchunk;
+  int rc = tmp.ensure(sizeof(double) * (size_t)(M * N * nz));
+  if (rc) return rc;
+  g.c = tmp.as<double>(); g.c_is = N; g.c_ns = 1;
+  g.kchunk = kchunk; g.part_stride = M * N;
+  dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN), (unsigned)nz);
+  dgemm_kernel<<<grid, GT, 0, st>>>(g);
+  KGP_LAUNCH("dgemm_kernel (split-K)");
+  finish_partials_kernel<<<(unsigned)((M * N + 255) / 256), 256, 0, st>>>(M, N, (int)nz, tmp.as<double>(), alpha,
+                                                                            beta, src, s_is, s_ns, c, c_is, c_ns);
+  KGP_LAUNCH("finish_partials_kernel");
+  return KGP_OK;
+}
 
 // T = U^T B (m x k, row-major), U^T = p->wt (m x n); split over n with fixed-order partials
 int lowrank_project_impl(kgp_precond_s* p, int64_t k, const double* b, int64_t b_rs, int64_t b_cs, double* T,
@@ -159,6 +214,7 @@ int lowrank_apply_impl(kgp_precond_s* p, double beta, double alpha, int64_t k, c
 // Woodbury inverse: B / s - W (W^T B) / s^2
 int precond_apply_impl(kgp_precond_s* p, int64_t k, const double* b, int64_t b_rs, int64_t b_cs, double* out,
                        int64_t o_rs, int64_t o_cs, cudaStream_t st) {
+  if (p->kind == KGP_PRECOND_AFN) return afn_apply_impl(p, k, b, b_rs, b_cs, out, o_rs, o_cs, st);
   return lowrank_apply_impl(p, 1.0 / p->s, -1.0 / (p->s * p->s), k, b, b_rs, b_cs, out, o_rs, o_cs, st);
 }
 

@@ -11,6 +11,12 @@ the two Cholesky factorisations and triangular solves through cuSOLVER/cuBLAS
 Apply (precond.py:74-92), every PCG iteration, in libkgp:
     M^-1 B = B/s - W (W^T B)/s^2          M B = s B + f^2 V (V^T B)
 which equals the reference's cho_solve form in exact arithmetic.
+
+``build_afn`` / ``build_adaptive``: the AFN preconditioner the north star names
+(landmark Cholesky block + FSAI factor of the Schur complement, afn.cu). The
+reference has no AFN (SPEC.md:17, 219-227 substitute Nystrom), so its factors are
+checked against the numpy statement in tests/afn_ref.py; it plugs in wherever the
+Nystrom object does (``.handle``, ``.apply_inverse``, ``.rank``, ``.landmark_indices``).
 """
 
 from __future__ import annotations
@@ -155,3 +161,151 @@ def build(engine, m: int | None = None) -> NystromPreconditioner:
     del wt
     fwd = _LowRank(vt, p.s)
     return NystromPreconditioner(_device.to_host(idx).astype(np.intp), p.s, inv, fwd, f2, n)
+
+
+# ----------------------------------------------------------------------------- AFN
+AFN_DEFAULT_NPT = 32     # FSAI neighbours per row
+AFN_MAX_NPT = 64
+
+
+def knn_prev_device(xd, npt: int):
+    """(n, npt) int64: for each point its npt nearest earlier points (-1 padded)."""
+    torch = _device.torch()
+    n, d = xd.shape
+    out = torch.empty((n, npt), dtype=torch.int64, device=xd.device)
+    call("kgp_knn_prev", n, d, xd.data_ptr(), npt, out.data_ptr(), _device.stream_ptr())
+    return out
+
+
+class AFNPreconditioner:
+    """M = L diag(K11, (G^T G)^-1) L^T in the landmark-first ordering; factors in HBM."""
+
+    kind = "afn"
+
+    def __init__(self, handle, landmark_indices, shift, n, npt):
+        self._h = handle
+        self.landmark_indices = landmark_indices
+        self.shift = float(shift)
+        self.n = int(n)
+        self.fsai_npt = int(npt)
+
+    @property
+    def rank(self) -> int:
+        return len(self.landmark_indices)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def apply_inverse(self, b):
+        """inv(M) @ B: landmark solve + FSAI products (afn.cu)."""
+        torch = _device.torch()
+        host = not _device.is_tensor(b)
+        if host:
+            b = np.asarray(b, dtype=np.float64)
+        squeeze = b.ndim == 1
+        bd = _device.to_device(b) if host else b
+        if squeeze:
+            bd = bd[:, None]
+        if bd.shape[0] != self.n:
+            raise ValueError(f"B has {bd.shape[0]} rows, preconditioner has {self.n}")
+        out = torch.empty((bd.shape[0], bd.shape[1]), dtype=torch.float64, device=bd.device)
+        call("kgp_precond_apply_inverse", self._h, bd.shape[1], bd.data_ptr(), bd.stride(0), bd.stride(1),
+             out.data_ptr(), out.stride(0), out.stride(1), _device.stream_ptr())
+        if squeeze:
+            out = out[:, 0]
+        return _device.to_host(out) if host else out
+
+    def close(self):
+        if self._h:
+            call("kgp_precond_destroy", self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def build_afn(engine, m: int | None = None, fsai_npt: int = AFN_DEFAULT_NPT) -> AFNPreconditioner:
+    """AFN for an engine's Khat: m FPS landmarks (exact block) + FSAI of the Schur complement."""
+    torch = _device.torch()
+    n = engine.n
+    if m is None:
+        m = default_rank(n)
+    if not 1 <= m < n:
+        raise ValueError(f"AFN needs 1 <= m < n, got m={m}, n={n}")
+    if not 1 <= fsai_npt <= AFN_MAX_NPT:
+        raise ValueError(f"fsai_npt must be in [1, {AFN_MAX_NPT}], got {fsai_npt}")
+    p = engine.params
+    f2 = p.f * p.f
+    xd = engine.x_device()
+    kid = engine._kid
+    dev = xd.device
+    idx = fps_device(xd, m, 0)
+    mask = torch.ones(n, dtype=torch.bool, device=dev)
+    mask[idx] = False
+    rest = torch.nonzero(mask).squeeze(1)
+    perm = torch.cat([idx, rest]).contiguous()
+    n2 = n - m
+    x1 = xd.index_select(0, idx).contiguous()
+    x2 = xd.index_select(0, rest).contiguous()
+    k11 = device_panel(kid, 0, x1, x1, p.l).mul_(f2)
+    k11.diagonal().add_(p.s)
+    low, info = torch.linalg.cholesky_ex(k11)
+    if int(info) != 0:
+        raise BreakdownError("AFN landmark block is not positive definite; increase s or reduce m")
+    wt = torch.linalg.solve_triangular(low, device_panel(kid, 0, x1, x2, p.l).mul_(f2), upper=False)
+    w = wt.T.contiguous()
+    del wt
+    linv = torch.linalg.solve_triangular(low, torch.eye(m, dtype=torch.float64, device=dev), upper=False)
+    linv = linv.contiguous()
+    npt = int(fsai_npt)
+    nbr = knn_prev_device(x2, npt)
+    gval = torch.empty((npt + 1, n2), dtype=torch.float64, device=dev)
+    gcol = torch.empty((npt + 1, n2), dtype=torch.int32, device=dev)
+    call("kgp_afn_fsai", kid, n2, x2.shape[1], x2.data_ptr(), float(p.l), float(p.f), float(p.s), m, w.data_ptr(),
+         npt, nbr.data_ptr(), gval.data_ptr(), gcol.data_ptr(), _device.stream_ptr())
+    # G^T as CSR: entries sorted by (column, row)
+    rows = torch.arange(n2, dtype=torch.int64, device=dev).expand(npt + 1, n2).reshape(-1)
+    cols = gcol.reshape(-1).to(torch.int64)
+    ok = cols >= 0
+    rows, cols, vals = rows[ok], cols[ok], gval.reshape(-1)[ok]
+    order = torch.argsort(cols * n2 + rows)
+    gtrow = rows[order].to(torch.int32).contiguous()
+    gtval = vals[order].contiguous()
+    gtptr = torch.zeros(n2 + 1, dtype=torch.int64, device=dev)
+    gtptr[1:] = torch.cumsum(torch.bincount(cols, minlength=n2), 0)
+    gtptr = gtptr.to(torch.int32).contiguous()
+    h = ctypes.c_void_p()
+    call("kgp_afn_create", ctypes.byref(h), n, m, perm.data_ptr(), linv.data_ptr(), w.data_ptr(), npt + 1,
+         gval.data_ptr(), gcol.data_ptr(), int(gtrow.numel()), gtptr.data_ptr(), gtrow.data_ptr(),
+         gtval.data_ptr(), float(p.s), _device.stream_ptr())
+    return AFNPreconditioner(h, _device.to_host(idx).astype(np.intp), p.s, n, npt)
+
+
+def estimate_rank(engine, sample: int = 1000, seed: int = 0) -> int:
+    """Numerical rank of f^2 kappa(X, X) at the noise level s, from a seeded row sample:
+    eigenvalues of the sample kernel scaled by n/sample that exceed s."""
+    torch = _device.torch()
+    n = engine.n
+    ns = min(n, sample)
+    p = engine.params
+    rng = np.random.default_rng(seed)
+    pick = np.sort(rng.choice(n, ns, replace=False)) if ns < n else np.arange(n)
+    xs = engine.x_device().index_select(0, torch.as_tensor(pick, device=engine.x_device().device))
+    ks = device_panel(engine._kid, 0, xs, xs, p.l).mul_(p.f * p.f * n / ns)
+    ev = torch.linalg.eigvalsh(ks)
+    return int((ev > p.s).sum())
+
+
+def build_adaptive(engine, m: int | None = None, fsai_npt: int = AFN_DEFAULT_NPT):
+    """AFN's adaptive choice: Nystrom(m) when the kernel's numerical rank fits in m
+    landmarks, the factorized AFN otherwise."""
+    n = engine.n
+    if m is None:
+        m = default_rank(n)
+    if m >= n or estimate_rank(engine) <= m:
+        return build(engine, m)
+    return build_afn(engine, m, fsai_npt)

@@ -68,12 +68,12 @@ def _engine_of(apply_a):
 
 
 def _precond_of(apply_minv):
-    from paper_2503_02259_b200.precond import NystromPreconditioner
+    from paper_2503_02259_b200.precond import AFNPreconditioner, NystromPreconditioner
 
     owner = getattr(apply_minv, "__self__", None)
-    if isinstance(owner, NystromPreconditioner) and \
-            getattr(apply_minv, "__func__", None) is NystromPreconditioner.apply_inverse:
-        return owner
+    for cls in (NystromPreconditioner, AFNPreconditioner):
+        if isinstance(owner, cls) and getattr(apply_minv, "__func__", None) is cls.apply_inverse:
+            return owner
     return None
 
 
