@@ -90,8 +90,9 @@ struct PcgGraph {
   cudaGraphExec_t exec = nullptr;
   int64_t k = 0;
   const void* pc = nullptr;
-  double tol = 0.0;
-  int max_iter = 0;
+  int64_t kpc = 0;
+  double tol1 = 0.0, tol2 = 0.0;
+  int it1 = 0, it2 = 0;
   uint64_t epoch = 0;
   int64_t kernels = 0;  // kernel nodes per replay (launch accounting)
 };
@@ -181,6 +182,12 @@ int gemm_f64(int64_t M, int64_t N, int64_t K, const double* a, int64_t a_is, int
 int pcg_solve_impl(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, const double* y, double tol, int max_iter,
                    double* x_out, double* alphas, double* betas, int32_t* iters, double* rel, int32_t* conv,
                    cudaStream_t st);
+// PCG over two column groups sharing one operator application per iteration:
+// [0, kpc) preconditioned (tol1, cap it1), [kpc, k) unpreconditioned (tol2, cap it2);
+// alpha/beta arrays have per-column stride max(it1, it2).
+int pcg_grouped_impl(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, int64_t kpc, const double* y, double tol1,
+                     int it1, double tol2, int it2, double* x_out, double* alphas, double* betas, int32_t* iters,
+                     double* rel, int32_t* conv, cudaStream_t st);
 int slq_impl(int64_t k, int max_iter, const double* alphas, const double* betas, const int32_t* iters,
              const double* norms_sq, double* logdet, cudaStream_t st);
 int col_dots(int64_t k, int64_t n, const double* a, const double* b, double* out, double* partial, cudaStream_t st);

@@ -68,8 +68,21 @@ struct PcgState {
   double* err_val;
 };
 
-__global__ void pcg_init_kernel(int k, double tol, const double* ynorm_sq, double* ynorm, double* rel, int32_t* active,
-                                int32_t* iters, int32_t* status) {
+// Columns [0, kpc) form group 1 (preconditioned when a preconditioner is given; tol1, cap it1),
+// columns [kpc, k) group 2 (never preconditioned; tol2, cap it2): one operator application per
+// iteration serves both, e.g. the w-solve and the probe solves of nlml_grad_iterative
+// (gp.py:154-160) as Khat [p_w, P_Z]. Each column's recurrence is independent of the others.
+struct PcgGroups {
+  int kpc;
+  double tol1, tol2;
+  int it1, it2;
+  int stride;  // per-column stride of the alpha/beta arrays (max(it1, it2))
+  __device__ double tol(int c) const { return c < kpc ? tol1 : tol2; }
+  __device__ int cap(int c) const { return c < kpc ? it1 : it2; }
+};
+
+__global__ void pcg_init_kernel(int k, PcgGroups g, const double* ynorm_sq, double* ynorm, double* rel,
+                                int32_t* active, int32_t* iters, int32_t* status) {
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c == 0) {
     status[1] = 0;
@@ -80,14 +93,14 @@ __global__ void pcg_init_kernel(int k, double tol, const double* ynorm_sq, doubl
   ynorm[c] = yn;
   double rl = yn > 0.0 ? 1.0 : 0.0;  // solver.py:150
   rel[c] = rl;
-  int a = rl > tol ? 1 : 0;
+  int a = rl > g.tol(c) ? 1 : 0;
   active[c] = a;
   iters[c] = 0;
   if (a) atomicAdd(&status[0], 1);
 }
 
 // alpha step (solver.py:159-168)
-__global__ void pcg_alpha_kernel(int k, int max_iter, const double* pap, const double* rz, const int32_t* active,
+__global__ void pcg_alpha_kernel(int k, int stride, const double* pap, const double* rz, const int32_t* active,
                                  const int32_t* iters, double* alpha, double* alphas, int32_t* status,
                                  double* err_val) {
   int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -102,7 +115,7 @@ __global__ void pcg_alpha_kernel(int k, int max_iter, const double* pap, const d
   }
   double a = rz[c] / v;
   alpha[c] = a;
-  alphas[(int64_t)c * max_iter + iters[c]] = a;
+  alphas[(int64_t)c * stride + iters[c]] = a;
 }
 
 // x += alpha p; r -= alpha Ap on active columns
@@ -121,7 +134,7 @@ __global__ void pcg_update_xr_kernel(int64_t n, int k, const int32_t* active, co
 // beta step and freeze decision (solver.py:170-182)
 // One block (k <= 1024). Also publishes (active count, error code) of this iteration to
 // hist[2 * it], a host-mapped array the driver polls a few iterations behind the device.
-__global__ void pcg_beta_kernel(int k, int max_iter, double tol, bool precond, const double* rr, const double* rzn,
+__global__ void pcg_beta_kernel(int k, PcgGroups g, bool precond, const double* rr, const double* rzn,
                                 double* rz, const double* ynorm, int32_t* active, int32_t* iters, double* beta,
                                 double* betas, double* rel, int32_t* status, int32_t* it_counter,
                                 volatile int32_t* hist) {
@@ -134,16 +147,16 @@ __global__ void pcg_beta_kernel(int k, int max_iter, double tol, bool precond, c
       atomicMin(&status[2], c);
       status[1] = KGP_ERR_NUMERICAL;
     } else {
-      double rn = precond ? rzn[c] : v;
+      double rn = (precond && c < g.kpc) ? rzn[c] : v;
       double b = rn / rz[c];
       int it = iters[c];
-      betas[(int64_t)c * max_iter + it] = b;
+      betas[(int64_t)c * g.stride + it] = b;
       iters[c] = it + 1;
       rz[c] = rn;
       double rl = sqrt(v) / ynorm[c];
       rel[c] = rl;
       beta[c] = b;
-      if (rl <= tol) {
+      if (rl <= g.tol(c) || it + 1 >= g.cap(c)) {  // converged, or this column's iteration cap
         active[c] = 0;
       } else {
         atomicAdd(&status[0], 1);
@@ -160,20 +173,21 @@ __global__ void pcg_beta_kernel(int k, int max_iter, double tol, bool precond, c
   }
 }
 
-// p = z + beta p on the still-active columns
-__global__ void pcg_update_p_kernel(int64_t n, int k, const int32_t* active, const double* beta, const double* z,
-                                    double* p) {
+// p = z + beta p on the still-active columns (z = r on the unpreconditioned group)
+__global__ void pcg_update_p_kernel(int64_t n, int k, int kpc, const int32_t* active, const double* beta,
+                                    const double* z, const double* r, double* p) {
   const int c = blockIdx.y;
   if (!active[c]) return;
   const double b = beta[c];
   const int64_t off = (int64_t)c * n;
+  const double* zc = (c < kpc ? z : r) + off;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    p[off + i] = fma(b, p[off + i], z[off + i]);
+    p[off + i] = fma(b, p[off + i], zc[i]);
 }
 
-__global__ void pcg_finish_kernel(int k, double tol, const double* rel, int32_t* conv) {
+__global__ void pcg_finish_kernel(int k, PcgGroups g, const double* rel, int32_t* conv) {
   int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < k) conv[c] = rel[c] <= tol ? 1 : 0;
+  if (c < k) conv[c] = rel[c] <= g.tol(c) ? 1 : 0;
 }
 
 // ---------------------------------------------------------------- SLQ
@@ -299,7 +313,7 @@ struct PcgBuffers {
   int32_t *iters, *it_counter;
 };
 
-int enqueue_iteration(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, double tol, int max_iter, const PcgBuffers& B,
+int enqueue_iteration(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, const PcgGroups& g, const PcgBuffers& B,
                       cudaStream_t st) {
   const int64_t n = e->n;
   const PcgState& S = B.S;
@@ -309,44 +323,47 @@ int enqueue_iteration(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, double tol,
   if (rc) return rc;
   rc = col_dots(k, n, S.p, S.ap, S.dots1, S.partial, st);
   if (rc) return rc;
-  pcg_alpha_kernel<<<kb, 128, 0, st>>>((int)k, max_iter, S.dots1, S.rz, S.active, B.iters, S.alpha, B.alphas,
+  pcg_alpha_kernel<<<kb, 128, 0, st>>>((int)k, g.stride, S.dots1, S.rz, S.active, B.iters, S.alpha, B.alphas,
                                         S.status, S.err_val);
   KGP_LAUNCH("pcg_alpha_kernel");
   pcg_update_xr_kernel<<<vgrid, 256, 0, st>>>(n, (int)k, S.active, S.alpha, S.p, S.ap, B.x, S.r);
   KGP_LAUNCH("pcg_update_xr_kernel");
-  if (pc) {
-    rc = precond_apply_impl(pc, k, S.r, 1, n, S.z, 1, n, st);
+  if (pc && g.kpc > 0) {  // M^-1 on the preconditioned group only
+    rc = precond_apply_impl(pc, g.kpc, S.r, 1, n, S.z, 1, n, st);
     if (rc) return rc;
-    rc = col_dots(k, n, S.r, S.z, S.dots2, S.partial, st);
+    rc = col_dots(g.kpc, n, S.r, S.z, S.dots2, S.partial, st);
     if (rc) return rc;
   }
   rc = col_dots(k, n, S.r, S.r, S.dots1, S.partial, st);
   if (rc) return rc;
-  pcg_beta_kernel<<<1, 1024, 0, st>>>((int)k, max_iter, tol, pc != nullptr, S.dots1, S.dots2, S.rz, S.ynorm,
-                                      S.active, B.iters, S.beta, B.betas, B.rel, S.status, B.it_counter,
-                                      e->hist_dev);
+  pcg_beta_kernel<<<1, 1024, 0, st>>>((int)k, g, pc != nullptr, S.dots1, S.dots2, S.rz, S.ynorm, S.active, B.iters,
+                                      S.beta, B.betas, B.rel, S.status, B.it_counter, e->hist_dev);
   KGP_LAUNCH("pcg_beta_kernel");
-  pcg_update_p_kernel<<<vgrid, 256, 0, st>>>(n, (int)k, S.active, S.beta, S.z, S.p);
+  pcg_update_p_kernel<<<vgrid, 256, 0, st>>>(n, (int)k, pc ? g.kpc : 0, S.active, S.beta, S.z, S.r, S.p);
   KGP_LAUNCH("pcg_update_p_kernel");
   return KGP_OK;
 }
 
+bool same_groups(const PcgGraph& c, int64_t k, const kgp_precond_s* pc, const PcgGroups& g) {
+  return c.exec && c.k == k && c.pc == pc && c.kpc == g.kpc && c.tol1 == g.tol1 && c.tol2 == g.tol2 &&
+         c.it1 == g.it1 && c.it2 == g.it2 && c.epoch == graph_epoch();
+}
+
 // returns the graph for this configuration, capturing it on first use
-int pcg_graph(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, double tol, int max_iter, const PcgBuffers& B,
-              cudaStream_t st, cudaGraphExec_t* out, int64_t* kernels) {
-  for (auto& g : e->gcache)
-    if (g.exec && g.k == k && g.pc == pc && g.tol == tol && g.max_iter == max_iter && g.epoch == graph_epoch()) {
-      *out = g.exec;
-      *kernels = g.kernels;
+int pcg_graph(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, const PcgGroups& g, const PcgBuffers& B,
+              cudaGraphExec_t* out, int64_t* kernels) {
+  for (auto& c : e->gcache)
+    if (same_groups(c, k, pc, g)) {
+      *out = c.exec;
+      *kernels = c.kernels;
       return KGP_OK;
     }
   // captured on the engine's private stream (the legacy default stream cannot be captured);
   // nothing is executed during capture, so no ordering with the caller's stream is needed
-  (void)st;
   cudaGraph_t graph = nullptr;
   const int64_t counted = kgp_launch_count();
   KGP_CUDA(cudaStreamBeginCapture(e->cstream, cudaStreamCaptureModeThreadLocal));
-  int rc = enqueue_iteration(e, pc, k, tol, max_iter, B, e->cstream);
+  int rc = enqueue_iteration(e, pc, k, g, B, e->cstream);
   cudaError_t ce = cudaStreamEndCapture(e->cstream, &graph);
   count_launches(counted - kgp_launch_count());  // captured, not launched
   if (rc) {
@@ -373,12 +390,15 @@ int pcg_graph(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, double tol, int max
   slot.exec = exec;
   slot.k = k;
   slot.pc = pc;
-  slot.tol = tol;
-  slot.max_iter = max_iter;
+  slot.kpc = g.kpc;
+  slot.tol1 = g.tol1;
+  slot.tol2 = g.tol2;
+  slot.it1 = g.it1;
+  slot.it2 = g.it2;
   slot.epoch = graph_epoch();
   slot.kernels = nkern;
   *out = exec;
-  *kernels = slot.kernels;
+  *kernels = nkern;
   return KGP_OK;
 }
 
@@ -397,10 +417,24 @@ int status_error(const PcgState& S, int code, int32_t col) {
 int pcg_solve_impl(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, const double* y, double tol, int max_iter,
                    double* x_out, double* alphas, double* betas, int32_t* iters, double* rel, int32_t* conv,
                    cudaStream_t st) {
+  return pcg_grouped_impl(e, pc, k, k, y, tol, max_iter, tol, max_iter, x_out, alphas, betas, iters, rel, conv, st);
+}
+
+int pcg_grouped_impl(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, int64_t kpc, const double* y, double tol1,
+                     int it1, double tol2, int it2, double* x_out, double* alphas, double* betas, int32_t* iters,
+                     double* rel, int32_t* conv, cudaStream_t st) {
   const int64_t n = e->n;
   const int nb = (int)((n + DOT_CHUNK - 1) / DOT_CHUNK);
   KGP_REQUIRE(k <= 1024, KGP_ERR_INVALID, "pcg supports at most 1024 right-hand sides per call, got %lld",
               (long long)k);
+  KGP_REQUIRE(kpc >= 0 && kpc <= k && it1 >= 1 && (kpc == k || it2 >= 1), KGP_ERR_INVALID, "bad column groups");
+  PcgGroups g{(int)kpc, tol1, kpc < k ? tol2 : tol1, it1, kpc < k ? it2 : it1, 0};
+  if (kpc == 0) {
+    g.tol1 = g.tol2;
+    g.it1 = g.it2;
+  }
+  const int max_iter = g.it1 > g.it2 ? g.it1 : g.it2;
+  g.stride = max_iter;
   // engine-owned state: r, p, ap, [z], x : (k, n); coefficient arrays; scalars
   const size_t vec = (size_t)k * n;
   const size_t coef = (size_t)k * max_iter;
@@ -453,20 +487,27 @@ int pcg_solve_impl(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, const double* 
   KGP_CUDA(cudaMemsetAsync(B.alphas, 0, sizeof(double) * 2 * coef, st));
   rc = col_dots(k, n, S.r, S.r, S.dots1, S.partial, st);
   if (rc) return rc;
-  pcg_init_kernel<<<kb, 128, 0, st>>>((int)k, tol, S.dots1, S.ynorm, B.rel, S.active, B.iters, S.status);
+  pcg_init_kernel<<<kb, 128, 0, st>>>((int)k, g, S.dots1, S.ynorm, B.rel, S.active, B.iters, S.status);
   KGP_LAUNCH("pcg_init_kernel");
   rc = read_status(S.status, hstatus, st);
   if (rc) return rc;
   if (hstatus[0] > 0) {
-    if (pc) {
-      rc = precond_apply_impl(pc, k, S.r, 1, n, S.z, 1, n, st);
+    const int64_t kz = pc ? g.kpc : 0;  // columns whose z is M^-1 r
+    if (kz > 0) {
+      rc = precond_apply_impl(pc, kz, S.r, 1, n, S.z, 1, n, st);
+      if (rc) return rc;
+      KGP_CUDA(cudaMemcpyAsync(S.p, S.z, sizeof(double) * kz * n, cudaMemcpyDeviceToDevice, st));
+      rc = col_dots(kz, n, S.r, S.z, S.rz, S.partial, st);
       if (rc) return rc;
     }
-    KGP_CUDA(cudaMemcpyAsync(S.p, S.z, sizeof(double) * vec, cudaMemcpyDeviceToDevice, st));
-    rc = col_dots(k, n, S.r, S.z, S.rz, S.partial, st);
-    if (rc) return rc;
+    if (kz < k) {
+      KGP_CUDA(cudaMemcpyAsync(S.p + kz * n, S.r + kz * n, sizeof(double) * (k - kz) * n, cudaMemcpyDeviceToDevice,
+                               st));
+      rc = col_dots(k - kz, n, S.r + kz * n, S.r + kz * n, S.rz + kz, S.partial, st);
+      if (rc) return rc;
+    }
     // iteration 0 uncaptured: it also performs every lazy allocation / first-launch setup
-    rc = enqueue_iteration(e, pc, k, tol, max_iter, B, st);
+    rc = enqueue_iteration(e, pc, k, g, B, st);
     if (rc) return rc;
     KGP_CUDA(cudaStreamSynchronize(st));
     volatile int32_t* H = e->hist_host;
@@ -475,7 +516,7 @@ int pcg_solve_impl(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, const double* 
     if (!done && max_iter > 1) {
       cudaGraphExec_t exec = nullptr;
       int64_t gk = 0;
-      rc = pcg_graph(e, pc, k, tol, max_iter, B, st, &exec, &gk);
+      rc = pcg_graph(e, pc, k, g, B, &exec, &gk);
       if (rc) return rc;
       int launched = 1, checked = 1;
       while (launched < max_iter && !done) {
@@ -504,7 +545,7 @@ int pcg_solve_impl(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, const double* 
       }
     }
   }
-  pcg_finish_kernel<<<kb, 128, 0, st>>>((int)k, tol, B.rel, conv);
+  pcg_finish_kernel<<<kb, 128, 0, st>>>((int)k, g, B.rel, conv);
   KGP_LAUNCH("pcg_finish_kernel");
   KGP_CUDA(cudaMemcpyAsync(x_out, B.x, sizeof(double) * vec, cudaMemcpyDeviceToDevice, st));
   KGP_CUDA(cudaMemcpyAsync(alphas, B.alphas, sizeof(double) * coef, cudaMemcpyDeviceToDevice, st));
@@ -584,20 +625,19 @@ extern "C" int kgp_nlml_grad(kgp_engine* e, kgp_precond* p, const double* y, int
   int32_t* iters = reinterpret_cast<int32_t*>(partial + (size_t)kv * nb + 8);
   int32_t* conv = iters + kv;
 
-  // (1) w = PCG(Khat, M, y, tol)   -> U row 0, and V row 0 = w
-  rc = pcg_solve_impl(e, p, 1, y, tol, max_iter, U, alphas, betas, iters, rel, conv, st);
-  if (rc) return rc;
-  int32_t wconv = 0;
-  KGP_CUDA(cudaMemcpyAsync(&wconv, conv, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  // (2) u = CG(Khat, Z, probe_tol), unpreconditioned: coefficients rebuild Lanczos of Khat itself
-  rc = pcg_solve_impl(e, nullptr, k_z, probes, probe_tol, pmax, U + n, alphas + max_iter, betas + max_iter,
-                      iters + 1, rel + 1, conv + 1, st);
+  // (1)+(2) w = PCG(Khat, M, y, tol) and u = CG(Khat, Z, probe_tol) (gp.py:154-160) as ONE
+  // grouped solve: every iteration applies Khat once to [p_w, P_Z] (the north star's
+  // Khat [y, Z]); column 0 is preconditioned, the probe columns are not, so their
+  // coefficients rebuild the Lanczos tridiagonals of Khat itself.
+  KGP_CUDA(cudaMemcpyAsync(V, y, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  KGP_CUDA(cudaMemcpyAsync(V + n, probes, sizeof(double) * k_z * n, cudaMemcpyDeviceToDevice, st));
+  rc = pcg_grouped_impl(e, p, kv, 1, V, tol, max_iter, probe_tol, pmax, U, alphas, betas, iters, rel, conv, st);
   if (rc) return rc;
   // (3) log|Khat| by SLQ over the probe traces
   rc = col_dots(k_z, n, probes, probes, nz2, partial, st);
   if (rc) return rc;
   double logdet = 0.0;
-  rc = slq_impl(k_z, pmax, alphas + max_iter, betas + max_iter, iters + 1, nz2, &logdet, st);
+  rc = slq_impl(k_z, wide, alphas + wide, betas + wide, iters + 1, nz2, &logdet, st);
   if (rc) return rc;
   // (4) loss = 1/2 (y.w + logdet + n log 2 pi)
   rc = col_dots(1, n, y, U, dots, partial, st);
@@ -635,6 +675,5 @@ extern "C" int kgp_nlml_grad(kgp_engine* e, kgp_precond* p, const double* y, int
   out[2] = grads[1];
   out[3] = grads[2];
   *out_converged = ok;
-  (void)wconv;
   return KGP_OK;
 }
