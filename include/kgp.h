@@ -68,6 +68,14 @@ int kgp_engine_set_precision(kgp_engine* e, int precision);
 /* Row partition for multi-GPU: this engine produces rows [row0, row0 + nrows) of Khat.B. */
 int kgp_engine_set_rows(kgp_engine* e, int64_t row0, int64_t nrows);
 int kgp_engine_destroy(kgp_engine* e); /* second destroy of the same handle -> KGP_ERR_STATE */
+/* Heteroscedastic shift for GP classification (no reference counterpart: SPEC.md:382 lists
+ * GPC and heteroscedastic noise as non-goals; the Dirichlet-based GPC of gpc.py needs it):
+ * column c of every later Khat product becomes f^2 kappa b_c + (s + dn[map[c]]) o b_c.
+ * dn: (classes, n) device fp64, class-major (copied); map: ncols int32 on the HOST (copied);
+ * products with more than ncols columns are rejected. classes = 0 removes it. The
+ * derivative outputs are unaffected (the diagonal is data, not a hyperparameter). */
+int kgp_engine_set_diag(kgp_engine* e, int classes, const double* dn, int64_t ncols, const int32_t* map,
+                        void* stream);
 
 /* KernelEngine.matmul / grad_matmul (kmat.py:145-189), fused in one pass:
  *   out_k  = f^2 kappa(X_rows, X) B + s B_rows        (matmul)
@@ -135,13 +143,15 @@ int kgp_lowrank_expand(kgp_precond* p, double beta, double alpha, int64_t k, con
  * kgp_afn_fsai: row i of the FSAI factor G of S = Khat22 - W W^T on the pattern
  *   {nbr[i, :], i}: gval/gcol (npt + 1, n2) slot-major (entry t of row i at t*n2 + i),
  *   the diagonal last, -1/0 padded. x2 (n2, d) the non-landmark points, w (n2, m)
- *   row-major. A non-SPD pattern block -> KGP_ERR_BREAKDOWN.
+ *   row-major. dshift (n2) adds a per-point diagonal to S (heteroscedastic noise, gpc.py;
+ *   NULL: none). A non-SPD pattern block -> KGP_ERR_BREAKDOWN.
  * kgp_afn_create: handle from device factors (all copied): perm (n) permuted position ->
  *   original row, linv (m, m) row-major L11^-1, w (n2, m), the ELL factor from
  *   kgp_afn_fsai, and G^T as CSR (gtptr n2 + 1, gtrow/gtval nnz; rows ascending). */
 int kgp_knn_prev(int64_t n, int d, const double* x, int npt, int64_t* idx_out, void* stream);
-int kgp_afn_fsai(int kernel, int64_t n2, int d, const double* x2, double l, double f, double s, int64_t m,
-                 const double* w, int npt, const int64_t* nbr, double* gval, int32_t* gcol, void* stream);
+int kgp_afn_fsai(int kernel, int64_t n2, int d, const double* x2, double l, double f, double s,
+                 const double* dshift, int64_t m, const double* w, int npt, const int64_t* nbr, double* gval,
+                 int32_t* gcol, void* stream);
 int kgp_afn_create(kgp_precond** out, int64_t n, int64_t m, const int64_t* perm, const double* linv,
                    const double* w, int npt1, const double* gval, const int32_t* gcol, int64_t nnz,
                    const int32_t* gtptr, const int32_t* gtrow, const double* gtval, double s, void* stream);
@@ -156,6 +166,15 @@ int kgp_precond_kind(kgp_precond* p, int* kind);
 int kgp_pcg(kgp_engine* e, kgp_precond* p, int64_t k, const double* y, double tol, int32_t max_iter,
             double* x_out, double* alphas, double* betas, int32_t* iters, double* rel, int32_t* converged,
             void* stream);
+
+/* kgp_pcg over two column groups sharing one operator application per iteration:
+ * columns [0, kpc) preconditioned (tol1, at most it1 iterations), [kpc, k) unpreconditioned
+ * (tol2, it2). pcs: 0, 1 (shared by the group) or kpc handles (one per column, e.g. one
+ * per GPC class). alphas/betas: (k, max(it1, it2)). The engine's kgp_engine_set_diag
+ * state, if any, applies (it must map k columns). */
+int kgp_pcg_grouped(kgp_engine* e, kgp_precond* const* pcs, int npcs, int64_t k, int64_t kpc, const double* y,
+                    double tol1, int32_t it1, double tol2, int32_t it2, double* x_out, double* alphas,
+                    double* betas, int32_t* iters, double* rel, int32_t* converged, void* stream);
 
 /* slq_logdet (solver.py:238-265): per-probe e1^T log(T) e1 from the CG
  * coefficients on the device; returns the probe mean of |z|^2 e1^T log(T) e1 in
@@ -181,6 +200,19 @@ int kgp_nlml_grad(kgp_engine* e, kgp_precond* p, const double* y, int64_t k_z, c
 int64_t kgp_launch_count(void);
 int kgp_engine_set_timing(kgp_engine* e, int enable);
 int kgp_engine_kernel_time(kgp_engine* e, double* ms, int64_t* launches);
+
+/* Dirichlet GP classification (gpc.py; no reference counterpart): `classes`
+ * GP regressions sharing (l, f, s), class c with Khat + diag(dn_c) and target y_c, solved
+ * together (one operator application per iteration serves every class's target and
+ * probe columns). dn, y: (classes, n) device, class-major; probes (classes * k_z, n)
+ * device, class c's probes at rows [c*k_z, (c+1)*k_z). pcs: 0, 1 (shared) or `classes`
+ * preconditioner handles (AFN/Nystrom built for class c's diagonal). out[0..3] = summed
+ * loss, grad_l, grad_f, grad_s (host). Replaces any kgp_engine_set_diag state; on return
+ * the engine has none. */
+int kgp_gpc_nlml_grad(kgp_engine* e, int classes, kgp_precond* const* pcs, int npcs, const double* dn,
+                      const double* y, int64_t k_z, const double* probes, double tol, int32_t max_iter,
+                      double probe_tol, int32_t probe_max_iter, double* out, int32_t* out_converged,
+                      void* stream);
 
 #ifdef __cplusplus
 }

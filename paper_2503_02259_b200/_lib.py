@@ -67,8 +67,13 @@ _SIGNATURES = {
     "kgp_nlml_grad": [c_vp, c_vp, c_vp, c_i64, c_vp, c_dbl, c_i32, c_dbl, c_i32, _P(c_dbl), _P(c_i32), c_vp],
     "kgp_engine_set_timing": [c_vp, ctypes.c_int],
     "kgp_knn_prev": [c_i64, ctypes.c_int, c_vp, ctypes.c_int, c_vp, c_vp],
-    "kgp_afn_fsai": [ctypes.c_int, c_i64, ctypes.c_int, c_vp, c_dbl, c_dbl, c_dbl, c_i64, c_vp, ctypes.c_int, c_vp,
-                     c_vp, c_vp, c_vp],
+    "kgp_afn_fsai": [ctypes.c_int, c_i64, ctypes.c_int, c_vp, c_dbl, c_dbl, c_dbl, c_vp, c_i64, c_vp, ctypes.c_int,
+                     c_vp, c_vp, c_vp, c_vp],
+    "kgp_engine_set_diag": [c_vp, ctypes.c_int, c_vp, c_i64, c_vp, c_vp],
+    "kgp_pcg_grouped": [c_vp, c_vp, ctypes.c_int, c_i64, c_i64, c_vp, c_dbl, c_i32, c_dbl, c_i32, c_vp, c_vp, c_vp,
+                        c_vp, c_vp, c_vp, c_vp],
+    "kgp_gpc_nlml_grad": [c_vp, ctypes.c_int, c_vp, ctypes.c_int, c_vp, c_vp, c_i64, c_vp, c_dbl, c_i32, c_dbl, c_i32,
+                          _P(c_dbl), _P(c_i32), c_vp],
     "kgp_afn_create": [_P(c_vp), c_i64, c_i64, c_vp, c_vp, c_vp, ctypes.c_int, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp,
                        c_dbl, c_vp],
     "kgp_precond_kind": [c_vp, _P(ctypes.c_int)],

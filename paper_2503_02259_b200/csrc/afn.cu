@@ -98,6 +98,7 @@ template <int KT>
 __global__ void __launch_bounds__(FS_T) fsai_kernel(int64_t n2, int d, const double* __restrict__ x2, double l,
                                                     double f2, double s, int64_t mw, const double* __restrict__ w,
                                                     int npt, const int64_t* __restrict__ nbr,
+                                                    const double* __restrict__ dshift,
                                                     double* __restrict__ gval, int32_t* __restrict__ gcol,
                                                     int32_t* __restrict__ status) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -127,7 +128,7 @@ __global__ void __launch_bounds__(FS_T) fsai_kernel(int64_t n2, int d, const dou
       const double df = sm.xs[a * d + c] - sm.xs[b * d + c];
       r2 = fma(df, df, r2);
     }
-    sm.S[a * m + b] = f2 * kappa64<KT>(r2, l) + (a == b ? s : 0.0);
+    sm.S[a * m + b] = f2 * kappa64<KT>(r2, l) + (a == b ? s + (dshift ? dshift[sm.idx[a]] : 0.0) : 0.0);
   }
   // - W_P W_P^T, accumulated over the m_w landmark columns in chunks
   const int nent = m * (m + 1) / 2;
@@ -332,8 +333,8 @@ extern "C" int kgp_knn_prev(int64_t n, int d, const double* x, int npt, int64_t*
 }
 
 extern "C" int kgp_afn_fsai(int kernel, int64_t n2, int d, const double* x2, double l, double f, double s,
-                            int64_t m, const double* w, int npt, const int64_t* nbr, double* gval, int32_t* gcol,
-                            void* stream) {
+                            const double* dshift, int64_t m, const double* w, int npt, const int64_t* nbr,
+                            double* gval, int32_t* gcol, void* stream) {
   KGP_REQUIRE(kernel >= 0 && kernel <= 2, KGP_ERR_INVALID, "unknown kernel id %d", kernel);
   KGP_REQUIRE(d >= 1 && d <= 16, KGP_ERR_INVALID, "dimension d=%d outside [1, 16]", d);
   KGP_REQUIRE(npt >= 1 && npt <= KNN_MAX, KGP_ERR_INVALID, "npt=%d outside [1, %d]", npt, KNN_MAX);
@@ -355,8 +356,8 @@ extern "C" int kgp_afn_fsai(int kernel, int64_t n2, int d, const double* x2, dou
       KGP_CUDA(cudaFuncSetAttribute(fsai_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
       configured = true;                                                                                   \
     }                                                                                                      \
-    fsai_kernel<K><<<(unsigned)n2, FS_T, smem, st>>>(n2, d, x2, l, f2, s, m, w, npt, nbr, gval, gcol,      \
-                                                    status.as<int32_t>());                                 \
+    fsai_kernel<K><<<(unsigned)n2, FS_T, smem, st>>>(n2, d, x2, l, f2, s, m, w, npt, nbr, dshift, gval,    \
+                                                    gcol, status.as<int32_t>());                           \
     break;                                                                                                 \
   }
     KGP_FSAI_CASE(0) KGP_FSAI_CASE(1) KGP_FSAI_CASE(2)

@@ -188,10 +188,40 @@ static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t 
   return KGP_OK;
 }
 
+// out[i, c] += dn[map[c]][row0 + i] * B[row0 + i, c]: the heteroscedastic part of the shift
+__global__ void diag_shift_kernel(int64_t nrows, int64_t n, int64_t row0, const double* __restrict__ dn,
+                                  const int32_t* __restrict__ map, const double* __restrict__ b, int64_t b_rs,
+                                  int64_t b_cs, double* __restrict__ out, int64_t o_rs, int64_t o_cs) {
+  const int c = blockIdx.y;
+  const double* dc = dn + (int64_t)map[c] * n + row0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nrows; i += (int64_t)gridDim.x * blockDim.x)
+    out[i * o_rs + c * o_cs] += dc[i] * b[(row0 + i) * b_rs + c * b_cs];
+}
+
+static int engine_matmul_core(kgp_engine_s* e, int64_t k, const double* b, int64_t b_rs, int64_t b_cs,
+                              double* out_k, double* out_dl, double* out_df, int64_t o_rs, int64_t o_cs,
+                              cudaStream_t st);
+
 int engine_matmul_impl(kgp_engine_s* e, int64_t k, const double* b, int64_t b_rs, int64_t b_cs, double* out_k,
                        double* out_dl, double* out_df, int64_t o_rs, int64_t o_cs, cudaStream_t st) {
   if (k <= 0 || e->nrows <= 0) return KGP_OK;
   if (!out_k && !out_dl && !out_df) return KGP_OK;
+  KGP_REQUIRE(!(out_k && e->dn_classes > 0) || k <= e->dn_ncols, KGP_ERR_INVALID,
+              "engine diagonal maps %lld columns, B has %lld", (long long)e->dn_ncols, (long long)k);
+  int rc = engine_matmul_core(e, k, b, b_rs, b_cs, out_k, out_dl, out_df, o_rs, o_cs, st);
+  if (rc || !out_k || e->dn_classes == 0) return rc;
+  int64_t bx = (e->nrows + 255) / 256;
+  if (bx > 256) bx = 256;
+  diag_shift_kernel<<<dim3((unsigned)bx, (unsigned)k), 256, 0, st>>>(e->nrows, e->n, e->row0, e->dn.as<double>(),
+                                                                    e->dmap.as<int32_t>(), b, b_rs, b_cs, out_k,
+                                                                    o_rs, o_cs);
+  KGP_LAUNCH("diag_shift_kernel");
+  return KGP_OK;
+}
+
+static int engine_matmul_core(kgp_engine_s* e, int64_t k, const double* b, int64_t b_rs, int64_t b_cs,
+                              double* out_k, double* out_dl, double* out_df, int64_t o_rs, int64_t o_cs,
+                              cudaStream_t st) {
   if (e->precision == KGP_FP64) {
     F64Params p{};
     p.xr = e->x64.as<double>() + e->row0 * e->d;
@@ -358,6 +388,33 @@ extern "C" int kgp_engine_set_rows(kgp_engine* e, int64_t row0, int64_t nrows) {
   e->nrows = nrows;
   e->prepared = false;
   bump_graph_epoch();
+  return KGP_OK;
+}
+
+extern "C" int kgp_engine_set_diag(kgp_engine* e, int classes, const double* dn, int64_t ncols, const int32_t* map,
+                                   void* stream) {
+  CHECK_ENGINE(e);
+  KGP_REQUIRE(classes >= 0, KGP_ERR_INVALID, "classes must be >= 0");
+  bump_graph_epoch();
+  if (classes == 0) {
+    e->dn_classes = 0;
+    e->dn_ncols = 0;
+    return KGP_OK;
+  }
+  KGP_REQUIRE(dn != nullptr && map != nullptr && ncols >= 1, KGP_ERR_INVALID, "NULL diagonal or column map");
+  for (int64_t c = 0; c < ncols; ++c)
+    KGP_REQUIRE(map[c] >= 0 && map[c] < classes, KGP_ERR_INVALID, "column %lld maps to class %d of %d",
+                (long long)c, map[c], classes);
+  KGP_CUDA(cudaSetDevice(e->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = e->dn.ensure(sizeof(double) * (size_t)classes * e->n);
+  if (!rc) rc = e->dmap.ensure(sizeof(int32_t) * (size_t)ncols);
+  if (rc) return rc;
+  KGP_CUDA(cudaMemcpyAsync(e->dn.p, dn, sizeof(double) * (size_t)classes * e->n, cudaMemcpyDeviceToDevice, st));
+  KGP_CUDA(cudaMemcpyAsync(e->dmap.p, map, sizeof(int32_t) * (size_t)ncols, cudaMemcpyHostToDevice, st));
+  KGP_CUDA(cudaStreamSynchronize(st));
+  e->dn_classes = classes;
+  e->dn_ncols = ncols;
   return KGP_OK;
 }
 

@@ -89,7 +89,7 @@ void bump_graph_epoch();
 struct PcgGraph {
   cudaGraphExec_t exec = nullptr;
   int64_t k = 0;
-  const void* pc = nullptr;
+  std::vector<const void*> pcs;
   int64_t kpc = 0;
   double tol1 = 0.0, tol2 = 0.0;
   int it1 = 0, it2 = 0;
@@ -127,6 +127,11 @@ struct kgp_engine_s {
   int hist_cap = 0;
   cudaEvent_t events[kgp::PCG_LOOKAHEAD] = {};
   cudaStream_t cstream = nullptr;  // private stream used only for graph capture (the caller's may be legacy)
+  // optional heteroscedastic diagonal (kgp_engine_set_diag): Khat column c gets + diag(dn[:, dmap[c]])
+  int dn_classes = 0;
+  int64_t dn_ncols = 0;
+  kgp::DevBuf dn;    // (classes, n): class-major
+  kgp::DevBuf dmap;  // dn_ncols int32: RHS column -> class
   // optional main-kernel timing (kgp_engine_set_timing)
   bool timing = false;
   std::vector<cudaEvent_t> tev;  // start/stop pairs
@@ -185,7 +190,11 @@ int pcg_solve_impl(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, const double* 
 // PCG over two column groups sharing one operator application per iteration:
 // [0, kpc) preconditioned (tol1, cap it1), [kpc, k) unpreconditioned (tol2, cap it2);
 // alpha/beta arrays have per-column stride max(it1, it2).
-int pcg_grouped_impl(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, int64_t kpc, const double* y, double tol1,
+struct PcSet {
+  kgp_precond_s* const* h;
+  int count;  // 0: none; 1: one handle for every preconditioned column; kpc: one per column
+};
+int pcg_grouped_impl(kgp_engine_s* e, const PcSet& pcs, int64_t k, int64_t kpc, const double* y, double tol1,
                      int it1, double tol2, int it2, double* x_out, double* alphas, double* betas, int32_t* iters,
                      double* rel, int32_t* conv, cudaStream_t st);
 int slq_impl(int64_t k, int max_iter, const double* alphas, const double* betas, const int32_t* iters,

@@ -313,8 +313,19 @@ struct PcgBuffers {
   int32_t *iters, *it_counter;
 };
 
-int enqueue_iteration(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, const PcgGroups& g, const PcgBuffers& B,
+// M^-1 on the first kpc columns: one handle for all of them, or one handle per column
+int apply_pcs(const PcSet& pcs, int64_t kpc, int64_t n, const double* r, double* z, cudaStream_t st) {
+  if (pcs.count == 1) return precond_apply_impl(pcs.h[0], kpc, r, 1, n, z, 1, n, st);
+  for (int64_t c = 0; c < kpc; ++c) {
+    int rc = precond_apply_impl(pcs.h[c], 1, r + c * n, 1, n, z + c * n, 1, n, st);
+    if (rc) return rc;
+  }
+  return KGP_OK;
+}
+
+int enqueue_iteration(kgp_engine_s* e, const PcSet& pcs, int64_t k, const PcgGroups& g, const PcgBuffers& B,
                       cudaStream_t st) {
+  const bool pc = pcs.count > 0;
   const int64_t n = e->n;
   const PcgState& S = B.S;
   const unsigned kb = (unsigned)((k + 127) / 128);
@@ -329,14 +340,14 @@ int enqueue_iteration(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, const PcgGr
   pcg_update_xr_kernel<<<vgrid, 256, 0, st>>>(n, (int)k, S.active, S.alpha, S.p, S.ap, B.x, S.r);
   KGP_LAUNCH("pcg_update_xr_kernel");
   if (pc && g.kpc > 0) {  // M^-1 on the preconditioned group only
-    rc = precond_apply_impl(pc, g.kpc, S.r, 1, n, S.z, 1, n, st);
+    rc = apply_pcs(pcs, g.kpc, n, S.r, S.z, st);
     if (rc) return rc;
     rc = col_dots(g.kpc, n, S.r, S.z, S.dots2, S.partial, st);
     if (rc) return rc;
   }
   rc = col_dots(k, n, S.r, S.r, S.dots1, S.partial, st);
   if (rc) return rc;
-  pcg_beta_kernel<<<1, 1024, 0, st>>>((int)k, g, pc != nullptr, S.dots1, S.dots2, S.rz, S.ynorm, S.active, B.iters,
+  pcg_beta_kernel<<<1, 1024, 0, st>>>((int)k, g, pc, S.dots1, S.dots2, S.rz, S.ynorm, S.active, B.iters,
                                       S.beta, B.betas, B.rel, S.status, B.it_counter, e->hist_dev);
   KGP_LAUNCH("pcg_beta_kernel");
   pcg_update_p_kernel<<<vgrid, 256, 0, st>>>(n, (int)k, pc ? g.kpc : 0, S.active, S.beta, S.z, S.r, S.p);
@@ -344,16 +355,19 @@ int enqueue_iteration(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, const PcgGr
   return KGP_OK;
 }
 
-bool same_groups(const PcgGraph& c, int64_t k, const kgp_precond_s* pc, const PcgGroups& g) {
-  return c.exec && c.k == k && c.pc == pc && c.kpc == g.kpc && c.tol1 == g.tol1 && c.tol2 == g.tol2 &&
+bool same_groups(const PcgGraph& c, int64_t k, const PcSet& pcs, const PcgGroups& g) {
+  if (!c.exec || (int)c.pcs.size() != pcs.count) return false;
+  for (int i = 0; i < pcs.count; ++i)
+    if (c.pcs[i] != pcs.h[i]) return false;
+  return c.k == k && c.kpc == g.kpc && c.tol1 == g.tol1 && c.tol2 == g.tol2 &&
          c.it1 == g.it1 && c.it2 == g.it2 && c.epoch == graph_epoch();
 }
 
 // returns the graph for this configuration, capturing it on first use
-int pcg_graph(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, const PcgGroups& g, const PcgBuffers& B,
+int pcg_graph(kgp_engine_s* e, const PcSet& pcs, int64_t k, const PcgGroups& g, const PcgBuffers& B,
               cudaGraphExec_t* out, int64_t* kernels) {
   for (auto& c : e->gcache)
-    if (same_groups(c, k, pc, g)) {
+    if (same_groups(c, k, pcs, g)) {
       *out = c.exec;
       *kernels = c.kernels;
       return KGP_OK;
@@ -363,7 +377,7 @@ int pcg_graph(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, const PcgGroups& g,
   cudaGraph_t graph = nullptr;
   const int64_t counted = kgp_launch_count();
   KGP_CUDA(cudaStreamBeginCapture(e->cstream, cudaStreamCaptureModeThreadLocal));
-  int rc = enqueue_iteration(e, pc, k, g, B, e->cstream);
+  int rc = enqueue_iteration(e, pcs, k, g, B, e->cstream);
   cudaError_t ce = cudaStreamEndCapture(e->cstream, &graph);
   count_launches(counted - kgp_launch_count());  // captured, not launched
   if (rc) {
@@ -389,7 +403,7 @@ int pcg_graph(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, const PcgGroups& g,
   if (slot.exec) cudaGraphExecDestroy(slot.exec);
   slot.exec = exec;
   slot.k = k;
-  slot.pc = pc;
+  slot.pcs.assign(pcs.h, pcs.h + pcs.count);
   slot.kpc = g.kpc;
   slot.tol1 = g.tol1;
   slot.tol2 = g.tol2;
@@ -417,10 +431,12 @@ int status_error(const PcgState& S, int code, int32_t col) {
 int pcg_solve_impl(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, const double* y, double tol, int max_iter,
                    double* x_out, double* alphas, double* betas, int32_t* iters, double* rel, int32_t* conv,
                    cudaStream_t st) {
-  return pcg_grouped_impl(e, pc, k, k, y, tol, max_iter, tol, max_iter, x_out, alphas, betas, iters, rel, conv, st);
+  kgp_precond_s* one[1] = {pc};
+  return pcg_grouped_impl(e, PcSet{one, pc ? 1 : 0}, k, k, y, tol, max_iter, tol, max_iter, x_out, alphas, betas,
+                          iters, rel, conv, st);
 }
 
-int pcg_grouped_impl(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, int64_t kpc, const double* y, double tol1,
+int pcg_grouped_impl(kgp_engine_s* e, const PcSet& pcs, int64_t k, int64_t kpc, const double* y, double tol1,
                      int it1, double tol2, int it2, double* x_out, double* alphas, double* betas, int32_t* iters,
                      double* rel, int32_t* conv, cudaStream_t st) {
   const int64_t n = e->n;
@@ -428,6 +444,11 @@ int pcg_grouped_impl(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, int64_t kpc,
   KGP_REQUIRE(k <= 1024, KGP_ERR_INVALID, "pcg supports at most 1024 right-hand sides per call, got %lld",
               (long long)k);
   KGP_REQUIRE(kpc >= 0 && kpc <= k && it1 >= 1 && (kpc == k || it2 >= 1), KGP_ERR_INVALID, "bad column groups");
+  KGP_REQUIRE(pcs.count <= 1 || pcs.count == kpc, KGP_ERR_INVALID,
+              "need one preconditioner or one per preconditioned column (%d for %lld)", pcs.count, (long long)kpc);
+  for (int i = 0; i < pcs.count; ++i)
+    KGP_REQUIRE(pcs.h[i] != nullptr && pcs.h[i]->n == e->n, KGP_ERR_INVALID, "preconditioner %d missing or of wrong size", i);
+  const bool pc = pcs.count > 0;
   PcgGroups g{(int)kpc, tol1, kpc < k ? tol2 : tol1, it1, kpc < k ? it2 : it1, 0};
   if (kpc == 0) {
     g.tol1 = g.tol2;
@@ -494,7 +515,7 @@ int pcg_grouped_impl(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, int64_t kpc,
   if (hstatus[0] > 0) {
     const int64_t kz = pc ? g.kpc : 0;  // columns whose z is M^-1 r
     if (kz > 0) {
-      rc = precond_apply_impl(pc, kz, S.r, 1, n, S.z, 1, n, st);
+      rc = apply_pcs(pcs, kz, n, S.r, S.z, st);
       if (rc) return rc;
       KGP_CUDA(cudaMemcpyAsync(S.p, S.z, sizeof(double) * kz * n, cudaMemcpyDeviceToDevice, st));
       rc = col_dots(kz, n, S.r, S.z, S.rz, S.partial, st);
@@ -507,7 +528,7 @@ int pcg_grouped_impl(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, int64_t kpc,
       if (rc) return rc;
     }
     // iteration 0 uncaptured: it also performs every lazy allocation / first-launch setup
-    rc = enqueue_iteration(e, pc, k, g, B, st);
+    rc = enqueue_iteration(e, pcs, k, g, B, st);
     if (rc) return rc;
     KGP_CUDA(cudaStreamSynchronize(st));
     volatile int32_t* H = e->hist_host;
@@ -516,7 +537,7 @@ int pcg_grouped_impl(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, int64_t kpc,
     if (!done && max_iter > 1) {
       cudaGraphExec_t exec = nullptr;
       int64_t gk = 0;
-      rc = pcg_graph(e, pc, k, g, B, &exec, &gk);
+      rc = pcg_graph(e, pcs, k, g, B, &exec, &gk);
       if (rc) return rc;
       int launched = 1, checked = 1;
       while (launched < max_iter && !done) {
@@ -586,26 +607,19 @@ int slq_impl(int64_t k, int max_iter, const double* alphas, const double* betas,
   return KGP_OK;
 }
 
-}  // namespace kgp
-
-using namespace kgp;
-
-// nlml_grad_iterative (gp.py:133-179)
-extern "C" int kgp_nlml_grad(kgp_engine* e, kgp_precond* p, const double* y, int64_t k_z, const double* probes,
-                             double tol, int32_t max_iter, double probe_tol, int32_t probe_max_iter, double* out,
-                             int32_t* out_converged, void* stream) {
-  KGP_REQUIRE(e != nullptr && e->magic == ENGINE_MAGIC, KGP_ERR_STATE, "invalid engine handle");
-  KGP_REQUIRE(p == nullptr || p->magic == PRECOND_MAGIC, KGP_ERR_STATE, "invalid preconditioner handle");
-  KGP_REQUIRE(k_z >= 1 && max_iter >= 1 && tol >= 0.0 && probe_tol >= 0.0, KGP_ERR_INVALID, "bad solver arguments");
-  KGP_REQUIRE(out != nullptr && out_converged != nullptr, KGP_ERR_INVALID, "NULL output pointer");
-  KGP_CUDA(cudaSetDevice(e->device));
-  cudaStream_t st = (cudaStream_t)stream;
+// nlml_grad_iterative (gp.py:133-179) for C independent right-hand sides sharing the
+// kernel hyperparameters: C = 1 is GP regression; C > 1 is the Dirichlet GP
+// classification of gpc.py (class c: Khat + diag(dn_c), target y_c). Loss and gradient
+// are sums over the classes.
+static int nlml_impl(kgp_engine_s* e, const PcSet& pcs, int64_t C, const double* y, int64_t k_z,
+                     const double* probes, double tol, int32_t max_iter, double probe_tol, int32_t probe_max_iter,
+                     double* out, int32_t* out_converged, cudaStream_t st) {
   const int64_t n = e->n;
-  const int64_t kv = 1 + k_z;
+  const int64_t kv = C * (1 + k_z);
   const int nb = (int)((n + DOT_CHUNK - 1) / DOT_CHUNK);
   const int32_t pmax = probe_max_iter > 0 ? probe_max_iter : max_iter;
   const int32_t wide = pmax > max_iter ? pmax : max_iter;  // per-column stride of the coefficient arrays
-  // workspace: V = [w, Z] (kv, n); U' = [w, u] (kv, n); dV_l, dV_f (kv, n); traces; scalars
+  // workspace: V = [y_1..y_C, Z_1..Z_C] (kv, n); U = [w, u]; dV_l, dV_f; traces; scalars
   size_t vec = (size_t)kv * n;
   size_t bytes = sizeof(double) * (4 * vec + 2 * (size_t)kv * wide + 4 * kv + (size_t)kv * nb + 16) +
                  sizeof(int32_t) * (4 * kv + 8);
@@ -627,42 +641,51 @@ extern "C" int kgp_nlml_grad(kgp_engine* e, kgp_precond* p, const double* y, int
 
   // (1)+(2) w = PCG(Khat, M, y, tol) and u = CG(Khat, Z, probe_tol) (gp.py:154-160) as ONE
   // grouped solve: every iteration applies Khat once to [p_w, P_Z] (the north star's
-  // Khat [y, Z]); column 0 is preconditioned, the probe columns are not, so their
-  // coefficients rebuild the Lanczos tridiagonals of Khat itself.
-  KGP_CUDA(cudaMemcpyAsync(V, y, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-  KGP_CUDA(cudaMemcpyAsync(V + n, probes, sizeof(double) * k_z * n, cudaMemcpyDeviceToDevice, st));
-  rc = pcg_grouped_impl(e, p, kv, 1, V, tol, max_iter, probe_tol, pmax, U, alphas, betas, iters, rel, conv, st);
+  // Khat [y, Z]); the C target columns are preconditioned, the probe columns are not, so
+  // their coefficients rebuild the Lanczos tridiagonals of Khat itself.
+  KGP_CUDA(cudaMemcpyAsync(V, y, sizeof(double) * C * n, cudaMemcpyDeviceToDevice, st));
+  KGP_CUDA(cudaMemcpyAsync(V + C * n, probes, sizeof(double) * C * k_z * n, cudaMemcpyDeviceToDevice, st));
+  rc = pcg_grouped_impl(e, pcs, kv, C, V, tol, max_iter, probe_tol, pmax, U, alphas, betas, iters, rel, conv, st);
   if (rc) return rc;
-  // (3) log|Khat| by SLQ over the probe traces
-  rc = col_dots(k_z, n, probes, probes, nz2, partial, st);
+  // (3) log|Khat_c| by SLQ over each class's probe traces
+  const double* Z = V + C * n;
+  rc = col_dots(C * k_z, n, Z, Z, nz2, partial, st);
   if (rc) return rc;
   double logdet = 0.0;
-  rc = slq_impl(k_z, wide, alphas + wide, betas + wide, iters + 1, nz2, &logdet, st);
-  if (rc) return rc;
-  // (4) loss = 1/2 (y.w + logdet + n log 2 pi)
-  rc = col_dots(1, n, y, U, dots, partial, st);
-  if (rc) return rc;
-  double yw = 0.0;
-  KGP_CUDA(cudaMemcpyAsync(&yw, dots, sizeof(double), cudaMemcpyDeviceToHost, st));
-  // (5) one fused derivative pass over V = [w, Z]
-  KGP_CUDA(cudaMemcpyAsync(V, U, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-  KGP_CUDA(cudaMemcpyAsync(V + n, probes, sizeof(double) * k_z * n, cudaMemcpyDeviceToDevice, st));
-  rc = engine_matmul_impl(e, kv, V, 1, n, nullptr, dL, dF, 1, n, st);
+  for (int64_t c = 0; c < C; ++c) {
+    double ld = 0.0;
+    const size_t off = (size_t)(C + c * k_z) * wide;
+    rc = slq_impl(k_z, wide, alphas + off, betas + off, iters + C + c * k_z, nz2 + c * k_z, &ld, st);
+    if (rc) return rc;
+    logdet += ld;
+  }
+  // (4) loss = 1/2 (y.w + logdet + n log 2 pi), summed over the classes
+  rc = col_dots(C, n, y, U, dots, partial, st);
   if (rc) return rc;
   std::vector<double> hd(kv);
+  KGP_CUDA(cudaMemcpyAsync(hd.data(), dots, sizeof(double) * C, cudaMemcpyDeviceToHost, st));
+  KGP_CUDA(cudaStreamSynchronize(st));
+  double yw = 0.0;
+  for (int64_t c = 0; c < C; ++c) yw += hd[c];
+  // (5) one fused derivative pass over V = [w, Z] (the diagonal is data: no derivative term)
+  KGP_CUDA(cudaMemcpyAsync(V, U, sizeof(double) * C * n, cudaMemcpyDeviceToDevice, st));
+  rc = engine_matmul_impl(e, kv, V, 1, n, nullptr, dL, dF, 1, n, st);
+  if (rc) return rc;
   double grads[3];
   const double* dV[3] = {dL, dF, V};  // Theta.L, Theta.F, Theta.S (dKhat/ds = I, kmat.py:157-158)
   for (int th = 0; th < 3; ++th) {
-    // column dots of [w, u_1..u_kz] against dV columns: quad from column 0, trace from the rest
+    // column dots of [w, u] against dV columns: quad from the targets, trace from the probes
     rc = col_dots(kv, n, U, dV[th], dots, partial, st);
     if (rc) return rc;
     KGP_CUDA(cudaMemcpyAsync(hd.data(), dots, sizeof(double) * kv, cudaMemcpyDeviceToHost, st));
     KGP_CUDA(cudaStreamSynchronize(st));
-    double quad = -hd[0];
-    double tr = 0.0;
-    for (int64_t c = 1; c < kv; ++c) tr += hd[c];
-    tr /= (double)k_z;
-    grads[th] = 0.5 * (quad + tr);
+    double g = 0.0;
+    for (int64_t c = 0; c < C; ++c) {
+      double tr = 0.0;
+      for (int64_t j = 0; j < k_z; ++j) tr += hd[C + c * k_z + j];
+      g += 0.5 * (-hd[c] + tr / (double)k_z);
+    }
+    grads[th] = g;
   }
   std::vector<int32_t> hc(kv);
   KGP_CUDA(cudaMemcpyAsync(hc.data(), conv, sizeof(int32_t) * kv, cudaMemcpyDeviceToHost, st));
@@ -670,10 +693,68 @@ extern "C" int kgp_nlml_grad(kgp_engine* e, kgp_precond* p, const double* y, int
   int ok = 1;
   for (int64_t c = 0; c < kv; ++c) ok &= hc[c] ? 1 : 0;
   const double LOG_2PI = 1.8378770664093453;
-  out[0] = 0.5 * (yw + logdet + (double)n * LOG_2PI);
+  out[0] = 0.5 * (yw + logdet + (double)(C * n) * LOG_2PI);
   out[1] = grads[0];
   out[2] = grads[1];
   out[3] = grads[2];
   *out_converged = ok;
   return KGP_OK;
+}
+
+}  // namespace kgp
+
+using namespace kgp;
+
+extern "C" int kgp_nlml_grad(kgp_engine* e, kgp_precond* p, const double* y, int64_t k_z, const double* probes,
+                             double tol, int32_t max_iter, double probe_tol, int32_t probe_max_iter, double* out,
+                             int32_t* out_converged, void* stream) {
+  KGP_REQUIRE(e != nullptr && e->magic == ENGINE_MAGIC, KGP_ERR_STATE, "invalid engine handle");
+  KGP_REQUIRE(p == nullptr || p->magic == PRECOND_MAGIC, KGP_ERR_STATE, "invalid preconditioner handle");
+  KGP_REQUIRE(k_z >= 1 && max_iter >= 1 && tol >= 0.0 && probe_tol >= 0.0, KGP_ERR_INVALID, "bad solver arguments");
+  KGP_REQUIRE(out != nullptr && out_converged != nullptr, KGP_ERR_INVALID, "NULL output pointer");
+  KGP_REQUIRE(e->dn_classes == 0, KGP_ERR_INVALID, "engine has a per-class diagonal; use kgp_gpc_nlml_grad");
+  KGP_CUDA(cudaSetDevice(e->device));
+  kgp_precond_s* one[1] = {p};
+  return nlml_impl(e, PcSet{one, p ? 1 : 0}, 1, y, k_z, probes, tol, max_iter, probe_tol, probe_max_iter, out,
+                   out_converged, (cudaStream_t)stream);
+}
+
+extern "C" int kgp_gpc_nlml_grad(kgp_engine* e, int classes, kgp_precond* const* pcs, int npcs, const double* dn,
+                                 const double* y, int64_t k_z, const double* probes, double tol, int32_t max_iter,
+                                 double probe_tol, int32_t probe_max_iter, double* out, int32_t* out_converged,
+                                 void* stream) {
+  KGP_REQUIRE(e != nullptr && e->magic == ENGINE_MAGIC, KGP_ERR_STATE, "invalid engine handle");
+  KGP_REQUIRE(classes >= 1 && (npcs == 0 || npcs == 1 || npcs == classes), KGP_ERR_INVALID,
+              "need classes >= 1 and 0, 1 or `classes` preconditioners");
+  KGP_REQUIRE(npcs == 0 || pcs != nullptr, KGP_ERR_INVALID, "NULL preconditioner array");
+  for (int i = 0; i < npcs; ++i)
+    KGP_REQUIRE(pcs[i] != nullptr && pcs[i]->magic == PRECOND_MAGIC, KGP_ERR_STATE, "invalid preconditioner handle");
+  KGP_REQUIRE(k_z >= 1 && max_iter >= 1 && tol >= 0.0 && probe_tol >= 0.0, KGP_ERR_INVALID, "bad solver arguments");
+  KGP_REQUIRE(dn != nullptr && y != nullptr && probes != nullptr, KGP_ERR_INVALID, "NULL input pointer");
+  KGP_REQUIRE(out != nullptr && out_converged != nullptr, KGP_ERR_INVALID, "NULL output pointer");
+  KGP_REQUIRE(e->row0 == 0 && e->nrows == e->n, KGP_ERR_INVALID, "kgp_gpc_nlml_grad needs an unpartitioned engine");
+  const int64_t kv = (int64_t)classes * (1 + k_z);
+  std::vector<int32_t> map(kv);
+  for (int64_t c = 0; c < kv; ++c) map[c] = (int32_t)(c < classes ? c : (c - classes) / k_z);
+  int rc = kgp_engine_set_diag(e, classes, dn, kv, map.data(), stream);
+  if (rc) return rc;
+  rc = nlml_impl(e, PcSet{pcs, npcs}, classes, y, k_z, probes, tol, max_iter, probe_tol, probe_max_iter, out,
+                 out_converged, (cudaStream_t)stream);
+  kgp_engine_set_diag(e, 0, nullptr, 0, nullptr, stream);
+  return rc;
+}
+
+extern "C" int kgp_pcg_grouped(kgp_engine* e, kgp_precond* const* pcs, int npcs, int64_t k, int64_t kpc,
+                               const double* y, double tol1, int32_t it1, double tol2, int32_t it2, double* x_out,
+                               double* alphas, double* betas, int32_t* iters, double* rel, int32_t* converged,
+                               void* stream) {
+  KGP_REQUIRE(e != nullptr && e->magic == ENGINE_MAGIC, KGP_ERR_STATE, "invalid engine handle");
+  KGP_REQUIRE(npcs >= 0 && (npcs == 0 || pcs != nullptr), KGP_ERR_INVALID, "bad preconditioner array");
+  for (int i = 0; i < npcs; ++i)
+    KGP_REQUIRE(pcs[i] != nullptr && pcs[i]->magic == PRECOND_MAGIC, KGP_ERR_STATE, "invalid preconditioner handle");
+  KGP_REQUIRE(k >= 1 && tol1 >= 0.0 && tol2 >= 0.0, KGP_ERR_INVALID, "bad solver arguments");
+  KGP_REQUIRE(e->row0 == 0 && e->nrows == e->n, KGP_ERR_INVALID, "kgp_pcg_grouped needs an unpartitioned engine");
+  KGP_CUDA(cudaSetDevice(e->device));
+  return pcg_grouped_impl(e, PcSet{pcs, npcs}, k, kpc, y, tol1, it1, tol2, it2, x_out, alphas, betas, iters, rel,
+                          converged, (cudaStream_t)stream);
 }

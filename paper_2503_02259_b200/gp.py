@@ -166,7 +166,8 @@ def nlml_grad_iterative(engine, y, preconditioner, probes: ProbeSet, tol: float 
     if probe_tol is None:
         probe_tol = tol
     ours = isinstance(engine, KernelEngine)
-    pre_ok = preconditioner is None or isinstance(preconditioner, precond_mod.NystromPreconditioner)
+    pre_ok = preconditioner is None or isinstance(
+        preconditioner, (precond_mod.NystromPreconditioner, precond_mod.AFNPreconditioner))
     if not (ours and pre_ok):
         if probe_max_iter is not None:
             raise ValueError("probe_max_iter needs this package's KernelEngine")

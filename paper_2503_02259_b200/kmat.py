@@ -127,6 +127,15 @@ class KernelEngine:
              self.params.f, self.params.s, _device.stream_ptr())
         self.x.setflags(write=False)
 
+    def set_params(self, params) -> None:
+        """Reset (l, f, s) in place, keeping X resident (a training loop's per-step update;
+        the reference builds a new engine per step, train.py:198-204)."""
+        if not isinstance(params, Hyperparams):
+            params = Hyperparams(float(params.l), float(params.f), float(params.s))
+        call("kgp_engine_set_params", self._handle, params.l, params.f, params.s, _device.stream_ptr())
+        self.params = params
+        self._khat = None
+
     # ----------------------------------------------------------------- lifetime
     @property
     def handle(self):

@@ -228,8 +228,10 @@ class AFNPreconditioner:
             pass
 
 
-def build_afn(engine, m: int | None = None, fsai_npt: int = AFN_DEFAULT_NPT) -> AFNPreconditioner:
-    """AFN for an engine's Khat: m FPS landmarks (exact block) + FSAI of the Schur complement."""
+def build_afn(engine, m: int | None = None, fsai_npt: int = AFN_DEFAULT_NPT, diag=None) -> AFNPreconditioner:
+    """AFN for an engine's Khat: m FPS landmarks (exact block) + FSAI of the Schur complement.
+    ``diag`` (n,) adds a per-point shift: the preconditioner then targets Khat + diag(diag)
+    (one class of the Dirichlet GPC, gpc.py)."""
     torch = _device.torch()
     n = engine.n
     if m is None:
@@ -251,8 +253,16 @@ def build_afn(engine, m: int | None = None, fsai_npt: int = AFN_DEFAULT_NPT) -> 
     n2 = n - m
     x1 = xd.index_select(0, idx).contiguous()
     x2 = xd.index_select(0, rest).contiguous()
+    dd = None
+    if diag is not None:
+        dd = diag if _device.is_tensor(diag) else torch.from_numpy(np.asarray(diag, dtype=np.float64))
+        dd = dd.to(device=dev, dtype=torch.float64).reshape(-1)
+        if dd.shape[0] != n:
+            raise ValueError(f"diag must have length {n}, got {dd.shape[0]}")
     k11 = device_panel(kid, 0, x1, x1, p.l).mul_(f2)
     k11.diagonal().add_(p.s)
+    if dd is not None:
+        k11.diagonal().add_(dd.index_select(0, idx))
     low, info = torch.linalg.cholesky_ex(k11)
     if int(info) != 0:
         raise BreakdownError("AFN landmark block is not positive definite; increase s or reduce m")
@@ -265,8 +275,10 @@ def build_afn(engine, m: int | None = None, fsai_npt: int = AFN_DEFAULT_NPT) -> 
     nbr = knn_prev_device(x2, npt)
     gval = torch.empty((npt + 1, n2), dtype=torch.float64, device=dev)
     gcol = torch.empty((npt + 1, n2), dtype=torch.int32, device=dev)
-    call("kgp_afn_fsai", kid, n2, x2.shape[1], x2.data_ptr(), float(p.l), float(p.f), float(p.s), m, w.data_ptr(),
-         npt, nbr.data_ptr(), gval.data_ptr(), gcol.data_ptr(), _device.stream_ptr())
+    d2 = None if dd is None else dd.index_select(0, rest).contiguous()
+    call("kgp_afn_fsai", kid, n2, x2.shape[1], x2.data_ptr(), float(p.l), float(p.f), float(p.s),
+         None if d2 is None else d2.data_ptr(), m, w.data_ptr(), npt, nbr.data_ptr(), gval.data_ptr(),
+         gcol.data_ptr(), _device.stream_ptr())
     # G^T as CSR: entries sorted by (column, row)
     rows = torch.arange(n2, dtype=torch.int64, device=dev).expand(npt + 1, n2).reshape(-1)
     cols = gcol.reshape(-1).to(torch.int64)

@@ -74,14 +74,19 @@ def cfg3(n: int = 262144, seed: int = 0, k_z: int = 32) -> Workload:
 
 
 def cfg4(n: int = 131072, seed: int = 0) -> Workload:
-    """GPC 3-class shape: Gaussian, d=8, X~N(0,I) fp32, 16 probes, rank 512.
+    """GPC 3-class (BASELINE configs[3]): Gaussian, d=8, X~N(0,I) fp32, labels = argmax of
+    3 latent GP draws (l=1) from the seed, 16 probes, AFN rank 512, 10 training steps.
 
-    The reference has no GPC and no large-n GP sampler, so the
-    latent draws are left to the caller; this returns the operator inputs only."""
+    The reference has no GPC and no large-n GP sampler: the latent draws
+    are random-Fourier-feature draws of the l=1 Gaussian GP (gpc.sample_latent_labels),
+    labels in extra["labels"]."""
+    from paper_2503_02259_b200.gpc import sample_latent_labels
+
     rng = np.random.default_rng(seed)
     x = rng.standard_normal((n, 8)).astype(np.float32).astype(np.float64)
+    labels = sample_latent_labels(x, 3, l=1.0, seed=seed)
     return Workload("cfg4", "gaussian", x, 1.0, 1.0, 1e-2, k_z=16, probe_seed=seed,
-                    rank=min(512, n))
+                    rank=min(512, n), extra={"labels": labels, "classes": 3, "train_steps": 10})
 
 
 def cfg5(n: int = 1048576, m_test: int = 262144, seed: int = 0) -> Workload:

@@ -108,7 +108,8 @@ def test_lazy_exports_match_reference_surface():
                  "cg_solve", "pcg_solve", "build_tridiag", "slq_logdet", "LossGrad", "Prediction", "ProbeSet",
                  "nlml_exact", "grad_exact", "nlml_grad_iterative", "predict", "RawParams", "TrainConfig",
                  "TrainResult", "fit"}
-    assert set(p.__all__) == ref_names
+    extensions = {"AFNPreconditioner"}  # north-star additions beyond kernelgp/__init__.py:16-44
+    assert set(p.__all__) == ref_names | extensions
     for name in ref_names:
         getattr(p, name)
 
