@@ -20,7 +20,7 @@ from paper_2503_02259_b200.errors import (
 )
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libkgp.so")
+LIB_PATH = os.environ.get("KGP_LIB") or os.path.join(HERE, "libkgp.so")  # KGP_LIB: tuning builds only
 
 OK, ERR_INVALID, ERR_RESOURCE, ERR_BREAKDOWN, ERR_NUMERICAL, ERR_CUDA, ERR_STATE = range(7)
 KERNEL_IDS = {"gaussian": 0, "matern32": 1, "matern52": 2}

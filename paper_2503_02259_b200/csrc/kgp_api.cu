@@ -130,10 +130,15 @@ static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t 
   const int nout = out_dl ? 2 : 1;
   const int tpo = split == 3 ? 2 : 1;
   const int nblk = (int)((e->n + 31) / 32);
-  const int kmax = tc_max_kp(e->dpad, nout, split);
+  // two accumulator buffers when the RHS block fits, else one (the drain then briefly
+  // stalls the MMA every `flush` blocks, still far cheaper than a second pass)
+  const int kmax2 = tc_max_kp(e->dpad, nout, split, 2);
+  const int kmax1 = tc_max_kp(e->dpad, nout, split, 1);
+  const int kmax = k <= kmax2 ? kmax2 : kmax1;
   for (int64_t c0 = 0; c0 < k; c0 += kmax) {
     const int kc = (int)((k - c0) < kmax ? (k - c0) : kmax);
     const int kp = (kc + 15) / 16 * 16;
+    const int nab = kp <= kmax2 ? 2 : 1;
     int rc = e->bsplit.ensure((size_t)nblk * tpo * kp * 128);
     if (rc) return rc;
     rc = prep_rhs(split, e->n, k, c0, kp, b, b_rs, b_cs, e->bsplit.as<uint8_t>(), st);
@@ -147,6 +152,7 @@ static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t 
     p.kp = kp;
     p.k = kc;
     p.nsa = tc_nsa(e->dpad, nout, split, kp);
+    p.nab = nab;
     const int nsplit = tc_col_split(nrows, nblk);
     p.nper = (nblk + nsplit - 1) / nsplit;
     p.part = nullptr;

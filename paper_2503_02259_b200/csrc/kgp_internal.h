@@ -22,6 +22,7 @@ struct TcParams {
   int k;                  // true RHS count in this launch
   int nsa;                // TMEM A-stage ring depth
   int nsb;                // shared-memory ring depth (set at launch)
+  int nab;                // TMEM accumulator buffers: 2 (drain overlaps the MMA) or 1 (wider kp)
   int flush;              // blocks per TMEM accumulation segment before promotion to fp32 smem
   int debug;              // diagnostic bit flags (env KGP_TC_DEBUG): 1 no contraction MMA, 2 no distance MMA, 4 no transform
   double f2, s, two_f, scale_dl;
@@ -33,11 +34,12 @@ struct TcParams {
   cudaEvent_t ev_start, ev_stop;  // host side: optional timing bracket around the main kernel
 };
 int tc_pad_dim(int d);
-int tc_max_kp(int dpad, int nout, int split);
+int tc_max_kp(int dpad, int nout, int split, int nab);
 int tc_col_split(int64_t nrows, int nblk);
 int tc_nsa(int dpad, int nout, int split, int kp);
 int tc_col_block_bytes(int dpad);
 bool tc_direct(int dpad);
+int tc_dist_mode(int dpad);  // 0 direct differences, 1 tensor-core expansion, 2 FP32 expansion
 int launch_kmm_tc(int kt, int dpad, int nout, int split, const TcParams& p, cudaStream_t st);
 
 // ------------------------------------------------------------------ fp64 operator

@@ -37,14 +37,20 @@ namespace kgp {
 
 namespace {
 
-constexpr int NCW = 8;                    // compute warps (2 per TMEM lane quadrant)
-constexpr int WPROD = NCW, WMMA = NCW + 1, WDIST = NCW + 2;
-constexpr int NTHREADS = (NCW + 7) * 32;  // + producer, contraction MMA, distance MMA, 4 drain = 480
+// Compute warp sets: set e handles blocks t = e (mod NS); every ring a set touches (TMEM
+// A stages, distance buffers) has NS slots so each slot has exactly one writer set.
+// NS = 2 when the A stages are wide (two outputs, hi/lo), 3 otherwise (TMEM budget).
+#ifndef KGP_TC_NSET
+#define KGP_TC_NSET 0  // 0: per-configuration default (ns_for)
+#endif
+constexpr int ns_for(int nout, int split) {
+  return KGP_TC_NSET ? KGP_TC_NSET : ((nout == 2 && split == 3) ? 2 : 3);
+}
+constexpr int WPS = 4;                    // warps per set = one per TMEM lane quadrant
+constexpr int MAXNS = 4;
 constexpr int MAXNSB = 8;                 // shared-memory ring depth: runtime p.nsb in {4, 8}
 constexpr int BJ = 32;                    // columns per block
-constexpr int ND = 2;                     // distance accumulator buffers in TMEM (one per warp set)
-constexpr int NSET = 2;                   // compute warp sets: set e handles blocks t = e (mod 2)
-constexpr int WPS = NCW / NSET;           // warps per set = one per TMEM lane quadrant
+constexpr int nthreads_for(int ns) { return (ns * WPS + 7) * 32; }  // + producer, 2 MMA issuers, 4 drain
 
 KGP_DEV float ex2f(float x) {
   float y;
@@ -117,18 +123,30 @@ KGP_DEV void store_tile(uint32_t taddr, const float2 (&v)[2][4]) {
   }
 }
 
+#ifndef KGP_TC_XP
+#define KGP_TC_XP 0  // measured: the FP32 expansion is slower than the tensor-core distance at d = 8 (FP32-pipe bound)
+#endif
 template <int D>
 struct Geo {
-  static constexpr bool DMMA = (D > 4);                      // distance on the tensor core
+  // d > 4: t2 by the expansion q_i + q_j + u_i.v_j, on the FP32 pipe (XP) or as a tensor-core
+  // MMA into TMEM (DMMA); d <= 4: direct differences on the FP32 pipe
+  static constexpr bool XP = (D > 4) && KGP_TC_XP;
+  static constexpr bool DMMA = (D > 4) && !KGP_TC_XP;
   static constexpr int KD = ((D + 2) + 7) / 8 * 8;           // augmented K of the distance MMA
   static constexpr uint32_t VBYTES = DMMA ? 2u * BJ * KD * 4u : (uint32_t)(D + 1) * BJ * 4u;  // per block
   static constexpr uint32_t UBYTES = 0u;  // U' lives in TMEM
 };
 
 template <int KT, int D, int NOUT, int SPLIT>
-__global__ void __launch_bounds__(NTHREADS, 1) kmm_tc_kernel(const TcParams p) {
+__global__ void __launch_bounds__(nthreads_for(ns_for(NOUT, SPLIT)), 1) kmm_tc_kernel(const TcParams p) {
+  constexpr int NS = ns_for(NOUT, SPLIT);
+  constexpr int NSET = NS, ND = NS, NSA = NS;   // sets, distance buffers, A stages
+  constexpr int NCW = NS * WPS;                 // compute warps
+  constexpr int WPROD = NCW, WMMA = NCW + 1, WDIST = NCW + 2;
+  static_assert(NS <= MAXNS, "ring slots");
   using G = Geo<D>;
   constexpr bool DMMA = G::DMMA;
+  constexpr bool XP = G::XP;
   constexpr int KD = G::KD;
   constexpr int KDS = (KD + 15) / 16 * 16;  // TMEM column stride of U' hi -> lo
   constexpr int TPO = (SPLIT == 3) ? 2 : 1;  // TMEM tiles per output (hi, lo)
@@ -150,17 +168,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmm_tc_kernel(const TcParams p) {
   uint64_t* full = bars;
   uint64_t* empty = bars + MAXNSB;
   uint64_t* afull = bars + 2 * MAXNSB;
-  uint64_t* aempty = bars + 2 * MAXNSB + 4;
-  uint64_t* accfull = bars + 2 * MAXNSB + 8;
-  uint64_t* accempty = bars + 2 * MAXNSB + 10;
-  uint64_t* dfull = bars + 2 * MAXNSB + 12;
-  uint64_t* dempty = bars + 2 * MAXNSB + 12 + ND;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * MAXNSB + 12 + 2 * ND);
+  uint64_t* aempty = afull + MAXNS;
+  uint64_t* accfull = aempty + MAXNS;
+  uint64_t* accempty = accfull + 2;
+  uint64_t* dfull = accempty + 2;
+  uint64_t* dempty = dfull + MAXNS;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dempty + MAXNS);
+  static_assert(8 * (2 * MAXNSB + 4 * MAXNS + 4) + 4 <= 512, "barrier area");
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int NSA = p.nsa;
-  const int dbase = 2 * NACC;                      // distance buffers follow the accumulators
+  const int NAB = p.nab;                           // accumulator buffers (2: ping-pong with the drain)
+  const int dbase = NAB * NACC;                    // distance buffers follow the accumulators
   const int ucol = dbase + (DMMA ? ND * BJ : 0);   // then U' hi | lo (KD columns each)
   const int abase = ucol + (DMMA ? 2 * KDS : 0);   // then the A stages
   // column split (grid.y): this CTA sweeps column blocks [t0, t0 + nblk)
@@ -271,8 +290,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmm_tc_kernel(const TcParams p) {
       __syncwarp();
       if (last) {
         pos = 0;
-        if (ab == 1) ph_acc ^= 1;
-        ab ^= 1;
+        if (++ab == NAB) { ab = 0; ph_acc ^= 1; }
       } else {
         ++pos;
       }
@@ -320,21 +338,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmm_tc_kernel(const TcParams p) {
     const int g = lane & 3;
     // rows owned by this thread: 32 qd + lane/4 + {0, 8, 16, 24}; columns 2g + {0,1} + 8m, m < 4
     float u[4][DMMA ? 1 : D];
+    float qi[4];
     if (!DMMA) {
 #pragma unroll
       for (int rr = 0; rr < 4; ++rr) {
         const int64_t r = (int64_t)blockIdx.x * 128 + qd * 32 + (lane >> 2) + 8 * rr;
         const bool ok = r < p.nrows;
         const float* xr = p.xrow + (ok ? r : 0) * (D + 1);
+        qi[rr] = ok ? xr[0] : 0.f;
 #pragma unroll
         for (int k = 0; k < (DMMA ? 1 : D); ++k) u[rr][k] = ok ? xr[1 + k] : 0.f;
       }
     }
     const uint32_t lane_base = tbase + ((uint32_t)(qd * 32) << 16);
-    const int nsa_log = (NSA == 4) ? 2 : 1;
     for (int t = set; t < nblk; t += NSET) {
-      const int s = t & (NSB - 1), a = t & (NSA - 1), db = t & (ND - 1);
-      const uint32_t ph_s = (t >> nsb_log) & 1, ph_a = (t >> nsa_log) & 1, ph_d = (t / ND) & 1;
+      const int s = t & (NSB - 1), a = t % NSA, db = t % ND;
+      const uint32_t ph_s = (t >> nsb_log) & 1, ph_a = (t / NSA) & 1, ph_d = (t / ND) & 1;
       float2 acc[4][4];  // [row][column pair m]: rows lane/4 + 8 rr, columns 2g + 8m + {0,1}
       if (DMMA) {
         mbar_wait(&dfull[db], ph_d);
@@ -358,10 +377,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmm_tc_kernel(const TcParams p) {
         mbar_wait(&full[s], ph_s);
         // this thread's 8 columns, permuted by prep_cols into two float4 at 8g
         const float* xs = reinterpret_cast<const float*>(sV + s * VBYTES) + 8 * g;
+        if (XP) {  // t2 = q_i + q_j + sum_k u_ik v_jk   (u = -2 gamma c_i, v = c_j, q = gamma |c|^2)
+          const float4 qa = *reinterpret_cast<const float4*>(xs);
+          const float4 qb = *reinterpret_cast<const float4*>(xs + 4);
+          const float2 qj[4] = {make_float2(qa.x, qa.y), make_float2(qa.z, qa.w), make_float2(qb.x, qb.y),
+                                make_float2(qb.z, qb.w)};
 #pragma unroll
-        for (int rr = 0; rr < 4; ++rr)
+          for (int rr = 0; rr < 4; ++rr)
 #pragma unroll
-          for (int m = 0; m < 4; ++m) acc[rr][m] = make_float2(0.f, 0.f);
+            for (int m = 0; m < 4; ++m) acc[rr][m] = __fadd2_rn(qj[m], make_float2(qi[rr], qi[rr]));
+        } else {
+#pragma unroll
+          for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+            for (int m = 0; m < 4; ++m) acc[rr][m] = make_float2(0.f, 0.f);
+        }
 #pragma unroll
         for (int k = 0; k < (DMMA ? 1 : D); ++k) {
           const float4 va = *reinterpret_cast<const float4*>(xs + (k + 1) * BJ);
@@ -373,8 +403,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmm_tc_kernel(const TcParams p) {
             const float2 uk = make_float2(u[rr][k], u[rr][k]);
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
-              const float2 dd = fsub2(vv[m], uk);
-              acc[rr][m] = __ffma2_rn(dd, dd, acc[rr][m]);
+              if (XP) {
+                acc[rr][m] = __ffma2_rn(uk, vv[m], acc[rr][m]);
+              } else {
+                const float2 dd = fsub2(vv[m], uk);
+                acc[rr][m] = __ffma2_rn(dd, dd, acc[rr][m]);
+              }
             }
           }
         }
@@ -432,8 +466,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) kmm_tc_kernel(const TcParams p) {
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&accempty[ab]);
-      if (ab == 1) ph ^= 1;
-      ab ^= 1;
+      if (++ab == NAB) { ab = 0; ph ^= 1; }
     }
     // epilogue: fp64 scaling, + s B on the diagonal rows, strided writes -- or, when the
     // columns are split over grid.y, the raw fp32 partial sums for tc_reduce_kernel
@@ -506,7 +539,7 @@ int launch_one(const TcParams& p_in, cudaStream_t st) {
   const int nsplit = (p.nblk + p.nper - 1) / p.nper;
   dim3 grid((unsigned)((p.nrows + 127) / 128), (unsigned)nsplit);
   if (p.ev_start) KGP_CUDA(cudaEventRecord(p.ev_start, st));
-  kern<<<grid, NTHREADS, smem, st>>>(p);
+  kern<<<grid, nthreads_for(ns_for(NOUT, SPLIT)), smem, st>>>(p);
   KGP_LAUNCH("kmm_tc_kernel");
   if (p.ev_stop) KGP_CUDA(cudaEventRecord(p.ev_stop, st));
   if (nsplit > 1) {
@@ -539,33 +572,37 @@ int launch_kt(const TcParams& p, int dpad, int nout, int split, cudaStream_t st)
 
 int tc_pad_dim(int d) { return d <= 2 ? 2 : d <= 4 ? 4 : d <= 8 ? 8 : 16; }
 bool tc_direct(int dpad) { return dpad <= 4; }
+int tc_dist_mode(int dpad) { return dpad <= 4 ? 0 : (KGP_TC_XP ? 2 : 1); }
 
 int tc_col_block_bytes(int dpad) {
-  if (dpad <= 4) return (dpad + 1) * BJ * 4;
+  if (tc_dist_mode(dpad) != 1) return (dpad + 1) * BJ * 4;
   const int kd = ((dpad + 2) + 7) / 8 * 8;
   return 2 * BJ * kd * 4;
 }
 
-static int tc_fixed_cols(int dpad) {
-  if (tc_direct(dpad)) return 0;
+static int tc_fixed_cols(int dpad, int ns) {
+  if (tc_dist_mode(dpad) != 1) return 0;
   const int kd = ((dpad + 2) + 7) / 8 * 8;
-  return ND * BJ + 2 * ((kd + 15) / 16 * 16);  // distance buffers + U' hi/lo
+  return ns * BJ + 2 * ((kd + 15) / 16 * 16);  // distance buffers + U' hi/lo
 }
 
-int tc_max_kp(int dpad, int nout, int split) {
-  // TMEM: two accumulator buffers (2 nout kp) + distance buffers + U' + at least two A stages
+// RHS columns per launch with `nab` accumulator buffers: TMEM holds nab x nout x kp
+// accumulator columns + distance buffers + U' + NS A stages
+int tc_max_kp(int dpad, int nout, int split, int nab) {
+  const int ns = ns_for(nout, split);
   const int stage = nout * (split == 3 ? 2 : 1) * 32;
-  int kp = (512 - tc_fixed_cols(dpad) - 2 * stage) / (2 * nout);
+  int kp = (512 - tc_fixed_cols(dpad, ns) - ns * stage) / (nab * nout);
   kp = kp / 16 * 16;
-  return kp > 128 ? 128 : kp;
+  if (kp > 128) kp = 128;
+  // shared memory (launch_one): fp32 promotion sums + at least a 4-deep operand ring
+  const int tpo = split == 3 ? 2 : 1;
+  while (kp > 16 && (size_t)nout * kp * 128 * 4 + 512 + 4 * ((size_t)tpo * kp * 128 + tc_col_block_bytes(dpad)) >
+                        225 * 1024)
+    kp -= 16;
+  return kp;
 }
 
-int tc_nsa(int dpad, int nout, int split, int kp) {
-  const int stage = nout * (split == 3 ? 2 : 1) * 32;
-  int nsa = (512 - tc_fixed_cols(dpad) - 2 * nout * kp) / stage;
-  // a power of two >= 2: the two compute warp sets step through the ring by 2
-  return nsa >= 4 ? 4 : 2;
-}
+int tc_nsa(int, int nout, int split, int) { return ns_for(nout, split); }
 
 // Column split factor that fills the last wave of 148 SMs (1 CTA/SM): the smallest
 // S <= 8 reaching 95% wave efficiency with >= 16 column blocks per CTA.

@@ -52,7 +52,7 @@ __global__ void prep_rows_kernel(int kt, int d, int dpad, bool direct, int64_t n
   o[0] = direct ? 0.0f : (float)(gamma * nrm);
 }
 
-__global__ void prep_cols_kernel(int kt, int d, int dpad, bool direct, int64_t n, int nblk,
+__global__ void prep_cols_kernel(int kt, int d, int dpad, int mode, int64_t n, int nblk,
                                  const double* __restrict__ x, const double* __restrict__ mean, double gamma,
                                  float* __restrict__ out) {
   int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -64,15 +64,16 @@ __global__ void prep_cols_kernel(int kt, int d, int dpad, bool direct, int64_t n
     c[k] = (j < n && k < d) ? x[j * d + k] - mean[k] : 0.0;
     nrm += c[k] * c[k];
   }
-  if (direct) {
+  if (mode != 1) {
     // position inside the block: the tile kernel's thread g reads columns
     // 2g + {0, 1} + 8m (m < 4) as two float4 at 8g
+    // mode 0 (direct differences): [0 | sqrt(gamma) c_j]; mode 2 (FP32 expansion): [gamma |c_j|^2 | c_j]
     const int m = jj >> 3, cc = jj & 7;
     const int pos = 8 * (cc >> 1) + 2 * m + (cc & 1);
     float* o = out + t * (int64_t)(dpad + 1) * 32;
-    const double sg = sqrt(gamma);
+    const double sg = mode == 0 ? sqrt(gamma) : 1.0;
     for (int k = 0; k < dpad; ++k) o[(1 + k) * 32 + pos] = (float)(sg * c[k]);
-    o[pos] = 0.0f;
+    o[pos] = mode == 0 ? 0.0f : (float)(gamma * nrm);
     return;
   }
   // tensor-core distance: V'_j = [c_j (dpad), 1, q_j, 0 ...] as tf32 hi / lo tiles
@@ -142,7 +143,7 @@ int prep_cols(int kt, int d, int dpad, int64_t n, const double* x, const double*
               cudaStream_t st) {
   int nblk = (int)((n + 31) / 32);
   int64_t tot = (int64_t)nblk * 32;
-  prep_cols_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(kt, d, dpad, tc_direct(dpad), n, nblk, x, mean,
+  prep_cols_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(kt, d, dpad, tc_dist_mode(dpad), n, nblk, x, mean,
                                                                     kernel_gamma(kt, l), out);
   KGP_LAUNCH("prep_cols_kernel");
   return KGP_OK;
