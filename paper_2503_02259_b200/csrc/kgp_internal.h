@@ -148,6 +148,7 @@ struct kgp_precond_s {
   kgp::DevBuf wt;    // Nystrom: (m, n) row-major
   kgp::DevBuf tmp;   // split-K partials
   kgp::DevBuf tproj; // (m, k) projection U^T B
+  kgp::DevBuf tmp2;  // expansion partials (kept apart from tmp: the projection result may live there)
   // AFN (afn.cu): landmarks first, then the rest (n2 = n - m points)
   int64_t n2 = 0, nnz = 0;
   int npt1 = 0;       // FSAI row width (neighbours + the diagonal)

@@ -111,12 +111,199 @@ __global__ void finish_partials_kernel(int64_t M, int64_t N, int nz, const doubl
   c[i * c_is + j * c_ns] = v;
 }
 
+// ------------------------------------------------------------------ skinny products (N <= 8 RHS)
+// The 64x64-tile kernel wastes 63/64 of its work and most of the machine when N is 1..8
+// (the PCG w-solve applies M^-1 to ONE column every iteration). These two kernels are
+// plain HBM/L2 streams over A with the N right-hand-side values broadcast, each writing
+// fixed-order split-K partials (deterministic) finished by finish_partials_kernel.
+constexpr int SK_MAXN = 8;
+
+// A rows contiguous along K (a_ks == 1): one CTA per (output row, K chunk); threads stride
+// the chunk with four independent loads in flight each, block-reduced in fixed order.
+template <int N>
+__global__ void __launch_bounds__(256) skinny_rowdot_kernel(int64_t M, int64_t K, int64_t kchunk,
+                                                            const double* __restrict__ a, int64_t a_is,
+                                                            const double* __restrict__ b, int64_t b_ks, int64_t b_ns,
+                                                            double* __restrict__ part) {
+  const int64_t i = blockIdx.x;
+  const int64_t q0 = (int64_t)blockIdx.y * kchunk;
+  const int64_t q1 = q0 + kchunk < K ? q0 + kchunk : K;
+  const double* ar = a + i * a_is;
+  double acc[4][N];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int c = 0; c < N; ++c) acc[u][c] = 0.0;
+  int64_t q = q0 + threadIdx.x;
+  for (; q + 3 * 256 < q1; q += 4 * 256) {
+    double av[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) av[u] = ar[q + u * 256];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int c = 0; c < N; ++c) acc[u][c] = fma(av[u], b[(q + u * 256) * b_ks + c * b_ns], acc[u][c]);
+  }
+  for (; q < q1; q += 256)
+#pragma unroll
+    for (int c = 0; c < N; ++c) acc[0][c] = fma(ar[q], b[q * b_ks + c * b_ns], acc[0][c]);
+  __shared__ double red[8][N];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    const double v = warp_sum((acc[0][c] + acc[1][c]) + (acc[2][c] + acc[3][c]));
+    if (lane == 0) red[w][c] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < N) {
+    double v = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v += red[k][threadIdx.x];
+    part[((int64_t)blockIdx.y * M + i) * N + threadIdx.x] = v;
+  }
+}
+
+// short rows (K chunk < 4096): one warp per output row, lanes stride K, 4 loads in flight
+template <int N>
+__global__ void __launch_bounds__(256) skinny_rowwarp_kernel(int64_t M, int64_t K, const double* __restrict__ a,
+                                                             int64_t a_is, const double* __restrict__ b,
+                                                             int64_t b_ks, int64_t b_ns, double* __restrict__ part) {
+  const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= M) return;
+  const double* ar = a + i * a_is;
+  double acc[4][N];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int c = 0; c < N; ++c) acc[u][c] = 0.0;
+  int64_t q = lane;
+  for (; q + 96 < K; q += 128) {
+    double av[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) av[u] = ar[q + 32 * u];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int c = 0; c < N; ++c) acc[u][c] = fma(av[u], b[(q + 32 * u) * b_ks + c * b_ns], acc[u][c]);
+  }
+  for (; q < K; q += 32)
+#pragma unroll
+    for (int c = 0; c < N; ++c) acc[0][c] = fma(ar[q], b[q * b_ks + c * b_ns], acc[0][c]);
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    const double v = warp_sum((acc[0][c] + acc[1][c]) + (acc[2][c] + acc[3][c]));
+    if (lane == 0) part[i * N + c] = v;
+  }
+}
+
+// A contiguous along M (a_is == 1): one thread per output row, the B chunk staged in smem.
+constexpr int SK_QC = 128;
+template <int N>
+__global__ void __launch_bounds__(256) skinny_col_kernel(int64_t M, int64_t K, int64_t kchunk,
+                                                         const double* __restrict__ a, int64_t a_ks,
+                                                         const double* __restrict__ b, int64_t b_ks, int64_t b_ns,
+                                                         double* __restrict__ part) {
+  __shared__ double bs[SK_QC * N];
+  const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  const int64_t q0 = (int64_t)blockIdx.y * kchunk;
+  const int64_t q1 = q0 + kchunk < K ? q0 + kchunk : K;
+  double acc[N];
+#pragma unroll
+  for (int c = 0; c < N; ++c) acc[c] = 0.0;
+  for (int64_t qb = q0; qb < q1; qb += SK_QC) {
+    const int nq = (int)(q1 - qb < SK_QC ? q1 - qb : SK_QC);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nq * N; e += 256) bs[e] = b[(qb + e / N) * b_ks + (e % N) * b_ns];
+    __syncthreads();
+    if (i < M) {
+      const double* ac = a + i + qb * a_ks;
+      int q = 0;
+      for (; q + 8 <= nq; q += 8) {
+        double av[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) av[u] = ac[(int64_t)(q + u) * a_ks];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+          for (int c = 0; c < N; ++c) acc[c] = fma(av[u], bs[(q + u) * N + c], acc[c]);
+      }
+      for (; q < nq; ++q)
+#pragma unroll
+        for (int c = 0; c < N; ++c) acc[c] = fma(ac[(int64_t)q * a_ks], bs[q * N + c], acc[c]);
+    }
+  }
+  if (i >= M) return;
+#pragma unroll
+  for (int c = 0; c < N; ++c) part[((int64_t)blockIdx.y * M + i) * N + c] = acc[c];
+}
+
+template <int N>
+int skinny_launch(int kind, int64_t M, int64_t K, int64_t nz, int64_t kchunk, const double* a, int64_t a_is,
+                  int64_t a_ks, const double* b, int64_t b_ks, int64_t b_ns, double* part, cudaStream_t st) {
+  if (kind == 2) {
+    skinny_rowwarp_kernel<N><<<(unsigned)((M + 7) / 8), 256, 0, st>>>(M, K, a, a_is, b, b_ks, b_ns, part);
+    KGP_LAUNCH("skinny_rowwarp_kernel");
+  } else if (kind == 1) {
+    skinny_rowdot_kernel<N><<<dim3((unsigned)M, (unsigned)nz), 256, 0, st>>>(M, K, kchunk, a, a_is, b, b_ks, b_ns,
+                                                                             part);
+    KGP_LAUNCH("skinny_rowdot_kernel");
+  } else {
+    skinny_col_kernel<N><<<dim3((unsigned)((M + 255) / 256), (unsigned)nz), 256, 0, st>>>(M, K, kchunk, a, a_ks, b,
+                                                                                          b_ks, b_ns, part);
+    KGP_LAUNCH("skinny_col_kernel");
+  }
+  return KGP_OK;
+}
+
+// C = alpha A B + beta SRC for N <= SK_MAXN; A has a unit stride along K or along M
+int skinny_gemm(int64_t M, int64_t N, int64_t K, const double* a, int64_t a_is, int64_t a_ks, const double* b,
+                int64_t b_ks, int64_t b_ns, double* c, int64_t c_is, int64_t c_ns, double alpha, double beta,
+                const double* src, int64_t s_is, int64_t s_ns, DevBuf& tmp, cudaStream_t st) {
+  // kind 1: CTA per (row, K chunk) for long rows; 2: warp per row for short rows; 0: column kernel
+  const int kind = (a_ks == 1) ? (K >= 8192 ? 1 : 2) : 0;
+  int64_t nz = 1, kchunk = K > 0 ? K : 1;
+  if (kind != 2) {
+    const int64_t gx = kind == 1 ? M : (M + 255) / 256;
+    // K chunks: enough CTAs for ~8 per SM, each streaming >= 4096 (row) / 512 (column) elements
+    nz = (1184 + gx - 1) / gx;
+    const int64_t min_chunk = kind == 1 ? 4096 : 512;
+    if (nz > (K + min_chunk - 1) / min_chunk) nz = (K + min_chunk - 1) / min_chunk;
+    if (nz < 1) nz = 1;
+    if (nz > 65535) nz = 65535;
+    kchunk = (K + nz - 1) / nz;
+    if (kchunk < 1) kchunk = 1;
+    nz = (K + kchunk - 1) / kchunk;
+    if (nz < 1) nz = 1;
+  }
+  int rc = tmp.ensure(sizeof(double) * (size_t)(M * N * nz));
+  if (rc) return rc;
+  double* part = tmp.as<double>();
+  if (K <= 0) {
+    KGP_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * M * N, st));
+  } else {
+    switch (N) {
+#define KGP_SK(NN) \
+  case NN: rc = skinny_launch<NN>(kind, M, K, nz, kchunk, a, a_is, a_ks, b, b_ks, b_ns, part, st); break;
+      KGP_SK(1) KGP_SK(2) KGP_SK(3) KGP_SK(4) KGP_SK(5) KGP_SK(6) KGP_SK(7) KGP_SK(8)
+#undef KGP_SK
+    }
+    if (rc) return rc;
+  }
+  finish_partials_kernel<<<(unsigned)((M * N + 255) / 256), 256, 0, st>>>(M, N, (int)nz, part, alpha, beta, src,
+                                                                          s_is, s_ns, c, c_is, c_ns);
+  KGP_LAUNCH("finish_partials_kernel");
+  return KGP_OK;
+}
+
 }  // namespace
 
 int gemm_f64(int64_t M, int64_t N, int64_t K, const double* a, int64_t a_is, int64_t a_ks, const double* b,
              int64_t b_ks, int64_t b_ns, double* c, int64_t c_is, int64_t c_ns, double alpha, double beta,
              const double* src, int64_t s_is, int64_t s_ns, DevBuf& tmp, cudaStream_t st) {
   if (M <= 0 || N <= 0) return KGP_OK;
+  if (N <= SK_MAXN && (a_ks == 1 || a_is == 1))
+    return skinny_gemm(M, N, K, a, a_is, a_ks, b, b_ks, b_ns, c, c_is, c_ns, alpha, beta, src, s_is, s_ns, tmp, st);
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   int64_t nz = 1;
   if (tiles < 148 && K > 4096) {  // too few output tiles to fill the SMs: split K, fixed-order reduction
@@ -158,6 +345,8 @@ int gemm_f64(int64_t M, int64_t N, int64_t K, const double* a, int64_t a_is, int
 int lowrank_project_impl(kgp_precond_s* p, int64_t k, const double* b, int64_t b_rs, int64_t b_cs, double* T,
                          cudaStream_t st) {
   const int64_t n = p->n, m = p->m;
+  if (k <= SK_MAXN)
+    return skinny_gemm(m, k, n, p->wt.as<double>(), n, 1, b, b_rs, b_cs, T, k, 1, 1.0, 0.0, nullptr, 0, 0, p->tmp, st);
   int64_t tiles = ((m + BM - 1) / BM) * ((k + BN - 1) / BN);
   int64_t nz = (n + 2047) / 2048;
   int64_t cap = 296 / tiles;
@@ -186,6 +375,9 @@ int lowrank_project_impl(kgp_precond_s* p, int64_t k, const double* b, int64_t b
 int lowrank_expand_impl(kgp_precond_s* p, double beta, double alpha, int64_t k, const double* b, int64_t b_rs,
                         int64_t b_cs, const double* T, double* out, int64_t o_rs, int64_t o_cs, cudaStream_t st) {
   const int64_t n = p->n, m = p->m;
+  if (k <= SK_MAXN)
+    return skinny_gemm(n, k, m, p->wt.as<double>(), 1, n, T, k, 1, out, o_rs, o_cs, alpha, beta, b, b_rs, b_cs,
+                       p->tmp2, st);
   GemmArgs h{};
   h.M = n; h.N = k; h.K = m;
   h.a = p->wt.as<double>(); h.a_is = 1; h.a_ks = n;
