@@ -148,12 +148,17 @@ __global__ void f64_reduce_kernel(const F64Params p, int nsplit) {
 template <int KT, int NOUT>
 int launch_nout(const F64Params& p, dim3 grid, cudaStream_t st) {
   int kslice = p.k < 64 ? p.k : 64;
+  // RHS slice padded to a multiple of 8 (k = 1 + k_z = 17 runs 24 columns, not 32)
   if (kslice <= 8)
     kmm_f64_kernel<KT, NOUT, 1><<<grid, NT, 0, st>>>(p);
   else if (kslice <= 16)
     kmm_f64_kernel<KT, NOUT, 2><<<grid, NT, 0, st>>>(p);
+  else if (kslice <= 24)
+    kmm_f64_kernel<KT, NOUT, 3><<<grid, NT, 0, st>>>(p);
   else if (kslice <= 32)
     kmm_f64_kernel<KT, NOUT, 4><<<grid, NT, 0, st>>>(p);
+  else if (kslice <= 48)
+    kmm_f64_kernel<KT, NOUT, 6><<<grid, NT, 0, st>>>(p);
   else
     kmm_f64_kernel<KT, NOUT, 8><<<grid, NT, 0, st>>>(p);
   KGP_LAUNCH("kmm_f64_kernel");
@@ -174,9 +179,9 @@ int launch_kmm_f64(int kt, const F64Params& p_in, DevBuf& ws, cudaStream_t st) {
   if (p_in.nrows <= 0) return KGP_OK;
   F64Params p = p_in;
   const int64_t rblk = (p.nrows + TR - 1) / TR, kslc = (p.k + 63) / 64;
-  // split the columns until ~4 CTAs per SM are in flight (148 SMs), at >= 512 columns per split
-  int64_t nsplit = (4 * 148 + rblk * kslc - 1) / (rblk * kslc);
-  const int64_t maxsplit = p.ncols / 512 > 0 ? p.ncols / 512 : 1;
+  // split the columns until ~8 CTAs per SM are in flight (148 SMs), at >= 256 columns per split
+  int64_t nsplit = (8 * 148 + rblk * kslc - 1) / (rblk * kslc);
+  const int64_t maxsplit = p.ncols / 256 > 0 ? p.ncols / 256 : 1;
   if (nsplit > maxsplit) nsplit = maxsplit;
   if (nsplit < 1) nsplit = 1;
   p.jchunk = ((p.ncols + nsplit - 1) / nsplit + TJ - 1) / TJ * TJ;
