@@ -342,18 +342,16 @@ def run_gpu(args):
     units = 2.0 * n * n * k  # both outputs, whole job
     value = units / t_step
 
-    # ---- e2e: C ABI call with HOST buffers, H2D of Z and D2H of both outputs inside the timed region
+    # ---- e2e: the C-ABI host-buffer entry (kgp_engine_matmul_host): H2D of Z and D2H of both
+    # outputs inside the timed region (pinned host memory; the output transfer is pipelined
+    # behind the computation in row chunks by the library)
     zh = torch.from_numpy(w.z).pin_memory()
     ok_h = torch.empty((rows, k), dtype=torch.float64).pin_memory()
     ol_h = torch.empty_like(ok_h).pin_memory()
-    zbuf = torch.empty_like(zd)
 
     def e2e_step():
-        zbuf.copy_(zh, non_blocking=True)
-        _lib.call("kgp_engine_matmul", eng.handle, k, zbuf.data_ptr(), zbuf.stride(0), zbuf.stride(1),
-                  out_k.data_ptr(), out_l.data_ptr(), None, out_k.stride(0), out_k.stride(1), stream.cuda_stream)
-        ok_h.copy_(out_k, non_blocking=True)
-        ol_h.copy_(out_l, non_blocking=True)
+        _lib.call("kgp_engine_matmul_host", eng.handle, k, zh.data_ptr(), ok_h.data_ptr(), ol_h.data_ptr(), None,
+                  stream.cuda_stream)
 
     for _ in range(3):
         e2e_step()

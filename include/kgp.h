@@ -87,6 +87,13 @@ int kgp_engine_matmul(kgp_engine* e, int64_t k, const double* b, int64_t b_rs, i
                       double* out_k, double* out_dl, double* out_df, int64_t o_rs, int64_t o_cs,
                       void* stream);
 
+/* The same product on HOST buffers (the reference's numpy-in/numpy-out matmul,
+ * kmat.py:145-163): b (n, k) and every requested output (nrows, k) row-major contiguous
+ * host fp64 (pinned memory gives asynchronous DMA). The output transfer is pipelined
+ * behind the computation in row chunks; returns when the outputs are written. */
+int kgp_engine_matmul_host(kgp_engine* e, int64_t k, const double* b, double* out_k, double* out_dl,
+                           double* out_df, void* stream);
+
 /* Rectangular f^2 kappa(Xs, X) B (no diagonal shift): the cross kernel of predict
  * (gp.py:223-241), never materialised. xs: (m, d) device fp64 row-major. */
 int kgp_engine_cross_matmul(kgp_engine* e, int64_t m, const double* xs, int64_t k, const double* b,

@@ -4,6 +4,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 #include <set>
@@ -72,6 +73,9 @@ static void engine_free_host_state(kgp_engine_s* e) {
   for (auto& ev : e->events)
     if (ev) cudaEventDestroy(ev);
   if (e->cstream) cudaStreamDestroy(e->cstream);
+  if (e->xstream) cudaStreamDestroy(e->xstream);
+  for (auto ev : e->xev)
+    if (ev) cudaEventDestroy(ev);
   for (auto ev : e->tev) cudaEventDestroy(ev);
 }
 
@@ -123,9 +127,11 @@ static double scale_dl_fast(int kt, double l, double f) {
 }
 
 // Shared by the square operator (xrow = engine rows, shift on) and the cross operator.
+// skip_prep: the RHS split of exactly this B is already in e->bsplit (row-chunked host
+// products prepare it once for all chunks; valid when k fits one launch)
 static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t diag_row0, int64_t k, const double* b,
                      int64_t b_rs, int64_t b_cs, double* out_k, double* out_dl, double* out_df, int64_t o_rs,
-                     int64_t o_cs, cudaStream_t st) {
+                     int64_t o_cs, cudaStream_t st, bool skip_prep = false) {
   const int split = (e->precision == KGP_FAST) ? 3 : 1;
   const int nout = out_dl ? 2 : 1;
   const int tpo = split == 3 ? 2 : 1;
@@ -139,10 +145,13 @@ static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t 
     const int kc = (int)((k - c0) < kmax ? (k - c0) : kmax);
     const int kp = (kc + 15) / 16 * 16;
     const int nab = kp <= kmax2 ? 2 : 1;
-    int rc = e->bsplit.ensure((size_t)nblk * tpo * kp * 128);
-    if (rc) return rc;
-    rc = prep_rhs(split, e->n, k, c0, kp, b, b_rs, b_cs, e->bsplit.as<uint8_t>(), st);
-    if (rc) return rc;
+    int rc = KGP_OK;
+    if (!(skip_prep && kc == k)) {
+      rc = e->bsplit.ensure((size_t)nblk * tpo * kp * 128);
+      if (rc) return rc;
+      rc = prep_rhs(split, e->n, k, c0, kp, b, b_rs, b_cs, e->bsplit.as<uint8_t>(), st);
+      if (rc) return rc;
+    }
     TcParams p{};
     p.xrow = xrow;
     p.xcol = e->xcol.as<float>();
@@ -448,6 +457,66 @@ extern "C" int kgp_engine_matmul(kgp_engine* e, int64_t k, const double* b, int6
   KGP_REQUIRE(b != nullptr, KGP_ERR_INVALID, "B pointer is NULL");
   KGP_CUDA(cudaSetDevice(e->device));
   return engine_matmul_impl(e, k, b, b_rs, b_cs, out_k, out_dl, out_df, o_rs, o_cs, (cudaStream_t)stream);
+}
+
+// Host-buffer product with the device->host transfer of the outputs pipelined behind the
+// computation: rows are processed in chunks, each chunk's outputs copied back on the
+// engine's copy stream while the next chunk computes. Returns when the host outputs hold
+// the result.
+extern "C" int kgp_engine_matmul_host(kgp_engine* e, int64_t k, const double* b, double* out_k, double* out_dl,
+                                      double* out_df, void* stream) {
+  CHECK_ENGINE(e);
+  KGP_REQUIRE(k >= 1 && b != nullptr, KGP_ERR_INVALID, "B must be a non-NULL host array with >= 1 column");
+  KGP_REQUIRE(out_k || out_dl || out_df, KGP_ERR_INVALID, "no output requested");
+  KGP_CUDA(cudaSetDevice(e->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = e->n, rows = e->nrows;
+  const int nout = (out_k ? 1 : 0) + (out_dl ? 1 : 0) + (out_df ? 1 : 0);
+  int rc = e->hostbuf.ensure(sizeof(double) * (size_t)k * (n + nout * rows));
+  if (rc) return rc;
+  double* db = e->hostbuf.as<double>();
+  double* dout = db + k * n;
+  double* dk = out_k ? dout : nullptr;
+  double* dl = out_dl ? dout + (out_k ? 1 : 0) * rows * k : nullptr;
+  double* df = out_df ? dout + (nout - 1) * rows * k : nullptr;
+  KGP_CUDA(cudaMemcpyAsync(db, b, sizeof(double) * n * k, cudaMemcpyHostToDevice, st));
+  // chunk only the tensor-core path without a heteroscedastic diagonal, when k fits one launch
+  const int split = (e->precision == KGP_FAST) ? 3 : 1;
+  const bool chunked = e->precision != KGP_FP64 && e->dn_classes == 0 &&
+                       k <= tc_max_kp(e->dpad, out_dl ? 2 : 1, split, 1) && rows >= 32768;
+  if (!e->xstream) {
+    KGP_CUDA(cudaStreamCreateWithFlags(&e->xstream, cudaStreamNonBlocking));
+    for (auto& ev : e->xev) KGP_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  }
+  const int nchunk = chunked ? 4 : 1;
+  if (chunked) {
+    rc = engine_prepare(e, st);
+    if (rc) return rc;
+  }
+  double* hosts[3] = {out_k, out_dl, out_df};
+  double* devs[3] = {dk, dl, df};
+  for (int c = 0; c < nchunk; ++c) {
+    // chunk boundaries on 128-row CTA tiles
+    const int64_t blocks = (rows + 127) / 128;
+    const int64_t r0 = std::min(rows, blocks * c / nchunk * 128), r1 = std::min(rows, blocks * (c + 1) / nchunk * 128);
+    if (r1 <= r0) continue;
+    if (chunked) {
+      rc = tc_matmul(e, e->xrow.as<float>() + r0 * (e->dpad + 1), r1 - r0, e->row0 + r0, k, db, k, 1,
+                     dk ? dk + r0 * k : nullptr, dl ? dl + r0 * k : nullptr, df ? df + r0 * k : nullptr, k, 1, st,
+                     c > 0);
+    } else {
+      rc = engine_matmul_impl(e, k, db, k, 1, dk, dl, df, k, 1, st);
+    }
+    if (rc) return rc;
+    KGP_CUDA(cudaEventRecord(e->xev[c], st));
+    KGP_CUDA(cudaStreamWaitEvent(e->xstream, e->xev[c], 0));
+    for (int o = 0; o < 3; ++o)
+      if (hosts[o])
+        KGP_CUDA(cudaMemcpyAsync(hosts[o] + r0 * k, devs[o] + r0 * k, sizeof(double) * (r1 - r0) * k,
+                                 cudaMemcpyDeviceToHost, e->xstream));
+  }
+  KGP_CUDA(cudaStreamSynchronize(e->xstream));
+  return KGP_OK;
 }
 
 extern "C" int kgp_engine_cross_matmul(kgp_engine* e, int64_t m, const double* xs, int64_t k, const double* b,

@@ -129,6 +129,10 @@ struct kgp_engine_s {
   int hist_cap = 0;
   cudaEvent_t events[kgp::PCG_LOOKAHEAD] = {};
   cudaStream_t cstream = nullptr;  // private stream used only for graph capture (the caller's may be legacy)
+  // host-buffer products (kgp_engine_matmul_host): device staging, copy stream, chunk events
+  kgp::DevBuf hostbuf;
+  cudaStream_t xstream = nullptr;
+  cudaEvent_t xev[4] = {};
   // optional heteroscedastic diagonal (kgp_engine_set_diag): Khat column c gets + diag(dn[:, dmap[c]])
   int dn_classes = 0;
   int64_t dn_ncols = 0;
