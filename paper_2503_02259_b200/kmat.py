@@ -221,11 +221,18 @@ class KernelEngine:
         return res
 
     def _host_apply(self, b, which):
+        """numpy in, numpy out (the reference's calling convention) through the host-buffer
+        entry kgp_engine_matmul_host: results land in pinned host memory, the device->host
+        transfer pipelined behind the computation."""
+        torch = _device.torch()
         b, squeeze = _as_matrix(b, self.n)
-        bd = _device.to_device(b)
-        res = self.apply(bd, *which)
-        outs = [None if t is None else _device.to_host(t) for t in res]
-        return [None if o is None else (o[:, 0] if squeeze else o) for o in outs]
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        k = b.shape[1]
+        outs = [torch.empty((self.n, k), dtype=torch.float64, pin_memory=True) if w else None for w in which]
+        call("kgp_engine_matmul_host", self._handle, k, b.ctypes.data,
+             *(None if t is None else t.data_ptr() for t in outs), _device.stream_ptr())
+        res = [None if t is None else t.numpy() for t in outs]
+        return [None if o is None else (o[:, 0] if squeeze else o) for o in res]
 
     def matmul(self, b):
         """Khat @ B (kmat.py:145-152)."""
