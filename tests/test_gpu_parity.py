@@ -272,6 +272,25 @@ def test_cfg1_full_matches_reference(pkg):
     assert np.all(np.abs(got - ref) <= 1e-6 * np.abs(ref)), (got, ref)
 
 
+def test_cfg1_fast_mode_within_tf32_bar(pkg):
+    """North star: NLML and gradient within 1e-3 of the reference in the TF32 (tensor-core)
+    mode. The 3xTF32 operator gives 3e-6 (loss) .. 6e-4 (grad_s) at configs[0] in tolerance
+    mode (measured, tools/nlml_precision.py); the single-pass tf32 operator does not meet it
+    (grad_f/grad_s amplify operator error ~1e4x) and is a throughput mode only."""
+    from paper_2503_02259_b200 import gp, precond, workloads
+
+    g = golden("cfg1_full.npz")
+    w = workloads.cfg1()
+    probes = gp.ProbeSet.generate(w.n, w.k_z, w.probe_seed)
+    e = pkg.KernelEngine(pkg.KernelType.GAUSSIAN, w.x, _hp(pkg, w.l, w.f, w.s), precision="fast")
+    lg = gp.nlml_grad_iterative(e, w.y, precond.build(e, w.rank), probes, tol=1e-10, max_iter=3000,
+                                probe_tol=1e-10)
+    got = np.array([lg.loss, lg.grad_l, lg.grad_f, lg.grad_s])
+    ref = g["iter_tight"][:4]
+    assert lg.converged
+    assert np.all(np.abs(got - ref) <= 1e-3 * np.abs(ref)), (got, ref)
+
+
 def test_nlml_deterministic(pkg):
     from paper_2503_02259_b200 import gp, precond
 
