@@ -208,6 +208,16 @@ int64_t kgp_launch_count(void);
 int kgp_engine_set_timing(kgp_engine* e, int enable);
 int kgp_engine_kernel_time(kgp_engine* e, double* ms, int64_t* launches);
 
+/* nlml_grad_iterative with PRECONDITIONED probes (an extension; the reference's probes are
+ * unpreconditioned, gp.py:154-160): the caller draws probes z ~ N(0, M) for the handle's
+ * M and passes logdet_m = log|M|. Probe solves are preconditioned by M, SLQ estimates
+ * log|M^-1/2 Khat M^-1/2| (weights z^T M^-1 z) and the trace terms use
+ * E[(M^-1 z)^T dK Khat^-1 z] = tr(Khat^-1 dK): unbiased for the same loss and gradient,
+ * with probe CG counts of the preconditioned system. Arguments as kgp_nlml_grad. */
+int kgp_nlml_grad_pp(kgp_engine* e, kgp_precond* p, const double* y, int64_t k_z, const double* probes,
+                     double logdet_m, double tol, int32_t max_iter, double probe_tol, int32_t probe_max_iter,
+                     double* out, int32_t* out_converged, void* stream);
+
 /* Dirichlet GP classification (gpc.py; no reference counterpart): `classes`
  * GP regressions sharing (l, f, s), class c with Khat + diag(dn_c) and target y_c, solved
  * together (one operator application per iteration serves every class's target and

@@ -92,7 +92,7 @@ struct PcgGraph {
   cudaGraphExec_t exec = nullptr;
   int64_t k = 0;
   std::vector<const void*> pcs;
-  int64_t kpc = 0;
+  int64_t kpc = 0, kz = 0;
   double tol1 = 0.0, tol2 = 0.0;
   int it1 = 0, it2 = 0;
   uint64_t epoch = 0;
@@ -203,7 +203,7 @@ struct PcSet {
 };
 int pcg_grouped_impl(kgp_engine_s* e, const PcSet& pcs, int64_t k, int64_t kpc, const double* y, double tol1,
                      int it1, double tol2, int it2, double* x_out, double* alphas, double* betas, int32_t* iters,
-                     double* rel, int32_t* conv, cudaStream_t st);
+                     double* rel, int32_t* conv, cudaStream_t st, bool precond_all = false);
 int slq_impl(int64_t k, int max_iter, const double* alphas, const double* betas, const int32_t* iters,
              const double* norms_sq, double* logdet, cudaStream_t st);
 int col_dots(int64_t k, int64_t n, const double* a, const double* b, double* out, double* partial, cudaStream_t st);

@@ -74,6 +74,7 @@ struct PcgState {
 // (gp.py:154-160) as Khat [p_w, P_Z]. Each column's recurrence is independent of the others.
 struct PcgGroups {
   int kpc;
+  int kz;      // leading columns whose z is M^-1 r (kpc, or k when the probes are preconditioned too)
   double tol1, tol2;
   int it1, it2;
   int stride;  // per-column stride of the alpha/beta arrays (max(it1, it2))
@@ -147,7 +148,7 @@ __global__ void pcg_beta_kernel(int k, PcgGroups g, bool precond, const double* 
       atomicMin(&status[2], c);
       status[1] = KGP_ERR_NUMERICAL;
     } else {
-      double rn = (precond && c < g.kpc) ? rzn[c] : v;
+      double rn = (precond && c < g.kz) ? rzn[c] : v;
       double b = rn / rz[c];
       int it = iters[c];
       betas[(int64_t)c * g.stride + it] = b;
@@ -339,10 +340,10 @@ int enqueue_iteration(kgp_engine_s* e, const PcSet& pcs, int64_t k, const PcgGro
   KGP_LAUNCH("pcg_alpha_kernel");
   pcg_update_xr_kernel<<<vgrid, 256, 0, st>>>(n, (int)k, S.active, S.alpha, S.p, S.ap, B.x, S.r);
   KGP_LAUNCH("pcg_update_xr_kernel");
-  if (pc && g.kpc > 0) {  // M^-1 on the preconditioned group only
-    rc = apply_pcs(pcs, g.kpc, n, S.r, S.z, st);
+  if (pc && g.kz > 0) {  // M^-1 on the preconditioned columns only
+    rc = apply_pcs(pcs, g.kz, n, S.r, S.z, st);
     if (rc) return rc;
-    rc = col_dots(g.kpc, n, S.r, S.z, S.dots2, S.partial, st);
+    rc = col_dots(g.kz, n, S.r, S.z, S.dots2, S.partial, st);
     if (rc) return rc;
   }
   rc = col_dots(k, n, S.r, S.r, S.dots1, S.partial, st);
@@ -350,7 +351,7 @@ int enqueue_iteration(kgp_engine_s* e, const PcSet& pcs, int64_t k, const PcgGro
   pcg_beta_kernel<<<1, 1024, 0, st>>>((int)k, g, pc, S.dots1, S.dots2, S.rz, S.ynorm, S.active, B.iters,
                                       S.beta, B.betas, B.rel, S.status, B.it_counter, e->hist_dev);
   KGP_LAUNCH("pcg_beta_kernel");
-  pcg_update_p_kernel<<<vgrid, 256, 0, st>>>(n, (int)k, pc ? g.kpc : 0, S.active, S.beta, S.z, S.r, S.p);
+  pcg_update_p_kernel<<<vgrid, 256, 0, st>>>(n, (int)k, pc ? g.kz : 0, S.active, S.beta, S.z, S.r, S.p);
   KGP_LAUNCH("pcg_update_p_kernel");
   return KGP_OK;
 }
@@ -359,7 +360,7 @@ bool same_groups(const PcgGraph& c, int64_t k, const PcSet& pcs, const PcgGroups
   if (!c.exec || (int)c.pcs.size() != pcs.count) return false;
   for (int i = 0; i < pcs.count; ++i)
     if (c.pcs[i] != pcs.h[i]) return false;
-  return c.k == k && c.kpc == g.kpc && c.tol1 == g.tol1 && c.tol2 == g.tol2 &&
+  return c.k == k && c.kpc == g.kpc && c.kz == g.kz && c.tol1 == g.tol1 && c.tol2 == g.tol2 &&
          c.it1 == g.it1 && c.it2 == g.it2 && c.epoch == graph_epoch();
 }
 
@@ -405,6 +406,7 @@ int pcg_graph(kgp_engine_s* e, const PcSet& pcs, int64_t k, const PcgGroups& g, 
   slot.k = k;
   slot.pcs.assign(pcs.h, pcs.h + pcs.count);
   slot.kpc = g.kpc;
+  slot.kz = g.kz;
   slot.tol1 = g.tol1;
   slot.tol2 = g.tol2;
   slot.it1 = g.it1;
@@ -433,12 +435,12 @@ int pcg_solve_impl(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, const double* 
                    cudaStream_t st) {
   kgp_precond_s* one[1] = {pc};
   return pcg_grouped_impl(e, PcSet{one, pc ? 1 : 0}, k, k, y, tol, max_iter, tol, max_iter, x_out, alphas, betas,
-                          iters, rel, conv, st);
+                          iters, rel, conv, st, false);
 }
 
 int pcg_grouped_impl(kgp_engine_s* e, const PcSet& pcs, int64_t k, int64_t kpc, const double* y, double tol1,
                      int it1, double tol2, int it2, double* x_out, double* alphas, double* betas, int32_t* iters,
-                     double* rel, int32_t* conv, cudaStream_t st) {
+                     double* rel, int32_t* conv, cudaStream_t st, bool precond_all) {
   const int64_t n = e->n;
   const int nb = (int)((n + DOT_CHUNK - 1) / DOT_CHUNK);
   KGP_REQUIRE(k <= 1024, KGP_ERR_INVALID, "pcg supports at most 1024 right-hand sides per call, got %lld",
@@ -449,7 +451,9 @@ int pcg_grouped_impl(kgp_engine_s* e, const PcSet& pcs, int64_t k, int64_t kpc, 
   for (int i = 0; i < pcs.count; ++i)
     KGP_REQUIRE(pcs.h[i] != nullptr && pcs.h[i]->n == e->n, KGP_ERR_INVALID, "preconditioner %d missing or of wrong size", i);
   const bool pc = pcs.count > 0;
-  PcgGroups g{(int)kpc, tol1, kpc < k ? tol2 : tol1, it1, kpc < k ? it2 : it1, 0};
+  KGP_REQUIRE(!precond_all || pcs.count == 1, KGP_ERR_INVALID, "preconditioning every column needs one handle");
+  PcgGroups g{(int)kpc, 0, tol1, kpc < k ? tol2 : tol1, it1, kpc < k ? it2 : it1, 0};
+  g.kz = pcs.count == 0 ? 0 : (precond_all ? (int)k : (int)kpc);
   if (kpc == 0) {
     g.tol1 = g.tol2;
     g.it1 = g.it2;
@@ -513,7 +517,7 @@ int pcg_grouped_impl(kgp_engine_s* e, const PcSet& pcs, int64_t k, int64_t kpc, 
   rc = read_status(S.status, hstatus, st);
   if (rc) return rc;
   if (hstatus[0] > 0) {
-    const int64_t kz = pc ? g.kpc : 0;  // columns whose z is M^-1 r
+    const int64_t kz = g.kz;  // columns whose z is M^-1 r
     if (kz > 0) {
       rc = apply_pcs(pcs, kz, n, S.r, S.z, st);
       if (rc) return rc;
@@ -611,9 +615,13 @@ int slq_impl(int64_t k, int max_iter, const double* alphas, const double* betas,
 // kernel hyperparameters: C = 1 is GP regression; C > 1 is the Dirichlet GP
 // classification of gpc.py (class c: Khat + diag(dn_c), target y_c). Loss and gradient
 // are sums over the classes.
+// pp (preconditioned probes, C = 1, one handle M): the probes are draws z ~ N(0, M); the
+// probe solves are preconditioned by M, SLQ then estimates log|M^-1/2 Khat M^-1/2| with
+// |M^-1/2 z|^2 = z^T M^-1 z as the quadrature weights, loss adds logdet_m = log|M|, and the
+// trace estimator uses E[(M^-1 z)^T dK (Khat^-1 z)] = tr(Khat^-1 dK).
 static int nlml_impl(kgp_engine_s* e, const PcSet& pcs, int64_t C, const double* y, int64_t k_z,
                      const double* probes, double tol, int32_t max_iter, double probe_tol, int32_t probe_max_iter,
-                     double* out, int32_t* out_converged, cudaStream_t st) {
+                     double* out, int32_t* out_converged, cudaStream_t st, bool pp = false, double logdet_m = 0.0) {
   const int64_t n = e->n;
   const int64_t kv = C * (1 + k_z);
   const int nb = (int)((n + DOT_CHUNK - 1) / DOT_CHUNK);
@@ -645,12 +653,21 @@ static int nlml_impl(kgp_engine_s* e, const PcSet& pcs, int64_t C, const double*
   // their coefficients rebuild the Lanczos tridiagonals of Khat itself.
   KGP_CUDA(cudaMemcpyAsync(V, y, sizeof(double) * C * n, cudaMemcpyDeviceToDevice, st));
   KGP_CUDA(cudaMemcpyAsync(V + C * n, probes, sizeof(double) * C * k_z * n, cudaMemcpyDeviceToDevice, st));
-  rc = pcg_grouped_impl(e, pcs, kv, C, V, tol, max_iter, probe_tol, pmax, U, alphas, betas, iters, rel, conv, st);
+  rc = pcg_grouped_impl(e, pcs, kv, C, V, tol, max_iter, probe_tol, pmax, U, alphas, betas, iters, rel, conv, st,
+                        pp);
   if (rc) return rc;
   // (3) log|Khat_c| by SLQ over each class's probe traces
-  const double* Z = V + C * n;
-  rc = col_dots(C * k_z, n, Z, Z, nz2, partial, st);
-  if (rc) return rc;
+  double* Z = V + C * n;
+  if (pp) {  // M^-1 Z (into dL as scratch), weights z^T M^-1 z, then V's probe rows := M^-1 Z
+    rc = precond_apply_impl(pcs.h[0], k_z, Z, 1, n, dL, 1, n, st);
+    if (rc) return rc;
+    rc = col_dots(k_z, n, Z, dL, nz2, partial, st);
+    if (rc) return rc;
+    KGP_CUDA(cudaMemcpyAsync(Z, dL, sizeof(double) * k_z * n, cudaMemcpyDeviceToDevice, st));
+  } else {
+    rc = col_dots(C * k_z, n, Z, Z, nz2, partial, st);
+    if (rc) return rc;
+  }
   double logdet = 0.0;
   for (int64_t c = 0; c < C; ++c) {
     double ld = 0.0;
@@ -693,7 +710,7 @@ static int nlml_impl(kgp_engine_s* e, const PcSet& pcs, int64_t C, const double*
   int ok = 1;
   for (int64_t c = 0; c < kv; ++c) ok &= hc[c] ? 1 : 0;
   const double LOG_2PI = 1.8378770664093453;
-  out[0] = 0.5 * (yw + logdet + (double)(C * n) * LOG_2PI);
+  out[0] = 0.5 * (yw + logdet + logdet_m + (double)(C * n) * LOG_2PI);
   out[1] = grads[0];
   out[2] = grads[1];
   out[3] = grads[2];
@@ -756,5 +773,20 @@ extern "C" int kgp_pcg_grouped(kgp_engine* e, kgp_precond* const* pcs, int npcs,
   KGP_REQUIRE(e->row0 == 0 && e->nrows == e->n, KGP_ERR_INVALID, "kgp_pcg_grouped needs an unpartitioned engine");
   KGP_CUDA(cudaSetDevice(e->device));
   return pcg_grouped_impl(e, PcSet{pcs, npcs}, k, kpc, y, tol1, it1, tol2, it2, x_out, alphas, betas, iters, rel,
-                          converged, (cudaStream_t)stream);
+                          converged, (cudaStream_t)stream, false);
+}
+
+extern "C" int kgp_nlml_grad_pp(kgp_engine* e, kgp_precond* p, const double* y, int64_t k_z, const double* probes,
+                                double logdet_m, double tol, int32_t max_iter, double probe_tol,
+                                int32_t probe_max_iter, double* out, int32_t* out_converged, void* stream) {
+  KGP_REQUIRE(e != nullptr && e->magic == ENGINE_MAGIC, KGP_ERR_STATE, "invalid engine handle");
+  KGP_REQUIRE(p != nullptr && p->magic == PRECOND_MAGIC, KGP_ERR_STATE, "preconditioned probes need a preconditioner");
+  KGP_REQUIRE(k_z >= 1 && max_iter >= 1 && tol >= 0.0 && probe_tol >= 0.0, KGP_ERR_INVALID, "bad solver arguments");
+  KGP_REQUIRE(out != nullptr && out_converged != nullptr, KGP_ERR_INVALID, "NULL output pointer");
+  KGP_REQUIRE(e->dn_classes == 0, KGP_ERR_INVALID, "engine has a per-class diagonal");
+  KGP_REQUIRE(p->n == e->n, KGP_ERR_INVALID, "preconditioner size mismatch");
+  KGP_CUDA(cudaSetDevice(e->device));
+  kgp_precond_s* one[1] = {p};
+  return nlml_impl(e, PcSet{one, 1}, 1, y, k_z, probes, tol, max_iter, probe_tol, probe_max_iter, out,
+                   out_converged, (cudaStream_t)stream, true, logdet_m);
 }

@@ -83,13 +83,29 @@ class _LowRank:
 class NystromPreconditioner:
     """M = s I + f^2 V V^T with Woodbury inverse, factors resident in HBM."""
 
-    def __init__(self, landmark_indices, shift, inv, fwd, f2, n):
+    def __init__(self, landmark_indices, shift, inv, fwd, f2, n, logdet=None):
         self.landmark_indices = landmark_indices
         self.shift = float(shift)
         self._inv = inv
         self._fwd = fwd
         self._f2 = float(f2)
         self.n = int(n)
+        self.logdet = logdet  # log|M| = n log s + m log f^2 + log|C|, C = I/f^2 + V^T V / s
+
+    def sample(self, w1, w2):
+        """Draws z = sqrt(s) w1 + f V w2 ~ N(0, M) from standard normals w1 (n, k), w2 (m, k)
+        (host or device); returns a (k, n) CUDA tensor (probe c contiguous)."""
+        torch = _device.torch()
+        w1 = w1 if _device.is_tensor(w1) else _device.to_device(np.asarray(w1, dtype=np.float64))
+        w2 = w2 if _device.is_tensor(w2) else _device.to_device(np.asarray(w2, dtype=np.float64))
+        n, k = w1.shape
+        if n != self.n or w2.shape != (self.rank, k):
+            raise ValueError(f"need w1 ({self.n}, k) and w2 ({self.rank}, k)")
+        t = w2.contiguous()
+        out = torch.empty((k, n), dtype=torch.float64, device=w1.device)
+        call("kgp_lowrank_expand", self._fwd.h, math.sqrt(self.shift), math.sqrt(self._f2), k, w1.data_ptr(),
+             w1.stride(0), w1.stride(1), t.data_ptr(), out.data_ptr(), 1, n, _device.stream_ptr())
+        return out
 
     @property
     def rank(self) -> int:
@@ -160,7 +176,8 @@ def build(engine, m: int | None = None) -> NystromPreconditioner:
     inv = _LowRank(wt, p.s)
     del wt
     fwd = _LowRank(vt, p.s)
-    return NystromPreconditioner(_device.to_host(idx).astype(np.intp), p.s, inv, fwd, f2, n)
+    logdet = n * math.log(p.s) + m * math.log(f2) + 2.0 * float(torch.log(torch.diagonal(lc)).sum())
+    return NystromPreconditioner(_device.to_host(idx).astype(np.intp), p.s, inv, fwd, f2, n, logdet)
 
 
 # ----------------------------------------------------------------------------- AFN

@@ -482,3 +482,63 @@ def test_matmul_host_matches_device(pkg, precision):
     ok2 = np.empty((n, k))
     _lib.call("kgp_engine_matmul_host", e.handle, k, b.ctypes.data, ok2.ctypes.data, None, None, None)
     assert rel_max(ok2, ref_k.cpu().numpy()) <= bar
+
+
+def test_preconditioned_probes_estimator(pkg):
+    """preconditioned_probes=True (extension): log|M| and the N(0, M) draws are exact, and the
+    device estimator equals its dense same-probe formula (1e-6 at tight tolerances)."""
+    import torch
+
+    from oracle import kgp_oracle as orc
+    from paper_2503_02259_b200 import gp, precond
+
+    rng = np.random.default_rng(11)
+    n, kt, l, f, s = 300, "matern32", 0.25, 1.3, 2e-2
+    x = rng.uniform(0, 1, (n, 2))
+    y = np.sin(5 * x[:, 0]) + 0.1 * rng.standard_normal(n)
+    e = pkg.KernelEngine(pkg.KernelType(kt), x, _hp(pkg, l, f, s))
+    pre = precond.build(e, 40)
+    m_dense = pre.apply(np.eye(n))
+    assert abs(pre.logdet - np.linalg.slogdet(m_dense)[1]) <= 1e-9 * abs(pre.logdet)
+    zv = pre.sample(np.zeros((n, 40)), np.eye(40)).cpu().numpy()        # rows: f V e_i
+    np.testing.assert_allclose(zv.T @ zv, m_dense - s * np.eye(n), atol=1e-10 * np.abs(m_dense).max())
+    probes = gp.ProbeSet.generate(n, 6, 3)
+    lg = gp.nlml_grad_iterative(e, y, pre, probes, tol=1e-11, max_iter=2000, probe_tol=1e-11,
+                                preconditioned_probes=True)
+    w2 = np.random.default_rng([3, gp.PP_TAIL_SEED]).standard_normal((40, 6))
+    z = pre.sample(probes.vectors, w2).cpu().numpy().T                   # (n, k_z) ~ N(0, M)
+    kh = orc.khat_dense(kt, x, l, f, s)
+    mi = np.linalg.inv(m_dense)
+    ev, vec = np.linalg.eigh(m_dense)
+    mh = (vec / np.sqrt(ev)) @ vec.T                                    # M^-1/2
+    ah = mh @ kh @ mh
+    ea, va = np.linalg.eigh(ah)
+    loga = (va * np.log(ea)) @ va.T
+    zh = mh @ z
+    w = np.linalg.solve(kh, y)
+    loss = 0.5 * (y @ w + pre.logdet + np.einsum("ij,ij->", zh, loga @ zh) / 6 + n * np.log(2 * np.pi))
+    kap = orc.eval_kernel(kt, x, x, l)
+    dks = [f * f * orc.eval_kernel_grad_l(kt, x, x, l), 2 * f * kap, np.eye(n)]
+    u = np.linalg.solve(kh, z)
+    grads = [0.5 * (-w @ dk @ w + np.einsum("ij,ij->", mi @ z, dk @ u) / 6) for dk in dks]
+    got = np.array([lg.loss, lg.grad_l, lg.grad_f, lg.grad_s])
+    ref = np.array([loss, *grads])
+    assert lg.converged
+    assert np.all(np.abs(got - ref) <= 1e-6 * np.abs(ref)), (got, ref)
+
+
+def test_preconditioned_probes_unbiased(pkg):
+    """Averaged over probe sets the preconditioned estimator approaches the exact gradient."""
+    from paper_2503_02259_b200 import gp, precond
+
+    rng = np.random.default_rng(5)
+    n = 400
+    x = rng.uniform(0, 1, (n, 3))
+    y = np.cos(4 * x[:, 1]) + 0.1 * rng.standard_normal(n)
+    e = pkg.KernelEngine(pkg.KernelType.GAUSSIAN, x, _hp(pkg, 0.3, 1.0, 1e-2))
+    pre = precond.build(e, 60)
+    ex = gp.grad_exact(e, y)
+    est = np.array([gp.nlml_grad_iterative(e, y, pre, gp.ProbeSet.generate(n, 32, r), tol=1e-10, max_iter=2000,
+                                           probe_tol=1e-8, preconditioned_probes=True).grads() for r in range(8)])
+    mean, sem = est.mean(axis=0), est.std(axis=0, ddof=1) / np.sqrt(len(est))
+    assert np.all(np.abs(mean - ex.grads()) <= 4 * sem + 1e-9 * np.abs(ex.grads())), (mean, ex.grads(), sem)
