@@ -213,10 +213,12 @@ int kgp_engine_kernel_time(kgp_engine* e, double* ms, int64_t* launches);
  * M and passes logdet_m = log|M|. Probe solves are preconditioned by M, SLQ estimates
  * log|M^-1/2 Khat M^-1/2| (weights z^T M^-1 z) and the trace terms use
  * E[(M^-1 z)^T dK Khat^-1 z] = tr(Khat^-1 dK): unbiased for the same loss and gradient,
- * with probe CG counts of the preconditioned system. Arguments as kgp_nlml_grad. */
-int kgp_nlml_grad_pp(kgp_engine* e, kgp_precond* p, const double* y, int64_t k_z, const double* probes,
-                     double logdet_m, double tol, int32_t max_iter, double probe_tol, int32_t probe_max_iter,
-                     double* out, int32_t* out_converged, void* stream);
+ * with probe CG counts of the preconditioned system. p is M (probes); p_w, if not NULL,
+ * preconditions the w-solve instead (e.g. AFN for w, Nystrom for the probes, whose N(0, M)
+ * draws are cheap). Other arguments as kgp_nlml_grad. */
+int kgp_nlml_grad_pp(kgp_engine* e, kgp_precond* p_w, kgp_precond* p, const double* y, int64_t k_z,
+                     const double* probes, double logdet_m, double tol, int32_t max_iter, double probe_tol,
+                     int32_t probe_max_iter, double* out, int32_t* out_converged, void* stream);
 
 /* Dirichlet GP classification (gpc.py; no reference counterpart): `classes`
  * GP regressions sharing (l, f, s), class c with Khat + diag(dn_c) and target y_c, solved

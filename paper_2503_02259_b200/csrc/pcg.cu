@@ -315,13 +315,21 @@ struct PcgBuffers {
 };
 
 // M^-1 on the first kpc columns: one handle for all of them, or one handle per column
-int apply_pcs(const PcSet& pcs, int64_t kpc, int64_t n, const double* r, double* z, cudaStream_t st) {
-  if (pcs.count == 1) return precond_apply_impl(pcs.h[0], kpc, r, 1, n, z, 1, n, st);
-  for (int64_t c = 0; c < kpc; ++c) {
-    int rc = precond_apply_impl(pcs.h[c], 1, r + c * n, 1, n, z + c * n, 1, n, st);
-    if (rc) return rc;
+// M^-1 on columns [0, kz): columns [0, kpc) by pcs.h (one handle, or one per column), columns
+// [kpc, kz) (preconditioned probes) by pcs.tail (default h[0]), batched
+int apply_pcs(const PcSet& pcs, int64_t kpc, int64_t kz, int64_t n, const double* r, double* z, cudaStream_t st) {
+  int rc = KGP_OK;
+  const int64_t head = kpc < kz ? kpc : kz;
+  kgp_precond_s* tail = pcs.tail ? pcs.tail : pcs.h[0];
+  if (pcs.count == 1 && tail == pcs.h[0]) return precond_apply_impl(pcs.h[0], kz, r, 1, n, z, 1, n, st);
+  if (pcs.count == 1) {
+    if (head > 0) rc = precond_apply_impl(pcs.h[0], head, r, 1, n, z, 1, n, st);
+  } else {
+    for (int64_t c = 0; c < head && !rc; ++c)
+      rc = precond_apply_impl(pcs.h[c], 1, r + c * n, 1, n, z + c * n, 1, n, st);
   }
-  return KGP_OK;
+  if (!rc && kz > head) rc = precond_apply_impl(tail, kz - head, r + head * n, 1, n, z + head * n, 1, n, st);
+  return rc;
 }
 
 int enqueue_iteration(kgp_engine_s* e, const PcSet& pcs, int64_t k, const PcgGroups& g, const PcgBuffers& B,
@@ -341,7 +349,7 @@ int enqueue_iteration(kgp_engine_s* e, const PcSet& pcs, int64_t k, const PcgGro
   pcg_update_xr_kernel<<<vgrid, 256, 0, st>>>(n, (int)k, S.active, S.alpha, S.p, S.ap, B.x, S.r);
   KGP_LAUNCH("pcg_update_xr_kernel");
   if (pc && g.kz > 0) {  // M^-1 on the preconditioned columns only
-    rc = apply_pcs(pcs, g.kz, n, S.r, S.z, st);
+    rc = apply_pcs(pcs, g.kpc, g.kz, n, S.r, S.z, st);
     if (rc) return rc;
     rc = col_dots(g.kz, n, S.r, S.z, S.dots2, S.partial, st);
     if (rc) return rc;
@@ -357,7 +365,7 @@ int enqueue_iteration(kgp_engine_s* e, const PcSet& pcs, int64_t k, const PcgGro
 }
 
 bool same_groups(const PcgGraph& c, int64_t k, const PcSet& pcs, const PcgGroups& g) {
-  if (!c.exec || (int)c.pcs.size() != pcs.count) return false;
+  if (!c.exec || (int)c.pcs.size() != pcs.count || c.tail != pcs.tail) return false;
   for (int i = 0; i < pcs.count; ++i)
     if (c.pcs[i] != pcs.h[i]) return false;
   return c.k == k && c.kpc == g.kpc && c.kz == g.kz && c.tol1 == g.tol1 && c.tol2 == g.tol2 &&
@@ -405,6 +413,7 @@ int pcg_graph(kgp_engine_s* e, const PcSet& pcs, int64_t k, const PcgGroups& g, 
   slot.exec = exec;
   slot.k = k;
   slot.pcs.assign(pcs.h, pcs.h + pcs.count);
+  slot.tail = pcs.tail;
   slot.kpc = g.kpc;
   slot.kz = g.kz;
   slot.tol1 = g.tol1;
@@ -451,7 +460,8 @@ int pcg_grouped_impl(kgp_engine_s* e, const PcSet& pcs, int64_t k, int64_t kpc, 
   for (int i = 0; i < pcs.count; ++i)
     KGP_REQUIRE(pcs.h[i] != nullptr && pcs.h[i]->n == e->n, KGP_ERR_INVALID, "preconditioner %d missing or of wrong size", i);
   const bool pc = pcs.count > 0;
-  KGP_REQUIRE(!precond_all || pcs.count == 1, KGP_ERR_INVALID, "preconditioning every column needs one handle");
+  KGP_REQUIRE(!precond_all || pcs.count == 1 || pcs.tail, KGP_ERR_INVALID,
+              "preconditioning every column needs one handle or a tail handle");
   PcgGroups g{(int)kpc, 0, tol1, kpc < k ? tol2 : tol1, it1, kpc < k ? it2 : it1, 0};
   g.kz = pcs.count == 0 ? 0 : (precond_all ? (int)k : (int)kpc);
   if (kpc == 0) {
@@ -519,7 +529,7 @@ int pcg_grouped_impl(kgp_engine_s* e, const PcSet& pcs, int64_t k, int64_t kpc, 
   if (hstatus[0] > 0) {
     const int64_t kz = g.kz;  // columns whose z is M^-1 r
     if (kz > 0) {
-      rc = apply_pcs(pcs, kz, n, S.r, S.z, st);
+      rc = apply_pcs(pcs, g.kpc, kz, n, S.r, S.z, st);
       if (rc) return rc;
       KGP_CUDA(cudaMemcpyAsync(S.p, S.z, sizeof(double) * kz * n, cudaMemcpyDeviceToDevice, st));
       rc = col_dots(kz, n, S.r, S.z, S.rz, S.partial, st);
@@ -659,7 +669,7 @@ static int nlml_impl(kgp_engine_s* e, const PcSet& pcs, int64_t C, const double*
   // (3) log|Khat_c| by SLQ over each class's probe traces
   double* Z = V + C * n;
   if (pp) {  // M^-1 Z (into dL as scratch), weights z^T M^-1 z, then V's probe rows := M^-1 Z
-    rc = precond_apply_impl(pcs.h[0], k_z, Z, 1, n, dL, 1, n, st);
+    rc = precond_apply_impl(pcs.tail ? pcs.tail : pcs.h[0], k_z, Z, 1, n, dL, 1, n, st);
     if (rc) return rc;
     rc = col_dots(k_z, n, Z, dL, nz2, partial, st);
     if (rc) return rc;
@@ -776,17 +786,20 @@ extern "C" int kgp_pcg_grouped(kgp_engine* e, kgp_precond* const* pcs, int npcs,
                           converged, (cudaStream_t)stream, false);
 }
 
-extern "C" int kgp_nlml_grad_pp(kgp_engine* e, kgp_precond* p, const double* y, int64_t k_z, const double* probes,
-                                double logdet_m, double tol, int32_t max_iter, double probe_tol,
+extern "C" int kgp_nlml_grad_pp(kgp_engine* e, kgp_precond* p_w, kgp_precond* p, const double* y, int64_t k_z,
+                                const double* probes, double logdet_m, double tol, int32_t max_iter, double probe_tol,
                                 int32_t probe_max_iter, double* out, int32_t* out_converged, void* stream) {
   KGP_REQUIRE(e != nullptr && e->magic == ENGINE_MAGIC, KGP_ERR_STATE, "invalid engine handle");
   KGP_REQUIRE(p != nullptr && p->magic == PRECOND_MAGIC, KGP_ERR_STATE, "preconditioned probes need a preconditioner");
+  KGP_REQUIRE(p_w == nullptr || p_w->magic == PRECOND_MAGIC, KGP_ERR_STATE, "invalid w-solve preconditioner");
   KGP_REQUIRE(k_z >= 1 && max_iter >= 1 && tol >= 0.0 && probe_tol >= 0.0, KGP_ERR_INVALID, "bad solver arguments");
   KGP_REQUIRE(out != nullptr && out_converged != nullptr, KGP_ERR_INVALID, "NULL output pointer");
   KGP_REQUIRE(e->dn_classes == 0, KGP_ERR_INVALID, "engine has a per-class diagonal");
-  KGP_REQUIRE(p->n == e->n, KGP_ERR_INVALID, "preconditioner size mismatch");
+  KGP_REQUIRE(p->n == e->n && (p_w == nullptr || p_w->n == e->n), KGP_ERR_INVALID, "preconditioner size mismatch");
   KGP_CUDA(cudaSetDevice(e->device));
-  kgp_precond_s* one[1] = {p};
-  return nlml_impl(e, PcSet{one, 1}, 1, y, k_z, probes, tol, max_iter, probe_tol, probe_max_iter, out,
-                   out_converged, (cudaStream_t)stream, true, logdet_m);
+  kgp_precond_s* one[1] = {p_w ? p_w : p};
+  PcSet pcs{one, 1};
+  pcs.tail = p;
+  return nlml_impl(e, pcs, 1, y, k_z, probes, tol, max_iter, probe_tol, probe_max_iter, out, out_converged,
+                   (cudaStream_t)stream, true, logdet_m);
 }

@@ -157,13 +157,14 @@ PP_TAIL_SEED = 0x5EED  # second stream of the preconditioned-probe draws (see be
 
 def nlml_grad_iterative(engine, y, preconditioner, probes: ProbeSet, tol: float = solver.DEFAULT_TOL,
                         max_iter: int = solver.DEFAULT_MAX_ITER, probe_tol: float | None = None, *,
-                        probe_max_iter: int | None = None, preconditioned_probes: bool = False) -> LossGrad:
+                        probe_max_iter: int | None = None, preconditioned_probes=False) -> LossGrad:
     """Matrix-free loss and gradient from one probe set (gp.py:133-179).
 
     Keyword-only extensions: ``probe_max_iter`` caps the probe CG / Lanczos length
     separately from the w-solve (None keeps the reference's single ``max_iter``).
-    ``preconditioned_probes=True`` (Nystrom preconditioner only) switches to the
-    preconditioned estimator: probes z = sqrt(s) w1 + f V w2 ~ N(0, M) with w1 the probe
+    ``preconditioned_probes`` = True (``preconditioner`` must be a Nystrom M) or a
+    NystromPreconditioner M (then ``preconditioner`` -- e.g. AFN -- serves the w-solve only)
+    switches to the preconditioned estimator: probes z = sqrt(s) w1 + f V w2 ~ N(0, M) with w1 the probe
     set's vectors and w2 drawn from default_rng([seed..., PP_TAIL_SEED]); the probe solves
     are preconditioned (a fraction of the reference's unpreconditioned CG iterations),
     log|Khat| = log|M| + SLQ of M^-1/2 Khat M^-1/2, and the trace terms use
@@ -175,8 +176,9 @@ def nlml_grad_iterative(engine, y, preconditioner, probes: ProbeSet, tol: float 
         raise ValueError(f"probes have {probes.vectors.shape[0]} rows, need {n}")
     if probe_tol is None:
         probe_tol = tol
-    if preconditioned_probes:
-        return _nlml_grad_pp(engine, y, preconditioner, probes, tol, max_iter, probe_tol, probe_max_iter)
+    if preconditioned_probes is not False and preconditioned_probes is not None:
+        pm = preconditioner if preconditioned_probes is True else preconditioned_probes
+        return _nlml_grad_pp(engine, y, preconditioner, pm, probes, tol, max_iter, probe_tol, probe_max_iter)
     ours = isinstance(engine, KernelEngine)
     pre_ok = preconditioner is None or isinstance(
         preconditioner, (precond_mod.NystromPreconditioner, precond_mod.AFNPreconditioner))
@@ -197,7 +199,7 @@ def nlml_grad_iterative(engine, y, preconditioner, probes: ProbeSet, tol: float 
     return LossGrad(out[0], out[1], out[2], out[3], converged=bool(conv.value))
 
 
-def _nlml_grad_pp(engine, y, pre, probes, tol, max_iter, probe_tol, probe_max_iter) -> LossGrad:
+def _nlml_grad_pp(engine, y, pre_w, pre, probes, tol, max_iter, probe_tol, probe_max_iter) -> LossGrad:
     if not isinstance(engine, KernelEngine) or not isinstance(pre, precond_mod.NystromPreconditioner):
         raise ValueError("preconditioned_probes needs this package's KernelEngine and a NystromPreconditioner")
     torch = _device.torch()
@@ -208,7 +210,8 @@ def _nlml_grad_pp(engine, y, pre, probes, tol, max_iter, probe_tol, probe_max_it
     yd = torch.from_numpy(y).to(zt.device)
     out = (ctypes.c_double * 4)()
     conv = ctypes.c_int32()
-    call("kgp_nlml_grad_pp", engine.handle, pre.handle, yd.data_ptr(), probes.k_z, zt.data_ptr(), float(pre.logdet),
+    call("kgp_nlml_grad_pp", engine.handle, None if pre_w is None or pre_w is pre else pre_w.handle, pre.handle,
+         yd.data_ptr(), probes.k_z, zt.data_ptr(), float(pre.logdet),
          float(tol), int(max_iter), float(probe_tol), int(probe_max_iter or 0), out, ctypes.byref(conv),
          _device.stream_ptr())
     return LossGrad(out[0], out[1], out[2], out[3], converged=bool(conv.value))
