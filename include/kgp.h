@@ -153,15 +153,24 @@ int kgp_lowrank_expand(kgp_precond* p, double beta, double alpha, int64_t k, con
  *   row-major. dshift (n2) adds a per-point diagonal to S (heteroscedastic noise, gpc.py;
  *   NULL: none). A non-SPD pattern block -> KGP_ERR_BREAKDOWN.
  * kgp_afn_create: handle from device factors (all copied): perm (n) permuted position ->
- *   original row, linv (m, m) row-major L11^-1, w (n2, m), the ELL factor from
+ *   original row, linv (m, m) row-major L11^-1, l11 (m, m) L11 itself (NULL: no sampling),
+ *   w (n2, m), the ELL factor from
  *   kgp_afn_fsai, and G^T as CSR (gtptr n2 + 1, gtrow/gtval nnz; rows ascending). */
 int kgp_knn_prev(int64_t n, int d, const double* x, int npt, int64_t* idx_out, void* stream);
 int kgp_afn_fsai(int kernel, int64_t n2, int d, const double* x2, double l, double f, double s,
                  const double* dshift, int64_t m, const double* w, int npt, const int64_t* nbr, double* gval,
                  int32_t* gcol, void* stream);
 int kgp_afn_create(kgp_precond** out, int64_t n, int64_t m, const int64_t* perm, const double* linv,
-                   const double* w, int npt1, const double* gval, const int32_t* gcol, int64_t nnz,
-                   const int32_t* gtptr, const int32_t* gtrow, const double* gtval, double s, void* stream);
+                   const double* l11, const double* w, int npt1, const double* gval, const int32_t* gcol,
+                   int64_t nnz, const int32_t* gtptr, const int32_t* gtrow, const double* gtval, double s,
+                   void* stream);
+/* z ~ N(0, M) from standard normals for the preconditioned-probe estimator (kgp_nlml_grad_pp):
+ * with w = [w1 (m rows); w2 (n2 rows)] in the landmark-first order, z = L F w with
+ * F = diag(L11, G^-1): z1 = L11 w1, z2 = W w1 + G^-1 w2 (forward substitution scheduled by
+ * dependency level), scattered back to the original row order. w (n, k) strided device;
+ * z (k, n) device, draw c contiguous. Needs the handle created with l11. */
+int kgp_afn_sample(kgp_precond* p, int64_t k, const double* w, int64_t w_rs, int64_t w_cs, double* z,
+                   void* stream);
 int kgp_precond_kind(kgp_precond* p, int* kind);
 
 /* ------------------------------------------------------------------ solvers

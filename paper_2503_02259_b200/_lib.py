@@ -77,8 +77,9 @@ _SIGNATURES = {
                         c_vp, c_vp, c_vp, c_vp],
     "kgp_gpc_nlml_grad": [c_vp, ctypes.c_int, c_vp, ctypes.c_int, c_vp, c_vp, c_i64, c_vp, c_dbl, c_i32, c_dbl, c_i32,
                           _P(c_dbl), _P(c_i32), c_vp],
-    "kgp_afn_create": [_P(c_vp), c_i64, c_i64, c_vp, c_vp, c_vp, ctypes.c_int, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp,
-                       c_dbl, c_vp],
+    "kgp_afn_create": [_P(c_vp), c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, ctypes.c_int, c_vp, c_vp, c_i64, c_vp, c_vp,
+                       c_vp, c_dbl, c_vp],
+    "kgp_afn_sample": [c_vp, c_i64, c_vp, c_i64, c_i64, c_vp, c_vp],
     "kgp_precond_kind": [c_vp, _P(ctypes.c_int)],
     "kgp_engine_kernel_time": [c_vp, _P(c_dbl), _P(c_i64)],
 }

@@ -22,6 +22,8 @@
 // Cholesky, W) is cuSOLVER/cuBLAS through torch on the host side (precond.py).
 #include <math.h>
 
+#include <vector>
+
 #include "kgp_common.cuh"
 #include "kgp_internal.h"
 
@@ -257,6 +259,69 @@ __global__ void scatter_rows_kernel(int64_t n, int64_t m, const int64_t* __restr
   }
 }
 
+// ------------------------------------------------------------------ sampling z ~ N(0, M)
+// level relaxation for the forward substitution G x = b: level(i) = 1 + max level of the
+// earlier neighbours; Jacobi sweeps converge in (depth) sweeps (values only increase)
+__global__ void afn_level_relax_kernel(int64_t n2, int npt1, const int32_t* __restrict__ gcol, int32_t* level,
+                                       int32_t* changed) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n2) return;
+  int l = 0;
+  for (int t = 0; t < npt1; ++t) {
+    const int32_t j = gcol[(int64_t)t * n2 + i];
+    if (j >= 0 && j != i) {
+      const int lj = ((volatile int32_t*)level)[j] + 1;
+      l = lj > l ? lj : l;
+    }
+  }
+  if (l > level[i]) {
+    level[i] = l;
+    *changed = 1;
+  }
+}
+
+// one level of the forward substitution, every column: x_i = (b_i - sum_j G_ij x_j) / G_ii
+__global__ void afn_level_solve_kernel(const int32_t* __restrict__ rows, int cnt, int64_t n2, int npt1,
+                                       const double* __restrict__ gval, const int32_t* __restrict__ gcol,
+                                       const double* __restrict__ b, double* __restrict__ x) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= cnt) return;
+  const int c = blockIdx.y;
+  const int64_t i = rows[e];
+  const double* xc = x + (int64_t)c * n2;
+  double acc = b[(int64_t)c * n2 + i], diag = 1.0;
+  for (int t = 0; t < npt1; ++t) {
+    const int32_t j = gcol[(int64_t)t * n2 + i];
+    if (j < 0) continue;
+    const double v = gval[(int64_t)t * n2 + i];
+    if (j == i)
+      diag = v;
+    else
+      acc = fma(-v, xc[j], acc);
+  }
+  x[(int64_t)c * n2 + i] = acc / diag;
+}
+
+// z[c*n + perm[r]] = r < m ? z1[c*m + r] : t[c*n2 + r - m] + x[c*n2 + r - m]
+__global__ void afn_assemble_kernel(int64_t n, int64_t m, const int64_t* __restrict__ perm,
+                                    const double* __restrict__ z1, const double* __restrict__ t,
+                                    const double* __restrict__ x, double* __restrict__ z) {
+  const int c = blockIdx.y;
+  const int64_t n2 = n - m;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    const double v = r < m ? z1[(int64_t)c * m + r] : t[(int64_t)c * n2 + r - m] + x[(int64_t)c * n2 + r - m];
+    z[(int64_t)c * n + perm[r]] = v;
+  }
+}
+
+// b[c*n2 + i] = w[(m + i) * w_rs + c * w_cs]
+__global__ void afn_gather_tail_kernel(int64_t n2, int64_t m, const double* __restrict__ w, int64_t w_rs,
+                                       int64_t w_cs, double* __restrict__ b) {
+  const int c = blockIdx.y;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x)
+    b[(int64_t)c * n2 + i] = w[(m + i) * w_rs + c * w_cs];
+}
+
 inline dim3 vec_grid(int64_t n, int64_t k) {
   int64_t bx = (n + 255) / 256;
   if (bx > 592) bx = 592;
@@ -307,9 +372,83 @@ int afn_apply_impl(kgp_precond_s* p, int64_t k, const double* b, int64_t b_rs, i
   return KGP_OK;
 }
 
+// rows of the FSAI factor grouped by dependency level (computed once per handle)
+static int afn_levels(kgp_precond_s* p, cudaStream_t st) {
+  if (!p->lvl_ptr.empty()) return KGP_OK;
+  const int64_t n2 = p->n2;
+  DevBuf lv;
+  int rc = lv.ensure(sizeof(int32_t) * (n2 + 1));
+  if (rc) return rc;
+  int32_t* level = lv.as<int32_t>();
+  int32_t* changed = level + n2;
+  KGP_CUDA(cudaMemsetAsync(level, 0, sizeof(int32_t) * (n2 + 1), st));
+  for (int it = 0;; ++it) {
+    KGP_REQUIRE(it <= n2 + 1, KGP_ERR_NUMERICAL, "FSAI dependency levels did not converge");
+    int32_t h = 0;
+    KGP_CUDA(cudaMemsetAsync(changed, 0, sizeof(int32_t), st));
+    afn_level_relax_kernel<<<(unsigned)((n2 + 255) / 256), 256, 0, st>>>(n2, p->npt1, p->gcol.as<int32_t>(), level,
+                                                                        changed);
+    KGP_LAUNCH("afn_level_relax_kernel");
+    KGP_CUDA(cudaMemcpyAsync(&h, changed, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    KGP_CUDA(cudaStreamSynchronize(st));
+    if (!h) break;
+  }
+  std::vector<int32_t> hl(n2);
+  KGP_CUDA(cudaMemcpy(hl.data(), level, sizeof(int32_t) * n2, cudaMemcpyDeviceToHost));
+  int32_t depth = 0;
+  for (int32_t v : hl) depth = v + 1 > depth ? v + 1 : depth;
+  std::vector<int64_t> ptr(depth + 1, 0);
+  for (int32_t v : hl) ++ptr[v + 1];
+  for (int32_t L = 0; L < depth; ++L) ptr[L + 1] += ptr[L];
+  std::vector<int32_t> rows(n2);
+  std::vector<int64_t> pos(ptr.begin(), ptr.end() - 1);
+  for (int64_t i = 0; i < n2; ++i) rows[pos[hl[i]]++] = (int32_t)i;  // ascending rows within a level
+  rc = p->lvl_rows.ensure(sizeof(int32_t) * n2);
+  if (rc) return rc;
+  KGP_CUDA(cudaMemcpy(p->lvl_rows.p, rows.data(), sizeof(int32_t) * n2, cudaMemcpyHostToDevice));
+  p->lvl_ptr = ptr;
+  return KGP_OK;
+}
+
 }  // namespace kgp
 
 using namespace kgp;
+
+extern "C" int kgp_afn_sample(kgp_precond* p, int64_t k, const double* w, int64_t w_rs, int64_t w_cs, double* z,
+                              void* stream) {
+  KGP_REQUIRE(p != nullptr && p->magic == PRECOND_MAGIC && p->kind == KGP_PRECOND_AFN, KGP_ERR_STATE,
+              "kgp_afn_sample needs an AFN handle");
+  KGP_REQUIRE(p->l11.p != nullptr, KGP_ERR_INVALID, "this AFN handle was created without its landmark factor");
+  KGP_REQUIRE(k >= 1 && k <= 65535 && w != nullptr && z != nullptr, KGP_ERR_INVALID, "bad sample arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = afn_levels(p, st);
+  if (rc) return rc;
+  const int64_t n = p->n, m = p->m, n2 = p->n2;
+  rc = p->swork.ensure(sizeof(double) * (size_t)k * (m + 3 * n2));
+  if (rc) return rc;
+  double* z1 = p->swork.as<double>();
+  double* t = z1 + k * m;
+  double* b = t + k * n2;
+  double* x = b + k * n2;
+  // z1 = L11 w1;  t = W w1  (w1: rows 0..m-1 of w)
+  rc = gemm_f64(m, k, m, p->l11.as<double>(), m, 1, w, w_rs, w_cs, z1, 1, m, 1.0, 0.0, nullptr, 0, 0, p->tmp, st);
+  if (rc) return rc;
+  rc = gemm_f64(n2, k, m, p->w.as<double>(), m, 1, w, w_rs, w_cs, t, 1, n2, 1.0, 0.0, nullptr, 0, 0, p->tmp, st);
+  if (rc) return rc;
+  // x = G^-1 w2, level by level
+  afn_gather_tail_kernel<<<vec_grid(n2, k), 256, 0, st>>>(n2, m, w, w_rs, w_cs, b);
+  KGP_LAUNCH("afn_gather_tail_kernel");
+  const int32_t* rows = p->lvl_rows.as<int32_t>();
+  for (size_t L = 0; L + 1 < p->lvl_ptr.size(); ++L) {
+    const int64_t r0 = p->lvl_ptr[L], cnt = p->lvl_ptr[L + 1] - r0;
+    afn_level_solve_kernel<<<dim3((unsigned)((cnt + 127) / 128), (unsigned)k), 128, 0, st>>>(
+        rows + r0, (int)cnt, n2, p->npt1, p->gval.as<double>(), p->gcol.as<int32_t>(), b, x);
+    KGP_LAUNCH("afn_level_solve_kernel");
+  }
+  afn_assemble_kernel<<<vec_grid(n, k), 256, 0, st>>>(n, m, p->perm.as<int64_t>(), z1, t, x, z);
+  KGP_LAUNCH("afn_assemble_kernel");
+  return KGP_OK;
+}
 
 extern "C" int kgp_knn_prev(int64_t n, int d, const double* x, int npt, int64_t* idx_out, void* stream) {
   KGP_REQUIRE(n >= 0 && d >= 1 && d <= 16, KGP_ERR_INVALID, "dimension d=%d outside [1, 16]", d);

@@ -587,8 +587,8 @@ extern "C" int kgp_precond_create(kgp_precond** out, int64_t n, int64_t m, const
 }
 
 extern "C" int kgp_afn_create(kgp_precond** out, int64_t n, int64_t m, const int64_t* perm, const double* linv,
-                              const double* w, int npt1, const double* gval, const int32_t* gcol, int64_t nnz,
-                              const int32_t* gtptr, const int32_t* gtrow, const double* gtval, double s,
+                              const double* l11, const double* w, int npt1, const double* gval, const int32_t* gcol,
+                              int64_t nnz, const int32_t* gtptr, const int32_t* gtrow, const double* gtval, double s,
                               void* stream) {
   KGP_REQUIRE(out != nullptr && perm != nullptr && linv != nullptr && w != nullptr && gval != nullptr &&
                   gcol != nullptr && gtptr != nullptr && gtrow != nullptr && gtval != nullptr,
@@ -620,6 +620,11 @@ extern "C" int kgp_afn_create(kgp_precond** out, int64_t n, int64_t m, const int
     rc = c.dst->ensure(c.bytes);
     if (!rc) rc = cuda_check(cudaMemcpyAsync(c.dst->p, c.src, c.bytes, cudaMemcpyDeviceToDevice, st), "copy AFN factor");
     if (rc) break;
+  }
+  if (!rc && l11) {
+    rc = p->l11.ensure(sizeof(double) * m * m);
+    if (!rc) rc = cuda_check(cudaMemcpyAsync(p->l11.p, l11, sizeof(double) * m * m, cudaMemcpyDeviceToDevice, st),
+                             "copy AFN factor");
   }
   if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "AFN create");
   if (rc) {

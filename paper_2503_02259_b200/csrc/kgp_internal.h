@@ -166,6 +166,10 @@ struct kgp_precond_s {
   kgp::DevBuf gtrow;  // nnz int32
   kgp::DevBuf gtval;  // nnz
   kgp::DevBuf work;   // apply workspace
+  kgp::DevBuf l11;    // (m, m) row-major landmark Cholesky factor (sampling; optional)
+  kgp::DevBuf swork;  // sampling workspace
+  kgp::DevBuf lvl_rows;             // FSAI rows grouped by dependency level
+  std::vector<int64_t> lvl_ptr;     // level offsets into lvl_rows (host)
 };
 
 namespace kgp {

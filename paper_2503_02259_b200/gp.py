@@ -152,7 +152,7 @@ def _generic_iterative(engine, y, preconditioner, probes, tol, max_iter, probe_t
     return LossGrad(loss, g[0], g[1], g[2], converged=wr.all_converged and ur.all_converged)
 
 
-PP_TAIL_SEED = 0x5EED  # second stream of the preconditioned-probe draws (see below)
+PP_TAIL_SEED = precond_mod.PP_TAIL_SEED
 
 
 def nlml_grad_iterative(engine, y, preconditioner, probes: ProbeSet, tol: float = solver.DEFAULT_TOL,
@@ -162,11 +162,12 @@ def nlml_grad_iterative(engine, y, preconditioner, probes: ProbeSet, tol: float 
 
     Keyword-only extensions: ``probe_max_iter`` caps the probe CG / Lanczos length
     separately from the w-solve (None keeps the reference's single ``max_iter``).
-    ``preconditioned_probes`` = True (``preconditioner`` must be a Nystrom M) or a
-    NystromPreconditioner M (then ``preconditioner`` -- e.g. AFN -- serves the w-solve only)
-    switches to the preconditioned estimator: probes z = sqrt(s) w1 + f V w2 ~ N(0, M) with w1 the probe
-    set's vectors and w2 drawn from default_rng([seed..., PP_TAIL_SEED]); the probe solves
-    are preconditioned (a fraction of the reference's unpreconditioned CG iterations),
+    ``preconditioned_probes`` = True (M = ``preconditioner``) or a preconditioner M (then
+    ``preconditioner`` serves the w-solve only) switches to the preconditioned estimator:
+    probes z ~ N(0, M) -- Nystrom: z = sqrt(s) w1 + f V w2 with w1 the probe set's vectors
+    and w2 drawn from default_rng([seed..., PP_TAIL_SEED]); AFN: z = L diag(L11, G^-1) w with
+    w the probe set's vectors (kgp_afn_sample) -- the probe solves are preconditioned (a
+    fraction of the reference's unpreconditioned CG iterations),
     log|Khat| = log|M| + SLQ of M^-1/2 Khat M^-1/2, and the trace terms use
     E[(M^-1 z)^T dK Khat^-1 z]. Unbiased for the same loss and gradient; not the reference's
     same-probe numbers."""
@@ -200,13 +201,10 @@ def nlml_grad_iterative(engine, y, preconditioner, probes: ProbeSet, tol: float 
 
 
 def _nlml_grad_pp(engine, y, pre_w, pre, probes, tol, max_iter, probe_tol, probe_max_iter) -> LossGrad:
-    if not isinstance(engine, KernelEngine) or not isinstance(pre, precond_mod.NystromPreconditioner):
-        raise ValueError("preconditioned_probes needs this package's KernelEngine and a NystromPreconditioner")
+    if not isinstance(engine, KernelEngine) or getattr(pre, "logdet", None) is None:
+        raise ValueError("preconditioned_probes needs this package's KernelEngine and a Nystrom/AFN preconditioner")
     torch = _device.torch()
-    seed = probes.rng_seed if probes.rng_seed is not None else 0
-    seed = list(seed) if isinstance(seed, (tuple, list)) else [seed]
-    w2 = np.random.default_rng([*seed, PP_TAIL_SEED]).standard_normal((pre.rank, probes.k_z))
-    zt = pre.sample(probes.vectors, w2)                      # (k_z, n) on the device
+    zt = pre.draw_probes(probes)                             # (k_z, n) on the device, z ~ N(0, M)
     yd = torch.from_numpy(y).to(zt.device)
     out = (ctypes.c_double * 4)()
     conv = ctypes.c_int32()

@@ -32,6 +32,7 @@ from paper_2503_02259_b200.errors import BreakdownError
 from paper_2503_02259_b200.kernels import as_points, device_panel
 
 RIDGE_SCALE = 1e-10
+PP_TAIL_SEED = 0x5EED  # second stream of the Nystrom preconditioned-probe draws
 
 
 def default_rank(n: int) -> int:
@@ -91,6 +92,14 @@ class NystromPreconditioner:
         self._f2 = float(f2)
         self.n = int(n)
         self.logdet = logdet  # log|M| = n log s + m log f^2 + log|C|, C = I/f^2 + V^T V / s
+
+    def draw_probes(self, probes):
+        """Preconditioned-probe draws: w1 = the probe set's vectors, w2 from a second seeded
+        stream default_rng([seed..., PP_TAIL_SEED]) (gp.nlml_grad_iterative)."""
+        seed = probes.rng_seed if probes.rng_seed is not None else 0
+        seed = list(seed) if isinstance(seed, (tuple, list)) else [seed]
+        w2 = np.random.default_rng([*seed, PP_TAIL_SEED]).standard_normal((self.rank, probes.k_z))
+        return self.sample(probes.vectors, w2)
 
     def sample(self, w1, w2):
         """Draws z = sqrt(s) w1 + f V w2 ~ N(0, M) from standard normals w1 (n, k), w2 (m, k)
@@ -199,12 +208,28 @@ class AFNPreconditioner:
 
     kind = "afn"
 
-    def __init__(self, handle, landmark_indices, shift, n, npt):
+    def __init__(self, handle, landmark_indices, shift, n, npt, logdet=None):
         self._h = handle
         self.landmark_indices = landmark_indices
         self.shift = float(shift)
         self.n = int(n)
         self.fsai_npt = int(npt)
+        self.logdet = logdet  # log|M| = log|K11| - 2 sum log G_ii
+
+    def sample(self, w):
+        """z ~ N(0, M) from standard normals w (n, k) (host or device): (k, n) CUDA tensor."""
+        torch = _device.torch()
+        w = w if _device.is_tensor(w) else _device.to_device(np.asarray(w, dtype=np.float64))
+        if w.dim() != 2 or w.shape[0] != self.n:
+            raise ValueError(f"w must be ({self.n}, k)")
+        out = torch.empty((w.shape[1], self.n), dtype=torch.float64, device=w.device)
+        call("kgp_afn_sample", self._h, w.shape[1], w.data_ptr(), w.stride(0), w.stride(1), out.data_ptr(),
+             _device.stream_ptr())
+        return out
+
+    def draw_probes(self, probes):
+        """Preconditioned-probe draws for gp.nlml_grad_iterative(preconditioned_probes=...)."""
+        return self.sample(probes.vectors)
 
     @property
     def rank(self) -> int:
@@ -307,11 +332,14 @@ def build_afn(engine, m: int | None = None, fsai_npt: int = AFN_DEFAULT_NPT, dia
     gtptr = torch.zeros(n2 + 1, dtype=torch.int64, device=dev)
     gtptr[1:] = torch.cumsum(torch.bincount(cols, minlength=n2), 0)
     gtptr = gtptr.to(torch.int32).contiguous()
+    low = low.contiguous()
     h = ctypes.c_void_p()
-    call("kgp_afn_create", ctypes.byref(h), n, m, perm.data_ptr(), linv.data_ptr(), w.data_ptr(), npt + 1,
-         gval.data_ptr(), gcol.data_ptr(), int(gtrow.numel()), gtptr.data_ptr(), gtrow.data_ptr(),
+    call("kgp_afn_create", ctypes.byref(h), n, m, perm.data_ptr(), linv.data_ptr(), low.data_ptr(), w.data_ptr(),
+         npt + 1, gval.data_ptr(), gcol.data_ptr(), int(gtrow.numel()), gtptr.data_ptr(), gtrow.data_ptr(),
          gtval.data_ptr(), float(p.s), _device.stream_ptr())
-    return AFNPreconditioner(h, _device.to_host(idx).astype(np.intp), p.s, n, npt)
+    diag_g = gval[gcol == torch.arange(n2, dtype=torch.int32, device=dev)[None, :]]  # G_ii (one per row)
+    logdet = 2.0 * float(torch.log(torch.diagonal(low)).sum()) - 2.0 * float(torch.log(diag_g).sum())
+    return AFNPreconditioner(h, _device.to_host(idx).astype(np.intp), p.s, n, npt, logdet)
 
 
 def estimate_rank(engine, sample: int = 1000, seed: int = 0) -> int:

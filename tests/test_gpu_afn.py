@@ -141,3 +141,52 @@ def test_afn_errors(pkg):
     pre = precond.build_afn(e, 10, fsai_npt=4)
     with pytest.raises(ValueError):
         pre.apply_inverse(np.ones(99))
+
+
+def test_afn_sampling_and_logdet(pkg):
+    """kgp_afn_sample draws exactly N(0, M) (covariance of the linear map = M) and
+    AFNPreconditioner.logdet = log|M|, M = (the application's inverse)^-1."""
+    from paper_2503_02259_b200 import precond
+
+    x, _ = _problem("matern32", 500, 3, 0.2, 1e-3)
+    e = pkg.KernelEngine(pkg.KernelType.MATERN32, x, pkg.Hyperparams(l=0.2, f=1.1, s=1e-3))
+    pre = precond.build_afn(e, 40, fsai_npt=8)
+    minv = pre.apply_inverse(np.eye(500))
+    m = np.linalg.inv(minv)
+    z = pre.sample(np.eye(500)).cpu().numpy()            # row r = L F e_r
+    np.testing.assert_allclose(z.T @ z, m, atol=1e-8 * np.abs(m).max())
+    assert abs(pre.logdet - np.linalg.slogdet(m)[1]) <= 1e-9 * abs(pre.logdet)
+
+
+def test_afn_preconditioned_probes_estimator(pkg):
+    """preconditioned_probes=True with AFN equals its dense same-probe formula."""
+    from oracle import kgp_oracle as orc
+    from paper_2503_02259_b200 import gp, precond
+
+    n, kt, l, f, s = 300, "matern52", 0.2, 1.2, 5e-3
+    x, y = _problem(kt, n, 2, l, s, seed=4)
+    e = pkg.KernelEngine(pkg.KernelType(kt), x, pkg.Hyperparams(l=l, f=f, s=s))
+    pre = precond.build_afn(e, 30, fsai_npt=10)
+    probes = gp.ProbeSet.generate(n, 5, 9)
+    lg = gp.nlml_grad_iterative(e, y, pre, probes, tol=1e-11, max_iter=3000, probe_tol=1e-11,
+                                preconditioned_probes=True)
+    z = pre.sample(probes.vectors).cpu().numpy().T
+    kh = orc.khat_dense(kt, x, l, f, s)
+    m = np.linalg.inv(pre.apply_inverse(np.eye(n)))
+    m = 0.5 * (m + m.T)
+    ev, vec = np.linalg.eigh(m)
+    mh = (vec / np.sqrt(ev)) @ vec.T
+    ea, va = np.linalg.eigh(mh @ kh @ mh)
+    loga = (va * np.log(ea)) @ va.T
+    zh = mh @ z
+    w = np.linalg.solve(kh, y)
+    loss = 0.5 * (y @ w + pre.logdet + np.einsum("ij,ij->", zh, loga @ zh) / 5 + n * np.log(2 * np.pi))
+    kap = orc.eval_kernel(kt, x, x, l)
+    dks = [f * f * orc.eval_kernel_grad_l(kt, x, x, l), 2 * f * kap, np.eye(n)]
+    u = np.linalg.solve(kh, z)
+    mz = np.linalg.solve(m, z)
+    grads = [0.5 * (-w @ dk @ w + np.einsum("ij,ij->", mz, dk @ u) / 5) for dk in dks]
+    got = np.array([lg.loss, lg.grad_l, lg.grad_f, lg.grad_s])
+    ref = np.array([loss, *grads])
+    assert lg.converged
+    assert np.all(np.abs(got - ref) <= 1e-6 * np.abs(ref)), (got, ref)

@@ -23,6 +23,10 @@ afn, tb = timed(lambda: precond.build_afn(e, rank, 32))
 lg, t = timed(lambda: gp.nlml_grad_iterative(e, w.y, afn, probes, tol=1e-6, max_iter=max_iter))
 print(f"reference estimator, AFN w-solve: {t:.2f} s (+{tb:.2f} s build) loss {lg.loss:.6f} "
       f"grad ({lg.grad_l:.5g}, {lg.grad_f:.5g}, {lg.grad_s:.5g}) converged {lg.converged}", flush=True)
+lg, t = timed(lambda: gp.nlml_grad_iterative(e, w.y, afn, probes, tol=1e-6, max_iter=max_iter,
+                                             preconditioned_probes=True))
+print(f"preconditioned probes (AFN draws, AFN everywhere): {t:.2f} s loss {lg.loss:.6f} "
+      f"grad ({lg.grad_l:.5g}, {lg.grad_f:.5g}, {lg.grad_s:.5g}) converged {lg.converged}", flush=True)
 ny, tb = timed(lambda: precond.build(e, rank))
 lg, t = timed(lambda: gp.nlml_grad_iterative(e, w.y, afn, probes, tol=1e-6, max_iter=max_iter,
                                              preconditioned_probes=ny))
