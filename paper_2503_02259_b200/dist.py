@@ -1,5 +1,11 @@
 """Row-partitioned multi-GPU PCG / NLML+gradient.
 
+A preconditioner whose application does not shard by rows (AFN: its FSAI factor couples
+each row to its nearest earlier points anywhere in X) is REPLICATED instead: every rank
+holds the full factor, the residual is all-gathered (one more n x k exchange per
+iteration, the same volume as the operator's) and each rank keeps its rows of M^-1 r
+(``ops.replicated_minv``).
+
 One process per GPU. X is replicated (n*d*8 bytes); every n-vector -- the PCG
 state, y, the probes -- is split into contiguous row blocks, rank g owning rows
 I_g. One operator application is
@@ -97,9 +103,14 @@ def dist_pcg(ops, comm: Comm, y_loc, tol: float, max_iter: int, precondition: bo
     def dots(a, b):
         return comm.allreduce((a * b).sum(dim=1)).cpu().numpy()
 
+    full_minv = getattr(ops, "replicated_minv", None)
+    r0, r1 = comm.ranges[comm.rank]
+
     def minv(r):
         if not precondition:
             return r
+        if full_minv is not None:  # replicated preconditioner (AFN): gather, apply, keep own rows
+            return full_minv(comm.allgather_rows(r))[:, r0:r1].contiguous()
         t = comm.allreduce(ops.project(r))
         return ops.expand(r, t, 1.0 / shift, -1.0 / (shift * shift))
 
@@ -178,7 +189,7 @@ def dist_nlml_grad(ops, comm: Comm, y_loc, probes_loc, norms_sq, tol, max_iter, 
 class CudaRowOps:
     """GPU local ops: this rank's rows of the fused operator and of the Woodbury factor."""
 
-    def __init__(self, engine, r0: int, r1: int, precond_wt=None):
+    def __init__(self, engine, r0: int, r1: int, precond_wt=None, replicated=None):
         from paper_2503_02259_b200 import _device
         from paper_2503_02259_b200._lib import PRECISIONS, call
         from paper_2503_02259_b200.kmat import KernelEngine
@@ -189,11 +200,22 @@ class CudaRowOps:
         self.engine = KernelEngine(engine.kt, engine.x, engine.params, precision=engine.precision)
         call("kgp_engine_set_rows", self.engine.handle, r0, r1 - r0)
         self.pre = None
+        if replicated is not None:  # e.g. an AFNPreconditioner built on every rank
+            self._rep = replicated
+            self.replicated_minv = self._replicated_minv
         if precond_wt is not None:
             from paper_2503_02259_b200.precond import _LowRank
 
             self.pre = _LowRank(precond_wt[:, r0:r1], engine.params.s)
             self.m = precond_wt.shape[0]
+
+    def _replicated_minv(self, r_full):
+        torch = self._device.torch()
+        k, n = r_full.shape
+        out = torch.empty_like(r_full)
+        self._call("kgp_precond_apply_inverse", self._rep.handle, k, r_full.data_ptr(), 1, n, out.data_ptr(), 1, n,
+                   self._device.stream_ptr())
+        return out
 
     def _out(self, k):
         torch = self._device.torch()

@@ -98,6 +98,44 @@ def _worker(rank, world, port, errfile):
         raise
 
 
+class ReplicatedAfnOps(OracleRowOps):
+    """Local operator rows from the oracle, M^-1 replicated: the numpy AFN on full vectors."""
+
+    def __init__(self, x, r0, r1, afn):
+        super().__init__(x, r0, r1, None)
+        self.afn = afn
+
+    def replicated_minv(self, r_full):
+        return torch.from_numpy(np.ascontiguousarray(self.afn.apply_inverse(r_full.numpy().T).T))
+
+
+def _afn_worker(rank, world, port, errfile):
+    try:
+        import afn_ref
+
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        x, y, z = _problem()
+        n = len(y)
+        afn = afn_ref.AFN(KT, x, L, F, S, 24, 6)
+        comm = kdist.Comm(n)
+        r0, r1 = kdist.row_range(n, world, rank)
+        ops = ReplicatedAfnOps(x, r0, r1, afn)
+        res = kdist.dist_pcg(ops, comm, torch.from_numpy(np.ascontiguousarray(z.T[:, r0:r1])), 1e-10, 500, True)
+        sol, al, be, rel, conv = orc.pcg(lambda b: orc.khat_matmul(KT, x, L, F, S, b), afn.apply_inverse, z, 1e-10,
+                                         500)
+        full = comm.allgather_rows(res.x).numpy().T
+        assert np.max(np.abs(full - sol)) <= 1e-6 * np.max(np.abs(sol)), "solution"
+        assert np.all(np.abs(res.iters - np.array([len(a) for a in al])) <= 2), (res.iters, [len(a) for a in al])
+        assert all(res.converged)
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as exc:
+        with open(errfile, "a") as fh:
+            fh.write(f"rank {rank}: {type(exc).__name__}: {exc}\n")
+        raise
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -118,3 +156,10 @@ def test_row_ranges_cover_and_balance():
         assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
         sizes = [b - a for a, b in rs]
         assert max(sizes) - min(sizes) <= 1
+
+
+def test_row_partitioned_pcg_replicated_afn_gloo(tmp_path):
+    """AFN (not row-shardable) replicated on every rank: gather r, apply, keep own rows."""
+    errfile = str(tmp_path / "err.txt")
+    mp.spawn(_afn_worker, args=(2, _free_port(), errfile), nprocs=2, join=True)
+    assert not os.path.exists(errfile), open(errfile).read()
