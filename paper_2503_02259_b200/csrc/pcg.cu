@@ -60,9 +60,67 @@ __global__ void dot_final_kernel(int k, int nb, const double* __restrict__ parti
   if (threadIdx.x == 0) out[c] = s;
 }
 
+// One-launch column dots for the PCG loop: out[c] = a_c . b_c (c < k) and, when a2 is
+// given, out2[c] = a2_c . b2_c (c < k2). Each block writes its chunk's partials; the last
+// block of a column (ticket counter) sums them in block order -- the same fixed order as
+// dot_partial + dot_final, so results are run-to-run identical -- and re-arms the ticket.
+__global__ void dot_fused_kernel(int64_t n, int nb, int k2, const double* __restrict__ a, const double* __restrict__ b,
+                                 const double* __restrict__ a2, const double* __restrict__ b2,
+                                 double* __restrict__ partial, double* __restrict__ out, double* __restrict__ out2,
+                                 unsigned* __restrict__ tickets) {
+  const int c = blockIdx.y, blk = blockIdx.x;
+  const bool two = a2 != nullptr && c < k2;
+  const int64_t off = (int64_t)c * n;
+  const int64_t i0 = (int64_t)blk * DOT_CHUNK;
+  const int64_t i1 = i0 + DOT_CHUNK < n ? i0 + DOT_CHUNK : n;
+  double s = 0.0, s2 = 0.0;
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += DOT_THREADS) {
+    s = fma(a[off + i], b[off + i], s);
+    if (two) s2 = fma(a2[off + i], b2[off + i], s2);
+  }
+  __shared__ double red[2][DOT_THREADS / 32];
+  __shared__ bool last;
+  s = warp_sum(s);
+  s2 = warp_sum(s2);
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = s;
+    red[1][threadIdx.x >> 5] = s2;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < DOT_THREADS / 32 ? red[0][threadIdx.x] : 0.0;
+    double v2 = threadIdx.x < DOT_THREADS / 32 ? red[1][threadIdx.x] : 0.0;
+    v = warp_sum(v);
+    v2 = warp_sum(v2);
+    if (threadIdx.x == 0) {
+      partial[((int64_t)c * nb + blk) * 2] = v;
+      partial[((int64_t)c * nb + blk) * 2 + 1] = v2;
+      __threadfence();
+      last = atomicAdd(&tickets[c], 1u) == (unsigned)(nb - 1);
+    }
+  }
+  __syncthreads();
+  if (!last || threadIdx.x >= 32) return;
+  __threadfence();
+  const volatile double* pv = partial + (int64_t)c * nb * 2;
+  double t = 0.0, t2 = 0.0;
+  for (int i = threadIdx.x; i < nb; i += 32) {
+    t += pv[2 * i];
+    t2 += pv[2 * i + 1];
+  }
+  t = warp_sum(t);
+  t2 = warp_sum(t2);
+  if (threadIdx.x == 0) {
+    out[c] = t;
+    if (two) out2[c] = t2;
+    tickets[c] = 0u;
+  }
+}
+
 struct PcgState {
   double *x, *r, *z, *p, *ap;  // (k, n)
   double *rz, *ynorm, *alpha, *beta, *dots1, *dots2, *partial;
+  unsigned* tickets;  // k zero-initialised counters for dot_fused_kernel
   int32_t* active;
   int32_t* status;  // [0] active count, [1] error code, [2] error column (min), [3] pad
   double* err_val;
@@ -100,31 +158,24 @@ __global__ void pcg_init_kernel(int k, PcgGroups g, const double* ynorm_sq, doub
   if (a) atomicAdd(&status[0], 1);
 }
 
-// alpha step (solver.py:159-168)
-__global__ void pcg_alpha_kernel(int k, int stride, const double* pap, const double* rz, const int32_t* active,
-                                 const int32_t* iters, double* alpha, double* alphas, int32_t* status,
-                                 double* err_val) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= k || !active[c]) return;
-  double v = pap[c];
-  if (!isfinite(v) || v <= 0.0) {
-    int old = atomicMin(&status[2], c);
-    status[1] = KGP_ERR_BREAKDOWN;
-    if (c <= old) err_val[0] = v;
-    alpha[c] = 0.0;
-    return;
-  }
-  double a = rz[c] / v;
-  alpha[c] = a;
-  alphas[(int64_t)c * stride + iters[c]] = a;
-}
-
-// x += alpha p; r -= alpha Ap on active columns
-__global__ void pcg_update_xr_kernel(int64_t n, int k, const int32_t* active, const double* alpha, const double* p,
-                                     const double* ap, double* x, double* r) {
+// alpha step (solver.py:159-168) fused with x += alpha p; r -= alpha Ap on active columns:
+// every block derives alpha_c = rz_c / pAp_c itself, block 0 of the column records it
+__global__ void pcg_alpha_update_kernel(int64_t n, int k, int stride, const double* pap, const double* rz,
+                                        const int32_t* active, const int32_t* iters, double* alphas, int32_t* status,
+                                        double* err_val, const double* p, const double* ap, double* x, double* r) {
   const int c = blockIdx.y;
   if (!active[c]) return;
-  const double a = alpha[c];
+  const double v = pap[c];
+  if (!isfinite(v) || v <= 0.0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      int old = atomicMin(&status[2], c);
+      status[1] = KGP_ERR_BREAKDOWN;
+      if (c <= old) err_val[0] = v;
+    }
+    return;
+  }
+  const double a = rz[c] / v;
+  if (blockIdx.x == 0 && threadIdx.x == 0) alphas[(int64_t)c * stride + iters[c]] = a;
   const int64_t off = (int64_t)c * n;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     x[off + i] = fma(a, p[off + i], x[off + i]);
@@ -337,25 +388,24 @@ int enqueue_iteration(kgp_engine_s* e, const PcSet& pcs, int64_t k, const PcgGro
   const bool pc = pcs.count > 0;
   const int64_t n = e->n;
   const PcgState& S = B.S;
-  const unsigned kb = (unsigned)((k + 127) / 128);
   dim3 vgrid((unsigned)((n + 255) / 256 < 64 ? (n + 255) / 256 : 64), (unsigned)k);
+  const int nb = (int)((n + DOT_CHUNK - 1) / DOT_CHUNK);
   int rc = engine_matmul_impl(e, k, S.p, 1, n, S.ap, nullptr, nullptr, 1, n, st);
   if (rc) return rc;
-  rc = col_dots(k, n, S.p, S.ap, S.dots1, S.partial, st);
-  if (rc) return rc;
-  pcg_alpha_kernel<<<kb, 128, 0, st>>>((int)k, g.stride, S.dots1, S.rz, S.active, B.iters, S.alpha, B.alphas,
-                                        S.status, S.err_val);
-  KGP_LAUNCH("pcg_alpha_kernel");
-  pcg_update_xr_kernel<<<vgrid, 256, 0, st>>>(n, (int)k, S.active, S.alpha, S.p, S.ap, B.x, S.r);
-  KGP_LAUNCH("pcg_update_xr_kernel");
+  dot_fused_kernel<<<dim3((unsigned)nb, (unsigned)k), DOT_THREADS, 0, st>>>(
+      n, nb, 0, S.p, S.ap, nullptr, nullptr, S.partial, S.dots1, nullptr, S.tickets);
+  KGP_LAUNCH("dot_fused_kernel");
+  pcg_alpha_update_kernel<<<vgrid, 256, 0, st>>>(n, (int)k, g.stride, S.dots1, S.rz, S.active, B.iters, B.alphas,
+                                                 S.status, S.err_val, S.p, S.ap, B.x, S.r);
+  KGP_LAUNCH("pcg_alpha_update_kernel");
   if (pc && g.kz > 0) {  // M^-1 on the preconditioned columns only
     rc = apply_pcs(pcs, g.kpc, g.kz, n, S.r, S.z, st);
     if (rc) return rc;
-    rc = col_dots(g.kz, n, S.r, S.z, S.dots2, S.partial, st);
-    if (rc) return rc;
   }
-  rc = col_dots(k, n, S.r, S.r, S.dots1, S.partial, st);
-  if (rc) return rc;
+  // r.r on every column and r.z on the preconditioned ones, one launch
+  dot_fused_kernel<<<dim3((unsigned)nb, (unsigned)k), DOT_THREADS, 0, st>>>(
+      n, nb, pc ? g.kz : 0, S.r, S.r, pc ? S.r : nullptr, pc ? S.z : nullptr, S.partial, S.dots1, S.dots2, S.tickets);
+  KGP_LAUNCH("dot_fused_kernel");
   pcg_beta_kernel<<<1, 1024, 0, st>>>((int)k, g, pc, S.dots1, S.dots2, S.rz, S.ynorm, S.active, B.iters,
                                       S.beta, B.betas, B.rel, S.status, B.it_counter, e->hist_dev);
   KGP_LAUNCH("pcg_beta_kernel");
@@ -473,8 +523,8 @@ int pcg_grouped_impl(kgp_engine_s* e, const PcSet& pcs, int64_t k, int64_t kpc, 
   // engine-owned state: r, p, ap, [z], x : (k, n); coefficient arrays; scalars
   const size_t vec = (size_t)k * n;
   const size_t coef = (size_t)k * max_iter;
-  size_t bytes = sizeof(double) * (vec * (pc ? 5 : 4) + 2 * coef + (size_t)k * (9 + nb) + 8) +
-                 sizeof(int32_t) * (2 * k + 16);
+  size_t bytes = sizeof(double) * (vec * (pc ? 5 : 4) + 2 * coef + (size_t)k * (9 + 2 * nb) + 8) +
+                 sizeof(int32_t) * (3 * k + 16);
   int rc = e->ws.ensure(bytes);
   if (rc) return rc;
   if (e->hist_cap < max_iter + 1) {  // mapped host history: 2 ints per iteration
@@ -507,10 +557,11 @@ int pcg_grouped_impl(kgp_engine_s* e, const PcSet& pcs, int64_t k, int64_t kpc, 
   S.err_val = sc + 6 * k;
   B.rel = sc + 7 * k;
   S.partial = sc + 8 * k;
-  S.active = reinterpret_cast<int32_t*>(S.partial + (size_t)k * nb + 8);
+  S.active = reinterpret_cast<int32_t*>(S.partial + (size_t)2 * k * nb + 8);
   S.status = S.active + k;  // 4 ints
   B.iters = S.status + 4;
   B.it_counter = B.iters + k;
+  S.tickets = reinterpret_cast<unsigned*>(B.it_counter + 4);
 
   int32_t* hstatus = e->hstatus;
   const unsigned kb = (unsigned)((k + 127) / 128);
@@ -519,6 +570,7 @@ int pcg_grouped_impl(kgp_engine_s* e, const PcSet& pcs, int64_t k, int64_t kpc, 
   KGP_CUDA(cudaMemcpyAsync(S.r, y, sizeof(double) * vec, cudaMemcpyDeviceToDevice, st));
   KGP_CUDA(cudaMemsetAsync(S.status, 0, sizeof(int32_t) * 4, st));
   KGP_CUDA(cudaMemsetAsync(B.it_counter, 0, sizeof(int32_t), st));
+  KGP_CUDA(cudaMemsetAsync(S.tickets, 0, sizeof(unsigned) * k, st));
   KGP_CUDA(cudaMemsetAsync(B.alphas, 0, sizeof(double) * 2 * coef, st));
   rc = col_dots(k, n, S.r, S.r, S.dots1, S.partial, st);
   if (rc) return rc;

@@ -261,13 +261,15 @@ int skinny_gemm(int64_t M, int64_t N, int64_t K, const double* a, int64_t a_is, 
                 int64_t b_ks, int64_t b_ns, double* c, int64_t c_is, int64_t c_ns, double alpha, double beta,
                 const double* src, int64_t s_is, int64_t s_ns, DevBuf& tmp, cudaStream_t st) {
   // kind 1: CTA per (row, K chunk) for long rows; 2: warp per row for short rows; 0: column kernel
-  const int kind = (a_ks == 1) ? (K >= 8192 ? 1 : 2) : 0;
+  // (a warp per row only when there are enough rows to fill the machine with warps and the
+  // rows are short; otherwise CTAs stream row chunks)
+  const int kind = (a_ks == 1) ? ((K < 8192 && M >= 4096) ? 2 : 1) : 0;
   int64_t nz = 1, kchunk = K > 0 ? K : 1;
   if (kind != 2) {
     const int64_t gx = kind == 1 ? M : (M + 255) / 256;
-    // K chunks: enough CTAs for ~8 per SM, each streaming >= 4096 (row) / 512 (column) elements
+    // K chunks: enough CTAs for ~8 per SM, each streaming >= 1024 (row) / 32 (column) elements
     nz = (1184 + gx - 1) / gx;
-    const int64_t min_chunk = kind == 1 ? 4096 : 512;
+    const int64_t min_chunk = kind == 1 ? 1024 : 32;
     if (nz > (K + min_chunk - 1) / min_chunk) nz = (K + min_chunk - 1) / min_chunk;
     if (nz < 1) nz = 1;
     if (nz > 65535) nz = 65535;
