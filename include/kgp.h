@@ -242,6 +242,14 @@ int kgp_gpc_nlml_grad(kgp_engine* e, int classes, kgp_precond* const* pcs, int n
                       double probe_tol, int32_t probe_max_iter, double* out, int32_t* out_converged,
                       void* stream);
 
+/* kgp_gpc_nlml_grad with preconditioned probes: class c's probes (rows [c*k_z, (c+1)*k_z)
+ * of `probes`) are draws from N(0, M_c) for pcs[c] (one handle per class, e.g.
+ * kgp_afn_sample of an AFN built for Khat + diag(dn_c)), logdet_m = sum_c log|M_c|. */
+int kgp_gpc_nlml_grad_pp(kgp_engine* e, int classes, kgp_precond* const* pcs, const double* dn, const double* y,
+                         int64_t k_z, const double* probes, double logdet_m, double tol, int32_t max_iter,
+                         double probe_tol, int32_t probe_max_iter, double* out, int32_t* out_converged,
+                         void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,6 +66,8 @@ _SIGNATURES = {
     "kgp_slq_logdet": [c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, _P(c_dbl), c_vp],
     "kgp_nlml_grad": [c_vp, c_vp, c_vp, c_i64, c_vp, c_dbl, c_i32, c_dbl, c_i32, _P(c_dbl), _P(c_i32), c_vp],
     "kgp_engine_set_timing": [c_vp, ctypes.c_int],
+    "kgp_gpc_nlml_grad_pp": [c_vp, ctypes.c_int, c_vp, c_vp, c_vp, c_i64, c_vp, c_dbl, c_dbl, c_i32, c_dbl, c_i32,
+                             _P(c_dbl), _P(c_i32), c_vp],
     "kgp_nlml_grad_pp": [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_dbl, c_dbl, c_i32, c_dbl, c_i32, _P(c_dbl), _P(c_i32),
                          c_vp],
     "kgp_engine_matmul_host": [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp],

@@ -93,6 +93,7 @@ struct PcgGraph {
   int64_t k = 0;
   std::vector<const void*> pcs;
   const void* tail = nullptr;
+  int64_t probe_kz = 0;
   int64_t kpc = 0, kz = 0;
   double tol1 = 0.0, tol2 = 0.0;
   int it1 = 0, it2 = 0;
@@ -206,6 +207,7 @@ struct PcSet {
   kgp_precond_s* const* h;
   int count;  // 0: none; 1: one handle for every preconditioned column; kpc: one per column
   kgp_precond_s* tail = nullptr;  // precond_all: handle of columns [kpc, k) (default h[0])
+  int64_t probe_kz = 0;           // precond_all with one handle per class: probe blocks of this width
 };
 int pcg_grouped_impl(kgp_engine_s* e, const PcSet& pcs, int64_t k, int64_t kpc, const double* y, double tol1,
                      int it1, double tol2, int it2, double* x_out, double* alphas, double* betas, int32_t* iters,

@@ -379,7 +379,17 @@ int apply_pcs(const PcSet& pcs, int64_t kpc, int64_t kz, int64_t n, const double
     for (int64_t c = 0; c < head && !rc; ++c)
       rc = precond_apply_impl(pcs.h[c], 1, r + c * n, 1, n, z + c * n, 1, n, st);
   }
-  if (!rc && kz > head) rc = precond_apply_impl(tail, kz - head, r + head * n, 1, n, z + head * n, 1, n, st);
+  if (!rc && kz > head) {
+    if (pcs.probe_kz > 0 && pcs.count == kpc) {
+      // per-class probe blocks (preconditioned-probe GPC): block c preconditioned by class c's handle
+      for (int64_t c = 0; c < kpc && !rc; ++c) {
+        const int64_t c0 = head + c * pcs.probe_kz;
+        rc = precond_apply_impl(pcs.h[c], pcs.probe_kz, r + c0 * n, 1, n, z + c0 * n, 1, n, st);
+      }
+    } else {
+      rc = precond_apply_impl(tail, kz - head, r + head * n, 1, n, z + head * n, 1, n, st);
+    }
+  }
   return rc;
 }
 
@@ -415,7 +425,7 @@ int enqueue_iteration(kgp_engine_s* e, const PcSet& pcs, int64_t k, const PcgGro
 }
 
 bool same_groups(const PcgGraph& c, int64_t k, const PcSet& pcs, const PcgGroups& g) {
-  if (!c.exec || (int)c.pcs.size() != pcs.count || c.tail != pcs.tail) return false;
+  if (!c.exec || (int)c.pcs.size() != pcs.count || c.tail != pcs.tail || c.probe_kz != pcs.probe_kz) return false;
   for (int i = 0; i < pcs.count; ++i)
     if (c.pcs[i] != pcs.h[i]) return false;
   return c.k == k && c.kpc == g.kpc && c.kz == g.kz && c.tol1 == g.tol1 && c.tol2 == g.tol2 &&
@@ -464,6 +474,7 @@ int pcg_graph(kgp_engine_s* e, const PcSet& pcs, int64_t k, const PcgGroups& g, 
   slot.k = k;
   slot.pcs.assign(pcs.h, pcs.h + pcs.count);
   slot.tail = pcs.tail;
+  slot.probe_kz = pcs.probe_kz;
   slot.kpc = g.kpc;
   slot.kz = g.kz;
   slot.tol1 = g.tol1;
@@ -510,8 +521,9 @@ int pcg_grouped_impl(kgp_engine_s* e, const PcSet& pcs, int64_t k, int64_t kpc, 
   for (int i = 0; i < pcs.count; ++i)
     KGP_REQUIRE(pcs.h[i] != nullptr && pcs.h[i]->n == e->n, KGP_ERR_INVALID, "preconditioner %d missing or of wrong size", i);
   const bool pc = pcs.count > 0;
-  KGP_REQUIRE(!precond_all || pcs.count == 1 || pcs.tail, KGP_ERR_INVALID,
-              "preconditioning every column needs one handle or a tail handle");
+  KGP_REQUIRE(!precond_all || pcs.count == 1 || pcs.tail || (pcs.probe_kz > 0 && pcs.count == kpc &&
+                                                              kpc + kpc * pcs.probe_kz == k),
+              KGP_ERR_INVALID, "preconditioning every column needs one handle, a tail handle or per-class blocks");
   PcgGroups g{(int)kpc, 0, tol1, kpc < k ? tol2 : tol1, it1, kpc < k ? it2 : it1, 0};
   g.kz = pcs.count == 0 ? 0 : (precond_all ? (int)k : (int)kpc);
   if (kpc == 0) {
@@ -721,11 +733,19 @@ static int nlml_impl(kgp_engine_s* e, const PcSet& pcs, int64_t C, const double*
   // (3) log|Khat_c| by SLQ over each class's probe traces
   double* Z = V + C * n;
   if (pp) {  // M^-1 Z (into dL as scratch), weights z^T M^-1 z, then V's probe rows := M^-1 Z
-    rc = precond_apply_impl(pcs.tail ? pcs.tail : pcs.h[0], k_z, Z, 1, n, dL, 1, n, st);
+    if (C > 1) {  // class c's probes by class c's preconditioner
+      for (int64_t c = 0; c < C; ++c) {
+        rc = precond_apply_impl(pcs.count == C ? pcs.h[c] : pcs.h[0], k_z, Z + c * k_z * n, 1, n,
+                                dL + c * k_z * n, 1, n, st);
+        if (rc) return rc;
+      }
+    } else {
+      rc = precond_apply_impl(pcs.tail ? pcs.tail : pcs.h[0], k_z, Z, 1, n, dL, 1, n, st);
+      if (rc) return rc;
+    }
+    rc = col_dots(C * k_z, n, Z, dL, nz2, partial, st);
     if (rc) return rc;
-    rc = col_dots(k_z, n, Z, dL, nz2, partial, st);
-    if (rc) return rc;
-    KGP_CUDA(cudaMemcpyAsync(Z, dL, sizeof(double) * k_z * n, cudaMemcpyDeviceToDevice, st));
+    KGP_CUDA(cudaMemcpyAsync(Z, dL, sizeof(double) * C * k_z * n, cudaMemcpyDeviceToDevice, st));
   } else {
     rc = col_dots(C * k_z, n, Z, Z, nz2, partial, st);
     if (rc) return rc;
@@ -819,6 +839,31 @@ extern "C" int kgp_gpc_nlml_grad(kgp_engine* e, int classes, kgp_precond* const*
   if (rc) return rc;
   rc = nlml_impl(e, PcSet{pcs, npcs}, classes, y, k_z, probes, tol, max_iter, probe_tol, probe_max_iter, out,
                  out_converged, (cudaStream_t)stream);
+  kgp_engine_set_diag(e, 0, nullptr, 0, nullptr, stream);
+  return rc;
+}
+
+extern "C" int kgp_gpc_nlml_grad_pp(kgp_engine* e, int classes, kgp_precond* const* pcs, const double* dn,
+                                    const double* y, int64_t k_z, const double* probes, double logdet_m, double tol,
+                                    int32_t max_iter, double probe_tol, int32_t probe_max_iter, double* out,
+                                    int32_t* out_converged, void* stream) {
+  KGP_REQUIRE(e != nullptr && e->magic == ENGINE_MAGIC, KGP_ERR_STATE, "invalid engine handle");
+  KGP_REQUIRE(classes >= 1 && pcs != nullptr, KGP_ERR_INVALID, "need classes >= 1 and one preconditioner per class");
+  for (int i = 0; i < classes; ++i)
+    KGP_REQUIRE(pcs[i] != nullptr && pcs[i]->magic == PRECOND_MAGIC, KGP_ERR_STATE, "invalid preconditioner handle");
+  KGP_REQUIRE(k_z >= 1 && max_iter >= 1 && tol >= 0.0 && probe_tol >= 0.0, KGP_ERR_INVALID, "bad solver arguments");
+  KGP_REQUIRE(dn != nullptr && y != nullptr && probes != nullptr, KGP_ERR_INVALID, "NULL input pointer");
+  KGP_REQUIRE(out != nullptr && out_converged != nullptr, KGP_ERR_INVALID, "NULL output pointer");
+  KGP_REQUIRE(e->row0 == 0 && e->nrows == e->n, KGP_ERR_INVALID, "needs an unpartitioned engine");
+  const int64_t kv = (int64_t)classes * (1 + k_z);
+  std::vector<int32_t> map(kv);
+  for (int64_t c = 0; c < kv; ++c) map[c] = (int32_t)(c < classes ? c : (c - classes) / k_z);
+  int rc = kgp_engine_set_diag(e, classes, dn, kv, map.data(), stream);
+  if (rc) return rc;
+  PcSet set{pcs, classes};
+  set.probe_kz = k_z;
+  rc = nlml_impl(e, set, classes, y, k_z, probes, tol, max_iter, probe_tol, probe_max_iter, out, out_converged,
+                 (cudaStream_t)stream, true, logdet_m);
   kgp_engine_set_diag(e, 0, nullptr, 0, nullptr, stream);
   return rc;
 }

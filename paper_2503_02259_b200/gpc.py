@@ -105,8 +105,13 @@ def build_preconditioners(engine, problem: GPCProblem, rank: int | None = None, 
 
 def nlml_grad_iterative(engine: KernelEngine, problem: GPCProblem, preconditioners, probes,
                         tol: float = solver.DEFAULT_TOL, max_iter: int = solver.DEFAULT_MAX_ITER,
-                        probe_tol: float | None = None, *, probe_max_iter: int | None = None) -> LossGrad:
-    """Summed Dirichlet-GPC loss and (l, f, s) gradient, one libkgp call (kgp_gpc_nlml_grad)."""
+                        probe_tol: float | None = None, *, probe_max_iter: int | None = None,
+                        preconditioned_probes: bool = False) -> LossGrad:
+    """Summed Dirichlet-GPC loss and (l, f, s) gradient, one libkgp call (kgp_gpc_nlml_grad).
+
+    ``preconditioned_probes=True`` (one AFN/Nystrom preconditioner per class): the probe rows
+    of class c are standard normals turned into draws from N(0, M_c) and every solve is
+    preconditioned (kgp_gpc_nlml_grad_pp; gp.nlml_grad_iterative documents the estimator)."""
     torch = _device.torch()
     n, c = problem.n, problem.num_classes
     if engine.n != n:
@@ -127,6 +132,21 @@ def nlml_grad_iterative(engine: KernelEngine, problem: GPCProblem, preconditione
     arr = (ctypes.c_void_p * max(1, len(pcs)))(*[p.handle for p in pcs]) if pcs else None
     out = (ctypes.c_double * 4)()
     conv = ctypes.c_int32()
+    if preconditioned_probes:
+        if len(pcs) != c or any(getattr(p, "logdet", None) is None for p in pcs):
+            raise ValueError("preconditioned probes need one AFN/Nystrom preconditioner per class")
+        draws = []
+        for k in range(c):
+            w = zd[k * k_z:(k + 1) * k_z].T                     # (n, k_z) standard normals
+            pk = pcs[k]
+            draws.append(pk.sample(w) if isinstance(pk, precond_mod.AFNPreconditioner)
+                         else pk.sample(w, torch.from_numpy(np.random.default_rng(
+                             [k, precond_mod.PP_TAIL_SEED]).standard_normal((pk.rank, k_z))).to(dev)))
+        zd = torch.cat(draws, dim=0).contiguous()
+        call("kgp_gpc_nlml_grad_pp", engine.handle, c, arr, dn.data_ptr(), yd.data_ptr(), k_z, zd.data_ptr(),
+             float(sum(p.logdet for p in pcs)), float(tol), int(max_iter), float(probe_tol),
+             int(probe_max_iter or 0), out, ctypes.byref(conv), _device.stream_ptr())
+        return LossGrad(out[0], out[1], out[2], out[3], converged=bool(conv.value))
     call("kgp_gpc_nlml_grad", engine.handle, c, arr, len(pcs), dn.data_ptr(), yd.data_ptr(), k_z, zd.data_ptr(),
          float(tol), int(max_iter), float(probe_tol), int(probe_max_iter or 0), out, ctypes.byref(conv),
          _device.stream_ptr())
@@ -243,7 +263,7 @@ def fit(kt, problem: GPCProblem, init: Hyperparams | None = None, steps: int = 1
         k_z: int = 16, rank: int | None = None, fsai_npt: int = precond_mod.AFN_DEFAULT_NPT,
         tol: float = solver.DEFAULT_TOL, max_iter: int = solver.DEFAULT_MAX_ITER,
         probe_tol: float | None = None, rng_seed: int = 0, precision: str | None = None,
-        preconditioner: str = "afn") -> GPCTrainResult:
+        preconditioner: str = "afn", preconditioned_probes: bool = False) -> GPCTrainResult:
     """Adam in softplus space over (l, f, s) (train.py's optimiser), probes redrawn per step
     from (rng_seed, step); one engine reused across steps (hyperparameters reset in place)."""
     from paper_2503_02259_b200.train import Adam, RawParams, chain_grads
@@ -259,7 +279,8 @@ def fit(kt, problem: GPCProblem, init: Hyperparams | None = None, steps: int = 1
             engine.set_params(hp)
             pcs = build_preconditioners(engine, problem, rank, preconditioner, fsai_npt)
             probes = generate_probes(problem.n, problem.num_classes, k_z, (rng_seed, step))
-            lg = nlml_grad_iterative(engine, problem, pcs, probes, tol=tol, max_iter=max_iter, probe_tol=probe_tol)
+            lg = nlml_grad_iterative(engine, problem, pcs, probes, tol=tol, max_iter=max_iter, probe_tol=probe_tol,
+                                     preconditioned_probes=preconditioned_probes)
             for p in pcs:
                 p.close()
             g_rho = chain_grads(raw, lg.grads())

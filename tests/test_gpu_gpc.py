@@ -137,3 +137,44 @@ def test_gpc_fit_runs(pkg):
     assert len(res.loss_history) == 4 and np.all(np.isfinite(res.loss_history))
     assert res.params.l > 0 and res.params.f > 0 and res.params.s > 0
     assert res.loss_history[-1] < res.loss_history[0]
+
+
+def test_gpc_preconditioned_probes_estimator(pkg):
+    """Per-class AFN draws z_c ~ N(0, M_c): the device estimator equals the dense same-probe
+    formula (sum over classes of the GPR preconditioned estimator), 1e-6."""
+    from oracle import kgp_oracle as orc
+    from paper_2503_02259_b200 import gpc
+
+    x, lab = _data()
+    prob = gpc.setup(x, lab)
+    l, f, s = 0.25, 1.1, 0.02
+    e = pkg.KernelEngine(pkg.KernelType.MATERN32, x, pkg.Hyperparams(l=l, f=f, s=s), precision="fp64")
+    probes = gpc.generate_probes(400, 3, 4, 7)
+    pcs = gpc.build_preconditioners(e, prob, 40, "afn", fsai_npt=8)
+    lg = gpc.nlml_grad_iterative(e, prob, pcs, probes, tol=1e-11, max_iter=2000, probe_tol=1e-11,
+                                 preconditioned_probes=True)
+    n = 400
+    kap = orc.eval_kernel("matern32", x, x, l)
+    kb = f * f * kap + s * np.eye(n)
+    dks = [f * f * orc.eval_kernel_grad_l("matern32", x, x, l), 2 * f * kap, np.eye(n)]
+    loss, g = 0.0, np.zeros(3)
+    for c in range(3):
+        kh = kb + np.diag(prob.noise[c])
+        m = np.linalg.inv(pcs[c].apply_inverse(np.eye(n)))
+        m = 0.5 * (m + m.T)
+        z = pcs[c].sample(probes[c * 4:(c + 1) * 4].T).cpu().numpy().T
+        ev, vec = np.linalg.eigh(m)
+        mh = (vec / np.sqrt(ev)) @ vec.T
+        ea, va = np.linalg.eigh(mh @ kh @ mh)
+        zh = mh @ z
+        w = np.linalg.solve(kh, prob.targets[c])
+        loss += 0.5 * (prob.targets[c] @ w + pcs[c].logdet + np.einsum("ij,ij->", zh, ((va * np.log(ea)) @ va.T) @ zh)
+                       / 4 + n * np.log(2 * np.pi))
+        u = np.linalg.solve(kh, z)
+        mz = np.linalg.solve(m, z)
+        for i, dk in enumerate(dks):
+            g[i] += 0.5 * (-w @ dk @ w + np.einsum("ij,ij->", mz, dk @ u) / 4)
+    got = np.array([lg.loss, lg.grad_l, lg.grad_f, lg.grad_s])
+    ref = np.array([loss, *g])
+    assert lg.converged
+    assert np.all(np.abs(got - ref) <= 1e-6 * np.abs(ref)), (got, ref)
