@@ -261,9 +261,20 @@ def predict(kt, x, y, xstar, params, mode: str = "exact", tol: float = solver.DE
     return Prediction(mean=_device.to_host(mean), stddev=_device.to_host(stddev))
 
 
+def _build_pre(engine, kind: str, rank):
+    if kind == "afn":
+        return precond_mod.build_afn(engine, rank)
+    if kind == "adaptive":
+        return precond_mod.build_adaptive(engine, rank)
+    if kind != "nystrom":
+        raise ValueError(f"preconditioner must be 'nystrom', 'afn' or 'adaptive', got {kind!r}")
+    return precond_mod.build(engine, rank)
+
+
 def predict_hutchinson(kt, x, y, xstar, params, tol: float = solver.DEFAULT_TOL,
                        max_iter: int = solver.DEFAULT_MAX_ITER, precond_rank: int | None = None,
-                       num_probes: int = 64, seed=0, precision: str | None = None) -> Prediction:
+                       num_probes: int = 64, seed=0, precision: str | None = None,
+                       preconditioner: str = "nystrom") -> Prediction:
     """Large-scale prediction (BASELINE configs[4]): no n x m_test cross kernel is formed.
 
     mean = f^2 kappa(X*, X) w with w = Khat^-1 y, one fused cross product (gp.py:241);
@@ -283,7 +294,7 @@ def predict_hutchinson(kt, x, y, xstar, params, tol: float = solver.DEFAULT_TOL,
     f2 = params.f * params.f
     engine = KernelEngine(kt, x, params, precision=precision)          # columns: training points
     star = KernelEngine(kt, xstar, params, precision=precision)        # columns: test points
-    pre = precond_mod.build(engine, precond_rank)
+    pre = _build_pre(engine, preconditioner, precond_rank)
     xd, xsd = engine.x_device(), star.x_device()
     rng = np.random.default_rng(seed)
     zs = torch.from_numpy(rng.choice([-1.0, 1.0], size=(m, num_probes))).to(xd.device)
