@@ -173,6 +173,17 @@ int kgp_afn_sample(kgp_precond* p, int64_t k, const double* w, int64_t w_rs, int
                    void* stream);
 int kgp_precond_kind(kgp_precond* p, int* kind);
 
+/* ------------------------------------------------------------------ local predictive variance
+ * Large-m prediction variance (an extension; the reference computes the exact variance,
+ * gp.py:240-243, one solve per test point): var(x*) ~= f^2 - c^T (Khat_NN)^-1 c over the
+ * npt (<= 64) nearest training points N of x* (local kriging). kgp_knn_cross: idx_out
+ * (nq, npt) int64 nearest training rows of each query (ties to the lower index);
+ * kgp_local_variance: var (nq) from those lists. xq (nq, d), x (nx, d) device fp64. */
+int kgp_knn_cross(int64_t nq, const double* xq, int64_t nx, const double* x, int d, int npt, int64_t* idx_out,
+                  void* stream);
+int kgp_local_variance(int kernel, int64_t nq, int d, const double* xq, const double* x, double l, double f,
+                       double s, int npt, const int64_t* nbr, double* var, void* stream);
+
 /* ------------------------------------------------------------------ solvers
  * pcg_solve (solver.py:122-192): batched PCG, per-column alpha/beta capture,
  * converged columns freeze in place. y and x_out: (k, n) device (column c

@@ -35,27 +35,31 @@ namespace {
 constexpr int KNN_T = 128;
 constexpr int KNN_MAX = 64;
 
-template <int D>
-__global__ void __launch_bounds__(KNN_T) knn_prev_kernel(int64_t n, const double* __restrict__ x, int npt,
-                                                         int64_t* __restrict__ out) {
+// PREV: queries are the candidates themselves (xq == x) and only j < i count (FSAI pattern);
+// otherwise every candidate counts (nearest training points of test points).
+template <int D, bool PREV>
+__global__ void __launch_bounds__(KNN_T) knn_kernel(int64_t nq, const double* __restrict__ xq, int64_t nx,
+                                                    const double* __restrict__ x, int npt, int64_t* __restrict__ out) {
   __shared__ double xs[KNN_T * D];
   const int64_t i = (int64_t)blockIdx.x * KNN_T + threadIdx.x;
   double q[D];
 #pragma unroll
-  for (int c = 0; c < D; ++c) q[c] = i < n ? x[i * D + c] : 0.0;
+  for (int c = 0; c < D; ++c) q[c] = i < nq ? xq[i * D + c] : 0.0;
   double bd[KNN_MAX];
   int64_t bj[KNN_MAX];
   int cnt = 0;
-  const int64_t last = (int64_t)(blockIdx.x + 1) * KNN_T < n ? (int64_t)(blockIdx.x + 1) * KNN_T : n;
+  int64_t last = nx;
+  if (PREV) last = (int64_t)(blockIdx.x + 1) * KNN_T < nx ? (int64_t)(blockIdx.x + 1) * KNN_T : nx;
   for (int64_t j0 = 0; j0 < last; j0 += KNN_T) {
     __syncthreads();
     for (int e = threadIdx.x; e < KNN_T * D; e += KNN_T) {
       const int64_t g = j0 * D + e;
-      xs[e] = g < n * D ? x[g] : 0.0;
+      xs[e] = g < nx * D ? x[g] : 0.0;
     }
     __syncthreads();
-    int64_t lim = i - j0;  // candidates j < i
+    int64_t lim = PREV ? i - j0 : nx - j0;  // PREV: candidates j < i
     if (lim > KNN_T) lim = KNN_T;
+    if (!PREV && i >= nq) lim = 0;
     for (int t = 0; t < lim; ++t) {
       double r = 0.0;
 #pragma unroll
@@ -76,7 +80,7 @@ __global__ void __launch_bounds__(KNN_T) knn_prev_kernel(int64_t n, const double
       }
     }
   }
-  if (i >= n) return;
+  if (i >= nq) return;
   for (int t = 0; t < npt; ++t) out[i * npt + t] = t < cnt ? bj[t] : -1;
 }
 
@@ -322,6 +326,99 @@ __global__ void afn_gather_tail_kernel(int64_t n2, int64_t m, const double* __re
     b[(int64_t)c * n2 + i] = w[(m + i) * w_rs + c * w_cs];
 }
 
+// ------------------------------------------------------------------ local predictive variance
+// var(x*) ~= f^2 - c^T (Khat_NN)^-1 c over the K nearest training points N of x* (local
+// kriging): one CTA per test point, S_NN = f^2 kappa + s I and c = f^2 kappa(x*, x_N) in
+// shared memory, Cholesky, var = f^2 - |L^-1 c|^2.
+struct LvSmem {
+  double S[FS_MAXM * FS_MAXM];
+  double xs[FS_MAXM * 16];
+  double c[FS_MAXM];
+  double q[16];
+  int idx[FS_MAXM];
+  int m;
+  int fail;
+};
+
+template <int KT>
+__global__ void __launch_bounds__(FS_T) local_var_kernel(int64_t nq, int d, const double* __restrict__ xq,
+                                                         const double* __restrict__ x, double l, double f2, double s,
+                                                         int npt, const int64_t* __restrict__ nbr,
+                                                         double* __restrict__ var, int32_t* __restrict__ status) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  LvSmem& sm = *reinterpret_cast<LvSmem*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int64_t i = blockIdx.x;
+  if (tid == 0) {
+    int m = 0;
+    for (int t = 0; t < npt; ++t) {
+      const int64_t j = nbr[i * npt + t];
+      if (j >= 0) sm.idx[m++] = (int)j;
+    }
+    sm.m = m;
+    sm.fail = 0;
+  }
+  if (tid < d) sm.q[tid] = xq[i * d + tid];
+  __syncthreads();
+  const int m = sm.m;
+  for (int e = tid; e < m * d; e += FS_T) sm.xs[e] = x[(int64_t)sm.idx[e / d] * d + e % d];
+  __syncthreads();
+  for (int e = tid; e < m * m + m; e += FS_T) {
+    double r2 = 0.0;
+    if (e < m * m) {
+      const int a = e / m, b = e % m;
+      if (b > a) continue;
+      for (int c = 0; c < d; ++c) {
+        const double df = sm.xs[a * d + c] - sm.xs[b * d + c];
+        r2 = fma(df, df, r2);
+      }
+      sm.S[a * m + b] = f2 * kappa64<KT>(r2, l) + (a == b ? s : 0.0);
+    } else {
+      const int a = e - m * m;
+      for (int c = 0; c < d; ++c) {
+        const double df = sm.xs[a * d + c] - sm.q[c];
+        r2 = fma(df, df, r2);
+      }
+      sm.c[a] = f2 * kappa64<KT>(r2, l);
+    }
+  }
+  __syncthreads();
+  for (int j = 0; j < m; ++j) {  // in-place lower Cholesky
+    if (tid == 0) {
+      const double v = sm.S[j * m + j];
+      if (!(v > 0.0) || !isfinite(v)) sm.fail = 1;
+      sm.S[j * m + j] = sqrt(v > 0.0 ? v : 1.0);
+    }
+    __syncthreads();
+    const double djj = sm.S[j * m + j];
+    for (int a = j + 1 + tid; a < m; a += FS_T) sm.S[a * m + j] /= djj;
+    __syncthreads();
+    const int rr = m - j - 1;
+    for (int e = tid; e < rr * rr; e += FS_T) {
+      const int a = j + 1 + e / rr, b = j + 1 + e % rr;
+      if (b <= a) sm.S[a * m + b] -= sm.S[a * m + j] * sm.S[b * m + j];
+    }
+    __syncthreads();
+  }
+  if (tid < 32) {  // forward solve L y = c (in place in c), var = f^2 - |y|^2
+    for (int a = 0; a < m; ++a) {
+      double v = 0.0;
+      for (int b = tid; b < a; b += 32) v = fma(sm.S[a * m + b], sm.c[b], v);
+      v = warp_sum(v);
+      if (tid == 0) sm.c[a] = (sm.c[a] - v) / sm.S[a * m + a];
+      __syncwarp();
+    }
+    double ss = 0.0;
+    for (int a = tid; a < m; a += 32) ss = fma(sm.c[a], sm.c[a], ss);
+    ss = warp_sum(ss);
+    if (tid == 0) {
+      const double v = f2 - ss;
+      var[i] = v > 0.0 ? v : 0.0;
+      if (sm.fail) atomicMin(status, (int)i);
+    }
+  }
+}
+
 inline dim3 vec_grid(int64_t n, int64_t k) {
   int64_t bx = (n + 255) / 256;
   if (bx > 592) bx = 592;
@@ -460,14 +557,72 @@ extern "C" int kgp_knn_prev(int64_t n, int d, const double* x, int npt, int64_t*
   switch (d) {
 #define KGP_KNN_CASE(D)                                                \
   case D:                                                              \
-    knn_prev_kernel<D><<<grid, KNN_T, 0, st>>>(n, x, npt, idx_out);   \
+    knn_kernel<D, true><<<grid, KNN_T, 0, st>>>(n, x, n, x, npt, idx_out); \
     break;
     KGP_KNN_CASE(1) KGP_KNN_CASE(2) KGP_KNN_CASE(3) KGP_KNN_CASE(4) KGP_KNN_CASE(5) KGP_KNN_CASE(6)
     KGP_KNN_CASE(7) KGP_KNN_CASE(8) KGP_KNN_CASE(9) KGP_KNN_CASE(10) KGP_KNN_CASE(11) KGP_KNN_CASE(12)
     KGP_KNN_CASE(13) KGP_KNN_CASE(14) KGP_KNN_CASE(15) KGP_KNN_CASE(16)
 #undef KGP_KNN_CASE
   }
-  KGP_LAUNCH("knn_prev_kernel");
+  KGP_LAUNCH("knn_kernel");
+  return KGP_OK;
+}
+
+extern "C" int kgp_knn_cross(int64_t nq, const double* xq, int64_t nx, const double* x, int d, int npt,
+                             int64_t* idx_out, void* stream) {
+  KGP_REQUIRE(nq >= 0 && nx >= 1 && d >= 1 && d <= 16, KGP_ERR_INVALID, "bad kNN shapes (d=%d)", d);
+  KGP_REQUIRE(npt >= 1 && npt <= KNN_MAX, KGP_ERR_INVALID, "npt=%d outside [1, %d]", npt, KNN_MAX);
+  KGP_REQUIRE(nq == 0 || (xq != nullptr && x != nullptr && idx_out != nullptr), KGP_ERR_INVALID, "NULL pointer");
+  if (nq == 0) return KGP_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned grid = (unsigned)((nq + KNN_T - 1) / KNN_T);
+  switch (d) {
+#define KGP_KNNX_CASE(D)                                                        \
+  case D:                                                                       \
+    knn_kernel<D, false><<<grid, KNN_T, 0, st>>>(nq, xq, nx, x, npt, idx_out);  \
+    break;
+    KGP_KNNX_CASE(1) KGP_KNNX_CASE(2) KGP_KNNX_CASE(3) KGP_KNNX_CASE(4) KGP_KNNX_CASE(5) KGP_KNNX_CASE(6)
+    KGP_KNNX_CASE(7) KGP_KNNX_CASE(8) KGP_KNNX_CASE(9) KGP_KNNX_CASE(10) KGP_KNNX_CASE(11) KGP_KNNX_CASE(12)
+    KGP_KNNX_CASE(13) KGP_KNNX_CASE(14) KGP_KNNX_CASE(15) KGP_KNNX_CASE(16)
+#undef KGP_KNNX_CASE
+  }
+  KGP_LAUNCH("knn_kernel");
+  return KGP_OK;
+}
+
+extern "C" int kgp_local_variance(int kernel, int64_t nq, int d, const double* xq, const double* x, double l,
+                                  double f, double s, int npt, const int64_t* nbr, double* var, void* stream) {
+  KGP_REQUIRE(kernel >= 0 && kernel <= 2, KGP_ERR_INVALID, "unknown kernel id %d", kernel);
+  KGP_REQUIRE(d >= 1 && d <= 16 && npt >= 1 && npt <= KNN_MAX && nq >= 0 && nq < ((int64_t)1 << 31),
+              KGP_ERR_INVALID, "bad local-variance shapes");
+  KGP_REQUIRE(l > 0.0 && s > 0.0, KGP_ERR_INVALID, "length scale and noise must be positive");
+  if (nq == 0) return KGP_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  DevBuf status;
+  int rc = status.ensure(sizeof(int32_t));
+  if (rc) return rc;
+  KGP_CUDA(cudaMemsetAsync(status.p, 0x7f, sizeof(int32_t), st));
+  const size_t smem = sizeof(LvSmem);
+  switch (kernel) {
+#define KGP_LV_CASE(K)                                                                                          \
+  case K: {                                                                                                     \
+    static bool configured = false;                                                                             \
+    if (!configured) {                                                                                          \
+      KGP_CUDA(cudaFuncSetAttribute(local_var_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+      configured = true;                                                                                        \
+    }                                                                                                           \
+    local_var_kernel<K><<<(unsigned)nq, FS_T, smem, st>>>(nq, d, xq, x, l, f * f, s, npt, nbr, var,            \
+                                                          status.as<int32_t>());                                \
+    break;                                                                                                      \
+  }
+    KGP_LV_CASE(0) KGP_LV_CASE(1) KGP_LV_CASE(2)
+#undef KGP_LV_CASE
+  }
+  KGP_LAUNCH("local_var_kernel");
+  int32_t bad = 0;
+  KGP_CUDA(cudaMemcpyAsync(&bad, status.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  KGP_CUDA(cudaStreamSynchronize(st));
+  KGP_REQUIRE(bad == 0x7f7f7f7f, KGP_ERR_NUMERICAL, "local covariance block of test point %d is not SPD", bad);
   return KGP_OK;
 }
 

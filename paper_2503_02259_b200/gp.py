@@ -308,3 +308,33 @@ def predict_hutchinson(kt, x, y, xstar, params, tol: float = solver.DEFAULT_TOL,
     diag = (zs * az[:, 1:]).mean(dim=1)
     stddev = torch.sqrt(torch.clamp(f2 - diag, min=0.0))
     return Prediction(mean=_device.to_host(mean), stddev=_device.to_host(stddev))
+
+
+def predict_local(kt, x, y, xstar, params, tol: float = solver.DEFAULT_TOL, max_iter: int = solver.DEFAULT_MAX_ITER,
+                  precond_rank: int | None = None, k_nn: int = 64, precision: str | None = None,
+                  preconditioner: str = "afn") -> Prediction:
+    """Large-scale prediction with a LOCAL variance (extension; SURVEY §8(f)2 leaves large-m
+    variance open): mean = f^2 kappa(X*, X) w (w = Khat^-1 y by device PCG, one fused cross
+    product), variance = f^2 - c^T Khat_NN^-1 c over the k_nn nearest training points of each
+    test point (kgp_knn_cross + kgp_local_variance). Equal to the exact variance when k_nn
+    covers the training set; otherwise an approximation that is good when the kernel's
+    correlation length is short against the data's extent (measured in DESIGN.md)."""
+    torch = _device.torch()
+    x = as_points(x, "X")
+    n = x.shape[0]
+    y = _check_y(y, n)
+    xstar = as_points(np.asarray(xstar, dtype=np.float64).reshape(-1, x.shape[1]), "Xstar")
+    m = xstar.shape[0]
+    k_nn = int(min(k_nn, n))
+    engine = KernelEngine(kt, x, params, precision=precision)
+    pre = _build_pre(engine, preconditioner, precond_rank)
+    xd = engine.x_device()
+    xsd = _device.to_device(xstar)
+    w = solver.pcg_device(engine, pre, _device.to_device(y)[None, :].contiguous(), tol, max_iter)[0]
+    mean = engine.cross_matmul(xsd, w.T.contiguous())[:, 0]
+    nbr = torch.empty((m, k_nn), dtype=torch.int64, device=xd.device)
+    call("kgp_knn_cross", m, xsd.data_ptr(), n, xd.data_ptr(), x.shape[1], k_nn, nbr.data_ptr(), _device.stream_ptr())
+    var = torch.empty(m, dtype=torch.float64, device=xd.device)
+    call("kgp_local_variance", kernel_id(kt), m, x.shape[1], xsd.data_ptr(), xd.data_ptr(), float(params.l),
+         float(params.f), float(params.s), k_nn, nbr.data_ptr(), var.data_ptr(), _device.stream_ptr())
+    return Prediction(mean=_device.to_host(mean), stddev=_device.to_host(torch.sqrt(var)))

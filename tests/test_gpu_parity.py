@@ -542,3 +542,41 @@ def test_preconditioned_probes_unbiased(pkg):
                                            probe_tol=1e-8, preconditioned_probes=True).grads() for r in range(8)])
     mean, sem = est.mean(axis=0), est.std(axis=0, ddof=1) / np.sqrt(len(est))
     assert np.all(np.abs(mean - ex.grads()) <= 4 * sem + 1e-9 * np.abs(ex.grads())), (mean, ex.grads(), sem)
+
+
+
+def test_predict_local_variance(pkg):
+    """predict_local: exact when the neighbourhood is the whole training set; the cross kNN
+    matches a numpy search; a 64-neighbour variance is close to the exact one for a short
+    length scale."""
+    import torch
+
+    from oracle import kgp_oracle as orc
+    from paper_2503_02259_b200 import _lib, gp
+
+    rng = np.random.default_rng(21)
+    x = rng.uniform(0, 1, (60, 2))
+    y = np.sin(4 * x[:, 0]) + 0.05 * rng.standard_normal(60)
+    xs = rng.uniform(0, 1, (25, 2))
+    hp = _hp(pkg, 0.3, 1.2, 1e-2)
+    ex = gp.predict(pkg.KernelType.MATERN52, x, y, xs, hp, mode="exact")
+    lo = gp.predict_local(pkg.KernelType.MATERN52, x, y, xs, hp, tol=1e-12, max_iter=500, k_nn=64,
+                          preconditioner="nystrom", precond_rank=20)
+    assert rel_max(lo.stddev, ex.stddev) <= 1e-8
+    assert rel_max(lo.mean, ex.mean) <= 1e-8
+    # cross kNN against numpy (distances, ties to the lower index)
+    nbr = torch.empty((25, 7), dtype=torch.int64, device="cuda")
+    xd, xsd = torch.from_numpy(x).cuda(), torch.from_numpy(xs).cuda()
+    _lib.call("kgp_knn_cross", 25, xsd.data_ptr(), 60, xd.data_ptr(), 2, 7, nbr.data_ptr(), None)
+    d2 = orc.sqdist(xs, x)
+    want = np.array([np.lexsort((np.arange(60), r))[:7] for r in d2])
+    np.testing.assert_array_equal(nbr.cpu().numpy(), want)
+    # short length scale, 3000 points: 64 neighbours carry almost all the information
+    x = rng.uniform(0, 1, (3000, 2))
+    y = np.cos(6 * x[:, 1]) + 0.05 * rng.standard_normal(3000)
+    xs = rng.uniform(0, 1, (200, 2))
+    hp = _hp(pkg, 0.05, 1.0, 1e-2)
+    ex = gp.predict(pkg.KernelType.MATERN32, x, y, xs, hp, mode="exact")
+    lo = gp.predict_local(pkg.KernelType.MATERN32, x, y, xs, hp, tol=1e-10, max_iter=2000, k_nn=64)
+    assert np.max(np.abs(lo.stddev - ex.stddev) / ex.stddev) <= 0.05, np.max(np.abs(lo.stddev - ex.stddev) / ex.stddev)
+    assert rel_max(lo.mean, ex.mean) <= 1e-6

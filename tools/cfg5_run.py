@@ -32,3 +32,14 @@ pr, t = timed(lambda: gp.predict_hutchinson(kgp.KernelType.MATERN52, w.x, w.y, w
 truth = np.sin(4 * np.pi * w.extra["xstar"][:, 0]) + np.cos(4 * np.pi * w.extra["xstar"][:, 1])
 print(f"predict (Hutchinson, m={mt}, 64 probes): {t:.2f} s, rmse vs noise-free truth "
       f"{np.sqrt(np.mean((pr.mean - truth) ** 2)):.4f}, mean stddev {pr.stddev.mean():.4f}", flush=True)
+
+pl, t = timed(lambda: gp.predict_local(kgp.KernelType.MATERN52, w.x, w.y, w.extra["xstar"], hp, tol=1e-6,
+                                       max_iter=500, precond_rank=w.rank, k_nn=64, precision="fast"))
+print(f"predict (local variance, 64 neighbours, m={mt}): {t:.2f} s, rmse {np.sqrt(np.mean((pl.mean - truth) ** 2)):.4f}, "
+      f"mean stddev {pl.stddev.mean():.4f} (min {pl.stddev.min():.4f}, max {pl.stddev.max():.4f})", flush=True)
+# accuracy of the local variance against the exact one on a subsample of the problem
+ns, ms = 8192, 512
+pe = gp.predict(kgp.KernelType.MATERN52, w.x[:ns], w.y[:ns], w.extra["xstar"][:ms], hp, mode="exact")
+pq = gp.predict_local(kgp.KernelType.MATERN52, w.x[:ns], w.y[:ns], w.extra["xstar"][:ms], hp, tol=1e-10, k_nn=64)
+print(f"local vs exact variance (n={ns}, m={ms}): max rel err of stddev "
+      f"{np.max(np.abs(pq.stddev - pe.stddev) / pe.stddev):.3e}", flush=True)
