@@ -28,7 +28,6 @@ CPU with gloo (tests/test_dist.py injects an oracle-backed implementation);
 
 from __future__ import annotations
 
-import ctypes
 import math
 from dataclasses import dataclass
 
@@ -191,7 +190,7 @@ class CudaRowOps:
 
     def __init__(self, engine, r0: int, r1: int, precond_wt=None, replicated=None):
         from paper_2503_02259_b200 import _device
-        from paper_2503_02259_b200._lib import PRECISIONS, call
+        from paper_2503_02259_b200._lib import call
         from paper_2503_02259_b200.kmat import KernelEngine
 
         self._device, self._call = _device, call
