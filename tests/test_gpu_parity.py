@@ -580,3 +580,20 @@ def test_predict_local_variance(pkg):
     lo = gp.predict_local(pkg.KernelType.MATERN32, x, y, xs, hp, tol=1e-10, max_iter=2000, k_nn=64)
     assert np.max(np.abs(lo.stddev - ex.stddev) / ex.stddev) <= 0.05, np.max(np.abs(lo.stddev - ex.stddev) / ex.stddev)
     assert rel_max(lo.mean, ex.mean) <= 1e-6
+
+
+@pytest.mark.parametrize("n", [1, 2, 31, 33, 127, 129, 4097])
+@pytest.mark.parametrize("d", [1, 3, 8])
+def test_fast_operator_tiny_and_ragged_n(pkg, n, d):
+    """Row/column counts off the 32-column block and 128-row CTA tiles, down to one point."""
+    rng = np.random.default_rng(n * 31 + d)
+    x = rng.standard_normal((n, d))
+    b = rng.standard_normal((n, 5))
+    hp = _hp(pkg, 0.8 * np.sqrt(d), 1.1, 0.3)
+    ref = pkg.KernelEngine(pkg.KernelType.MATERN52, x, hp, precision="fp64").matmul_with_grads(b)
+    for prec, bar in (("fast", 2e-5), ("tf32", 1e-3)):
+        got = pkg.KernelEngine(pkg.KernelType.MATERN52, x, hp, precision=prec).matmul_with_grads(b)
+        assert rel_max(got[0], ref[0]) <= bar, prec
+        assert rel_max(got[2], ref[2]) <= bar, prec
+        if n > 1:
+            assert rel_max(got[1], ref[1]) <= 10 * bar, prec
