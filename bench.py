@@ -155,6 +155,14 @@ def cpu_baseline(w, rows, steps=1):
     return units / best, best, oc.max_threads()
 
 
+def bench_config(args, w, world):
+    """The workload description both arms print (the driver compares them)."""
+    return {"workload": "cfg2 standalone fused MatMul (BASELINE.json configs[1])", "n": w.n, "d": w.d,
+            "k": w.z.shape[1], "kernel": "gaussian", "l": w.l, "f": w.f, "s": w.s,
+            "outputs": ["Khat.Z", "dKhat/dl.Z"], "precision": args.precision,
+            "l2": "flushed (256 MB write) between timed iterations", "parallelism": f"rows{world}"}
+
+
 def run_reference(args):
     """--impl reference: the reference's CPU algorithm (oracle port) on this box's host cores."""
     rank = int(os.environ.get("RANK", "0"))
@@ -177,8 +185,7 @@ def run_reference(args):
         "value": value, "unit": "entries*RHS/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": float(np.median(times)) * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, cfg2 shapes)",
-        "config": {"workload": "cfg2 standalone fused MatMul", "n": args.n, "d": 8, "k": args.k,
-                   "kernel": "gaussian", "outputs": ["Khat.Z", "dKhat/dl.Z"]},
+        "config": bench_config(args, w, args.gpus),
         "cpu_baseline": {"value": value, "unit": "entries*RHS/s", "cores": cores, "kind": "port",
                          "sample": f"{args.ref_rows} of {args.n} rows per step, both outputs, fp64; "
                                    "oracle/kgp_oracle.c (C restatement of kmat.py:165-189)"},
@@ -438,10 +445,7 @@ def run_gpu(args):
             "scaling": "strong", "vs_baseline": None,
             "dtype": {"fast": "f32 tile + 3xtf32 mma", "tf32": "f32 tile + tf32 mma", "fp64": "f64"}[args.precision],
             "data": "synthetic (seeded numpy default_rng, BASELINE configs[1] shapes and distributions)",
-            "config": {"workload": "cfg2 standalone fused MatMul (BASELINE.json configs[1])", "n": n, "d": 8,
-                       "k": k, "kernel": "gaussian", "l": w.l, "f": w.f, "s": w.s,
-                       "outputs": ["Khat.Z", "dKhat/dl.Z"], "precision": args.precision,
-                       "l2": "flushed (256 MB write) between timed iterations", "parallelism": f"rows{world}"},
+            "config": bench_config(args, w, world),
             "e2e": {"value": units / t_e2e, "unit": "entries*RHS/s", "h2d_bytes_per_step": int(zh.numel() * 8),
                     "d2h_bytes_per_step": int(2 * ok_h.numel() * 8), "ms_per_step": t_e2e * 1e3},
             "gpu_launches": launches,
