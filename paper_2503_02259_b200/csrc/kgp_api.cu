@@ -488,7 +488,11 @@ extern "C" int kgp_engine_matmul_host(kgp_engine* e, int64_t k, const double* b,
     KGP_CUDA(cudaStreamCreateWithFlags(&e->xstream, cudaStreamNonBlocking));
     for (auto& ev : e->xev) KGP_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }
-  const int nchunk = chunked ? 4 : 1;
+  // 2 row chunks measured best at cfg2 (e2e 4.13 ms; 1: 4.39, 3: 4.18, 4: 4.17): each chunk
+  // keeps ~7 waves of CTAs, and the exposed tail transfer is half the output
+  const int max_chunks = (int)(sizeof(e->xev) / sizeof(e->xev[0]));
+  int nchunk = chunked ? tc_env_int("KGP_HOST_CHUNKS", 2) : 1;
+  nchunk = nchunk < 1 ? 1 : (nchunk > max_chunks ? max_chunks : nchunk);
   if (chunked) {
     rc = engine_prepare(e, st);
     if (rc) return rc;
