@@ -488,10 +488,11 @@ extern "C" int kgp_engine_matmul_host(kgp_engine* e, int64_t k, const double* b,
     KGP_CUDA(cudaStreamCreateWithFlags(&e->xstream, cudaStreamNonBlocking));
     for (auto& ev : e->xev) KGP_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }
-  // 2 row chunks measured best at cfg2 (e2e 4.13 ms; 1: 4.39, 3: 4.18, 4: 4.17): each chunk
-  // keeps ~7 waves of CTAs, and the exposed tail transfer is half the output
+  // 3 row chunks, the last one a third of an even share (KGP_HOST_CHUNKS / KGP_HOST_TAIL;
+  // tools/e2e_tail.sh): cfg2 e2e 3.97 ms (one chunk 4.39; 2 even 4.13; 4 even 4.17) -- the
+  // transfer of each chunk's outputs hides behind the next chunk and the exposed tail is short
   const int max_chunks = (int)(sizeof(e->xev) / sizeof(e->xev[0]));
-  int nchunk = chunked ? tc_env_int("KGP_HOST_CHUNKS", 2) : 1;
+  int nchunk = chunked ? tc_env_int("KGP_HOST_CHUNKS", 3) : 1;
   nchunk = nchunk < 1 ? 1 : (nchunk > max_chunks ? max_chunks : nchunk);
   if (chunked) {
     rc = engine_prepare(e, st);
@@ -502,7 +503,17 @@ extern "C" int kgp_engine_matmul_host(kgp_engine* e, int64_t k, const double* b,
   for (int c = 0; c < nchunk; ++c) {
     // chunk boundaries on 128-row CTA tiles
     const int64_t blocks = (rows + 127) / 128;
-    const int64_t r0 = std::min(rows, blocks * c / nchunk * 128), r1 = std::min(rows, blocks * (c + 1) / nchunk * 128);
+    // chunk c ends at fraction (c+1)/nchunk of the rows, the last chunk shrunk to `tail_frac` of an
+    // even share so the exposed device->host tail is short (KGP_HOST_TAIL, percent)
+    auto edge = [&](int c2) -> int64_t {
+      if (c2 <= 0) return 0;
+      if (c2 >= nchunk) return rows;
+      const double tail = tc_env_int("KGP_HOST_TAIL", 35) / 100.0;
+      const double last = tail / (nchunk - 1 + tail);  // fraction of the rows in the last chunk
+      const double f = (double)c2 * (1.0 - last) / (nchunk - 1);
+      return std::min(rows, (int64_t)(f * blocks + 0.5) * 128);
+    };
+    const int64_t r0 = edge(c), r1 = edge(c + 1);
     if (r1 <= r0) continue;
     if (chunked) {
       rc = tc_matmul(e, e->xrow.as<float>() + r0 * (e->dpad + 1), r1 - r0, e->row0 + r0, k, db, k, 1,
