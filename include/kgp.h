@@ -68,6 +68,11 @@ int kgp_engine_set_precision(kgp_engine* e, int precision);
 /* Row partition for multi-GPU: this engine produces rows [row0, row0 + nrows) of Khat.B. */
 int kgp_engine_set_rows(kgp_engine* e, int64_t row0, int64_t nrows);
 int kgp_engine_destroy(kgp_engine* e); /* second destroy of the same handle -> KGP_ERR_STATE */
+/* DENSE mode (kmat.py:93-94, 107-123: the reference auto-selects it for n <= 20000):
+ * with precision KGP_FP64, single-output products Khat.B (unit-stride columns) use Khat
+ * materialised once in HBM (n^2 fp64, rebuilt when (l, f, s) change) and a cuBLAS DGEMM;
+ * derivative products stay on the fused kernel. enable = 0 frees the matrix. */
+int kgp_engine_set_dense(kgp_engine* e, int enable);
 /* Heteroscedastic shift for GP classification (no reference counterpart: SPEC.md:382 lists
  * GPC and heteroscedastic noise as non-goals; the Dirichlet-based GPC of gpc.py needs it):
  * column c of every later Khat product becomes f^2 kappa b_c + (s + dn[map[c]]) o b_c.

@@ -66,6 +66,7 @@ _SIGNATURES = {
     "kgp_slq_logdet": [c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, _P(c_dbl), c_vp],
     "kgp_nlml_grad": [c_vp, c_vp, c_vp, c_i64, c_vp, c_dbl, c_i32, c_dbl, c_i32, _P(c_dbl), _P(c_i32), c_vp],
     "kgp_engine_set_timing": [c_vp, ctypes.c_int],
+    "kgp_engine_set_dense": [c_vp, ctypes.c_int],
     "kgp_knn_cross": [c_i64, c_vp, c_i64, c_vp, ctypes.c_int, ctypes.c_int, c_vp, c_vp],
     "kgp_local_variance": [ctypes.c_int, c_i64, ctypes.c_int, c_vp, c_vp, c_dbl, c_dbl, c_dbl, ctypes.c_int, c_vp,
                            c_vp, c_vp],

@@ -9,6 +9,8 @@
 #include <mutex>
 #include <set>
 
+#include <cublas_v2.h>
+
 #include "kgp_common.cuh"
 #include "kgp_internal.h"
 
@@ -74,6 +76,7 @@ static void engine_free_host_state(kgp_engine_s* e) {
     if (ev) cudaEventDestroy(ev);
   if (e->cstream) cudaStreamDestroy(e->cstream);
   if (e->xstream) cudaStreamDestroy(e->xstream);
+  if (e->cublas) cublasDestroy((cublasHandle_t)e->cublas);
   for (auto ev : e->xev)
     if (ev) cudaEventDestroy(ev);
   for (auto ev : e->tev) cudaEventDestroy(ev);
@@ -234,9 +237,53 @@ int engine_matmul_impl(kgp_engine_s* e, int64_t k, const double* b, int64_t b_rs
   return KGP_OK;
 }
 
+__global__ void dense_finish_kernel(int64_t n, double f2, double s, double* k) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += (int64_t)gridDim.x * blockDim.x) {
+    double v = f2 * k[e];
+    if (e / n == e % n) v += s;
+    k[e] = v;
+  }
+}
+
+// Khat = f^2 kappa(X, X) + s I, materialised once (kmat.py:107-123: the reference's DENSE
+// mode, auto-selected for n <= 20000), through the parity panel kernel (numba's rounding)
+static int dense_build(kgp_engine_s* e, cudaStream_t st) {
+  if (e->dense_valid) return KGP_OK;
+  int rc = e->dense.ensure(sizeof(double) * (size_t)e->n * e->n);
+  if (rc) return rc;
+  rc = kgp_eval_panel(e->kt, 0, e->n, e->n, e->d, e->x64.as<double>(), e->x64.as<double>(), e->l,
+                      e->dense.as<double>(), e->n, st);
+  if (rc) return rc;
+  dense_finish_kernel<<<1184, 256, 0, st>>>(e->n, e->f * e->f, e->s, e->dense.as<double>());
+  KGP_LAUNCH("dense_finish_kernel");
+  if (!e->cublas) {
+    cublasHandle_t h;
+    KGP_REQUIRE(cublasCreate(&h) == CUBLAS_STATUS_SUCCESS, KGP_ERR_CUDA, "cublasCreate failed");
+    e->cublas = h;
+  }
+  e->dense_valid = true;
+  return KGP_OK;
+}
+
 static int engine_matmul_core(kgp_engine_s* e, int64_t k, const double* b, int64_t b_rs, int64_t b_cs,
                               double* out_k, double* out_dl, double* out_df, int64_t o_rs, int64_t o_cs,
                               cudaStream_t st) {
+  if (e->precision == KGP_FP64 && e->dense_on && out_k && !out_dl && !out_df && b_rs == 1 && o_rs == 1 &&
+      b_cs >= e->n && o_cs >= e->nrows) {
+    // out (nrows x k, column-major) = Khat[row0:row0+nrows, :] B; Khat symmetric and row-major,
+    // i.e. column-major Khat^T = Khat, so the row block is op(A) = A^T of column block row0
+    int rc = dense_build(e, st);
+    if (rc) return rc;
+    cublasHandle_t h = (cublasHandle_t)e->cublas;
+    KGP_REQUIRE(cublasSetStream(h, st) == CUBLAS_STATUS_SUCCESS, KGP_ERR_CUDA, "cublasSetStream failed");
+    const double one = 1.0, zero = 0.0;
+    const cublasStatus_t cs = cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)e->nrows, (int)k, (int)e->n, &one,
+                                          e->dense.as<double>() + e->row0 * e->n, (int)e->n, b, (int)b_cs, &zero,
+                                          out_k, (int)o_cs);
+    KGP_REQUIRE(cs == CUBLAS_STATUS_SUCCESS, KGP_ERR_CUDA, "cublasDgemm failed (%d)", (int)cs);
+    count_launches(1);
+    return KGP_OK;
+  }
   if (e->precision == KGP_FP64) {
     F64Params p{};
     p.xr = e->x64.as<double>() + e->row0 * e->d;
@@ -378,6 +425,7 @@ extern "C" int kgp_engine_set_params(kgp_engine* e, double l, double f, double s
   int rc = check_params(l, f, s);
   if (rc) return rc;
   if (l != e->l) e->prepared = false;
+  if (l != e->l || f != e->f || s != e->s) e->dense_valid = false;
   if (l != e->l || f != e->f || s != e->s) bump_graph_epoch();
   e->l = l;
   e->f = f;
@@ -403,6 +451,18 @@ extern "C" int kgp_engine_set_rows(kgp_engine* e, int64_t row0, int64_t nrows) {
   e->nrows = nrows;
   e->prepared = false;
   bump_graph_epoch();
+  return KGP_OK;
+}
+
+extern "C" int kgp_engine_set_dense(kgp_engine* e, int enable) {
+  CHECK_ENGINE(e);
+  const bool on = enable != 0;
+  if (on != e->dense_on) bump_graph_epoch();
+  e->dense_on = on;
+  if (!on) {
+    e->dense.release();
+    e->dense_valid = false;
+  }
   return KGP_OK;
 }
 

@@ -140,6 +140,10 @@ struct kgp_engine_s {
   int64_t dn_ncols = 0;
   kgp::DevBuf dn;    // (classes, n): class-major
   kgp::DevBuf dmap;  // dn_ncols int32: RHS column -> class
+  // DENSE mode (kgp_engine_set_dense): Khat materialised once, products by cuBLAS DGEMM
+  bool dense_on = false, dense_valid = false;
+  kgp::DevBuf dense;        // (n, n) fp64 Khat = f^2 kappa + s I
+  void* cublas = nullptr;   // cublasHandle_t
   // optional main-kernel timing (kgp_engine_set_timing)
   bool timing = false;
   std::vector<cudaEvent_t> tev;  // start/stop pairs

@@ -126,6 +126,10 @@ class KernelEngine:
              PRECISIONS[self.precision], self.n, self.x.shape[1], self.x.ctypes.data, 0, self.params.l,
              self.params.f, self.params.s, _device.stream_ptr())
         self.x.setflags(write=False)
+        if self.mode == EngineMode.DENSE and self.precision == "fp64":
+            # the reference's DENSE mode (kmat.py:93-94): Khat materialised once on the device,
+            # K.B by cuBLAS DGEMM; derivative products stay on the fused kernel
+            call("kgp_engine_set_dense", self._handle, 1)
 
     def set_params(self, params) -> None:
         """Reset (l, f, s) in place, keeping X resident (a training loop's per-step update;
