@@ -93,10 +93,16 @@ __global__ void dot_fused_kernel(int64_t n, int nb, int k2, const double* __rest
     v = warp_sum(v);
     v2 = warp_sum(v2);
     if (threadIdx.x == 0) {
-      partial[((int64_t)c * nb + blk) * 2] = v;
-      partial[((int64_t)c * nb + blk) * 2 + 1] = v2;
-      __threadfence();
-      last = atomicAdd(&tickets[c], 1u) == (unsigned)(nb - 1);
+      if (nb == 1) {  // one block per column: it holds the whole dot
+        out[c] = v;
+        if (two) out2[c] = v2;
+        last = false;
+      } else {
+        partial[((int64_t)c * nb + blk) * 2] = v;
+        partial[((int64_t)c * nb + blk) * 2 + 1] = v2;
+        __threadfence();
+        last = atomicAdd(&tickets[c], 1u) == (unsigned)(nb - 1);
+      }
     }
   }
   __syncthreads();

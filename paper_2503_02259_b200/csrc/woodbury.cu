@@ -118,13 +118,31 @@ __global__ void finish_partials_kernel(int64_t M, int64_t N, int nz, const doubl
 // fixed-order split-K partials (deterministic) finished by finish_partials_kernel.
 constexpr int SK_MAXN = 8;
 
+// single K chunk: the kernels write C = alpha acc + beta SRC themselves (no partials pass)
+struct SkEpi {
+  double alpha, beta;
+  const double* src;
+  int64_t s_is, s_ns;
+  double* c;
+  int64_t c_is, c_ns;
+  KGP_DEV void put(double* part, int64_t M, int N, int64_t i, int col, double v) const {
+    if (gridDim.y == 1) {
+      double o = alpha * v;
+      if (src) o += beta * src[i * s_is + col * s_ns];
+      c[i * c_is + col * c_ns] = o;
+    } else {
+      part[((int64_t)blockIdx.y * M + i) * N + col] = v;
+    }
+  }
+};
+
 // A rows contiguous along K (a_ks == 1): one CTA per (output row, K chunk); threads stride
 // the chunk with four independent loads in flight each, block-reduced in fixed order.
 template <int N>
 __global__ void __launch_bounds__(256) skinny_rowdot_kernel(int64_t M, int64_t K, int64_t kchunk,
                                                             const double* __restrict__ a, int64_t a_is,
                                                             const double* __restrict__ b, int64_t b_ks, int64_t b_ns,
-                                                            double* __restrict__ part) {
+                                                            double* __restrict__ part, SkEpi epi) {
   const int64_t i = blockIdx.x;
   const int64_t q0 = (int64_t)blockIdx.y * kchunk;
   const int64_t q1 = q0 + kchunk < K ? q0 + kchunk : K;
@@ -159,7 +177,7 @@ __global__ void __launch_bounds__(256) skinny_rowdot_kernel(int64_t M, int64_t K
     double v = 0.0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) v += red[k][threadIdx.x];
-    part[((int64_t)blockIdx.y * M + i) * N + threadIdx.x] = v;
+    epi.put(part, M, N, i, threadIdx.x, v);
   }
 }
 
@@ -167,7 +185,8 @@ __global__ void __launch_bounds__(256) skinny_rowdot_kernel(int64_t M, int64_t K
 template <int N>
 __global__ void __launch_bounds__(256) skinny_rowwarp_kernel(int64_t M, int64_t K, const double* __restrict__ a,
                                                              int64_t a_is, const double* __restrict__ b,
-                                                             int64_t b_ks, int64_t b_ns, double* __restrict__ part) {
+                                                             int64_t b_ks, int64_t b_ns, double* __restrict__ part,
+                                                             SkEpi epi) {
   const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (i >= M) return;
@@ -193,7 +212,7 @@ __global__ void __launch_bounds__(256) skinny_rowwarp_kernel(int64_t M, int64_t 
 #pragma unroll
   for (int c = 0; c < N; ++c) {
     const double v = warp_sum((acc[0][c] + acc[1][c]) + (acc[2][c] + acc[3][c]));
-    if (lane == 0) part[i * N + c] = v;
+    if (lane == 0) epi.put(part, M, N, i, c, v);
   }
 }
 
@@ -203,7 +222,7 @@ template <int N>
 __global__ void __launch_bounds__(256) skinny_col_kernel(int64_t M, int64_t K, int64_t kchunk,
                                                          const double* __restrict__ a, int64_t a_ks,
                                                          const double* __restrict__ b, int64_t b_ks, int64_t b_ns,
-                                                         double* __restrict__ part) {
+                                                         double* __restrict__ part, SkEpi epi) {
   __shared__ double bs[SK_QC * N];
   const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
   const int64_t q0 = (int64_t)blockIdx.y * kchunk;
@@ -235,22 +254,23 @@ __global__ void __launch_bounds__(256) skinny_col_kernel(int64_t M, int64_t K, i
   }
   if (i >= M) return;
 #pragma unroll
-  for (int c = 0; c < N; ++c) part[((int64_t)blockIdx.y * M + i) * N + c] = acc[c];
+  for (int c = 0; c < N; ++c) epi.put(part, M, N, i, c, acc[c]);
 }
 
 template <int N>
 int skinny_launch(int kind, int64_t M, int64_t K, int64_t nz, int64_t kchunk, const double* a, int64_t a_is,
-                  int64_t a_ks, const double* b, int64_t b_ks, int64_t b_ns, double* part, cudaStream_t st) {
+                  int64_t a_ks, const double* b, int64_t b_ks, int64_t b_ns, double* part, const SkEpi& epi,
+                  cudaStream_t st) {
   if (kind == 2) {
-    skinny_rowwarp_kernel<N><<<(unsigned)((M + 7) / 8), 256, 0, st>>>(M, K, a, a_is, b, b_ks, b_ns, part);
+    skinny_rowwarp_kernel<N><<<(unsigned)((M + 7) / 8), 256, 0, st>>>(M, K, a, a_is, b, b_ks, b_ns, part, epi);
     KGP_LAUNCH("skinny_rowwarp_kernel");
   } else if (kind == 1) {
     skinny_rowdot_kernel<N><<<dim3((unsigned)M, (unsigned)nz), 256, 0, st>>>(M, K, kchunk, a, a_is, b, b_ks, b_ns,
-                                                                             part);
+                                                                             part, epi);
     KGP_LAUNCH("skinny_rowdot_kernel");
   } else {
     skinny_col_kernel<N><<<dim3((unsigned)((M + 255) / 256), (unsigned)nz), 256, 0, st>>>(M, K, kchunk, a, a_ks, b,
-                                                                                          b_ks, b_ns, part);
+                                                                                          b_ks, b_ns, part, epi);
     KGP_LAUNCH("skinny_col_kernel");
   }
   return KGP_OK;
@@ -268,7 +288,9 @@ int skinny_gemm(int64_t M, int64_t N, int64_t K, const double* a, int64_t a_is, 
   if (kind != 2) {
     const int64_t gx = kind == 1 ? M : (M + 255) / 256;
     // K chunks: enough CTAs for ~8 per SM, each streaming >= 1024 (row) / 32 (column) elements
-    nz = (1184 + gx - 1) / gx;
+    // short rows: one CTA per row writes C directly (no partials pass); long rows / few
+    // rows: K chunks for memory-level parallelism
+    nz = (kind == 1 && K <= 8192) ? 1 : (1184 + gx - 1) / gx;
     const int64_t min_chunk = kind == 1 ? 1024 : 32;
     if (nz > (K + min_chunk - 1) / min_chunk) nz = (K + min_chunk - 1) / min_chunk;
     if (nz < 1) nz = 1;
@@ -281,17 +303,20 @@ int skinny_gemm(int64_t M, int64_t N, int64_t K, const double* a, int64_t a_is, 
   int rc = tmp.ensure(sizeof(double) * (size_t)(M * N * nz));
   if (rc) return rc;
   double* part = tmp.as<double>();
+  const SkEpi epi{alpha, beta, src, s_is, s_ns, c, c_is, c_ns};
+  const bool direct = K > 0 && (kind == 2 || nz == 1);  // the kernel writes C itself
   if (K <= 0) {
     KGP_CUDA(cudaMemsetAsync(part, 0, sizeof(double) * M * N, st));
   } else {
     switch (N) {
 #define KGP_SK(NN) \
-  case NN: rc = skinny_launch<NN>(kind, M, K, nz, kchunk, a, a_is, a_ks, b, b_ks, b_ns, part, st); break;
+  case NN: rc = skinny_launch<NN>(kind, M, K, nz, kchunk, a, a_is, a_ks, b, b_ks, b_ns, part, epi, st); break;
       KGP_SK(1) KGP_SK(2) KGP_SK(3) KGP_SK(4) KGP_SK(5) KGP_SK(6) KGP_SK(7) KGP_SK(8)
 #undef KGP_SK
     }
     if (rc) return rc;
   }
+  if (direct) return KGP_OK;
   finish_partials_kernel<<<(unsigned)((M * N + 255) / 256), 256, 0, st>>>(M, N, (int)nz, part, alpha, beta, src,
                                                                           s_is, s_ns, c, c_is, c_ns);
   KGP_LAUNCH("finish_partials_kernel");
