@@ -73,11 +73,24 @@ __global__ void dot_fused_kernel(int64_t n, int nb, int k2, const double* __rest
   const int64_t off = (int64_t)c * n;
   const int64_t i0 = (int64_t)blk * DOT_CHUNK;
   const int64_t i1 = i0 + DOT_CHUNK < n ? i0 + DOT_CHUNK : n;
-  double s = 0.0, s2 = 0.0;
-  for (int64_t i = i0 + threadIdx.x; i < i1; i += DOT_THREADS) {
-    s = fma(a[off + i], b[off + i], s);
-    if (two) s2 = fma(a2[off + i], b2[off + i], s2);
+  // four independent accumulators: four loads in flight per thread (the loop is latency-bound
+  // for the short columns of small problems); combined in a fixed order
+  double sa[4] = {0.0, 0.0, 0.0, 0.0}, sb[4] = {0.0, 0.0, 0.0, 0.0};
+  int64_t i = i0 + threadIdx.x;
+  for (; i + 3 * DOT_THREADS < i1; i += 4 * DOT_THREADS) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t j = off + i + u * DOT_THREADS;
+      sa[u] = fma(a[j], b[j], sa[u]);
+      if (two) sb[u] = fma(a2[j], b2[j], sb[u]);
+    }
   }
+  for (; i < i1; i += DOT_THREADS) {
+    sa[0] = fma(a[off + i], b[off + i], sa[0]);
+    if (two) sb[0] = fma(a2[off + i], b2[off + i], sb[0]);
+  }
+  double s = (sa[0] + sa[1]) + (sa[2] + sa[3]);
+  double s2 = (sb[0] + sb[1]) + (sb[2] + sb[3]);
   __shared__ double red[2][DOT_THREADS / 32];
   __shared__ bool last;
   s = warp_sum(s);
