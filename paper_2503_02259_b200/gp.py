@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -177,6 +178,9 @@ def nlml_grad_iterative(engine, y, preconditioner, probes: ProbeSet, tol: float 
         raise ValueError(f"probes have {probes.vectors.shape[0]} rows, need {n}")
     if probe_tol is None:
         probe_tol = tol
+    if getattr(engine, "precision", None) == "tf32":
+        warnings.warn("nlml_grad_iterative on a single-pass tf32 operator: loss/gradient errors reach "
+                      "1e-1 and more (DESIGN.md §4); use precision='fast' (3xTF32) or 'fp64'", stacklevel=2)
     if preconditioned_probes is not False and preconditioned_probes is not None:
         pm = preconditioner if preconditioned_probes is True else preconditioned_probes
         return _nlml_grad_pp(engine, y, preconditioner, pm, probes, tol, max_iter, probe_tol, probe_max_iter)
