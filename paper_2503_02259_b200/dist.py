@@ -91,12 +91,21 @@ class DistSolve:
     converged: np.ndarray
 
 
-def dist_pcg(ops, comm: Comm, y_loc, tol: float, max_iter: int, precondition: bool, shift: float = 1.0):
-    """Batched PCG over row-sharded state (solver.py:122-192). y_loc: (k, n_loc)."""
+def dist_pcg(ops, comm: Comm, y_loc, tol, max_iter: int, precondition, shift: float = 1.0):
+    """Batched PCG over row-sharded state (solver.py:122-192). y_loc: (k, n_loc).
+
+    Column groups as the device driver's (pcg.cu pcg_grouped_impl): ``tol`` and the
+    per-column iteration cap may be scalars or length-k arrays, and ``precondition`` a bool
+    or the number of LEADING columns to precondition -- so the NLML's w-solve and probe solves
+    share one operator application (one all-gather) per iteration."""
     torch = __import__("torch")
-    if tol < 0 or max_iter < 1:
-        raise ValueError("need tol >= 0 and max_iter >= 1")
     k = y_loc.shape[0]
+    tol = np.broadcast_to(np.asarray(tol, dtype=np.float64), (k,)).copy()
+    cap = np.broadcast_to(np.asarray(max_iter, dtype=np.int64), (k,)).copy()
+    if np.any(tol < 0) or np.any(cap < 1):
+        raise ValueError("need tol >= 0 and max_iter >= 1")
+    kp = k if precondition is True else (0 if precondition is False else int(precondition))
+    stride = int(cap.max())
     dev, f64 = y_loc.device, torch.float64
 
     def dots(a, b):
@@ -106,26 +115,29 @@ def dist_pcg(ops, comm: Comm, y_loc, tol: float, max_iter: int, precondition: bo
     r0, r1 = comm.ranges[comm.rank]
 
     def minv(r):
-        if not precondition:
+        if kp == 0:
             return r
+        head = r[:kp]
         if full_minv is not None:  # replicated preconditioner (AFN): gather, apply, keep own rows
-            return full_minv(comm.allgather_rows(r))[:, r0:r1].contiguous()
-        t = comm.allreduce(ops.project(r))
-        return ops.expand(r, t, 1.0 / shift, -1.0 / (shift * shift))
+            zh = full_minv(comm.allgather_rows(head))[:, r0:r1].contiguous()
+        else:
+            t = comm.allreduce(ops.project(head))
+            zh = ops.expand(head, t, 1.0 / shift, -1.0 / (shift * shift))
+        return zh if kp == k else torch.cat([zh, r[kp:]], dim=0)
 
     x = torch.zeros_like(y_loc)
     r = y_loc.clone()
     ynorm = np.sqrt(dots(r, r))
     rel = np.where(ynorm > 0, 1.0, 0.0)
     active = rel > tol
-    alphas = torch.zeros((k, max_iter), dtype=f64, device=dev)
-    betas = torch.zeros((k, max_iter), dtype=f64, device=dev)
+    alphas = torch.zeros((k, stride), dtype=f64, device=dev)
+    betas = torch.zeros((k, stride), dtype=f64, device=dev)
     iters = np.zeros(k, dtype=np.int64)
     if active.any():
         z = minv(r)
         p = z.clone()
         rz = dots(r, z)
-        for _ in range(max_iter):
+        for _ in range(stride):
             ap = ops.matmul_rows(comm.allgather_rows(p))
             pap = dots(p, ap)
             act = np.flatnonzero(active)
@@ -141,7 +153,9 @@ def dist_pcg(ops, comm: Comm, y_loc, tol: float, max_iter: int, precondition: bo
             alphas[idx, torch.from_numpy(iters[act]).to(dev)] = torch.from_numpy(alpha[act]).to(dev)
             z = minv(r)
             rr = dots(r, r)
-            rzn = rr if not precondition else dots(r, z)
+            rzn = rr.copy()
+            if kp:
+                rzn[:kp] = dots(r[:kp], z[:kp])
             if not np.all(np.isfinite(rr[act])):
                 raise NumericalError("residual became non-finite during PCG")
             beta = np.zeros(k)
@@ -150,7 +164,7 @@ def dist_pcg(ops, comm: Comm, y_loc, tol: float, max_iter: int, precondition: bo
             iters[act] += 1
             rz[act] = rzn[act]
             rel[act] = np.sqrt(rr[act]) / ynorm[act]
-            active[act] = rel[act] > tol
+            active[act] = (rel[act] > tol[act]) & (iters[act] < cap[act])
             keep = np.flatnonzero(active)
             if keep.size == 0:
                 break
@@ -169,8 +183,15 @@ def dist_nlml_grad(ops, comm: Comm, y_loc, probes_loc, norms_sq, tol, max_iter, 
     probe_tol = tol if probe_tol is None else probe_tol
     probe_max_iter = max_iter if probe_max_iter is None else probe_max_iter
     kz = probes_loc.shape[0]
-    ws = dist_pcg(ops, comm, y_loc[None, :], tol, max_iter, precondition, shift)
-    us = dist_pcg(ops, comm, probes_loc, probe_tol, probe_max_iter, False, shift)
+    # the w-solve (preconditioned) and the probe solves (not) as ONE grouped PCG: every
+    # iteration is one all-gather + one fused Khat [p_w, P_Z] on the local rows
+    torch_ = __import__("torch")
+    v0 = torch_.cat([y_loc[None, :], probes_loc], dim=0)
+    tols = np.array([tol] + [probe_tol] * kz)
+    caps = np.array([max_iter] + [probe_max_iter] * kz)
+    sol = dist_pcg(ops, comm, v0, tols, caps, 1 if precondition else False, shift)
+    us = DistSolve(sol.x[1:], sol.alphas[1:], sol.betas[1:], sol.iters[1:], sol.rel[1:], sol.converged[1:])
+    ws = DistSolve(sol.x[:1], sol.alphas[:1], sol.betas[:1], sol.iters[:1], sol.rel[:1], sol.converged[:1])
     logdet = ops.slq(us.alphas, us.betas, us.iters, norms_sq)
     w = ws.x[0]
     yw = float(comm.allreduce((y_loc * w).sum()[None])[0])
