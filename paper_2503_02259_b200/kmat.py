@@ -272,3 +272,7 @@ class KernelEngine:
         call("kgp_engine_cross_matmul", self._handle, m, xs_dev.data_ptr(), b.shape[1], b.data_ptr(),
              b.stride(0), b.stride(1), out.data_ptr(), out.stride(0), out.stride(1), _device.stream_ptr())
         return out
+
+
+# SURVEY.md §8(b) names the drop-in ``CudaKernelEngine``: this package's engine IS that class
+CudaKernelEngine = KernelEngine
