@@ -94,11 +94,18 @@ def generate_probes(n: int, num_classes: int, k_z: int, rng_seed) -> np.ndarray:
 
 def build_preconditioners(engine, problem: GPCProblem, rank: int | None = None, kind: str = "afn",
                           fsai_npt: int = precond_mod.AFN_DEFAULT_NPT):
-    """One preconditioner per class, each for Khat + diag(noise_c); kind 'afn' or 'none'."""
+    """One preconditioner per class for Khat + diag(noise_c): 'afn' (the class's noise on the
+    diagonal exactly), 'nystrom' (M = (s + mean noise_c) I + f^2 V V^T: cheap, and its
+    N(0, M) draws make a good preconditioned-probe estimator when the kernel is smooth), or
+    'none'."""
     if kind == "none":
         return []
+    if kind == "nystrom":
+        s = engine.params.s
+        return [precond_mod.build(engine, rank, shift=s + float(np.mean(problem.noise[c])))
+                for c in range(problem.num_classes)]
     if kind != "afn":
-        raise ValueError(f"kind must be 'afn' or 'none', got {kind!r}")
+        raise ValueError(f"kind must be 'afn', 'nystrom' or 'none', got {kind!r}")
     return [precond_mod.build_afn(engine, rank, fsai_npt, diag=problem.noise[c])
             for c in range(problem.num_classes)]
 

@@ -124,6 +124,11 @@ class NystromPreconditioner:
     def handle(self):
         return self._inv.h
 
+    def close(self):
+        """Free the device factors now (otherwise at garbage collection)."""
+        self._inv.close()
+        self._fwd.close()
+
     def _run(self, which, b, beta, alpha):
         torch = _device.torch()
         host = not _device.is_tensor(b)
@@ -150,8 +155,10 @@ class NystromPreconditioner:
         return self._run(self._fwd, b, self.shift, self._f2)
 
 
-def build(engine, m: int | None = None) -> NystromPreconditioner:
-    """Landmark preconditioner for an engine's Khat (precond.py:95-126)."""
+def build(engine, m: int | None = None, shift: float | None = None) -> NystromPreconditioner:
+    """Landmark preconditioner for an engine's Khat (precond.py:95-126). ``shift`` (extension)
+    replaces the noise s of M = shift I + f^2 V V^T, e.g. s + the mean heteroscedastic noise
+    of a GPC class."""
     torch = _device.torch()
     n = engine.n
     if m is None:
@@ -159,6 +166,9 @@ def build(engine, m: int | None = None) -> NystromPreconditioner:
     if not 1 <= m <= n:
         raise ValueError(f"need 1 <= m <= n, got m={m}, n={n}")
     p = engine.params
+    sh = float(p.s if shift is None else shift)
+    if not sh > 0:
+        raise ValueError("shift must be positive")
     xd = engine.x_device()
     idx = fps_device(xd, m, 0)
     xm = xd.index_select(0, idx)
@@ -176,17 +186,17 @@ def build(engine, m: int | None = None) -> NystromPreconditioner:
     if int(info) != 0:
         raise fail()
     vt = torch.linalg.solve_triangular(low, device_panel(kid, 0, xm, xd, p.l), upper=False)
-    cap = (vt @ vt.T) / p.s
+    cap = (vt @ vt.T) / sh
     cap.diagonal().add_(1.0 / f2)
     lc, info = torch.linalg.cholesky_ex(cap)
     if int(info) != 0 or not bool(torch.isfinite(vt).all()):
         raise fail()
     wt = torch.linalg.solve_triangular(lc, vt, upper=False)
-    inv = _LowRank(wt, p.s)
+    inv = _LowRank(wt, sh)
     del wt
-    fwd = _LowRank(vt, p.s)
-    logdet = n * math.log(p.s) + m * math.log(f2) + 2.0 * float(torch.log(torch.diagonal(lc)).sum())
-    return NystromPreconditioner(_device.to_host(idx).astype(np.intp), p.s, inv, fwd, f2, n, logdet)
+    fwd = _LowRank(vt, sh)
+    logdet = n * math.log(sh) + m * math.log(f2) + 2.0 * float(torch.log(torch.diagonal(lc)).sum())
+    return NystromPreconditioner(_device.to_host(idx).astype(np.intp), sh, inv, fwd, f2, n, logdet)
 
 
 # ----------------------------------------------------------------------------- AFN
