@@ -6,28 +6,31 @@
 //   acc_K = kappa(X_rows, X) . B        acc_G = (scaled dkappa/dl)(X_rows, X) . B
 //
 // The kernel matrix is never stored. One CTA owns 128 rows (the TMEM lanes) and
-// streams the columns in blocks of 32 (one 128-byte swizzle atom of tf32):
-//   * warp 8 (producer) bulk-copies each block's operands into a 4-stage SMEM
-//     ring: the RHS tiles, pre-split into tf32 hi/lo and already in the UMMA
-//     K-major 128B-swizzled layout, plus the block's column-point data;
-//   * DISTANCE (d > 4): the scaled squared distance t2 = gamma r^2 is itself an
-//     MMA: with U'_i = [-2 gamma c_i, q_i, 1] and V'_j = [c_j, 1, q_j]
-//     (q = gamma |c|^2, c centred), t2 = U' V'^T exactly, a K = d+2 (padded to
-//     16) 3xTF32 product into TMEM -- 6 small MMAs per block instead of d FFMA
-//     per entry on the FP32 pipe. (d <= 4 keeps direct differences on the FP32
-//     pipe: cheaper there and exact for near-coincident points.);
-//   * warps 0-7 (compute) read t2 from TMEM (tcgen05.ld 16x256b), apply the
-//     kernel transform (MUFU ex2/sqrt), split into tf32 hi/lo and store the tile
-//     back to TMEM (tcgen05.st 16x256b): the A operand of the contraction;
-//   * warp 9 issues the contraction tcgen05.mma (kind::tf32, cta_group::1) from
-//     one elected lane of a converged warp: hi*hi + hi*lo + lo*hi per output and
-//     K=8 chunk (3xTF32); warp 10 issues the distance MMAs independently, as soon
-//     as a block's V' lands, so they never queue behind a blocking wait;
-//   * warps 11-14 (drain) promote the TMEM accumulators every `flush` blocks into
-//     fp32 shared-memory sums (two accumulator buffers ping-pong). The tensor
-//     core's fp32 accumulation truncates: unpromoted it drifts linearly in n
-//     (measured 4.6e-4 at n = 65536); promoted it stays near 2e-6.
-// The drain warps finally apply f^2, 2f, s*B and the derivative scale in fp64.
+// streams the columns in blocks of 32 (one 128-byte swizzle atom of tf32). With NS
+// compute-warp sets (2 or 3, ns_for) the warps are:
+//   * compute (4*NS warps, one per TMEM lane quadrant per set; set e takes the blocks
+//     t = e mod NS): read the block's squared distances, apply the kernel transform (MUFU
+//     ex2/sqrt), split into tf32 hi/lo and store the tile into TMEM with tcgen05.st -- the
+//     A operand of the contraction (16x256b layout, or 32x32b for the fused two-output
+//     3xTF32 product);
+//   * producer (1): cp.async.bulk of each block's operands into a 4/8-stage SMEM ring: the
+//     RHS tiles, pre-split into tf32 hi/lo and already in the UMMA K-major 128B-swizzled
+//     layout, plus the block's column-point data;
+//   * contraction MMA issuer (1): tcgen05.mma kind::tf32, cta_group::1, A from TMEM, B from
+//     SMEM, one elected lane of a converged warp: hi*hi + hi*lo + lo*hi per output and K=8
+//     chunk (3xTF32; hi*hi only for KGP_TF32);
+//   * distance MMA issuer (1, d > 4): the scaled squared distance t2 = gamma r^2 is itself
+//     an MMA: with U'_i = [-2 gamma c_i, q_i, 1] (resident in TMEM) and V'_j = [c_j, 1, q_j]
+//     (q = gamma |c|^2, c centred), t2 = U' V'^T, a K = d+2 (padded to 16) 3xTF32 product
+//     into a per-set TMEM buffer, issued as soon as a block's V' lands. (d <= 4 keeps
+//     direct differences on the FP32 pipe in the compute warps: cheaper there and exact for
+//     near-coincident points);
+//   * drain (4): every `flush` blocks promote the TMEM accumulators into fp32 shared-memory
+//     sums (two buffers ping-pong, or one when the RHS block is wide). The tensor core's
+//     fp32 accumulation truncates: unpromoted it drifts linearly in n (measured 4.6e-4 at
+//     n = 65536); promoted it stays near 2e-6.
+// The drain warps finally apply f^2, 2f, s*B and the derivative scale in fp64 (or write
+// fp32 partials when the column sweep is split over grid.y; tc_reduce_kernel finishes).
 #include <cuda.h>
 
 #include "kgp_common.cuh"
