@@ -365,10 +365,10 @@ __global__ void __launch_bounds__(nthreads_for(ns_for(NOUT, SPLIT)), 1) kmm_tc_k
     }
   } else if (warp < NCW) {
     // ------------------------------------------------------------ compute warps
-    // Two sets of four warps (one per TMEM lane quadrant) take alternate blocks, so
-    // one set's TMEM/barrier latencies overlap the other set's transform work.
+    // NS sets of four warps (one per TMEM lane quadrant) take blocks round-robin, so one
+    // set's TMEM/barrier latencies overlap the other sets' transform work.
     const int qd = warp & 3;    // TMEM lane quadrant
-    const int set = warp >> 2;  // blocks t = set (mod 2)
+    const int set = warp >> 2;  // blocks t = set (mod NS)
     const int g = lane & 3;
     // rows owned by this thread: 32 qd + lane/4 + {0, 8, 16, 24}; columns 2g + {0,1} + 8m, m < 4
     float u[4][DMMA ? 1 : D];
