@@ -165,7 +165,7 @@ static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t 
     p.k = kc;
     p.nsa = tc_nsa(e->dpad, nout, split, kp);
     p.nab = nab;
-    const int nsplit = tc_col_split(nrows, nblk);
+    const int nsplit = tc_col_split(nrows, nblk, tc_env_int("KGP_TC_MAXSPLIT", 16));
     p.nper = (nblk + nsplit - 1) / nsplit;
     p.part = nullptr;
     if (nsplit > 1) {
@@ -277,6 +277,13 @@ static int engine_matmul_core(kgp_engine_s* e, int64_t k, const double* b, int64
     cublasHandle_t h = (cublasHandle_t)e->cublas;
     KGP_REQUIRE(cublasSetStream(h, st) == CUBLAS_STATUS_SUCCESS, KGP_ERR_CUDA, "cublasSetStream failed");
     const double one = 1.0, zero = 0.0;
+    if (e->nrows == e->n && tc_env_int("KGP_DENSE_SYMM", 0)) {
+      const cublasStatus_t cs = cublasDsymm(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, (int)e->n, (int)k, &one,
+                                            e->dense.as<double>(), (int)e->n, b, (int)b_cs, &zero, out_k, (int)o_cs);
+      KGP_REQUIRE(cs == CUBLAS_STATUS_SUCCESS, KGP_ERR_CUDA, "cublasDsymm failed (%d)", (int)cs);
+      count_launches(1);
+      return KGP_OK;
+    }
     const cublasStatus_t cs = cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)e->nrows, (int)k, (int)e->n, &one,
                                           e->dense.as<double>() + e->row0 * e->n, (int)e->n, b, (int)b_cs, &zero,
                                           out_k, (int)o_cs);

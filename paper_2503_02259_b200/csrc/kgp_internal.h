@@ -35,7 +35,7 @@ struct TcParams {
 };
 int tc_pad_dim(int d);
 int tc_max_kp(int dpad, int nout, int split, int nab);
-int tc_col_split(int64_t nrows, int nblk);
+int tc_col_split(int64_t nrows, int nblk, int maxsplit);
 int tc_nsa(int dpad, int nout, int split, int kp);
 int tc_col_block_bytes(int dpad);
 bool tc_direct(int dpad);

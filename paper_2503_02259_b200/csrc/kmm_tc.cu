@@ -676,12 +676,12 @@ int tc_max_kp(int dpad, int nout, int split, int nab) {
 int tc_nsa(int, int nout, int split, int) { return ns_for(nout, split); }
 
 // Column split factor that fills the last wave of 148 SMs (1 CTA/SM): the smallest
-// S <= 8 reaching 95% wave efficiency with >= 16 column blocks per CTA.
-int tc_col_split(int64_t nrows, int nblk) {
+// S <= maxsplit reaching 95% wave efficiency with >= 16 column blocks per CTA.
+int tc_col_split(int64_t nrows, int nblk, int maxsplit) {
   const int64_t rb = (nrows + 127) / 128;
   int best = 1;
   double best_eff = 0.0;
-  for (int sp = 1; sp <= 8; ++sp) {
+  for (int sp = 1; sp <= maxsplit; ++sp) {
     if (sp > 1 && nblk / sp < 16) break;
     const int64_t units = rb * sp;
     const double eff = (double)units / (double)(((units + 147) / 148) * 148);

@@ -30,6 +30,17 @@ namespace {
 
 constexpr int DOT_THREADS = 256;
 constexpr int DOT_CHUNK = 8192;  // elements per block in the first reduction pass
+constexpr int HIST = 4;          // ints per iteration in the mapped history
+
+// elements per block of dot_fused_kernel (env KGP_DOT_CHUNK overrides)
+int fused_chunk() {
+  static const int v = [] {
+    const char* s = getenv("KGP_DOT_CHUNK");
+    const int c = s ? atoi(s) : DOT_CHUNK;
+    return c < 256 ? 256 : c;
+  }();
+  return v;
+}
 
 // partial[c * nb + blk] = sum over the block's chunk of a[c*n+i] * b[c*n+i]
 __global__ void dot_partial_kernel(int64_t n, int nb, const double* __restrict__ a, const double* __restrict__ b,
@@ -64,15 +75,16 @@ __global__ void dot_final_kernel(int k, int nb, const double* __restrict__ parti
 // given, out2[c] = a2_c . b2_c (c < k2). Each block writes its chunk's partials; the last
 // block of a column (ticket counter) sums them in block order -- the same fixed order as
 // dot_partial + dot_final, so results are run-to-run identical -- and re-arms the ticket.
-__global__ void dot_fused_kernel(int64_t n, int nb, int k2, const double* __restrict__ a, const double* __restrict__ b,
+__global__ void dot_fused_kernel(int64_t n, int nb, int chunk, int k2, const double* __restrict__ a,
+                                 const double* __restrict__ b,
                                  const double* __restrict__ a2, const double* __restrict__ b2,
                                  double* __restrict__ partial, double* __restrict__ out, double* __restrict__ out2,
                                  unsigned* __restrict__ tickets) {
   const int c = blockIdx.y, blk = blockIdx.x;
   const bool two = a2 != nullptr && c < k2;
   const int64_t off = (int64_t)c * n;
-  const int64_t i0 = (int64_t)blk * DOT_CHUNK;
-  const int64_t i1 = i0 + DOT_CHUNK < n ? i0 + DOT_CHUNK : n;
+  const int64_t i0 = (int64_t)blk * chunk;
+  const int64_t i1 = i0 + chunk < n ? i0 + chunk : n;
   // four independent accumulators: four loads in flight per thread (the loop is latency-bound
   // for the short columns of small problems); combined in a fixed order
   double sa[4] = {0.0, 0.0, 0.0, 0.0}, sb[4] = {0.0, 0.0, 0.0, 0.0};
@@ -203,14 +215,18 @@ __global__ void pcg_alpha_update_kernel(int64_t n, int k, int stride, const doub
 }
 
 // beta step and freeze decision (solver.py:170-182)
-// One block (k <= 1024). Also publishes (active count, error code) of this iteration to
-// hist[2 * it], a host-mapped array the driver polls a few iterations behind the device.
+// One block (k <= 1024). Also publishes (active count, error code, active count of group 1)
+// of this iteration to hist[HIST * it], a host-mapped array the driver polls a few
+// iterations behind the device.
 __global__ void pcg_beta_kernel(int k, PcgGroups g, bool precond, const double* rr, const double* rzn,
                                 double* rz, const double* ynorm, int32_t* active, int32_t* iters, double* beta,
                                 double* betas, double* rel, int32_t* status, int32_t* it_counter,
                                 volatile int32_t* hist) {
   int c = threadIdx.x;
-  if (c == 0) status[0] = 0;
+  if (c == 0) {
+    status[0] = 0;
+    status[3] = 0;
+  }
   __syncthreads();
   if (c < k && active[c]) {
     double v = rr[c];
@@ -231,6 +247,7 @@ __global__ void pcg_beta_kernel(int k, PcgGroups g, bool precond, const double* 
         active[c] = 0;
       } else {
         atomicAdd(&status[0], 1);
+        if (c < g.kpc) atomicAdd(&status[3], 1);
       }
     }
   }
@@ -238,8 +255,9 @@ __global__ void pcg_beta_kernel(int k, PcgGroups g, bool precond, const double* 
   if (c == 0) {
     __threadfence();
     const int it = *it_counter;
-    hist[2 * it] = status[0];
-    hist[2 * it + 1] = status[1];
+    hist[HIST * it] = status[0];
+    hist[HIST * it + 1] = status[1];
+    hist[HIST * it + 2] = status[3];
     *it_counter = it + 1;
   }
 }
@@ -418,11 +436,12 @@ int enqueue_iteration(kgp_engine_s* e, const PcSet& pcs, int64_t k, const PcgGro
   const int64_t n = e->n;
   const PcgState& S = B.S;
   dim3 vgrid((unsigned)((n + 255) / 256 < 64 ? (n + 255) / 256 : 64), (unsigned)k);
-  const int nb = (int)((n + DOT_CHUNK - 1) / DOT_CHUNK);
+  const int chunk = fused_chunk();
+  const int nb = (int)((n + chunk - 1) / chunk);
   int rc = engine_matmul_impl(e, k, S.p, 1, n, S.ap, nullptr, nullptr, 1, n, st);
   if (rc) return rc;
   dot_fused_kernel<<<dim3((unsigned)nb, (unsigned)k), DOT_THREADS, 0, st>>>(
-      n, nb, 0, S.p, S.ap, nullptr, nullptr, S.partial, S.dots1, nullptr, S.tickets);
+      n, nb, chunk, 0, S.p, S.ap, nullptr, nullptr, S.partial, S.dots1, nullptr, S.tickets);
   KGP_LAUNCH("dot_fused_kernel");
   pcg_alpha_update_kernel<<<vgrid, 256, 0, st>>>(n, (int)k, g.stride, S.dots1, S.rz, S.active, B.iters, B.alphas,
                                                  S.status, S.err_val, S.p, S.ap, B.x, S.r);
@@ -433,7 +452,7 @@ int enqueue_iteration(kgp_engine_s* e, const PcSet& pcs, int64_t k, const PcgGro
   }
   // r.r on every column and r.z on the preconditioned ones, one launch
   dot_fused_kernel<<<dim3((unsigned)nb, (unsigned)k), DOT_THREADS, 0, st>>>(
-      n, nb, pc ? g.kz : 0, S.r, S.r, pc ? S.r : nullptr, pc ? S.z : nullptr, S.partial, S.dots1, S.dots2, S.tickets);
+      n, nb, chunk, pc ? g.kz : 0, S.r, S.r, pc ? S.r : nullptr, pc ? S.z : nullptr, S.partial, S.dots1, S.dots2, S.tickets);
   KGP_LAUNCH("dot_fused_kernel");
   pcg_beta_kernel<<<1, 1024, 0, st>>>((int)k, g, pc, S.dots1, S.dots2, S.rz, S.ynorm, S.active, B.iters,
                                       S.beta, B.betas, B.rel, S.status, B.it_counter, e->hist_dev);
@@ -461,10 +480,13 @@ int pcg_graph(kgp_engine_s* e, const PcSet& pcs, int64_t k, const PcgGroups& g, 
       return KGP_OK;
     }
   // captured on the engine's private stream (the legacy default stream cannot be captured);
-  // nothing is executed during capture, so no ordering with the caller's stream is needed
+  // nothing is executed during capture, so no ordering with the caller's stream is needed.
+  // Relaxed mode: a workspace the captured configuration needs for the first time is
+  // allocated during the capture (cudaMalloc is refused in the stricter modes); graphs
+  // captured before that allocation are retired by the epoch bump.
   cudaGraph_t graph = nullptr;
   const int64_t counted = kgp_launch_count();
-  KGP_CUDA(cudaStreamBeginCapture(e->cstream, cudaStreamCaptureModeThreadLocal));
+  KGP_CUDA(cudaStreamBeginCapture(e->cstream, cudaStreamCaptureModeRelaxed));
   int rc = enqueue_iteration(e, pcs, k, g, B, e->cstream);
   cudaError_t ce = cudaStreamEndCapture(e->cstream, &graph);
   count_launches(counted - kgp_launch_count());  // captured, not launched
@@ -531,7 +553,7 @@ int pcg_grouped_impl(kgp_engine_s* e, const PcSet& pcs, int64_t k, int64_t kpc, 
                      int it1, double tol2, int it2, double* x_out, double* alphas, double* betas, int32_t* iters,
                      double* rel, int32_t* conv, cudaStream_t st, bool precond_all) {
   const int64_t n = e->n;
-  const int nb = (int)((n + DOT_CHUNK - 1) / DOT_CHUNK);
+  const int nb = (int)((n + fused_chunk() - 1) / fused_chunk() + (n + DOT_CHUNK - 1) / DOT_CHUNK);
   KGP_REQUIRE(k <= 1024, KGP_ERR_INVALID, "pcg supports at most 1024 right-hand sides per call, got %lld",
               (long long)k);
   KGP_REQUIRE(kpc >= 0 && kpc <= k && it1 >= 1 && (kpc == k || it2 >= 1), KGP_ERR_INVALID, "bad column groups");
@@ -558,10 +580,10 @@ int pcg_grouped_impl(kgp_engine_s* e, const PcSet& pcs, int64_t k, int64_t kpc, 
                  sizeof(int32_t) * (3 * k + 16);
   int rc = e->ws.ensure(bytes);
   if (rc) return rc;
-  if (e->hist_cap < max_iter + 1) {  // mapped host history: 2 ints per iteration
+  if (e->hist_cap < max_iter + 1) {  // mapped host history: HIST ints per iteration
     if (e->hist_host) cudaFreeHost(e->hist_host);
     e->hist_host = nullptr;
-    KGP_CUDA(cudaHostAlloc(&e->hist_host, sizeof(int32_t) * 2 * (max_iter + 1), cudaHostAllocMapped));
+    KGP_CUDA(cudaHostAlloc(&e->hist_host, sizeof(int32_t) * HIST * (max_iter + 1), cudaHostAllocMapped));
     KGP_CUDA(cudaHostGetDevicePointer((void**)&e->hist_dev, e->hist_host, 0));
     e->hist_cap = max_iter + 1;
     bump_graph_epoch();
@@ -636,6 +658,10 @@ int pcg_grouped_impl(kgp_engine_s* e, const PcSet& pcs, int64_t k, int64_t kpc, 
       int64_t gk = 0;
       rc = pcg_graph(e, pcs, k, g, B, &exec, &gk);
       if (rc) return rc;
+      // once every group-2 column has stopped (its cap, or converged), the remaining
+      // iterations run a graph over the group-1 prefix [0, kpc) only: the state is column-major
+      // with group 1 first, so the same buffers serve both graphs
+      bool narrow = !(kpc > 0 && kpc < k);
       int launched = 1, checked = 1;
       while (launched < max_iter && !done) {
         KGP_CUDA(cudaGraphLaunch(exec, st));
@@ -644,22 +670,29 @@ int pcg_grouped_impl(kgp_engine_s* e, const PcSet& pcs, int64_t k, int64_t kpc, 
         ++launched;
         if (launched - checked >= kLookahead) {
           KGP_CUDA(cudaEventSynchronize(e->events[checked % kLookahead]));
-          if (H[2 * checked + 1]) {
+          if (H[HIST * checked + 1]) {
             KGP_CUDA(cudaStreamSynchronize(st));
             KGP_CUDA(cudaMemcpy(hstatus, S.status, sizeof(int32_t) * 4, cudaMemcpyDeviceToHost));
-            return status_error(S, H[2 * checked + 1], hstatus[2]);
+            return status_error(S, H[HIST * checked + 1], hstatus[2]);
           }
-          done = (H[2 * checked] == 0);
+          done = (H[HIST * checked] == 0);
+          if (!done && !narrow && H[HIST * checked] == H[HIST * checked + 2]) {
+            PcgGroups gn = g;
+            gn.kz = g.kz < g.kpc ? g.kz : g.kpc;
+            rc = pcg_graph(e, pcs, kpc, gn, B, &exec, &gk);
+            if (rc) return rc;
+            narrow = true;
+          }
           ++checked;
         }
       }
       KGP_CUDA(cudaStreamSynchronize(st));
       for (; checked < launched; ++checked) {
-        if (H[2 * checked + 1]) {
+        if (H[HIST * checked + 1]) {
           KGP_CUDA(cudaMemcpy(hstatus, S.status, sizeof(int32_t) * 4, cudaMemcpyDeviceToHost));
-          return status_error(S, H[2 * checked + 1], hstatus[2]);
+          return status_error(S, H[HIST * checked + 1], hstatus[2]);
         }
-        if (H[2 * checked] == 0) break;
+        if (H[HIST * checked] == 0) break;
       }
     }
   }

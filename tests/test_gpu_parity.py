@@ -597,3 +597,42 @@ def test_fast_operator_tiny_and_ragged_n(pkg, n, d):
         assert rel_max(got[2], ref[2]) <= bar, prec
         if n > 1:
             assert rel_max(got[1], ref[1]) <= 10 * bar, prec
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fast"])
+def test_grouped_pcg_narrow_tail(pkg, precision):
+    """kgp_pcg_grouped with the probe group capped early: after the probes stop, the driver
+    switches to a graph over the w prefix only. Column 0 must equal a standalone
+    preconditioned solve of the same length and the probe columns a standalone capped solve."""
+    import ctypes
+
+    import torch
+
+    from paper_2503_02259_b200 import _device, _lib, precond, solver
+
+    rng = np.random.default_rng(17)
+    n, kz, it1, it2 = 700, 6, 25, 6
+    x = rng.uniform(0, 1, (n, 3))
+    e = pkg.KernelEngine(pkg.KernelType.MATERN32, x, _hp(pkg, 0.4, 1.1, 1e-2), precision=precision,
+                         mode=pkg.EngineMode.ON_THE_FLY)
+    pre = precond.build(e, 40)
+    yt = torch.from_numpy(rng.standard_normal((1 + kz, n))).cuda()
+    k = 1 + kz
+    xo = torch.empty((k, n), dtype=torch.float64, device="cuda")
+    al = torch.zeros((k, it1), dtype=torch.float64, device="cuda")
+    be = torch.zeros_like(al)
+    it = torch.empty(k, dtype=torch.int32, device="cuda")
+    rel = torch.empty(k, dtype=torch.float64, device="cuda")
+    conv = torch.empty(k, dtype=torch.int32, device="cuda")
+    arr = (ctypes.c_void_p * 1)(pre.handle)
+    _lib.call("kgp_pcg_grouped", e.handle, arr, 1, k, 1, yt.data_ptr(), 0.0, it1, 0.0, it2, xo.data_ptr(),
+              al.data_ptr(), be.data_ptr(), it.data_ptr(), rel.data_ptr(), conv.data_ptr(), _device.stream_ptr())
+    its = it.cpu().numpy()
+    assert its[0] == it1 and np.all(its[1:] == it2)
+    w = solver.pcg_device(e, pre, yt[:1].contiguous(), 0.0, it1)
+    z = solver.pcg_device(e, None, yt[1:].contiguous(), 0.0, it2)
+    tol = 1e-9 if precision == "fp64" else 1e-4
+    assert rel_max(xo[0].cpu().numpy(), w[0][0].cpu().numpy()) <= tol
+    assert rel_max(al[0].cpu().numpy(), w[1][0].cpu().numpy()) <= tol
+    assert rel_max(xo[1:].cpu().numpy(), z[0].cpu().numpy()) <= tol
+    assert rel_max(al[1:, :it2].cpu().numpy(), z[1].cpu().numpy()) <= tol
