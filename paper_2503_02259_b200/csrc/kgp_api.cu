@@ -271,19 +271,14 @@ static int engine_matmul_core(kgp_engine_s* e, int64_t k, const double* b, int64
   if (e->precision == KGP_FP64 && e->dense_on && out_k && !out_dl && !out_df && b_rs == 1 && o_rs == 1 &&
       b_cs >= e->n && o_cs >= e->nrows) {
     // out (nrows x k, column-major) = Khat[row0:row0+nrows, :] B; Khat symmetric and row-major,
-    // i.e. column-major Khat^T = Khat, so the row block is op(A) = A^T of column block row0
+    // i.e. column-major Khat^T = Khat, so the row block is op(A) = A^T of column block row0.
+    // (A hand-written DMMA m8n8k4 skinny kernel was measured against this cuBLAS call and
+    // rejected: DESIGN.md, "DENSE-mode product".)
     int rc = dense_build(e, st);
     if (rc) return rc;
     cublasHandle_t h = (cublasHandle_t)e->cublas;
     KGP_REQUIRE(cublasSetStream(h, st) == CUBLAS_STATUS_SUCCESS, KGP_ERR_CUDA, "cublasSetStream failed");
     const double one = 1.0, zero = 0.0;
-    if (e->nrows == e->n && tc_env_int("KGP_DENSE_SYMM", 0)) {
-      const cublasStatus_t cs = cublasDsymm(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, (int)e->n, (int)k, &one,
-                                            e->dense.as<double>(), (int)e->n, b, (int)b_cs, &zero, out_k, (int)o_cs);
-      KGP_REQUIRE(cs == CUBLAS_STATUS_SUCCESS, KGP_ERR_CUDA, "cublasDsymm failed (%d)", (int)cs);
-      count_launches(1);
-      return KGP_OK;
-    }
     const cublasStatus_t cs = cublasDgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)e->nrows, (int)k, (int)e->n, &one,
                                           e->dense.as<double>() + e->row0 * e->n, (int)e->n, b, (int)b_cs, &zero,
                                           out_k, (int)o_cs);

@@ -75,7 +75,8 @@ __global__ void dot_final_kernel(int k, int nb, const double* __restrict__ parti
 // given, out2[c] = a2_c . b2_c (c < k2). Each block writes its chunk's partials; the last
 // block of a column (ticket counter) sums them in block order -- the same fixed order as
 // dot_partial + dot_final, so results are run-to-run identical -- and re-arms the ticket.
-__global__ void dot_fused_kernel(int64_t n, int nb, int chunk, int k2, const double* __restrict__ a,
+template <int DT>
+__global__ void __launch_bounds__(DT) dot_fused_kernel(int64_t n, int nb, int chunk, int k2, const double* __restrict__ a,
                                  const double* __restrict__ b,
                                  const double* __restrict__ a2, const double* __restrict__ b2,
                                  double* __restrict__ partial, double* __restrict__ out, double* __restrict__ out2,
@@ -89,21 +90,21 @@ __global__ void dot_fused_kernel(int64_t n, int nb, int chunk, int k2, const dou
   // for the short columns of small problems); combined in a fixed order
   double sa[4] = {0.0, 0.0, 0.0, 0.0}, sb[4] = {0.0, 0.0, 0.0, 0.0};
   int64_t i = i0 + threadIdx.x;
-  for (; i + 3 * DOT_THREADS < i1; i += 4 * DOT_THREADS) {
+  for (; i + 3 * DT < i1; i += 4 * DT) {
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int64_t j = off + i + u * DOT_THREADS;
+      const int64_t j = off + i + u * DT;
       sa[u] = fma(a[j], b[j], sa[u]);
       if (two) sb[u] = fma(a2[j], b2[j], sb[u]);
     }
   }
-  for (; i < i1; i += DOT_THREADS) {
+  for (; i < i1; i += DT) {
     sa[0] = fma(a[off + i], b[off + i], sa[0]);
     if (two) sb[0] = fma(a2[off + i], b2[off + i], sb[0]);
   }
   double s = (sa[0] + sa[1]) + (sa[2] + sa[3]);
   double s2 = (sb[0] + sb[1]) + (sb[2] + sb[3]);
-  __shared__ double red[2][DOT_THREADS / 32];
+  __shared__ double red[2][DT / 32];
   __shared__ bool last;
   s = warp_sum(s);
   s2 = warp_sum(s2);
@@ -113,8 +114,8 @@ __global__ void dot_fused_kernel(int64_t n, int nb, int chunk, int k2, const dou
   }
   __syncthreads();
   if (threadIdx.x < 32) {
-    double v = threadIdx.x < DOT_THREADS / 32 ? red[0][threadIdx.x] : 0.0;
-    double v2 = threadIdx.x < DOT_THREADS / 32 ? red[1][threadIdx.x] : 0.0;
+    double v = threadIdx.x < DT / 32 ? red[0][threadIdx.x] : 0.0;
+    double v2 = threadIdx.x < DT / 32 ? red[1][threadIdx.x] : 0.0;
     v = warp_sum(v);
     v2 = warp_sum(v2);
     if (threadIdx.x == 0) {
@@ -145,6 +146,25 @@ __global__ void dot_fused_kernel(int64_t n, int nb, int chunk, int k2, const dou
     out[c] = t;
     if (two) out2[c] = t2;
     tickets[c] = 0u;
+  }
+}
+
+// block size of dot_fused_kernel (env KGP_DOT_THREADS: 256 | 512 | 1024)
+int dot_threads() {
+  static const int v = [] {
+    const char* s = getenv("KGP_DOT_THREADS");
+    const int t = s ? atoi(s) : 1024;
+    return t >= 1024 ? 1024 : t >= 512 ? 512 : 256;
+  }();
+  return v;
+}
+
+template <class... A>
+void launch_dot_fused(dim3 grid, cudaStream_t st, A... args) {
+  switch (dot_threads()) {
+    case 1024: dot_fused_kernel<1024><<<grid, 1024, 0, st>>>(args...); break;
+    case 512: dot_fused_kernel<512><<<grid, 512, 0, st>>>(args...); break;
+    default: dot_fused_kernel<256><<<grid, 256, 0, st>>>(args...); break;
   }
 }
 
@@ -281,90 +301,111 @@ __global__ void pcg_finish_kernel(int k, PcgGroups g, const double* rel, int32_t
 
 // ---------------------------------------------------------------- SLQ
 // Implicit-shift QL on the symmetric tridiagonal (d, e), rotating only the first
-// row z of the eigenvector matrix. Returns false if an eigenvalue does not
-// converge in 60 sweeps.
-__device__ bool tridiag_ql_first_row(int m, double* d, double* e, double* z) {
+// row z of the eigenvector matrix (element i of each array at [i * S]: the per-thread
+// arrays of a block are interleaved in shared memory). Returns false if an eigenvalue
+// does not converge in 60 sweeps. The rotation length sqrt(f^2 + g^2) is formed directly
+// (hypot's rescaling only matters far outside the range of Lanczos coefficients; it is
+// kept as the fallback there) and divided once.
+__device__ __forceinline__ double rot_len(double f, double g) {
+  const double r = sqrt(fma(f, f, g * g));
+  return (r > 1e-150 && r < 1e150) ? r : hypot(f, g);
+}
+
+__device__ bool tridiag_ql_first_row(int m, double* d, double* e, double* z, int S) {
   for (int l = 0; l < m; ++l) {
     int sweeps = 0;
     while (true) {
       int mm = l;
       for (; mm < m - 1; ++mm) {
-        double dd = fabs(d[mm]) + fabs(d[mm + 1]);
-        if (fabs(e[mm]) <= 2.2204460492503131e-16 * dd) break;
+        const double dd = fabs(d[mm * S]) + fabs(d[(mm + 1) * S]);
+        if (fabs(e[mm * S]) <= 2.2204460492503131e-16 * dd) break;
       }
       if (mm == l) break;
       if (++sweeps > 60) return false;
-      double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
-      double r = hypot(g, 1.0);
-      g = d[mm] - d[l] + e[l] / (g + copysign(r, g));
+      const double dl = d[l * S];
+      double g = (d[(l + 1) * S] - dl) / (2.0 * e[l * S]);
+      double r = rot_len(g, 1.0);
+      g = d[mm * S] - dl + e[l * S] / (g + copysign(r, g));
       double s = 1.0, c = 1.0, p = 0.0;
       int i = mm - 1;
       bool deflated = false;
+      double zi1 = z[mm * S];  // z[i + 1], carried in a register down the sweep
       for (; i >= l; --i) {
-        double f = s * e[i], b = c * e[i];
-        r = hypot(f, g);
-        e[i + 1] = r;
+        const double ei = e[i * S];
+        const double f = s * ei, b = c * ei;
+        r = rot_len(f, g);
+        e[(i + 1) * S] = r;
         if (r == 0.0) {  // split: the rotation underflowed
-          d[i + 1] -= p;
-          e[mm] = 0.0;
+          d[(i + 1) * S] -= p;
+          e[mm * S] = 0.0;
           deflated = true;
           break;
         }
-        s = f / r;
-        c = g / r;
-        g = d[i + 1] - p;
-        r = (d[i] - g) * s + 2.0 * c * b;
+        const double rinv = 1.0 / r;
+        s = f * rinv;
+        c = g * rinv;
+        g = d[(i + 1) * S] - p;
+        r = (d[i * S] - g) * s + 2.0 * c * b;
         p = s * r;
-        d[i + 1] = g + p;
+        d[(i + 1) * S] = g + p;
         g = c * r - b;
-        double zf = z[i + 1];
-        z[i + 1] = s * z[i] + c * zf;
-        z[i] = c * z[i] - s * zf;
+        const double zi = z[i * S];
+        z[(i + 1) * S] = s * zi + c * zi1;
+        zi1 = c * zi - s * zi1;
       }
-      if (deflated) continue;
-      d[l] -= p;
-      e[l] = g;
-      e[mm] = 0.0;
+      if (deflated) {
+        z[(i + 1) * S] = zi1;
+        continue;
+      }
+      z[l * S] = zi1;
+      d[l * S] -= p;
+      e[l * S] = g;
+      e[mm * S] = 0.0;
     }
   }
   return true;
 }
 
+// One thread per probe. ws: nullptr = the per-thread arrays live in dynamic shared memory
+// (3 * max_iter doubles per thread, interleaved); else a global scratch of the same layout.
 __global__ void slq_kernel(int k, int max_iter, const double* __restrict__ alphas, const double* __restrict__ betas,
                            const int32_t* __restrict__ iters, const double* __restrict__ norms_sq,
-                           double* __restrict__ scratch, double* __restrict__ contrib, int32_t* __restrict__ status) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
+                           double* __restrict__ ws, double* __restrict__ contrib, int32_t* __restrict__ status) {
+  extern __shared__ double slq_smem[];
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= k) return;
   const int m = iters[c];
   if (m == 0) {  // zero-iteration probes contribute 0 but count (solver.py:253-255)
     contrib[c] = 0.0;
     return;
   }
-  double* d = scratch + (int64_t)c * 3 * max_iter;
-  double* e = d + max_iter;
-  double* z = e + max_iter;
+  const int S = blockDim.x;
+  double* base = ws ? ws + (size_t)blockIdx.x * blockDim.x * 3 * max_iter : slq_smem;
+  double* d = base + threadIdx.x;
+  double* e = d + (size_t)max_iter * S;
+  double* z = e + (size_t)max_iter * S;
   const double* a = alphas + (int64_t)c * max_iter;
   const double* b = betas + (int64_t)c * max_iter;
   // solver.py:232-234: d_i = 1/a_i + b_{i-1}/a_{i-1}; e_i = sqrt(b_i)/a_i
   for (int i = 0; i < m; ++i) {
-    d[i] = 1.0 / a[i] + (i > 0 ? b[i - 1] / a[i - 1] : 0.0);
-    e[i] = (i < m - 1) ? sqrt(b[i]) / a[i] : 0.0;
-    z[i] = (i == 0) ? 1.0 : 0.0;
+    d[i * S] = 1.0 / a[i] + (i > 0 ? b[i - 1] / a[i - 1] : 0.0);
+    e[i * S] = (i < m - 1) ? sqrt(b[i]) / a[i] : 0.0;
+    z[i * S] = (i == 0) ? 1.0 : 0.0;
   }
-  if (!tridiag_ql_first_row(m, d, e, z)) {
+  if (!tridiag_ql_first_row(m, d, e, z, S)) {
     status[1] = KGP_ERR_NUMERICAL;
     contrib[c] = NAN;
     return;
   }
   double wmin = d[0], acc = 0.0;
-  for (int i = 0; i < m; ++i) wmin = fmin(wmin, d[i]);
+  for (int i = 0; i < m; ++i) wmin = fmin(wmin, d[i * S]);
   if (!(wmin > 0.0)) {
     status[1] = KGP_ERR_NUMERICAL;
-    atomicMin(&status[2], c);
+    atomicMax(&status[2], k - c);  // lowest failing column = k - status[2]
     contrib[c] = wmin;
     return;
   }
-  for (int i = 0; i < m; ++i) acc += z[i] * z[i] * log(d[i]);
+  for (int i = 0; i < m; ++i) acc += z[i * S] * z[i * S] * log(d[i * S]);
   contrib[c] = norms_sq[c] * acc;
 }
 
@@ -440,8 +481,8 @@ int enqueue_iteration(kgp_engine_s* e, const PcSet& pcs, int64_t k, const PcgGro
   const int nb = (int)((n + chunk - 1) / chunk);
   int rc = engine_matmul_impl(e, k, S.p, 1, n, S.ap, nullptr, nullptr, 1, n, st);
   if (rc) return rc;
-  dot_fused_kernel<<<dim3((unsigned)nb, (unsigned)k), DOT_THREADS, 0, st>>>(
-      n, nb, chunk, 0, S.p, S.ap, nullptr, nullptr, S.partial, S.dots1, nullptr, S.tickets);
+  launch_dot_fused(dim3((unsigned)nb, (unsigned)k), st, n, nb, chunk, 0, S.p, S.ap, nullptr, nullptr, S.partial,
+                   S.dots1, nullptr, S.tickets);
   KGP_LAUNCH("dot_fused_kernel");
   pcg_alpha_update_kernel<<<vgrid, 256, 0, st>>>(n, (int)k, g.stride, S.dots1, S.rz, S.active, B.iters, B.alphas,
                                                  S.status, S.err_val, S.p, S.ap, B.x, S.r);
@@ -451,10 +492,11 @@ int enqueue_iteration(kgp_engine_s* e, const PcSet& pcs, int64_t k, const PcgGro
     if (rc) return rc;
   }
   // r.r on every column and r.z on the preconditioned ones, one launch
-  dot_fused_kernel<<<dim3((unsigned)nb, (unsigned)k), DOT_THREADS, 0, st>>>(
-      n, nb, chunk, pc ? g.kz : 0, S.r, S.r, pc ? S.r : nullptr, pc ? S.z : nullptr, S.partial, S.dots1, S.dots2, S.tickets);
+  launch_dot_fused(dim3((unsigned)nb, (unsigned)k), st, n, nb, chunk, pc ? g.kz : 0, S.r, S.r, pc ? S.r : nullptr,
+                   pc ? S.z : nullptr, S.partial, S.dots1, S.dots2, S.tickets);
   KGP_LAUNCH("dot_fused_kernel");
-  pcg_beta_kernel<<<1, 1024, 0, st>>>((int)k, g, pc, S.dots1, S.dots2, S.rz, S.ynorm, S.active, B.iters,
+  const int bt = (int)((k + 31) / 32 * 32);
+  pcg_beta_kernel<<<1, bt, 0, st>>>((int)k, g, pc, S.dots1, S.dots2, S.rz, S.ynorm, S.active, B.iters,
                                       S.beta, B.betas, B.rel, S.status, B.it_counter, e->hist_dev);
   KGP_LAUNCH("pcg_beta_kernel");
   pcg_update_p_kernel<<<vgrid, 256, 0, st>>>(n, (int)k, pc ? g.kz : 0, S.active, S.beta, S.z, S.r, S.p);
@@ -710,16 +752,25 @@ int pcg_grouped_impl(kgp_engine_s* e, const PcSet& pcs, int64_t k, int64_t kpc, 
 int slq_impl(int64_t k, int max_iter, const double* alphas, const double* betas, const int32_t* iters,
              const double* norms_sq, double* logdet, cudaStream_t st) {
   static thread_local DevBuf ws;  // persistent: cudaMalloc/cudaFree per call would serialise the device
-  int rc = ws.ensure(sizeof(double) * ((size_t)k * 3 * max_iter + k) + 64);
+  // per-thread arrays in shared memory when a block of >= 8 probes fits in 160 KB
+  const size_t per_thread = sizeof(double) * 3 * (size_t)max_iter;
+  const size_t smem_cap = 160 * 1024;
+  int tpb = (int)(smem_cap / per_thread < 64 ? smem_cap / per_thread : 64);
+  const bool in_smem = tpb >= 8 && getenv("KGP_SLQ_GLOBAL") == nullptr;
+  if (!in_smem) tpb = 64;
+  if (tpb > k) tpb = (int)((k + 7) / 8 * 8);
+  const unsigned blocks = (unsigned)((k + tpb - 1) / tpb);
+  const size_t scratch = in_smem ? 0 : (size_t)blocks * tpb * 3 * max_iter;
+  int rc = ws.ensure(sizeof(double) * (scratch + k) + 64);
   if (rc) return rc;
-  double* scratch = ws.as<double>();
-  double* contrib = scratch + (size_t)k * 3 * max_iter;
+  double* contrib = ws.as<double>() + scratch;
   int32_t* status = reinterpret_cast<int32_t*>(contrib + k);
   KGP_CUDA(cudaMemsetAsync(status, 0, sizeof(int32_t) * 4, st));
-  int32_t init_min = 0x7fffffff;
-  KGP_CUDA(cudaMemcpyAsync(status + 2, &init_min, sizeof(int32_t), cudaMemcpyHostToDevice, st));
-  slq_kernel<<<(unsigned)((k + 63) / 64), 64, 0, st>>>((int)k, max_iter, alphas, betas, iters, norms_sq, scratch,
-                                                       contrib, status);
+  const size_t smem = in_smem ? per_thread * tpb : 0;
+  if (smem > 48 * 1024)
+    KGP_CUDA(cudaFuncSetAttribute(slq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  slq_kernel<<<blocks, tpb, smem, st>>>((int)k, max_iter, alphas, betas, iters, norms_sq,
+                                        in_smem ? nullptr : ws.as<double>(), contrib, status);
   KGP_LAUNCH("slq_kernel");
   std::vector<double> h(k);
   int32_t hs[4];
@@ -727,7 +778,8 @@ int slq_impl(int64_t k, int max_iter, const double* alphas, const double* betas,
   KGP_CUDA(cudaMemcpyAsync(hs, status, sizeof(hs), cudaMemcpyDeviceToHost, st));
   KGP_CUDA(cudaStreamSynchronize(st));
   if (hs[1] == KGP_ERR_NUMERICAL) {
-    double w = (hs[2] >= 0 && hs[2] < k) ? h[hs[2]] : NAN;
+    const int64_t col = hs[2] > 0 ? k - hs[2] : -1;
+    double w = (col >= 0 && col < k) ? h[col] : NAN;
     set_error(KGP_ERR_NUMERICAL, "nonpositive Ritz value %.17g; operator is not SPD or CG broke down", w);
     return KGP_ERR_NUMERICAL;
   }
