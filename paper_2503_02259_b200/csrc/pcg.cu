@@ -75,19 +75,14 @@ __global__ void dot_final_kernel(int k, int nb, const double* __restrict__ parti
 // given, out2[c] = a2_c . b2_c (c < k2). Each block writes its chunk's partials; the last
 // block of a column (ticket counter) sums them in block order -- the same fixed order as
 // dot_partial + dot_final, so results are run-to-run identical -- and re-arms the ticket.
+// Block sums of a[i] b[i] (and a2[i] b2[i] when two) over [i0, i1) of one column (offset
+// off); the totals are valid in warp 0. Four independent accumulators per thread: four
+// loads in flight (the loop is latency-bound for the short columns of small problems),
+// combined in a fixed order. Every thread of the block must call it.
 template <int DT>
-__global__ void __launch_bounds__(DT) dot_fused_kernel(int64_t n, int nb, int chunk, int k2, const double* __restrict__ a,
-                                 const double* __restrict__ b,
-                                 const double* __restrict__ a2, const double* __restrict__ b2,
-                                 double* __restrict__ partial, double* __restrict__ out, double* __restrict__ out2,
-                                 unsigned* __restrict__ tickets) {
-  const int c = blockIdx.y, blk = blockIdx.x;
-  const bool two = a2 != nullptr && c < k2;
-  const int64_t off = (int64_t)c * n;
-  const int64_t i0 = (int64_t)blk * chunk;
-  const int64_t i1 = i0 + chunk < n ? i0 + chunk : n;
-  // four independent accumulators: four loads in flight per thread (the loop is latency-bound
-  // for the short columns of small problems); combined in a fixed order
+KGP_DEV void block_dots(int64_t off, int64_t i0, int64_t i1, const double* __restrict__ a,
+                        const double* __restrict__ b, const double* __restrict__ a2, const double* __restrict__ b2,
+                        bool two, double& v, double& v2) {
   double sa[4] = {0.0, 0.0, 0.0, 0.0}, sb[4] = {0.0, 0.0, 0.0, 0.0};
   int64_t i = i0 + threadIdx.x;
   for (; i + 3 * DT < i1; i += 4 * DT) {
@@ -105,7 +100,6 @@ __global__ void __launch_bounds__(DT) dot_fused_kernel(int64_t n, int nb, int ch
   double s = (sa[0] + sa[1]) + (sa[2] + sa[3]);
   double s2 = (sb[0] + sb[1]) + (sb[2] + sb[3]);
   __shared__ double red[2][DT / 32];
-  __shared__ bool last;
   s = warp_sum(s);
   s2 = warp_sum(s2);
   if ((threadIdx.x & 31) == 0) {
@@ -113,11 +107,30 @@ __global__ void __launch_bounds__(DT) dot_fused_kernel(int64_t n, int nb, int ch
     red[1][threadIdx.x >> 5] = s2;
   }
   __syncthreads();
+  v = v2 = 0.0;
   if (threadIdx.x < 32) {
-    double v = threadIdx.x < DT / 32 ? red[0][threadIdx.x] : 0.0;
-    double v2 = threadIdx.x < DT / 32 ? red[1][threadIdx.x] : 0.0;
+    v = threadIdx.x < DT / 32 ? red[0][threadIdx.x] : 0.0;
+    v2 = threadIdx.x < DT / 32 ? red[1][threadIdx.x] : 0.0;
     v = warp_sum(v);
     v2 = warp_sum(v2);
+  }
+}
+
+template <int DT>
+__global__ void __launch_bounds__(DT) dot_fused_kernel(int64_t n, int nb, int chunk, int k2, const double* __restrict__ a,
+                                 const double* __restrict__ b,
+                                 const double* __restrict__ a2, const double* __restrict__ b2,
+                                 double* __restrict__ partial, double* __restrict__ out, double* __restrict__ out2,
+                                 unsigned* __restrict__ tickets) {
+  const int c = blockIdx.y, blk = blockIdx.x;
+  const bool two = a2 != nullptr && c < k2;
+  const int64_t off = (int64_t)c * n;
+  const int64_t i0 = (int64_t)blk * chunk;
+  const int64_t i1 = i0 + chunk < n ? i0 + chunk : n;
+  __shared__ bool last;
+  double v, v2;
+  block_dots<DT>(off, i0, i1, a, b, a2, b2, two, v, v2);
+  if (threadIdx.x < 32) {
     if (threadIdx.x == 0) {
       if (nb == 1) {  // one block per column: it holds the whole dot
         out[c] = v;
