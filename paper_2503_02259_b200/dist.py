@@ -91,13 +91,19 @@ class DistSolve:
     converged: np.ndarray
 
 
-def dist_pcg(ops, comm: Comm, y_loc, tol, max_iter: int, precondition, shift: float = 1.0):
+def dist_pcg(ops, comm: Comm, y_loc, tol, max_iter: int, precondition, shift: float = 1.0, diag_loc=None,
+             minv_fn=None):
     """Batched PCG over row-sharded state (solver.py:122-192). y_loc: (k, n_loc).
 
     Column groups as the device driver's (pcg.cu pcg_grouped_impl): ``tol`` and the
     per-column iteration cap may be scalars or length-k arrays, and ``precondition`` a bool
     or the number of LEADING columns to precondition -- so the NLML's w-solve and probe solves
-    share one operator application (one all-gather) per iteration."""
+    share one operator application (one all-gather) per iteration.
+
+    ``diag_loc`` (k, n_loc): a per-column diagonal added to the operator on the local rows
+    (column j solves (Khat + diag(d_j)) x = y_j -- the Dirichlet GPC classes, the device
+    path's kgp_engine_set_diag). ``minv_fn(head_loc) -> z_loc`` replaces the built-in
+    preconditioner on the leading columns (e.g. one replicated handle per GPC class)."""
     torch = __import__("torch")
     k = y_loc.shape[0]
     tol = np.broadcast_to(np.asarray(tol, dtype=np.float64), (k,)).copy()
@@ -118,7 +124,9 @@ def dist_pcg(ops, comm: Comm, y_loc, tol, max_iter: int, precondition, shift: fl
         if kp == 0:
             return r
         head = r[:kp]
-        if full_minv is not None:  # replicated preconditioner (AFN): gather, apply, keep own rows
+        if minv_fn is not None:
+            zh = minv_fn(head)
+        elif full_minv is not None:  # replicated preconditioner (AFN): gather, apply, keep own rows
             zh = full_minv(comm.allgather_rows(head))[:, r0:r1].contiguous()
         else:
             t = comm.allreduce(ops.project(head))
@@ -139,6 +147,8 @@ def dist_pcg(ops, comm: Comm, y_loc, tol, max_iter: int, precondition, shift: fl
         rz = dots(r, z)
         for _ in range(stride):
             ap = ops.matmul_rows(comm.allgather_rows(p))
+            if diag_loc is not None:
+                ap = ap + diag_loc * p
             pap = dots(p, ap)
             act = np.flatnonzero(active)
             bad = [j for j in act if not np.isfinite(pap[j]) or pap[j] <= 0.0]
@@ -206,6 +216,56 @@ def dist_nlml_grad(ops, comm: Comm, y_loc, probes_loc, norms_sq, tol, max_iter, 
     return loss, grads[0], grads[1], grads[2], ok
 
 
+def dist_gpc_nlml_grad(ops, comm: Comm, targets_loc, noise_loc, probes_loc, norms_sq, tol, max_iter,
+                       probe_tol=None, probe_max_iter=None, minv_classes=None):
+    """Dirichlet GPC loss and (l, f, s) gradient (gpc.nlml_grad_iterative, the device path's
+    kgp_gpc_nlml_grad) over row-sharded vectors: class c solves (Khat + diag(noise_c)).
+
+    targets_loc, noise_loc: (C, n_loc); probes_loc: (C * k_z, n_loc), block c for class c;
+    norms_sq: (C * k_z,) full |z|^2. The C target solves (preconditioned by
+    ``minv_classes(r_head) -> z_head`` when given) and the C * k_z probe solves run as ONE
+    grouped PCG: one all-gather and one fused Khat [P] on the local rows per iteration.
+    Returns (loss, grad_l, grad_f, grad_s, converged), summed over classes, identical on every
+    rank."""
+    torch = __import__("torch")
+    probe_tol = tol if probe_tol is None else probe_tol
+    probe_max_iter = max_iter if probe_max_iter is None else probe_max_iter
+    c = targets_loc.shape[0]
+    kz = probes_loc.shape[0] // c
+    if probes_loc.shape[0] != c * kz or kz < 1:
+        raise ValueError(f"probes must hold k_z >= 1 rows per class ({c} classes), got {probes_loc.shape[0]}")
+    v0 = torch.cat([targets_loc, probes_loc], dim=0)
+    cls = np.concatenate([np.arange(c), np.repeat(np.arange(c), kz)])
+    diag = noise_loc[torch.from_numpy(cls).to(noise_loc.device)]
+    tols = np.array([tol] * c + [probe_tol] * (c * kz))
+    caps = np.array([max_iter] * c + [probe_max_iter] * (c * kz))
+    sol = dist_pcg(ops, comm, v0, tols, caps, c if minv_classes is not None else False, diag_loc=diag,
+                   minv_fn=minv_classes)
+    loss, grads = 0.0, np.zeros(3)
+    w = sol.x[:c]
+    yw = comm.allreduce((targets_loc * w).sum(dim=1)).cpu().numpy()
+    v_loc = torch.cat([w, probes_loc], dim=0)
+    u_loc = torch.cat([w, sol.x[c:]], dim=0)
+    dl, df = ops.grads_rows(comm.allgather_rows(v_loc))
+    part = torch.stack([(u_loc * dl).sum(dim=1), (u_loc * df).sum(dim=1), (u_loc * v_loc).sum(dim=1)])
+    part = comm.allreduce(part).cpu().numpy()
+    for k in range(c):
+        rows = slice(c + k * kz, c + (k + 1) * kz)
+        logdet = ops.slq(sol.alphas[rows], sol.betas[rows], sol.iters[rows], norms_sq[k * kz:(k + 1) * kz])
+        loss += 0.5 * (yw[k] + logdet + comm.n * LOG_2PI)
+        for t in range(3):
+            grads[t] += 0.5 * (-part[t, k] + part[t, rows].sum() / kz)
+    return loss, grads[0], grads[1], grads[2], bool(sol.converged.all())
+
+
+def dist_predict_mean(ops, comm: Comm, xs, alpha_loc):
+    """Predictive mean K(X*, X) alpha (gp.py:223-236) with alpha row-sharded like the training
+    points: each rank contracts the cross kernel against its own training columns
+    (``ops.cross_rows``, never materialised on the device) and one all-reduce of the m-vector
+    sums the shards. xs: (m, d) test points (replicated); alpha_loc: (k, n_loc)."""
+    return comm.allreduce(ops.cross_rows(xs, alpha_loc))
+
+
 class CudaRowOps:
     """GPU local ops: this rank's rows of the fused operator and of the Woodbury factor."""
 
@@ -269,6 +329,18 @@ class CudaRowOps:
         self._call("kgp_lowrank_expand", self.pre.h, beta, alpha, k, r_loc.data_ptr(), 1, nloc, t.contiguous().data_ptr(),
                    out.data_ptr(), 1, nloc, self._device.stream_ptr())
         return out
+
+    def cross_rows(self, xs, alpha_loc):
+        """K(xs, X[r0:r1]) alpha_loc: the cross kernel against this rank's training points, on
+        an engine built over those points only (kgp_engine_cross_matmul)."""
+        from paper_2503_02259_b200.kmat import KernelEngine
+
+        torch = self._device.torch()
+        if getattr(self, "_local", None) is None:
+            self._local = KernelEngine(self.engine.kt, self.engine.x[self.r0:self.r1], self.engine.params,
+                                       precision=self.engine.precision)
+        xs_d = torch.as_tensor(np.asarray(xs, dtype=np.float64)).to(self._device.device()).contiguous()
+        return self._local.cross_matmul(xs_d, alpha_loc.T.contiguous()).T.contiguous()
 
     def slq(self, alphas, betas, iters, norms_sq):
         from paper_2503_02259_b200 import solver

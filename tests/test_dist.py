@@ -52,6 +52,10 @@ class OracleRowOps:
         out = beta * r_loc.numpy().T + alpha * (self.ny.v[self.r0:self.r1] @ y)
         return torch.from_numpy(np.ascontiguousarray(out.T))
 
+    def cross_rows(self, xs, alpha_loc):
+        kx = F * F * orc.eval_kernel(KT, np.asarray(xs), self.x[self.r0:self.r1], L)
+        return torch.from_numpy(np.ascontiguousarray((kx @ alpha_loc.numpy().T).T))
+
     def slq(self, alphas, betas, iters, norms_sq):
         a = [alphas[j, :it].numpy() for j, it in enumerate(iters)]
         b = [betas[j, :it].numpy() for j, it in enumerate(iters)]
@@ -162,4 +166,53 @@ def test_row_partitioned_pcg_replicated_afn_gloo(tmp_path):
     """AFN (not row-shardable) replicated on every rank: gather r, apply, keep own rows."""
     errfile = str(tmp_path / "err.txt")
     mp.spawn(_afn_worker, args=(2, _free_port(), errfile), nprocs=2, join=True)
+    assert not os.path.exists(errfile), open(errfile).read()
+
+
+def _gpc_worker(rank, world, port, errfile):
+    """Dirichlet GPC loss/gradient and the predictive mean over row-sharded vectors."""
+    try:
+        import gpc_ref
+
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        x, y, z = _problem()
+        n, c, kz = len(y), 3, 4
+        labels = np.argmax(np.stack([np.sin(2 * x[:, 0]), np.cos(3 * x[:, 1]), x[:, 0] * x[:, 1]]), axis=0)
+        targets, noise = gpc_ref.transform(labels, c)
+        probes = np.random.default_rng(3).standard_normal((c * kz, n))
+        comm = kdist.Comm(n)
+        r0, r1 = kdist.row_range(n, world, rank)
+        ops = OracleRowOps(x, r0, r1, None)
+        t_loc = torch.from_numpy(np.ascontiguousarray(targets[:, r0:r1]))
+        d_loc = torch.from_numpy(np.ascontiguousarray(noise[:, r0:r1]))
+        z_loc = torch.from_numpy(np.ascontiguousarray(probes[:, r0:r1]))
+        loss, g = gpc_ref.estimator(KT, x, targets, noise, L, F, S, probes)
+        ref = np.array([loss, *g])
+        # a row-local (Jacobi) preconditioner per class exercises the minv_fn path
+        kdiag = F * F + S
+        jac = lambda head: head / (kdiag + d_loc)  # noqa: E731
+        for minv in (None, jac):
+            got = kdist.dist_gpc_nlml_grad(ops, comm, t_loc, d_loc, z_loc, np.einsum("ij,ij->i", probes, probes),
+                                           1e-11, 3000, minv_classes=minv)
+            assert got[4], "converged"
+            assert np.all(np.abs(np.array(got[:4]) - ref) <= 1e-6 * np.abs(ref)), (got, ref)
+        # predictive mean: alpha sharded like the training rows
+        xs = np.random.default_rng(4).uniform(-1, 1, (17, 2))
+        alpha = np.random.default_rng(5).standard_normal((2, n))
+        mean = kdist.dist_predict_mean(ops, comm, xs, torch.from_numpy(np.ascontiguousarray(alpha[:, r0:r1])))
+        want = F * F * orc.eval_kernel(KT, xs, x, L) @ alpha.T
+        assert np.max(np.abs(mean.numpy().T - want)) <= 1e-12 * np.max(np.abs(want))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as exc:
+        with open(errfile, "a") as fh:
+            fh.write(f"rank {rank}: {type(exc).__name__}: {exc}\n")
+        raise
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_partitioned_gpc_and_predict_gloo(tmp_path, world):
+    errfile = str(tmp_path / "err.txt")
+    mp.spawn(_gpc_worker, args=(world, _free_port(), errfile), nprocs=world, join=True)
     assert not os.path.exists(errfile), open(errfile).read()

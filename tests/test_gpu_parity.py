@@ -432,6 +432,67 @@ def test_row_partitioned_nlml_on_device(pkg, tmp_path):
     assert not os.path.exists(errfile), open(errfile).read()
 
 
+def _dist_gpc_gpu_worker(rank, world, port, errfile):
+    import os
+
+    import torch
+    import torch.distributed as tdist
+
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        tdist.init_process_group("gloo", rank=rank, world_size=world)  # host collectives: one GPU is safe
+        torch.cuda.set_device(0)
+        import paper_2503_02259_b200 as kgp
+        from paper_2503_02259_b200 import dist as kdist
+        from paper_2503_02259_b200 import gpc
+
+        rng = np.random.default_rng(7)
+        n, c, kz = 400, 3, 4
+        x = rng.uniform(0, 1, (n, 2))
+        lab = gpc.sample_latent_labels(x, c, l=0.3, seed=7)
+        prob = gpc.setup(x, lab)
+        hp = kgp.Hyperparams(l=0.25, f=1.1, s=0.02)
+        e = kgp.KernelEngine(kgp.KernelType.MATERN32, x, hp, precision="fp64")
+        probes = gpc.generate_probes(n, c, kz, 5)
+        r0, r1 = kdist.row_range(n, world, rank)
+        ops = kdist.CudaRowOps(e, r0, r1)
+        comm = kdist.Comm(n)
+        cuda = lambda a: torch.from_numpy(np.ascontiguousarray(a[:, r0:r1])).cuda()  # noqa: E731
+        got = kdist.dist_gpc_nlml_grad(ops, comm, cuda(prob.targets), cuda(prob.noise), cuda(probes),
+                                       np.einsum("ij,ij->i", probes, probes), 1e-11, 3000)
+        single = gpc.nlml_grad_iterative(e, prob, [], probes, tol=1e-11, max_iter=3000)
+        ref = np.array([single.loss, single.grad_l, single.grad_f, single.grad_s])
+        assert got[4] and single.converged
+        assert np.all(np.abs(np.array(got[:4]) - ref) <= 1e-8 * np.abs(ref)), (got, ref)
+        xs = rng.uniform(0, 1, (33, 2))
+        alpha = rng.standard_normal((2, n))
+        mean = kdist.dist_predict_mean(ops, comm, xs, cuda(alpha))
+        want = e.cross_matmul(torch.from_numpy(xs).cuda(), torch.from_numpy(alpha.T.copy()).cuda())
+        assert rel_max(mean.T.cpu().numpy(), want.cpu().numpy()) <= 1e-12
+        tdist.barrier()
+        tdist.destroy_process_group()
+    except Exception as exc:
+        with open(errfile, "a") as fh:
+            fh.write(f"rank {rank}: {type(exc).__name__}: {exc}\n")
+        raise
+
+
+def test_row_partitioned_gpc_and_predict_on_device(pkg, tmp_path):
+    """dist.dist_gpc_nlml_grad / dist_predict_mean over dist.CudaRowOps, 2 ranks on one GPU,
+    against the single-GPU GPC estimator (same probes) and the full cross-kernel product."""
+    import os
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    errfile = str(tmp_path / "err.txt")
+    mp.spawn(_dist_gpc_gpu_worker, args=(2, port, errfile), nprocs=2, join=True)
+    assert not os.path.exists(errfile), open(errfile).read()
+
+
 def test_predict_hutchinson_variance(pkg):
     """configs[4]'s estimator (no reference oracle): the mean equals the exact posterior mean,
     the Hutchinson variance is unbiased -- within 5 sigma of the exact diagonal, sigma from the
