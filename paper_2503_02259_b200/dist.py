@@ -58,22 +58,25 @@ class Comm:
         self.maxloc = max(r1 - r0 for r0, r1 in self.ranges)
         self.nccl = dist.get_backend(group) == "nccl"
 
-    def allgather_rows(self, x_loc):
-        """(k, n_loc) on every rank -> (k, n) full, rows in rank order."""
+    def allgather_rows(self, x_loc, ranges=None):
+        """(k, n_loc) on every rank -> (k, n) full, rows in rank order (``ranges``: another
+        balanced split than the training rows', e.g. of the test points)."""
         torch = __import__("torch")
         k, nloc = x_loc.shape
         if self.world == 1:
             return x_loc
-        pad = torch.zeros((k, self.maxloc), dtype=x_loc.dtype, device=x_loc.device)
+        ranges = self.ranges if ranges is None else ranges
+        maxloc = max(r1 - r0 for r0, r1 in ranges)
+        pad = torch.zeros((k, maxloc), dtype=x_loc.dtype, device=x_loc.device)
         pad[:, :nloc] = x_loc
         if self.nccl:
-            buf = torch.empty((self.world, k, self.maxloc), dtype=x_loc.dtype, device=x_loc.device)
+            buf = torch.empty((self.world, k, maxloc), dtype=x_loc.dtype, device=x_loc.device)
             self.dist.all_gather_into_tensor(buf, pad, group=self.group)
             parts = [buf[r] for r in range(self.world)]
         else:
             parts = [torch.empty_like(pad) for _ in range(self.world)]
             self.dist.all_gather(parts, pad, group=self.group)
-        return torch.cat([parts[r][:, :r1 - r0] for r, (r0, r1) in enumerate(self.ranges)], dim=1)
+        return torch.cat([parts[r][:, :r1 - r0] for r, (r0, r1) in enumerate(ranges)], dim=1)
 
     def allreduce(self, t):
         if self.world > 1:
@@ -266,6 +269,17 @@ def dist_predict_mean(ops, comm: Comm, xs, alpha_loc):
     return comm.allreduce(ops.cross_rows(xs, alpha_loc))
 
 
+def dist_local_variance(comm: Comm, xs, local_var_fn):
+    """Local predictive variance (gp.predict_local) with the TEST points split over the ranks:
+    the training points are replicated, so each rank runs the cross kNN + per-point kriging
+    (``local_var_fn(xs_slice) -> (m_loc,)``; ``CudaRowOps.local_variance`` on the GPU) on its
+    balanced slice of xs and one all-gather assembles the (m,) variance."""
+    m = len(xs)
+    ranges = [row_range(m, comm.world, r) for r in range(comm.world)]
+    q0, q1 = ranges[comm.rank]
+    return comm.allgather_rows(local_var_fn(np.asarray(xs)[q0:q1])[None, :], ranges)[0]
+
+
 class CudaRowOps:
     """GPU local ops: this rank's rows of the fused operator and of the Woodbury factor."""
 
@@ -341,6 +355,28 @@ class CudaRowOps:
                                        precision=self.engine.precision)
         xs_d = torch.as_tensor(np.asarray(xs, dtype=np.float64)).to(self._device.device()).contiguous()
         return self._local.cross_matmul(xs_d, alpha_loc.T.contiguous()).T.contiguous()
+
+    def local_variance(self, xs, k_nn: int = 64):
+        """f^2 - c^T Khat_NN^-1 c over the k_nn nearest training points of each test point in xs
+        (kgp_knn_cross + kgp_local_variance against the replicated X)."""
+        from paper_2503_02259_b200.kernels import kernel_id
+
+        torch = self._device.torch()
+        xd = self.engine.x_device()
+        n, d = xd.shape
+        xs_d = torch.as_tensor(np.asarray(xs, dtype=np.float64)).to(xd.device).contiguous()
+        m = xs_d.shape[0]
+        k_nn = int(min(k_nn, n))
+        nbr = torch.empty((m, k_nn), dtype=torch.int64, device=xd.device)
+        var = torch.empty(m, dtype=torch.float64, device=xd.device)
+        if m:
+            p = self.engine.params
+            self._call("kgp_knn_cross", m, xs_d.data_ptr(), n, xd.data_ptr(), d, k_nn, nbr.data_ptr(),
+                       self._device.stream_ptr())
+            self._call("kgp_local_variance", kernel_id(self.engine.kt), m, d, xs_d.data_ptr(), xd.data_ptr(),
+                       float(p.l), float(p.f), float(p.s), k_nn, nbr.data_ptr(), var.data_ptr(),
+                       self._device.stream_ptr())
+        return var
 
     def slq(self, alphas, betas, iters, norms_sq):
         from paper_2503_02259_b200 import solver

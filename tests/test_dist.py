@@ -203,6 +203,15 @@ def _gpc_worker(rank, world, port, errfile):
         mean = kdist.dist_predict_mean(ops, comm, xs, torch.from_numpy(np.ascontiguousarray(alpha[:, r0:r1])))
         want = F * F * orc.eval_kernel(KT, xs, x, L) @ alpha.T
         assert np.max(np.abs(mean.numpy().T - want)) <= 1e-12 * np.max(np.abs(want))
+        # local variance with the test points split over the ranks (k_nn = n: the exact variance)
+        kh = orc.khat_dense(KT, x, L, F, S)
+
+        def exact_var(xq):
+            cq = F * F * orc.eval_kernel(KT, xq, x, L)
+            return torch.from_numpy(F * F - np.einsum("ij,ji->i", cq, np.linalg.solve(kh, cq.T)))
+
+        var = kdist.dist_local_variance(comm, xs, exact_var)
+        np.testing.assert_allclose(var.numpy(), exact_var(xs).numpy(), rtol=1e-12)
         dist.barrier()
         dist.destroy_process_group()
     except Exception as exc:

@@ -469,6 +469,8 @@ def _dist_gpc_gpu_worker(rank, world, port, errfile):
         mean = kdist.dist_predict_mean(ops, comm, xs, cuda(alpha))
         want = e.cross_matmul(torch.from_numpy(xs).cuda(), torch.from_numpy(alpha.T.copy()).cuda())
         assert rel_max(mean.T.cpu().numpy(), want.cpu().numpy()) <= 1e-12
+        var = kdist.dist_local_variance(comm, xs, lambda q: ops.local_variance(q, 32))
+        np.testing.assert_array_equal(var.cpu().numpy(), ops.local_variance(xs, 32).cpu().numpy())
         tdist.barrier()
         tdist.destroy_process_group()
     except Exception as exc:
