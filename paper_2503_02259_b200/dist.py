@@ -269,6 +269,65 @@ def dist_predict_mean(ops, comm: Comm, xs, alpha_loc):
     return comm.allreduce(ops.cross_rows(xs, alpha_loc))
 
 
+def dist_fit(comm: Comm, y_loc, config, initial, make_ops):
+    """Hyperparameter training (train.fit, train.py:176-240) over row-sharded vectors: Adam in
+    softplus space on the distributed NLML gradient. Every rank evaluates the same loss and
+    gradient (all-reduced scalars), so the parameter trajectory is identical on all ranks.
+
+    y_loc: (n_loc,) this rank's targets; ``initial``: Hyperparams (train.initial_hyperparams
+    on the full data, computed identically everywhere); ``make_ops(hp) -> (ops, shift)``
+    builds this rank's local operator rows (and sharded preconditioner) at hp --
+    ``CudaRowOps`` on the GPU. Probes are the reference's per-step seeds
+    ``ProbeSet.generate(n, k_z, (rng_seed, step))``, cut to the local rows."""
+    from paper_2503_02259_b200 import gp
+    from paper_2503_02259_b200.train import Adam, RawParams, TrainResult, TrainStatus, chain_grads
+
+    torch = __import__("torch")
+    if config.mode != "iterative":
+        raise ValueError("the distributed trainer runs the iterative estimator (mode='iterative')")
+    r0, r1 = comm.ranges[comm.rank]
+    raw = RawParams.from_hyperparams(initial)
+    opt = Adam(config.learning_rate)
+    result = TrainResult(params=raw.to_hyperparams(), raw=raw)
+    warned = False
+    for step in range(config.max_steps):
+        hp = raw.to_hyperparams()
+        ops, shift = make_ops(hp)
+        probes = gp.ProbeSet.generate(comm.n, config.k_z, (config.rng_seed, step)).vectors
+        z_loc = torch.from_numpy(np.ascontiguousarray(probes.T[:, r0:r1])).to(y_loc.device)
+        loss, gl, gf, gs, ok = dist_nlml_grad(ops, comm, y_loc, z_loc, np.einsum("ij,ij->j", probes, probes),
+                                              config.tol, config.max_iter, config.probe_tol, precondition=True,
+                                              shift=shift)
+        warned |= not ok
+        g_rho = chain_grads(raw, [gl, gf, gs])
+        gnorm = float(np.linalg.norm(g_rho))
+        result.loss_history.append(loss)
+        result.grad_norm_history.append(gnorm)
+        if gnorm < config.grad_norm_tol:
+            result.status = TrainStatus.GRAD_TOL
+            break
+        raw = RawParams.from_array(opt.step(raw.as_array(), g_rho))
+    if warned:
+        result.status = TrainStatus.SOLVER_WARNING
+    result.raw = raw
+    result.params = raw.to_hyperparams()
+    return result
+
+
+def cuda_ops_factory(kt, x, comm: Comm, precond_rank: int, precision=None):
+    """make_ops for dist_fit on the GPU: a row-block engine + the replicated-build, row-sharded
+    Nystrom/Woodbury factor at each step's hyperparameters."""
+    from paper_2503_02259_b200.kmat import KernelEngine
+
+    r0, r1 = comm.ranges[comm.rank]
+
+    def make(hp):
+        engine = KernelEngine(kt, x, hp, precision=precision)
+        return CudaRowOps(engine, r0, r1, build_precond_factor(engine, precond_rank)), hp.s
+
+    return make
+
+
 def dist_local_variance(comm: Comm, xs, local_var_fn):
     """Local predictive variance (gp.predict_local) with the TEST points split over the ranks:
     the training points are replicated, so each rank runs the cross kNN + per-point kriging

@@ -30,18 +30,19 @@ def _problem(n=240, seed=8):
 
 
 class OracleRowOps:
-    def __init__(self, x, r0, r1, ny):
+    def __init__(self, x, r0, r1, ny, hp=(L, F, S)):
         self.x, self.r0, self.r1, self.ny = x, r0, r1, ny
         self.rows = np.arange(r0, r1)
+        self.l, self.f, self.s = hp
 
     def matmul_rows(self, p_full):
-        out = orc.khat_matmul(KT, self.x, L, F, S, p_full.numpy().T, rows=self.rows)
+        out = orc.khat_matmul(KT, self.x, self.l, self.f, self.s, p_full.numpy().T, rows=self.rows)
         return torch.from_numpy(np.ascontiguousarray(out.T))
 
     def grads_rows(self, v_full):
         b = v_full.numpy().T
-        dl = orc.khat_matmul(KT, self.x, L, F, S, b, theta="l", rows=self.rows)
-        df = orc.khat_matmul(KT, self.x, L, F, S, b, theta="f", rows=self.rows)
+        dl = orc.khat_matmul(KT, self.x, self.l, self.f, self.s, b, theta="l", rows=self.rows)
+        df = orc.khat_matmul(KT, self.x, self.l, self.f, self.s, b, theta="f", rows=self.rows)
         return torch.from_numpy(np.ascontiguousarray(dl.T)), torch.from_numpy(np.ascontiguousarray(df.T))
 
     def project(self, r_loc):
@@ -53,7 +54,7 @@ class OracleRowOps:
         return torch.from_numpy(np.ascontiguousarray(out.T))
 
     def cross_rows(self, xs, alpha_loc):
-        kx = F * F * orc.eval_kernel(KT, np.asarray(xs), self.x[self.r0:self.r1], L)
+        kx = self.f * self.f * orc.eval_kernel(KT, np.asarray(xs), self.x[self.r0:self.r1], self.l)
         return torch.from_numpy(np.ascontiguousarray((kx @ alpha_loc.numpy().T).T))
 
     def slq(self, alphas, betas, iters, norms_sq):
@@ -224,4 +225,50 @@ def _gpc_worker(rank, world, port, errfile):
 def test_row_partitioned_gpc_and_predict_gloo(tmp_path, world):
     errfile = str(tmp_path / "err.txt")
     mp.spawn(_gpc_worker, args=(world, _free_port(), errfile), nprocs=world, join=True)
+    assert not os.path.exists(errfile), open(errfile).read()
+
+
+def _fit_worker(rank, world, port, errfile):
+    """dist_fit: the distributed Adam trajectory equals a single-process loop over the oracle."""
+    try:
+        from paper_2503_02259_b200 import gp
+        from paper_2503_02259_b200.kmat import Hyperparams
+        from paper_2503_02259_b200.train import Adam, RawParams, TrainConfig, chain_grads
+
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        x, y, _ = _problem(n=160)
+        n, m = len(y), 20
+        cfg = TrainConfig(learning_rate=0.05, max_steps=3, mode="iterative", k_z=4, tol=1e-10, probe_tol=1e-10,
+                          max_iter=2000, rng_seed=2)
+        hp0 = Hyperparams(0.6, 1.0, 0.05)
+        comm = kdist.Comm(n)
+        r0, r1 = kdist.row_range(n, world, rank)
+
+        def make_ops(hp):
+            ny = orc.Nystrom(KT, x, hp.l, hp.f, hp.s, m)
+            return OracleRowOps(x, r0, r1, ny, (hp.l, hp.f, hp.s)), hp.s
+
+        res = kdist.dist_fit(comm, torch.from_numpy(y[r0:r1].copy()), cfg, hp0, make_ops)
+        raw, opt, hist = RawParams.from_hyperparams(hp0), Adam(cfg.learning_rate), []
+        for step in range(cfg.max_steps):
+            hp = raw.to_hyperparams()
+            z = gp.ProbeSet.generate(n, cfg.k_z, (cfg.rng_seed, step)).vectors
+            ref = orc.nlml_grad(KT, x, y, hp.l, hp.f, hp.s, z, orc.Nystrom(KT, x, hp.l, hp.f, hp.s, m), tol=1e-10,
+                                max_iter=2000)
+            hist.append(ref[0])
+            raw = RawParams.from_array(opt.step(raw.as_array(), chain_grads(raw, ref[1:4])))
+        np.testing.assert_allclose(res.loss_history, hist, rtol=1e-8)
+        np.testing.assert_allclose(res.raw.as_array(), raw.as_array(), rtol=1e-6)
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as exc:
+        with open(errfile, "a") as fh:
+            fh.write(f"rank {rank}: {type(exc).__name__}: {exc}\n")
+        raise
+
+
+def test_row_partitioned_fit_gloo(tmp_path):
+    errfile = str(tmp_path / "err.txt")
+    mp.spawn(_fit_worker, args=(2, _free_port(), errfile), nprocs=2, join=True)
     assert not os.path.exists(errfile), open(errfile).read()

@@ -495,6 +495,57 @@ def test_row_partitioned_gpc_and_predict_on_device(pkg, tmp_path):
     assert not os.path.exists(errfile), open(errfile).read()
 
 
+def _dist_fit_gpu_worker(rank, world, port, errfile):
+    import os
+
+    import torch
+    import torch.distributed as tdist
+
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        tdist.init_process_group("gloo", rank=rank, world_size=world)  # host collectives: one GPU is safe
+        torch.cuda.set_device(0)
+        import paper_2503_02259_b200 as kgp
+        from paper_2503_02259_b200 import dist as kdist
+        from paper_2503_02259_b200 import train
+
+        rng = np.random.default_rng(11)
+        n = 500
+        x = rng.uniform(0, 1, (n, 2))
+        y = np.sin(4 * x[:, 0]) + 0.1 * rng.standard_normal(n)
+        cfg = train.TrainConfig(learning_rate=0.05, max_steps=3, mode="iterative", k_z=6, tol=1e-10,
+                                probe_tol=1e-10, max_iter=3000, precond_rank=40, rng_seed=4, precision="fp64")
+        comm = kdist.Comm(n)
+        r0, r1 = kdist.row_range(n, world, rank)
+        hp0 = train.initial_hyperparams(x, y, cfg.rng_seed)
+        res = kdist.dist_fit(comm, torch.from_numpy(y[r0:r1].copy()).cuda(), cfg, hp0,
+                             kdist.cuda_ops_factory(kgp.KernelType.MATERN52, x, comm, 40, "fp64"))
+        single = train.fit(kgp.KernelType.MATERN52, x, y, cfg)
+        np.testing.assert_allclose(res.loss_history, single.loss_history, rtol=1e-8)
+        np.testing.assert_allclose(res.raw.as_array(), single.raw.as_array(), rtol=1e-6)
+        tdist.barrier()
+        tdist.destroy_process_group()
+    except Exception as exc:
+        with open(errfile, "a") as fh:
+            fh.write(f"rank {rank}: {type(exc).__name__}: {exc}\n")
+        raise
+
+
+def test_row_partitioned_fit_on_device(pkg, tmp_path):
+    """dist.dist_fit over dist.CudaRowOps (2 ranks on one GPU) follows train.fit's trajectory."""
+    import os
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    errfile = str(tmp_path / "err.txt")
+    mp.spawn(_dist_fit_gpu_worker, args=(2, port, errfile), nprocs=2, join=True)
+    assert not os.path.exists(errfile), open(errfile).read()
+
+
 def test_predict_hutchinson_variance(pkg):
     """configs[4]'s estimator (no reference oracle): the mean equals the exact posterior mean,
     the Hutchinson variance is unbiased -- within 5 sigma of the exact diagonal, sigma from the
