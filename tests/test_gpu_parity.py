@@ -750,3 +750,31 @@ def test_grouped_pcg_narrow_tail(pkg, precision):
     assert rel_max(al[0].cpu().numpy(), w[1][0].cpu().numpy()) <= tol
     assert rel_max(xo[1:].cpu().numpy(), z[0].cpu().numpy()) <= tol
     assert rel_max(al[1:, :it2].cpu().numpy(), z[1].cpu().numpy()) <= tol
+
+
+@pytest.mark.parametrize("precision", ["fast", "fp64"])
+def test_operator_workspace_linear_in_n(pkg, precision):
+    """The on-the-fly operator never stores a kernel panel: its device workspace grows like
+    n (k + d), not n^2 (the reference's scratch bound, test_kmat.py:157-182)."""
+    import torch
+
+    from paper_2503_02259_b200 import _lib
+
+    used = []
+    for n in (32768, 65536):
+        torch.cuda.synchronize()
+        free0 = torch.cuda.mem_get_info()[0]
+        x = np.random.default_rng(n).standard_normal((n, 8))
+        e = pkg.KernelEngine(pkg.KernelType.GAUSSIAN, x, _hp(pkg, 1.0, 1.0, 1e-2), precision=precision,
+                             mode=pkg.EngineMode.ON_THE_FLY)
+        z = torch.randn((33, n), dtype=torch.float64, device="cuda")
+        o = torch.empty_like(z)
+        _lib.call("kgp_engine_matmul", e.handle, 33, z.data_ptr(), 1, n, o.data_ptr(), None, None, 1, n,
+                  torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        used.append(free0 - torch.cuda.mem_get_info()[0])
+        e.close()
+        del z, o
+    n2 = 65536
+    assert used[1] <= 64 * n2 * (33 + 8) * 8 + (64 << 20), used  # far below one n x n panel (34 GB)
+    assert used[1] <= 2.5 * used[0] + (32 << 20), used
