@@ -137,7 +137,6 @@ static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t 
                      int64_t o_cs, cudaStream_t st, bool skip_prep = false) {
   const int split = (e->precision == KGP_FAST) ? 3 : 1;
   const int nout = out_dl ? 2 : 1;
-  const int tpo = split == 3 ? 2 : 1;
   const int nblk = (int)((e->n + 31) / 32);
   // two accumulator buffers when the RHS block fits, else one (the drain then briefly
   // stalls the MMA every `flush` blocks, still far cheaper than a second pass)
@@ -147,12 +146,13 @@ static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t 
   for (int64_t c0 = 0; c0 < k; c0 += kmax) {
     const int kc = (int)((k - c0) < kmax ? (k - c0) : kmax);
     const int kp = (kc + 15) / 16 * 16;
-    const int nab = kp <= kmax2 ? 2 : 1;
+    const bool lb = tc_lb_ok(e->dpad, nout, split, kp);
+    const int nab = lb ? (kp <= 32 ? 2 : 1) : (kp <= kmax2 ? 2 : 1);
     int rc = KGP_OK;
     if (!(skip_prep && kc == k)) {
-      rc = e->bsplit.ensure((size_t)nblk * tpo * kp * 128);
+      rc = e->bsplit.ensure((size_t)nblk * tc_rhs_block_bytes(split, lb, kp));
       if (rc) return rc;
-      rc = prep_rhs(split, e->n, k, c0, kp, b, b_rs, b_cs, e->bsplit.as<uint8_t>(), st);
+      rc = prep_rhs(split, lb ? 1 : 0, e->n, k, c0, kp, b, b_rs, b_cs, e->bsplit.as<uint8_t>(), st);
       if (rc) return rc;
     }
     TcParams p{};
@@ -165,6 +165,7 @@ static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t 
     p.k = kc;
     p.nsa = tc_nsa(e->dpad, nout, split, kp);
     p.nab = nab;
+    p.lb = lb ? 1 : 0;
     const int nsplit = tc_col_split(nrows, nblk, tc_env_int("KGP_TC_MAXSPLIT", 16));
     p.nper = (nblk + nsplit - 1) / nsplit;
     p.part = nullptr;

@@ -145,6 +145,24 @@ KGP_DEV void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint
       : "memory");
 }
 
+// D[tmem] (+)= A[tmem] * B[smem desc], kind::f16 (bf16 inputs per idesc), cta_group::1.
+// A in TMEM packs two 16-bit K elements per 32-bit column (lower K index in the low half).
+KGP_DEV void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+// 32 lanes x 32 bit, 8 consecutive columns.
+KGP_DEV void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+               "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
+
 // 32 lanes x 32 bit, 16 consecutive columns: thread t <-> lane (quadrant base + t).
 KGP_DEV void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
   asm volatile(
@@ -257,6 +275,21 @@ __host__ __device__ constexpr uint32_t idesc_tf32_m128(int n) {
          | (2u << 10)                    // B format TF32
          | ((uint32_t)(n >> 3) << 17)    // N >> 3
          | ((uint32_t)(128 >> 4) << 24); // M >> 4
+}
+
+// Instruction descriptor, kind::f16: D=F32, A=B=BF16, both K-major, M=128, N=n.
+__host__ __device__ constexpr uint32_t idesc_bf16_m128(int n) {
+  return (1u << 4)                       // D format F32
+         | (1u << 7)                     // A format BF16
+         | (1u << 10)                    // B format BF16
+         | ((uint32_t)(n >> 3) << 17)    // N >> 3
+         | ((uint32_t)(128 >> 4) << 24); // M >> 4
+}
+
+// Byte offset of element (row r, k) in a K-major no-swizzle 16-bit tile with `rows` rows
+// (core matrices of 8 rows x 8 elements, K chunks `rows` x 16 B apart).
+__host__ __device__ inline uint32_t interleave16_offset(uint32_t r, uint32_t k, uint32_t rows) {
+  return (k >> 3) * (rows * 16u) + (r >> 3) * 128u + (r & 7u) * 16u + (k & 7u) * 2u;
 }
 
 // Byte offset of element (row r, k-index j) of a K-major fp32 tile whose rows are

@@ -32,6 +32,8 @@
 // The drain warps finally apply f^2, 2f, s*B and the derivative scale in fp64 (or write
 // fp32 partials when the column sweep is split over grid.y; tc_reduce_kernel finishes).
 #include <cuda.h>
+#include <cuda_bf16.h>
+#include <stdlib.h>
 
 #include "kgp_common.cuh"
 #include "kgp_internal.h"
@@ -151,6 +153,23 @@ KGP_DEV void store_row16(uint32_t taddr, const float2 (&v)[8]) {
   }
 }
 
+// LB layout: 16 columns of one row as tf32 hi (truncated, 16 TMEM columns at taddr)
+// and the lo parts as 8 bf16 pairs (8 columns at the output's lo base + 8 per half)
+KGP_DEV void store_row16_lb(uint32_t taddr, uint32_t laddr, const float2 (&v)[8]) {
+  uint32_t w[16], wl[8];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    const float2 h = hi2(v[m]);  // truncation: one LOP per value (cvt.rna costs four)
+    w[2 * m] = __float_as_uint(h.x);
+    w[2 * m + 1] = __float_as_uint(h.y);
+    const float2 lo = fsub2(v[m], h);
+    const __nv_bfloat162 b = __floats2bfloat162_rn(lo.x, lo.y);  // .x (lower K) in the low half
+    wl[m] = *reinterpret_cast<const uint32_t*>(&b);
+  }
+  tmem_st16(taddr, w);
+  tmem_st8(laddr, wl);
+}
+
 // Compute-warp TMEM layout: 32x32b (thread = row, 16 columns per op) or 16x256b (thread =
 // 4 rows x 8 columns). Measured at cfg2 shape: 32x32b is 8.5% faster for the fused
 // two-output 3xTF32 product, 16x256b 1-2% faster for the others (and clearly faster for
@@ -171,10 +190,21 @@ struct Geo {
   static constexpr uint32_t UBYTES = 0u;  // U' lives in TMEM
 };
 
-template <int KT, int D, int NOUT, int SPLIT>
+// LB layout (fused two-output 3xTF32, tensor-core distance): each output's A tile is its tf32
+// hi part (32 TMEM columns) plus its lo part packed as bf16 pairs (16 columns); the
+// corrections are hi*B_lo (tf32) and lo*bf16(B) (kind::f16, K=16), so an A stage takes 96
+// columns instead of 128 and TMEM holds three of them. Error terms: |lo| < 2^-10 |A|
+// (truncated hi), bf16 rounding 2^-9 of lo and of B -> 2^-18 |A||B| per product.
+template <int KT, int D, int NOUT, int SPLIT, bool LB>
 __global__ void __launch_bounds__(nthreads_for(ns_for(NOUT, SPLIT)), 1) kmm_tc_kernel(const TcParams p) {
   constexpr int NS = ns_for(NOUT, SPLIT);
-  constexpr int NSET = NS, ND = NS, NSA = NS;   // sets, distance buffers, A stages
+  // sets, distance buffers, A stages. LB: a third A stage written alternately by the two
+  // sets (a stage is rewritten only after the MMAs of the block three back have read it, so
+  // a parity wait is never two phases behind)
+#ifndef KGP_TC_LBNSA
+#define KGP_TC_LBNSA 3
+#endif
+  constexpr int NSET = NS, ND = NS, NSA = LB ? KGP_TC_LBNSA : NS;
   constexpr int NCW = NS * WPS;                 // compute warps
   constexpr int WPROD = NCW, WMMA = NCW + 1, WDIST = NCW + 2;
   static_assert(NS <= MAXNS, "ring slots");
@@ -185,6 +215,9 @@ __global__ void __launch_bounds__(nthreads_for(ns_for(NOUT, SPLIT)), 1) kmm_tc_k
   constexpr int KDS = (KD + 15) / 16 * 16;  // TMEM column stride of U' hi -> lo
   constexpr int TPO = (SPLIT == 3) ? 2 : 1;  // TMEM tiles per output (hi, lo)
   constexpr int ATILES = NOUT * TPO;
+  constexpr int OCOLS = LB ? 48 : TPO * 32;         // TMEM columns per output in an A stage
+  constexpr int ASTAGE = NOUT * OCOLS;
+  static_assert(!LB || (NOUT == 2 && SPLIT == 3), "LB layout: fused two-output 3xTF32");
   constexpr uint32_t VBYTES = G::VBYTES;
   constexpr bool NEED_G = (NOUT == 2);
 
@@ -193,7 +226,7 @@ __global__ void __launch_bounds__(nthreads_for(ns_for(NOUT, SPLIT)), 1) kmm_tc_k
   const int NSB = p.nsb;                           // 4 or 8
   const int nsb_log = (NSB == 8) ? 3 : 2;
   const int NACC = NOUT * KP;                      // accumulator columns per buffer
-  const uint32_t BBYTES = (uint32_t)(TPO * KP * 128);
+  const uint32_t BBYTES = (uint32_t)((TPO * 128 + (LB ? 64 : 0)) * KP);  // tf32 hi | lo (| bf16)
   uint8_t* sB = smem;                              // NSB x BBYTES, 1024-aligned
   uint8_t* sV = smem + NSB * BBYTES;               // NSB x VBYTES (column data / V' tiles)
   uint8_t* sU = sV + NSB * VBYTES;                 // U' hi/lo (DMMA)
@@ -302,7 +335,26 @@ __global__ void __launch_bounds__(nthreads_for(ns_for(NOUT, SPLIT)), 1) kmm_tc_k
       const uint64_t dhi = sw128_kmajor_desc(bhi);
       const uint64_t dlo = sw128_kmajor_desc(bhi + KP * 128);
       const bool last = (pos + 1 == flush) || (t == nblk - 1);
-      if (elect_one()) {
+      if (LB && elect_one()) {
+        const uint32_t idesc_b = idesc_bf16_m128(KP);
+        const uint32_t bbf = bhi + 2 * KP * 128;  // bf16(B), interleaved K-major
+#pragma unroll
+        for (int o = 0; o < ((p.debug & 1) ? 0 : NOUT); ++o) {
+          const uint32_t dt = tbase + ab * NACC + o * KP;
+          const uint32_t ahi = tbase + abase + a * ASTAGE + o * OCOLS;
+#pragma unroll
+          for (int kk = 0; kk < BJ / 8; ++kk) {
+            mma_tf32_ts(dt, ahi + 8 * kk, dhi + 2 * kk, idesc, (pos > 0 || kk > 0) ? 1u : 0u);
+            mma_tf32_ts(dt, ahi + 8 * kk, dlo + 2 * kk, idesc, 1u);
+          }
+#pragma unroll
+          for (int k2 = 0; k2 < ((p.debug & 8) ? 0 : BJ / 16); ++k2)
+            mma_f16_ts(dt, ahi + 32 + 8 * k2, interleave_kmajor_desc(bbf + k2 * 2 * KP * 16, KP * 16, 128), idesc_b, 1u);
+        }
+        tc_commit(&empty[s]);
+        tc_commit(&aempty[a]);
+        if (last) tc_commit(&accfull[ab]);
+      } else if (!LB && elect_one()) {
 #pragma unroll
         for (int o = 0; o < ((p.debug & 1) ? 0 : NOUT); ++o) {
           const uint32_t dt = tbase + ab * NACC + o * KP;
@@ -402,7 +454,7 @@ __global__ void __launch_bounds__(nthreads_for(ns_for(NOUT, SPLIT)), 1) kmm_tc_k
         if (lane == 0) mbar_arrive(&dempty[db]);
         mbar_wait(&aempty[a], ph_a ^ 1);
         tc_fence_after();
-        const uint32_t tcol = lane_base + abase + a * ATILES * 32;
+        const uint32_t tcol = lane_base + abase + a * ASTAGE;
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
           float2 kv[8], gv[8];
@@ -416,8 +468,13 @@ __global__ void __launch_bounds__(nthreads_for(ns_for(NOUT, SPLIT)), 1) kmm_tc_k
               transform2<KT, NEED_G>(t2, kv[m], gv[m]);
             }
           }
-          store_row16<SPLIT>(tcol + 16 * half, kv);
-          if (NEED_G) store_row16<SPLIT>(tcol + TPO * 32 + 16 * half, gv);
+          if (LB) {
+            store_row16_lb(tcol + 16 * half, tcol + 32 + 8 * half, kv);
+            store_row16_lb(tcol + OCOLS + 16 * half, tcol + OCOLS + 32 + 8 * half, gv);
+          } else {
+            store_row16<SPLIT>(tcol + 16 * half, kv);
+            if (NEED_G) store_row16<SPLIT>(tcol + TPO * 32 + 16 * half, gv);
+          }
         }
         tc_wait_st();
         tc_fence_before();
@@ -591,12 +648,11 @@ __global__ void tc_reduce_kernel(const TcParams p, int nsplit, int nacc) {
   if (nacc > p.kp && p.out_dl) p.out_dl[o] = p.scale_dl * ag;
 }
 
-template <int KT, int D, int NOUT, int SPLIT>
+template <int KT, int D, int NOUT, int SPLIT, bool LB>
 int launch_one(const TcParams& p_in, cudaStream_t st) {
-  auto kern = kmm_tc_kernel<KT, D, NOUT, SPLIT>;
-  const int TPO = (SPLIT == 3) ? 2 : 1;
+  auto kern = kmm_tc_kernel<KT, D, NOUT, SPLIT, LB>;
   TcParams p = p_in;
-  const size_t stage = (size_t)(TPO * p.kp * 128) + Geo<D>::VBYTES;
+  const size_t stage = (size_t)tc_rhs_block_bytes(SPLIT, LB, p.kp) + Geo<D>::VBYTES;
   const size_t fixed = Geo<D>::UBYTES + (size_t)NOUT * p.kp * 128 * 4 + 512;
   const size_t limit = 225 * 1024;
   p.nsb = (fixed + 8 * stage <= limit) ? 8 : 4;  // deeper prefetch when shared memory allows
@@ -623,8 +679,12 @@ int launch_one(const TcParams& p_in, cudaStream_t st) {
 
 template <int KT, int D>
 int launch_kt_d(const TcParams& p, int nout, int split, cudaStream_t st) {
-  if (nout == 1) return split == 3 ? launch_one<KT, D, 1, 3>(p, st) : launch_one<KT, D, 1, 1>(p, st);
-  return split == 3 ? launch_one<KT, D, 2, 3>(p, st) : launch_one<KT, D, 2, 1>(p, st);
+  if (nout == 1) return split == 3 ? launch_one<KT, D, 1, 3, false>(p, st) : launch_one<KT, D, 1, 1, false>(p, st);
+  if (split != 3) return launch_one<KT, D, 2, 1, false>(p, st);
+  if constexpr (Geo<D>::DMMA && D == 8) {
+    if (p.lb) return launch_one<KT, D, 2, 3, true>(p, st);
+  }
+  return launch_one<KT, D, 2, 3, false>(p, st);
 }
 
 template <int KT>
@@ -674,6 +734,25 @@ int tc_max_kp(int dpad, int nout, int split, int nab) {
 }
 
 int tc_nsa(int, int nout, int split, int) { return ns_for(nout, split); }
+
+// LB layout for the fused two-output 3xTF32 product with the tensor-core distance at
+// dpad = 8 (U' takes 2 x 16 columns): TMEM holds nab x 2 x kp accumulators (nab kp <= 64),
+// two distance buffers, U' and three 96-column A stages: 2 nab kp + 64 + 32 + 288 <= 512.
+// Used for 32 < kp <= 64 (one accumulator buffer), where it measured faster (n = 65536,
+// k = 64: 5.83 -> 5.24 ms); at kp <= 32 it ties (k = 32: 3.40 ms both) or loses (k = 16:
+// 3.05 -> 3.24 ms), so the all-tf32 two-stage layout stays there. Env KGP_TC_LB=0 disables
+// it, KGP_TC_LB=2 forces it for every kp <= 64.
+bool tc_lb_ok(int dpad, int nout, int split, int kp) {
+  static const int env = [] {
+    const char* s = getenv("KGP_TC_LB");
+    return s ? atoi(s) : 1;
+  }();
+  return env != 0 && tc_dist_mode(dpad) == 1 && dpad == 8 && nout == 2 && split == 3 && kp <= 64 &&
+         (kp > 32 || env == 2);
+}
+
+// bytes of one 32-row RHS block in bsplit: tf32 hi (| lo) K-major 128B-swizzled (| bf16 interleaved)
+int tc_rhs_block_bytes(int split, bool lb, int kp) { return ((split == 3 ? 2 : 1) * 128 + (lb ? 64 : 0)) * kp; }
 
 // Column split factor that fills the last wave of 148 SMs (1 CTA/SM): the smallest
 // S <= maxsplit reaching 95% wave efficiency with >= 16 column blocks per CTA.

@@ -1,3 +1,4 @@
+#include <cuda_bf16.h>
 // Operand preparation for the tcgen05 operator (O(n (d + k)) work per call).
 //
 // Point data are mean-centred in fp64 and then rounded to fp32 (SURVEY.md §7,
@@ -96,7 +97,7 @@ __device__ inline uint32_t tf32_rna_bits(float v) {
   return r;
 }
 
-__global__ void prep_rhs_kernel(int split, int64_t n, int64_t k, int64_t c0, int kp, int nblk,
+__global__ void prep_rhs_kernel(int split, int lb, int64_t n, int64_t k, int64_t c0, int kp, int nblk,
                                 const double* __restrict__ b, int64_t b_rs, int64_t b_cs, uint8_t* __restrict__ out) {
   // one thread per (block t, rhs column c, in-block row jj); jj fastest for coalesced column-major reads
   int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -109,7 +110,7 @@ __global__ void prep_rhs_kernel(int split, int64_t n, int64_t k, int64_t c0, int
   const int64_t cc = c0 + c;
   double v = (j < n && cc < k) ? b[j * b_rs + cc * b_cs] : 0.0;
   const int tpo = (split == 3) ? 2 : 1;
-  uint8_t* tile = out + t * (int64_t)tpo * kp * 128;
+  uint8_t* tile = out + t * (int64_t)(tpo * 128 + (lb ? 64 : 0)) * kp;
   const uint32_t off = sw128_offset((uint32_t)c, (uint32_t)jj);
   float vf = (float)v;
   if (split == 3) {
@@ -117,6 +118,8 @@ __global__ void prep_rhs_kernel(int split, int64_t n, int64_t k, int64_t c0, int
     float lo = vf - __uint_as_float(hi);
     *reinterpret_cast<uint32_t*>(tile + off) = hi;
     *reinterpret_cast<float*>(tile + kp * 128 + off) = lo;
+    // lb: + bf16(B) in the interleaved K-major layout (B operand of the bf16 lo*hi correction)
+    if (lb) *reinterpret_cast<__nv_bfloat16*>(tile + 2 * kp * 128 + interleave16_offset((uint32_t)c, (uint32_t)jj, (uint32_t)kp)) = __float2bfloat16_rn(vf);
   } else {
     *reinterpret_cast<uint32_t*>(tile + off) = tf32_rna_bits(vf);
   }
@@ -149,11 +152,11 @@ int prep_cols(int kt, int d, int dpad, int64_t n, const double* x, const double*
   return KGP_OK;
 }
 
-int prep_rhs(int split, int64_t n, int64_t k, int64_t c0, int kp, const double* b, int64_t b_rs, int64_t b_cs,
+int prep_rhs(int split, int lb, int64_t n, int64_t k, int64_t c0, int kp, const double* b, int64_t b_rs, int64_t b_cs,
              uint8_t* out, cudaStream_t st) {
   int nblk = (int)((n + 31) / 32);
   int64_t total = (int64_t)nblk * kp * 32;
-  prep_rhs_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(split, n, k, c0, kp, nblk, b, b_rs, b_cs, out);
+  prep_rhs_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(split, lb, n, k, c0, kp, nblk, b, b_rs, b_cs, out);
   KGP_LAUNCH("prep_rhs_kernel");
   return KGP_OK;
 }
