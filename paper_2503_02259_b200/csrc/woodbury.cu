@@ -7,10 +7,57 @@
 // two tall-skinny fp64 GEMMs per application and no triangular solve in the
 // PCG loop. Both GEMMs run on one tiled fp64 kernel (64x64 tiles, split-K with
 // a fixed-order partial reduction so results are run-to-run deterministic).
+#include <cublas_v2.h>
+#include <stdlib.h>
+
+#include <map>
+
 #include "kgp_common.cuh"
 #include "kgp_internal.h"
 
 namespace kgp {
+
+// One cuBLAS handle per (host thread, device): a handle must not be used by two threads at
+// once, and the callers are stream-ordered on the stream passed in.
+static int cublas_for_device(cublasHandle_t* out) {
+  thread_local std::map<int, cublasHandle_t> handles;
+  int dev = 0;
+  KGP_CUDA(cudaGetDevice(&dev));
+  auto it = handles.find(dev);
+  if (it == handles.end()) {
+    cublasHandle_t h;
+    KGP_REQUIRE(cublasCreate(&h) == CUBLAS_STATUS_SUCCESS, KGP_ERR_CUDA, "cublasCreate failed");
+    it = handles.emplace(dev, h).first;
+  }
+  *out = it->second;
+  return KGP_OK;
+}
+
+// C = alpha op(A) op(B) + beta SRC through cublasDgemm when every operand has a unit stride
+// along one index and C is column-major (c_is == 1). Returns 1 when the layout does not fit.
+static int gemm_f64_cublas(int64_t M, int64_t N, int64_t K, const double* a, int64_t a_is, int64_t a_ks,
+                           const double* b, int64_t b_ks, int64_t b_ns, double* c, int64_t c_ns, double alpha,
+                           double beta, const double* src, int64_t s_is, int64_t s_ns, cudaStream_t st) {
+  const bool a_n = (a_is == 1), a_t = (a_ks == 1);
+  const bool b_n = (b_ks == 1), b_t = (b_ns == 1);
+  if (!(a_n || a_t) || !(b_n || b_t) || M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return 1;
+  if (beta != 0.0 && src != c) {
+    if (src == nullptr || s_is != 1) return 1;
+    KGP_CUDA(cudaMemcpy2DAsync(c, sizeof(double) * c_ns, src, sizeof(double) * s_ns, sizeof(double) * M, N,
+                               cudaMemcpyDeviceToDevice, st));
+  }
+  cublasHandle_t h;
+  int rc = cublas_for_device(&h);
+  if (rc) return rc;
+  KGP_REQUIRE(cublasSetStream(h, st) == CUBLAS_STATUS_SUCCESS, KGP_ERR_CUDA, "cublasSetStream failed");
+  const cublasStatus_t cs =
+      cublasDgemm(h, a_n ? CUBLAS_OP_N : CUBLAS_OP_T, b_n ? CUBLAS_OP_N : CUBLAS_OP_T, (int)M, (int)N, (int)K, &alpha, a,
+                  (int)(a_n ? (a_ks > 1 ? a_ks : M) : (a_is > 1 ? a_is : K)), b,
+                  (int)(b_n ? (b_ns > 1 ? b_ns : K) : (b_ks > 1 ? b_ks : N)), &beta, c, (int)(c_ns > 1 ? c_ns : M));
+  KGP_REQUIRE(cs == CUBLAS_STATUS_SUCCESS, KGP_ERR_CUDA, "cublasDgemm failed (%d)", (int)cs);
+  count_launches(1);
+  return KGP_OK;
+}
 
 namespace {
 
@@ -331,6 +378,16 @@ int gemm_f64(int64_t M, int64_t N, int64_t K, const double* a, int64_t a_is, int
   if (M <= 0 || N <= 0) return KGP_OK;
   if (N <= SK_MAXN && (a_ks == 1 || a_is == 1))
     return skinny_gemm(M, N, K, a, a_is, a_ks, b, b_ks, b_ns, c, c_is, c_ns, alpha, beta, src, s_is, s_ns, tmp, st);
+  // wider right-hand-side blocks: cuBLAS DGEMM (a plain library GEMM, DMMA; the tiled SIMT
+  // kernel below stays for layouts it cannot express). Env KGP_GEMM_CUBLAS=0 disables it.
+  static const bool use_cublas = [] {
+    const char* e = getenv("KGP_GEMM_CUBLAS");
+    return !(e && atoi(e) == 0);
+  }();
+  if (use_cublas && c_is == 1) {
+    const int rc = gemm_f64_cublas(M, N, K, a, a_is, a_ks, b, b_ks, b_ns, c, c_ns, alpha, beta, src, s_is, s_ns, st);
+    if (rc != 1) return rc;
+  }
   const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   int64_t nz = 1;
   if (tiles < 148 && K > 4096) {  // too few output tiles to fill the SMs: split K, fixed-order reduction
