@@ -24,6 +24,8 @@
 
 #include <vector>
 
+#include <stdlib.h>
+
 #include "kgp_common.cuh"
 #include "kgp_internal.h"
 
@@ -263,6 +265,71 @@ __global__ void scatter_rows_kernel(int64_t n, int64_t m, const int64_t* __restr
   }
 }
 
+// ---- point-major variants (k > 8 right-hand sides): every block stored (rows x k) with the
+// k values of a point contiguous, so the sparse products gather whole 8k-byte rows (one
+// coalesced read per neighbour instead of k scattered ones) and the dense products are the
+// transposed GEMMs (cuBLAS, column-major k x rows).
+constexpr int PM_T = 32;  // transpose tile (rows x columns)
+
+// bp[r * k + c] = b[perm[r] * b_rs + c * b_cs]   (tile transpose through shared memory)
+__global__ void pm_gather_kernel(int64_t n, int64_t k, const int64_t* __restrict__ perm, const double* __restrict__ b,
+                                 int64_t b_rs, int64_t b_cs, double* __restrict__ bp) {
+  __shared__ double tile[PM_T][PM_T + 1];
+  const int64_t r0 = (int64_t)blockIdx.x * PM_T, c0 = (int64_t)blockIdx.y * PM_T;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int64_t r = r0 + tx;
+  const int64_t pr = r < n ? perm[r] : 0;
+  for (int cc = ty; cc < PM_T; cc += blockDim.y)
+    if (r < n && c0 + cc < k) tile[cc][tx] = b[pr * b_rs + (c0 + cc) * b_cs];
+  __syncthreads();
+  for (int rr = ty; rr < PM_T; rr += blockDim.y)
+    if (r0 + rr < n && c0 + tx < k) bp[(r0 + rr) * k + c0 + tx] = tile[tx][rr];
+}
+
+// out[perm[r] * o_rs + c * o_cs] = r < m ? o1[r * k + c] : u2[(r - m) * k + c]
+__global__ void pm_scatter_kernel(int64_t n, int64_t m, int64_t k, const int64_t* __restrict__ perm,
+                                  const double* __restrict__ o1, const double* __restrict__ u2,
+                                  double* __restrict__ out, int64_t o_rs, int64_t o_cs) {
+  __shared__ double tile[PM_T][PM_T + 1];
+  const int64_t r0 = (int64_t)blockIdx.x * PM_T, c0 = (int64_t)blockIdx.y * PM_T;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int rr = ty; rr < PM_T; rr += blockDim.y) {
+    const int64_t r = r0 + rr;
+    if (r < n && c0 + tx < k) tile[tx][rr] = r < m ? o1[r * k + c0 + tx] : u2[(r - m) * k + c0 + tx];
+  }
+  __syncthreads();
+  const int64_t r = r0 + tx;
+  if (r >= n) return;
+  const int64_t pr = perm[r];
+  for (int cc = ty; cc < PM_T; cc += blockDim.y)
+    if (c0 + cc < k) out[pr * o_rs + (c0 + cc) * o_cs] = tile[cc][tx];
+}
+
+// y[i * k + c] = sum_t G[i, t] x[col(i, t) * k + c]   (ELL, slot-major; thread = (i, c))
+__global__ void pm_ell_kernel(int64_t n2, int64_t k, int npt1, const double* __restrict__ gval,
+                              const int32_t* __restrict__ gcol, const double* __restrict__ x, double* __restrict__ y) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n2 * k) return;
+  const int64_t i = e / k, c = e - i * k;
+  double v = 0.0;
+  for (int t = 0; t < npt1; ++t) {
+    const int32_t j = gcol[(int64_t)t * n2 + i];
+    if (j >= 0) v = fma(gval[(int64_t)t * n2 + i], x[(int64_t)j * k + c], v);
+  }
+  y[e] = v;
+}
+
+// u[j * k + c] = sum over rows i of column j of G: G[i, j] v[i * k + c]   (CSR of G^T, rows ascending)
+__global__ void pm_csr_kernel(int64_t n2, int64_t k, const int32_t* __restrict__ ptr, const int32_t* __restrict__ row,
+                              const double* __restrict__ val, const double* __restrict__ v, double* __restrict__ u) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n2 * k) return;
+  const int64_t j = e / k, c = e - j * k;
+  double a = 0.0;
+  for (int32_t q = ptr[j]; q < ptr[j + 1]; ++q) a = fma(val[q], v[(int64_t)row[q] * k + c], a);
+  u[e] = a;
+}
+
 // ------------------------------------------------------------------ sampling z ~ N(0, M)
 // level relaxation for the forward substitution G x = b: level(i) = 1 + max level of the
 // earlier neighbours; Jacobi sweeps converge in (depth) sweeps (values only increase)
@@ -294,14 +361,28 @@ __global__ void afn_level_solve_kernel(const int32_t* __restrict__ rows, int cnt
   const int64_t i = rows[e];
   const double* xc = x + (int64_t)c * n2;
   double acc = b[(int64_t)c * n2 + i], diag = 1.0;
-  for (int t = 0; t < npt1; ++t) {
-    const int32_t j = gcol[(int64_t)t * n2 + i];
-    if (j < 0) continue;
-    const double v = gval[(int64_t)t * n2 + i];
-    if (j == i)
-      diag = v;
-    else
-      acc = fma(-v, xc[j], acc);
+  // eight slots at a time: their index/value loads, then their x gathers, are issued
+  // together (the one-slot loop was a chain of dependent load pairs: ~29 us per level at
+  // n2 = 64512); accumulation order stays t ascending
+  for (int t0 = 0; t0 < npt1; t0 += 8) {
+    int32_t j[8];
+    double g[8], xv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int t = t0 + u;
+      j[u] = t < npt1 ? gcol[(int64_t)t * n2 + i] : -1;
+      g[u] = t < npt1 ? gval[(int64_t)t * n2 + i] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) xv[u] = (j[u] >= 0 && j[u] != i) ? xc[j[u]] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (j[u] < 0) continue;
+      if (j[u] == i)
+        diag = g[u];
+      else
+        acc = fma(-g[u], xv[u], acc);
+    }
   }
   x[(int64_t)c * n2 + i] = acc / diag;
 }
@@ -427,9 +508,58 @@ inline dim3 vec_grid(int64_t n, int64_t k) {
 
 }  // namespace
 
+// M^-1 B for k > 8 right-hand sides in the point-major layout (same algebra as below).
+static int afn_apply_pm(kgp_precond_s* p, int64_t k, const double* b, int64_t b_rs, int64_t b_cs, double* out,
+                        int64_t o_rs, int64_t o_cs, cudaStream_t st) {
+  const int64_t n = p->n, m = p->m, n2 = p->n2;
+  int rc = p->work.ensure(sizeof(double) * (size_t)k * (n + 3 * n2 + 3 * m));
+  if (rc) return rc;
+  double* bp = p->work.as<double>();  // (n x k): rows [0, m) = b1, [m, n) = b2
+  double* y1 = bp + k * n;
+  double* t2 = y1 + k * m;
+  double* v = t2 + k * n2;
+  double* u2 = v + k * n2;
+  double* z1 = u2 + k * n2;
+  double* o1 = z1 + k * m;
+  const int64_t* perm = p->perm.as<int64_t>();
+  const double* linv = p->linv.as<double>();
+  const double* w = p->w.as<double>();
+  const dim3 tgrid((unsigned)((n + PM_T - 1) / PM_T), (unsigned)((k + PM_T - 1) / PM_T));
+  pm_gather_kernel<<<tgrid, dim3(PM_T, 8), 0, st>>>(n, k, perm, b, b_rs, b_cs, bp);
+  KGP_LAUNCH("pm_gather_kernel");
+  // transposed products, C^T (k x rows, column-major) = B^T A^T:
+  // y1 = L^-1 b1
+  rc = gemm_f64(k, m, m, bp, 1, k, linv, 1, m, y1, 1, k, 1.0, 0.0, nullptr, 0, 0, p->tmp, st);
+  if (rc) return rc;
+  // t2 = b2 - W y1
+  rc = gemm_f64(k, n2, m, y1, 1, k, w, 1, m, t2, 1, k, -1.0, 1.0, bp + m * k, 1, k, p->tmp, st);
+  if (rc) return rc;
+  // u2 = G^T (G t2)
+  const unsigned sgrid = (unsigned)((n2 * k + 255) / 256);
+  pm_ell_kernel<<<sgrid, 256, 0, st>>>(n2, k, p->npt1, p->gval.as<double>(), p->gcol.as<int32_t>(), t2, v);
+  KGP_LAUNCH("pm_ell_kernel");
+  pm_csr_kernel<<<sgrid, 256, 0, st>>>(n2, k, p->gtptr.as<int32_t>(), p->gtrow.as<int32_t>(), p->gtval.as<double>(),
+                                       v, u2);
+  KGP_LAUNCH("pm_csr_kernel");
+  // z1 = y1 - W^T u2
+  rc = gemm_f64(k, m, n2, u2, 1, k, w, m, 1, z1, 1, k, -1.0, 1.0, y1, 1, k, p->tmp, st);
+  if (rc) return rc;
+  // o1 = L^-T z1
+  rc = gemm_f64(k, m, m, z1, 1, k, linv, m, 1, o1, 1, k, 1.0, 0.0, nullptr, 0, 0, p->tmp, st);
+  if (rc) return rc;
+  pm_scatter_kernel<<<tgrid, dim3(PM_T, 8), 0, st>>>(n, m, k, perm, o1, u2, out, o_rs, o_cs);
+  KGP_LAUNCH("pm_scatter_kernel");
+  return KGP_OK;
+}
+
 int afn_apply_impl(kgp_precond_s* p, int64_t k, const double* b, int64_t b_rs, int64_t b_cs, double* out,
                    int64_t o_rs, int64_t o_cs, cudaStream_t st) {
   KGP_REQUIRE(k <= 65535, KGP_ERR_INVALID, "too many right-hand sides (%lld)", (long long)k);
+  static const bool pm = [] {
+    const char* e = getenv("KGP_AFN_PM");
+    return !(e && atoi(e) == 0);
+  }();
+  if (pm && k > 8) return afn_apply_pm(p, k, b, b_rs, b_cs, out, o_rs, o_cs, st);
   const int64_t n = p->n, m = p->m, n2 = p->n2;
   // workspace (column-major blocks): bp (n), y1 (m), t2 (n2), v (n2), u2 (n2), z1 (m), o1 (m)
   int rc = p->work.ensure(sizeof(double) * (size_t)k * (n + 3 * n2 + 3 * m));
