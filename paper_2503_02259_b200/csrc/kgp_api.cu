@@ -87,14 +87,17 @@ static int tc_env_int(const char* name, int dflt) {
   return s ? atoi(s) : dflt;
 }
 
-// blocks (x32 columns) accumulated in TMEM before promotion; env KGP_TC_FLUSH overrides
-static int tc_flush_blocks() {
+// blocks (x32 columns) accumulated in TMEM before promotion: 8 with two accumulator buffers
+// (the drain overlaps the MMA), 16 with one (each promotion stalls the MMA: k = 64 two
+// outputs 4.93 -> 4.62 ms; error 2.7e-6 -> 3.9e-6, tools/flush_sweep.py); env KGP_TC_FLUSH
+// overrides both
+static int tc_flush_blocks(int nab) {
   static int v = [] {
     const char* s = getenv("KGP_TC_FLUSH");
-    int f = s ? atoi(s) : 8;
-    return f < 1 ? 1 : f;
+    int f = s ? atoi(s) : 0;
+    return f < 0 ? 0 : f;
   }();
-  return v;
+  return v > 0 ? v : (nab == 1 ? 16 : 8);
 }
 
 static std::mutex g_handles_mu;
@@ -146,8 +149,9 @@ static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t 
   for (int64_t c0 = 0; c0 < k; c0 += kmax) {
     const int kc = (int)((k - c0) < kmax ? (k - c0) : kmax);
     const int kp = (kc + 15) / 16 * 16;
-    const bool lb = tc_lb_ok(e->dpad, nout, split, kp);
-    const int nab = lb ? (kp <= 32 ? 2 : 1) : (kp <= kmax2 ? 2 : 1);
+    const int lbm = tc_lb_mode(e->dpad, nout, split, kp);
+    const bool lb = lbm != 0;
+    const int nab = lb ? tc_lb_nab(lbm, kp) : (kp <= kmax2 ? 2 : 1);
     int rc = KGP_OK;
     if (!(skip_prep && kc == k)) {
       rc = e->bsplit.ensure((size_t)nblk * tc_rhs_block_bytes(split, lb, kp));
@@ -165,7 +169,7 @@ static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t 
     p.k = kc;
     p.nsa = tc_nsa(e->dpad, nout, split, kp);
     p.nab = nab;
-    p.lb = lb ? 1 : 0;
+    p.lb = lbm;
     const int nsplit = tc_col_split(nrows, nblk, tc_env_int("KGP_TC_MAXSPLIT", 16));
     p.nper = (nblk + nsplit - 1) / nsplit;
     p.part = nullptr;
@@ -174,7 +178,7 @@ static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t 
       if (rc) return rc;
       p.part = e->tcpart.as<float>();
     }
-    p.flush = tc_flush_blocks();
+    p.flush = tc_flush_blocks(nab);
     p.debug = tc_env_int("KGP_TC_DEBUG", 0);
     p.f2 = e->f * e->f;
     p.s = e->s;

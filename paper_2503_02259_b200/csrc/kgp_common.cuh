@@ -1,6 +1,7 @@
 // Shared device helpers for libkgp (sm_100a only).
 #pragma once
 #include <cuda_runtime.h>
+#include <cstdio>
 #include <stdint.h>
 
 #include "../../include/kgp.h"
@@ -81,6 +82,27 @@ KGP_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+#ifdef KGP_MBAR_DEBUG
+KGP_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  for (long long it = 0;; ++it) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (it == (1ll << 24)) {
+      printf("mbar hang: block (%d,%d) warp %d lane %d bar+%u parity %u\n", blockIdx.x, blockIdx.y,
+             threadIdx.x >> 5, threadIdx.x & 31, addr & 0x3ff, parity);
+      __trap();
+    }
+  }
+}
+#else
 KGP_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t addr = smem_u32(bar);
   asm volatile(
@@ -91,6 +113,7 @@ KGP_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+#endif
 // 1-D bulk async copy global -> shared, completion signalled on an mbarrier (tx bytes).
 KGP_DEV void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
   asm volatile(

@@ -23,7 +23,7 @@ struct TcParams {
   int nsa;                // TMEM A-stage ring depth
   int nsb;                // shared-memory ring depth (set at launch)
   int nab;                // TMEM accumulator buffers: 2 (drain overlaps the MMA) or 1 (wider kp)
-  int lb;                 // LB layout (tc_lb_ok): A lo parts in bf16, bf16 lo*hi correction, 3 A stages
+  int lb;                 // LB layout (tc_lb_mode): A lo parts in bf16, bf16 lo*hi correction, 3 A stages
   int flush;              // blocks per TMEM accumulation segment before promotion to fp32 smem
   int debug;              // diagnostic bit flags (env KGP_TC_DEBUG): 1 no contraction MMA, 2 no distance MMA, 4 no transform
   double f2, s, two_f, scale_dl;
@@ -38,7 +38,8 @@ int tc_pad_dim(int d);
 int tc_max_kp(int dpad, int nout, int split, int nab);
 int tc_col_split(int64_t nrows, int nblk, int maxsplit);
 int tc_nsa(int dpad, int nout, int split, int kp);
-bool tc_lb_ok(int dpad, int nout, int split, int kp);
+int tc_lb_mode(int dpad, int nout, int split, int kp);
+int tc_lb_nab(int mode, int kp);
 int tc_rhs_block_bytes(int split, bool lb, int kp);
 int tc_col_block_bytes(int dpad);
 bool tc_direct(int dpad);

@@ -56,6 +56,8 @@ constexpr int MAXNS = 4;
 constexpr int MAXNSB = 8;                 // shared-memory ring depth: runtime p.nsb in {4, 8}
 constexpr int BJ = 32;                    // columns per block
 constexpr int nthreads_for(int ns) { return (ns * WPS + 7) * 32; }  // + producer, 2 MMA issuers, 4 drain
+// LB layouts (below): 1 = two compute sets and three A stages, 2 = three sets and three stages
+constexpr int ns_of(int nout, int split, int lbm) { return lbm == 2 ? 3 : ns_for(nout, split); }
 
 KGP_DEV float ex2f(float x) {
   float y;
@@ -195,16 +197,17 @@ struct Geo {
 // corrections are hi*B_lo (tf32) and lo*bf16(B) (kind::f16, K=16), so an A stage takes 96
 // columns instead of 128 and TMEM holds three of them. Error terms: |lo| < 2^-10 |A|
 // (truncated hi), bf16 rounding 2^-9 of lo and of B -> 2^-18 |A||B| per product.
-template <int KT, int D, int NOUT, int SPLIT, bool LB>
-__global__ void __launch_bounds__(nthreads_for(ns_for(NOUT, SPLIT)), 1) kmm_tc_kernel(const TcParams p) {
-  constexpr int NS = ns_for(NOUT, SPLIT);
-  // sets, distance buffers, A stages. LB: a third A stage written alternately by the two
+template <int KT, int D, int NOUT, int SPLIT, int LBM>
+__global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_tc_kernel(const TcParams p) {
+  constexpr bool LB = LBM > 0;
+  constexpr int NS = ns_of(NOUT, SPLIT, LBM);
+  // sets, distance buffers, A stages. LBM 1: a third A stage written alternately by the two
   // sets (a stage is rewritten only after the MMAs of the block three back have read it, so
-  // a parity wait is never two phases behind)
-#ifndef KGP_TC_LBNSA
-#define KGP_TC_LBNSA 3
-#endif
-  constexpr int NSET = NS, ND = NS, NSA = LB ? KGP_TC_LBNSA : NS;
+  // a parity wait is never two phases behind); LBM 2: three sets, one per A stage, and two
+  // distance buffers the sets take in turn. "Distance ready" is signalled per SET (dfull[set],
+  // one completion per block of that set), never per buffer: with three sets on two buffers a
+  // buffer's parity could not tell a set's block from the one two turns earlier
+  constexpr int NSET = NS, ND = (LBM == 2) ? 2 : NS, NSA = LB ? 3 : NS;
   constexpr int NCW = NS * WPS;                 // compute warps
   constexpr int WPROD = NCW, WMMA = NCW + 1, WDIST = NCW + 2;
   static_assert(NS <= MAXNS, "ring slots");
@@ -267,10 +270,8 @@ __global__ void __launch_bounds__(nthreads_for(ns_for(NOUT, SPLIT)), 1) kmm_tc_k
       mbar_init(&accfull[b], 1);
       mbar_init(&accempty[b], 4);
     }
-    for (int b = 0; b < ND; ++b) {
-      mbar_init(&dfull[b], 1);
-      mbar_init(&dempty[b], WPS);
-    }
+    for (int b = 0; b < NSET; ++b) mbar_init(&dfull[b], 1);  // one per compute set
+    for (int b = 0; b < ND; ++b) mbar_init(&dempty[b], WPS);  // one per distance buffer
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc<512>(tmem_slot);
@@ -407,8 +408,8 @@ __global__ void __launch_bounds__(nthreads_for(ns_for(NOUT, SPLIT)), 1) kmm_tc_k
             mma_tf32_ts(dd, uh, vl, idesc_d, 1u);
             mma_tf32_ts(dd, ul, vh, idesc_d, 1u);
           }
-          tc_commit(&dfull[db]);
-          tc_commit(&empty[s]);  // this stage's V' has been read
+          tc_commit(&dfull[t % NSET]);  // to the set that owns block t (its own phase sequence)
+          tc_commit(&empty[s]);         // this stage's V' has been read
         }
         __syncwarp();
         if (++s == NSB) { s = 0; ph_s ^= 1; }
@@ -439,10 +440,11 @@ __global__ void __launch_bounds__(nthreads_for(ns_for(NOUT, SPLIT)), 1) kmm_tc_k
     const uint32_t lane_base = tbase + ((uint32_t)(qd * 32) << 16);
     for (int t = set; t < nblk; t += NSET) {
       const int s = t & (NSB - 1), a = t % NSA, db = t % ND;
-      const uint32_t ph_s = (t >> nsb_log) & 1, ph_a = (t / NSA) & 1, ph_d = (t / ND) & 1;
+      const uint32_t ph_s = (t >> nsb_log) & 1, ph_a = (t / NSA) & 1;
+      const uint32_t ph_e = (t / NSET) & 1;  // this set's own block count: dfull[set] phase
       if (use_ld32(NOUT, SPLIT, DMMA)) {
         // thread = row qd*32 + lane; 32x32b loads/stores of 16 columns at a time
-        mbar_wait(&dfull[db], ph_d);
+        mbar_wait(&dfull[set], ph_e);
         tc_fence_after();
         uint32_t v0[16], v1[16];
         tmem_ld16(lane_base + dbase + db * BJ, v0);
@@ -484,7 +486,7 @@ __global__ void __launch_bounds__(nthreads_for(ns_for(NOUT, SPLIT)), 1) kmm_tc_k
       }
       float2 acc[4][4];  // [row][column pair m]: rows lane/4 + 8 rr, columns 2g + 8m + {0,1}
       if (DMMA) {
-        mbar_wait(&dfull[db], ph_d);
+        mbar_wait(&dfull[set], ph_e);
         tc_fence_after();
         const uint32_t dcol = lane_base + dbase + db * BJ;
 #pragma unroll
@@ -580,20 +582,33 @@ __global__ void __launch_bounds__(nthreads_for(ns_for(NOUT, SPLIT)), 1) kmm_tc_k
     for (int seg = 0; seg < nseg; ++seg) {
       mbar_wait(&accfull[ab], ph);
       tc_fence_after();
-      for (int cb = 0; cb < NACC; cb += 16) {
-        uint32_t v[16];
-        tmem_ld16(lane_base + ab * NACC + cb, v);
-        tc_wait_ld();
-        float* dst = sAcc + cb * 128 + row;
+      // groups of up to 64 columns: all loads of a group, one wait; the buffer is released
+      // as soon as the last group is in registers, before the shared-memory adds (with one
+      // accumulator buffer the MMA waits on exactly this release)
+      for (int g0 = 0; g0 < NACC; g0 += 64) {
+        uint32_t v[4][16];
 #pragma unroll
-        for (int jj = 0; jj < 16; ++jj) {
-          const float x = __uint_as_float(v[jj]);
-          dst[jj * 128] = (seg == 0) ? x : dst[jj * 128] + x;
+        for (int q = 0; q < 4; ++q)
+          if (g0 + 16 * q < NACC) tmem_ld16(lane_base + ab * NACC + g0 + 16 * q, v[q]);
+        tc_wait_ld();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) tc_wait_ld_tied(v[q]);
+        if (g0 + 64 >= NACC) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&accempty[ab]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (g0 + 16 * q >= NACC) break;
+          float* dst = sAcc + (g0 + 16 * q) * 128 + row;
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) {
+            const float x = __uint_as_float(v[q][jj]);
+            dst[jj * 128] = (seg == 0) ? x : dst[jj * 128] + x;
+          }
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&accempty[ab]);
       if (++ab == NAB) { ab = 0; ph ^= 1; }
     }
     // epilogue: fp64 scaling, + s B on the diagonal rows, strided writes -- or, when the
@@ -648,9 +663,10 @@ __global__ void tc_reduce_kernel(const TcParams p, int nsplit, int nacc) {
   if (nacc > p.kp && p.out_dl) p.out_dl[o] = p.scale_dl * ag;
 }
 
-template <int KT, int D, int NOUT, int SPLIT, bool LB>
+template <int KT, int D, int NOUT, int SPLIT, int LBM>
 int launch_one(const TcParams& p_in, cudaStream_t st) {
-  auto kern = kmm_tc_kernel<KT, D, NOUT, SPLIT, LB>;
+  constexpr bool LB = LBM > 0;
+  auto kern = kmm_tc_kernel<KT, D, NOUT, SPLIT, LBM>;
   TcParams p = p_in;
   const size_t stage = (size_t)tc_rhs_block_bytes(SPLIT, LB, p.kp) + Geo<D>::VBYTES;
   const size_t fixed = Geo<D>::UBYTES + (size_t)NOUT * p.kp * 128 * 4 + 512;
@@ -666,7 +682,7 @@ int launch_one(const TcParams& p_in, cudaStream_t st) {
   const int nsplit = (p.nblk + p.nper - 1) / p.nper;
   dim3 grid((unsigned)((p.nrows + 127) / 128), (unsigned)nsplit);
   if (p.ev_start) KGP_CUDA(cudaEventRecord(p.ev_start, st));
-  kern<<<grid, nthreads_for(ns_for(NOUT, SPLIT)), smem, st>>>(p);
+  kern<<<grid, nthreads_for(ns_of(NOUT, SPLIT, LBM)), smem, st>>>(p);
   KGP_LAUNCH("kmm_tc_kernel");
   if (p.ev_stop) KGP_CUDA(cudaEventRecord(p.ev_stop, st));
   if (nsplit > 1) {
@@ -679,12 +695,13 @@ int launch_one(const TcParams& p_in, cudaStream_t st) {
 
 template <int KT, int D>
 int launch_kt_d(const TcParams& p, int nout, int split, cudaStream_t st) {
-  if (nout == 1) return split == 3 ? launch_one<KT, D, 1, 3, false>(p, st) : launch_one<KT, D, 1, 1, false>(p, st);
-  if (split != 3) return launch_one<KT, D, 2, 1, false>(p, st);
+  if (nout == 1) return split == 3 ? launch_one<KT, D, 1, 3, 0>(p, st) : launch_one<KT, D, 1, 1, 0>(p, st);
+  if (split != 3) return launch_one<KT, D, 2, 1, 0>(p, st);
   if constexpr (Geo<D>::DMMA && D == 8) {
-    if (p.lb) return launch_one<KT, D, 2, 3, true>(p, st);
+    if (p.lb == 1) return launch_one<KT, D, 2, 3, 1>(p, st);
+    if (p.lb == 2) return launch_one<KT, D, 2, 3, 2>(p, st);
   }
-  return launch_one<KT, D, 2, 3, false>(p, st);
+  return launch_one<KT, D, 2, 3, 0>(p, st);
 }
 
 template <int KT>
@@ -742,13 +759,31 @@ int tc_nsa(int, int nout, int split, int) { return ns_for(nout, split); }
 // k = 64: 5.83 -> 5.24 ms); at kp <= 32 it ties (k = 32: 3.40 ms both) or loses (k = 16:
 // 3.05 -> 3.24 ms), so the all-tf32 two-stage layout stays there. Env KGP_TC_LB=0 disables
 // it, KGP_TC_LB=2 forces it for every kp <= 64.
-bool tc_lb_ok(int dpad, int nout, int split, int kp) {
+//
+// LB mode 2 (kp <= 32): three compute sets, three A stages and two distance buffers;
+// TMEM = 2 nab kp + 64 + 32 + 288 <= 512: two accumulator buffers up to kp = 32.
+// Measured at cfg2 shape (k = 32): 3.45 ms against 3.39 for the classic layout, so it is
+// off by default (env KGP_TC_LB3=1 selects it).
+int tc_lb_mode(int dpad, int nout, int split, int kp) {
   static const int env = [] {
     const char* s = getenv("KGP_TC_LB");
     return s ? atoi(s) : 1;
   }();
-  return env != 0 && tc_dist_mode(dpad) == 1 && dpad == 8 && nout == 2 && split == 3 && kp <= 64 &&
-         (kp > 32 || env == 2);
+  static const int env3 = [] {
+    const char* s = getenv("KGP_TC_LB3");
+    return s ? atoi(s) : 0;
+  }();
+  if (env == 0 || tc_dist_mode(dpad) != 1 || dpad != 8 || nout != 2 || split != 3 || kp > 64) return 0;
+  if (kp > 32) return 1;
+  if (env3) return 2;
+  return env == 2 ? 1 : 0;
+}
+
+// TMEM accumulator buffers for a LB mode (0: the caller's choice for the classic layout)
+int tc_lb_nab(int mode, int kp) {
+  if (mode == 2) return kp <= 32 ? 2 : 1;
+  if (mode == 1) return kp <= 32 ? 2 : 1;
+  return 0;
 }
 
 // bytes of one 32-row RHS block in bsplit: tf32 hi (| lo) K-major 128B-swizzled (| bf16 interleaved)
