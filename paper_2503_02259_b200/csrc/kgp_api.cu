@@ -261,6 +261,14 @@ static int dense_build(kgp_engine_s* e, cudaStream_t st) {
   if (rc) return rc;
   dense_finish_kernel<<<1184, 256, 0, st>>>(e->n, e->f * e->f, e->s, e->dense.as<double>());
   KGP_LAUNCH("dense_finish_kernel");
+  // the packed upper triangle for products with <= SYM_MAXK columns (and its partial-sum
+  // buffer, allocated here so no allocation happens inside a captured PCG graph)
+  rc = e->dpack.ensure(sizeof(double) * (size_t)sym_packed_elems(e->n));
+  if (rc) return rc;
+  rc = e->dq.ensure(sizeof(double) * (size_t)sym_q_elems(e->n));
+  if (rc) return rc;
+  rc = sym_pack(e->n, e->dense.as<double>(), e->dpack.as<double>(), st);
+  if (rc) return rc;
   if (!e->cublas) {
     cublasHandle_t h;
     KGP_REQUIRE(cublasCreate(&h) == CUBLAS_STATUS_SUCCESS, KGP_ERR_CUDA, "cublasCreate failed");
@@ -281,6 +289,14 @@ static int engine_matmul_core(kgp_engine_s* e, int64_t k, const double* b, int64
     // rejected: DESIGN.md, "DENSE-mode product".)
     int rc = dense_build(e, st);
     if (rc) return rc;
+    // few columns on the full operator: the packed symmetric product (symv.cu; half the
+    // bytes, L2-resident) -- env KGP_DENSE_SYM=0 keeps cuBLAS
+    static const bool sym_on = [] {
+      const char* s = getenv("KGP_DENSE_SYM");
+      return !(s && atoi(s) == 0);
+    }();
+    if (sym_on && k <= SYM_MAXK && e->nrows == e->n && e->row0 == 0)
+      return sym_matmul(e->n, e->dpack.as<double>(), (int)k, b, b_cs, out_k, o_cs, e->dq.as<double>(), st);
     cublasHandle_t h = (cublasHandle_t)e->cublas;
     KGP_REQUIRE(cublasSetStream(h, st) == CUBLAS_STATUS_SUCCESS, KGP_ERR_CUDA, "cublasSetStream failed");
     const double one = 1.0, zero = 0.0;

@@ -74,6 +74,14 @@ int prep_rhs(int split, int lb, int64_t n, int64_t k, int64_t c0, int kp, const 
              uint8_t* out, cudaStream_t st);
 int col_mean(int64_t n, int d, const double* x, double* mean, cudaStream_t st);
 
+// ------------------------------------------------------------------ symmetric DENSE product (symv.cu)
+constexpr int SYM_MAXK = 4;  // right-hand sides handled by the packed-triangle product
+int64_t sym_packed_elems(int64_t n);
+int64_t sym_q_elems(int64_t n);
+int sym_pack(int64_t n, const double* dense, double* packed, cudaStream_t st);
+int sym_matmul(int64_t n, const double* packed, int k, const double* b, int64_t b_cs, double* out, int64_t o_cs,
+               double* q, cudaStream_t st);
+
 // ------------------------------------------------------------------ device buffer helper
 struct DevBuf {
   void* p = nullptr;
@@ -147,6 +155,8 @@ struct kgp_engine_s {
   // DENSE mode (kgp_engine_set_dense): Khat materialised once, products by cuBLAS DGEMM
   bool dense_on = false, dense_valid = false;
   kgp::DevBuf dense;        // (n, n) fp64 Khat = f^2 kappa + s I
+  kgp::DevBuf dpack;        // upper triangle of Khat in 64 x 64 tiles (symv.cu), L2-resident
+  kgp::DevBuf dq;           // partial sums of the packed product
   void* cublas = nullptr;   // cublasHandle_t
   // optional main-kernel timing (kgp_engine_set_timing)
   bool timing = false;

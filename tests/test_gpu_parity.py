@@ -778,3 +778,31 @@ def test_operator_workspace_linear_in_n(pkg, precision):
     n2 = 65536
     assert used[1] <= 64 * n2 * (33 + 8) * 8 + (64 << 20), used  # far below one n x n panel (34 GB)
     assert used[1] <= 2.5 * used[0] + (32 << 20), used
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [1, 63, 1000, 4097])
+@pytest.mark.parametrize("k", [1, 3, 4, 5])
+def test_dense_mode_products_match_on_the_fly(pkg, n, k):
+    """DENSE mode (kmat.py:93-94): the packed symmetric product (k <= 4, symv.cu) and the
+    cuBLAS product (k > 4) both equal the fp64 on-the-fly operator (kmat.py:165-189)."""
+    rng = np.random.default_rng(n + 10 * k)
+    x = rng.uniform(0, 1, (n, 3))
+    b = rng.standard_normal((n, k))
+    hp = _hp(pkg, 0.3, 1.2, 1e-2)
+    import torch
+
+    dense = pkg.KernelEngine(pkg.KernelType.MATERN52, x, hp, mode=pkg.EngineMode.DENSE)
+    otf = pkg.KernelEngine(pkg.KernelType.MATERN52, x, hp, mode=pkg.EngineMode.ON_THE_FLY)
+    # column-major device blocks, the PCG state's layout (the DENSE product's operand layout)
+    bd = torch.from_numpy(np.ascontiguousarray(b.T)).cuda().T
+
+    def run(e):
+        out = torch.empty((k, n), dtype=torch.float64, device="cuda").T
+        e.apply(bd, outs=(out, None, None))
+        torch.cuda.synchronize()
+        return out.cpu().numpy()
+
+    got, ref = run(dense), run(otf)
+    assert rel_max(got, ref) <= 1e-13
+    assert np.array_equal(got, run(dense))  # fixed-order partial sums: run-to-run identical
