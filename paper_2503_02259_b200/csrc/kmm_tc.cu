@@ -69,6 +69,9 @@ KGP_DEV float sqrtf_approx(float x) {
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+#ifndef KGP_TC_SQRT_FMA
+#define KGP_TC_SQRT_FMA 0  // measured: Matern-3/2 d=4 k=33 one output 2.95 -> 4.19 ms (issue-bound, not XU-bound)
+#endif
 KGP_DEV float2 hi2(float2 v) {
   return make_float2(__uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u),
                      __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u));
@@ -89,7 +92,22 @@ KGP_DEV void transform2(float2 t2, float2& kv, float2& gv) {
     kv = make_float2(ex2f(-t2.x), ex2f(-t2.y));
     if (NEED_G) gv = __fmul2_rn(t2, kv);
   } else {
+#if KGP_TC_SQRT_FMA
+    // sqrt on the FMA pipe (the MUFU/XU pipe is the busiest one for Matern): rsqrt seed by the
+    // exponent-halving bit trick, three Newton steps, t = t2 * rsqrt(t2)
+    const float2 hx = __fmul2_rn(t2, make_float2(0.5f, 0.5f));
+    float2 y = make_float2(__uint_as_float(0x5f375a86u - (__float_as_uint(t2.x) >> 1)),
+                           __uint_as_float(0x5f375a86u - (__float_as_uint(t2.y) >> 1)));
+#pragma unroll
+    for (int it = 0; it < 3; ++it) {
+      const float2 h = __fmul2_rn(hx, y);
+      const float2 e = __ffma2_rn(make_float2(-h.x, -h.y), y, make_float2(1.5f, 1.5f));
+      y = __fmul2_rn(y, e);
+    }
+    float2 t = __fmul2_rn(t2, y);  // t2 = 0: y is finite (seed of +0), t = 0
+#else
     float2 t = make_float2(sqrtf_approx(t2.x), sqrtf_approx(t2.y));
+#endif
     float2 a = __fmul2_rn(t, make_float2(-1.4426950408889634f, -1.4426950408889634f));
     float2 e = make_float2(ex2f(a.x), ex2f(a.y));
     float2 u = __ffma2_rn(t, e, e);  // (1+t) e^-t
