@@ -84,10 +84,14 @@ KGP_DEV float2 lo2(float2 v) { return fsub2(v, hi2(v)); }
 //   Matern32  t2 = 3 r^2 / l^2             kappa = (1+t) e^-t         g = t2 e^-t
 //   Matern52  t2 = 5 r^2 / l^2             kappa = (1+t+t2/3) e^-t    g = t2 (1+t) e^-t
 // with t = sqrt(t2); dkappa/dl = scale_dl * g (scale folded into the epilogue).
-template <int KT, bool NEED_G>
+// CLAMP: t2 from the expansion can cancel below zero (_panels_numpy.py:26-27); direct
+// differences (d <= 4) are a sum of squares and skip the clamp (one FMNMX per entry).
+template <int KT, bool NEED_G, bool CLAMP = true>
 KGP_DEV void transform2(float2 t2, float2& kv, float2& gv) {
-  t2.x = fmaxf(t2.x, 0.0f);  // the expansion can cancel below zero (_panels_numpy.py:26-27)
-  t2.y = fmaxf(t2.y, 0.0f);
+  if (CLAMP) {
+    t2.x = fmaxf(t2.x, 0.0f);
+    t2.y = fmaxf(t2.y, 0.0f);
+  }
   if (KT == GAUSS) {
     kv = make_float2(ex2f(-t2.x), ex2f(-t2.y));
     if (NEED_G) gv = __fmul2_rn(t2, kv);
@@ -577,7 +581,7 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
             if (p.debug & 4) {
               kv[q][m] = gv[q][m] = acc[2 * half + q][m];
             } else {
-              transform2<KT, NEED_G>(acc[2 * half + q][m], kv[q][m], gv[q][m]);
+              transform2<KT, NEED_G, DMMA || XP>(acc[2 * half + q][m], kv[q][m], gv[q][m]);
             }
           }
         const uint32_t taddr = tcol + ((uint32_t)(16 * half) << 16);
