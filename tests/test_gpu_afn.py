@@ -75,6 +75,10 @@ def test_afn_apply_matches_numpy(pkg, kt):
     assert rel_max(pre.apply_inverse(b[:, 2]), ref.apply_inverse(b[:, 2])) <= 1e-8
     # run-to-run bitwise determinism (no atomics in the application)
     np.testing.assert_array_equal(pre.apply_inverse(b), pre.apply_inverse(b))
+    # k > 8: the point-major application (transposed cuBLAS products, coalesced G gathers)
+    b12 = np.random.default_rng(2).standard_normal((900, 12))
+    assert rel_max(pre.apply_inverse(b12), ref.apply_inverse(b12)) <= 1e-8
+    np.testing.assert_array_equal(pre.apply_inverse(b12), pre.apply_inverse(b12))
 
 
 def test_afn_preconditioned_pcg(pkg):
