@@ -99,6 +99,34 @@ int kgp_engine_matmul(kgp_engine* e, int64_t k, const double* b, int64_t b_rs, i
 int kgp_engine_matmul_host(kgp_engine* e, int64_t k, const double* b, double* out_k, double* out_dl,
                            double* out_df, void* stream);
 
+/* ------------------------------------------------------------------ fused all-gather + operator
+ * The multi-GPU row partition (the reference has no multi-GPU path, its
+ * product is kmat.py:165-189) without a separate all-gather of the RHS: rank q owns rows
+ * [row_start[q], row_start[q+1]) of B (boundaries on multiples of 32) and publishes them,
+ * already in the operator's tf32 tile layout, in a buffer every rank maps (CUDA IPC); each
+ * rank's operator kernel pulls the owners' tiles (over NVLink) block by block as its column
+ * sweep reaches them, so the exchange overlaps the math. Replaces dist.py's NCCL
+ * all_gather + K^[I_g, :] P. Per product, epoch e = 1, 2, ...:
+ *   kgp_engine_peer_publish: wait until every peer's done >= e - 1 (it finished reading the
+ *     previous tiles), write the own tiles, ready = e;
+ *   kgp_engine_peer_matmul: the kernel waits for each owner's ready >= e before its first
+ *     tile; afterwards done = e.
+ * Flags are system-scope release/acquire; waits are bounded (a peer that never arrives
+ * traps the kernel -> KGP_ERR_CUDA, never a hang). Buffers: [ready | done | pad to 1 KB]
+ * then the tiles; tensor-core precisions only; one launch's RHS block (k). */
+int kgp_peer_alloc(int64_t bytes, void** dptr, void* ipc_handle /* 64-byte cudaIpcMemHandle out, or NULL */);
+int kgp_peer_open(const void* ipc_handle, void** dptr); /* map a peer's buffer (cudaIpcOpenMemHandle) */
+int kgp_peer_close(void* dptr);                         /* unmap an opened peer buffer */
+int kgp_peer_free(void* dptr);                          /* free an own kgp_peer_alloc buffer */
+int kgp_engine_peer_buffer_bytes(kgp_engine* e, int64_t k, int64_t own_rows, int64_t* bytes);
+/* engine rows must already be rank's block (kgp_engine_set_rows); bases[q] = rank q's buffer */
+int kgp_engine_set_peers(kgp_engine* e, int world, int rank, const int64_t* row_start, void* const* bases);
+/* b_loc: this rank's rows (nrows x k, strides b_rs / b_cs), valid until the matching peer_matmul */
+int kgp_engine_peer_publish(kgp_engine* e, int64_t k, const double* b_loc, int64_t b_rs, int64_t b_cs,
+                            uint64_t epoch, void* stream);
+int kgp_engine_peer_matmul(kgp_engine* e, int64_t k, uint64_t epoch, double* out_k, double* out_dl, double* out_df,
+                           int64_t o_rs, int64_t o_cs, void* stream);
+
 /* Rectangular f^2 kappa(Xs, X) B (no diagonal shift): the cross kernel of predict
  * (gp.py:223-241), never materialised. xs: (m, d) device fp64 row-major. */
 int kgp_engine_cross_matmul(kgp_engine* e, int64_t m, const double* xs, int64_t k, const double* b,

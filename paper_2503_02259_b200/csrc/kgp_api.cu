@@ -137,7 +137,9 @@ static double scale_dl_fast(int kt, double l, double f) {
 // products prepare it once for all chunks; valid when k fits one launch)
 static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t diag_row0, int64_t k, const double* b,
                      int64_t b_rs, int64_t b_cs, double* out_k, double* out_dl, double* out_df, int64_t o_rs,
-                     int64_t o_cs, cudaStream_t st, bool skip_prep = false) {
+                     int64_t o_cs, cudaStream_t st, bool skip_prep = false, uint64_t peer_epoch = 0) {
+  // peer_epoch > 0: fused all-gather -- the RHS tiles come from the ranks' published buffers
+  // (kgp_engine_peer_publish), b is this rank's own rows (diag_row0 = 0 indexes them)
   const int split = (e->precision == KGP_FAST) ? 3 : 1;
   const int nout = out_dl ? 2 : 1;
   const int nblk = (int)((e->n + 31) / 32);
@@ -149,11 +151,11 @@ static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t 
   for (int64_t c0 = 0; c0 < k; c0 += kmax) {
     const int kc = (int)((k - c0) < kmax ? (k - c0) : kmax);
     const int kp = (kc + 15) / 16 * 16;
-    const int lbm = tc_lb_mode(e->dpad, nout, split, kp);
+    const int lbm = peer_epoch ? 0 : tc_lb_mode(e->dpad, nout, split, kp);  // published tiles: classic layout
     const bool lb = lbm != 0;
     const int nab = lb ? tc_lb_nab(lbm, kp) : (kp <= kmax2 ? 2 : 1);
     int rc = KGP_OK;
-    if (!(skip_prep && kc == k)) {
+    if (!peer_epoch && !(skip_prep && kc == k)) {
       rc = e->bsplit.ensure((size_t)nblk * tc_rhs_block_bytes(split, lb, kp));
       if (rc) return rc;
       rc = prep_rhs(split, lb ? 1 : 0, e->n, k, c0, kp, b, b_rs, b_cs, e->bsplit.as<uint8_t>(), st);
@@ -193,6 +195,16 @@ static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t 
     p.out_df = out_df ? out_df + c0 * o_cs : nullptr;
     p.o_rs = o_rs;
     p.o_cs = o_cs;
+    if (peer_epoch) {
+      p.npeer = e->pworld;
+      for (int q = 0; q < e->pworld; ++q) {
+        p.pblk0[q] = (int)(e->prow[q] / 32);
+        p.ptile[q] = e->pbase[q] + PEER_HDR;
+        p.pready[q] = reinterpret_cast<const unsigned long long*>(e->pbase[q]);
+      }
+      p.pblk0[e->pworld] = nblk;
+      p.epoch = peer_epoch;
+    }
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if (e->timing && cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusNone) {
       if (e->tev_used + 2 > e->tev.size()) {
@@ -809,4 +821,147 @@ extern "C" int kgp_slq_logdet(int64_t k, int32_t max_iter, const double* alphas,
   KGP_REQUIRE(k >= 1, KGP_ERR_INVALID, "need at least one probe trace");
   KGP_REQUIRE(logdet != nullptr, KGP_ERR_INVALID, "logdet pointer is NULL");
   return slq_impl(k, max_iter, alphas, betas, iters, norms_sq, logdet, (cudaStream_t)stream);
+}
+
+
+// ------------------------------------------------------------------ fused all-gather + operator
+namespace {
+
+__global__ void peer_wait_done_kernel(int world, int rank, unsigned long long want,
+                                      const unsigned long long* f0, const unsigned long long* f1,
+                                      const unsigned long long* f2, const unsigned long long* f3,
+                                      const unsigned long long* f4, const unsigned long long* f5,
+                                      const unsigned long long* f6, const unsigned long long* f7) {
+  const unsigned long long* f[8] = {f0, f1, f2, f3, f4, f5, f6, f7};
+  const int q = threadIdx.x;
+  if (q < world && q != rank) kgp::peer_wait_flag(f[q], want);
+}
+
+__global__ void peer_flag_kernel(unsigned long long* flag, unsigned long long v) { kgp::peer_set_flag(flag, v); }
+
+}  // namespace
+
+extern "C" int kgp_peer_alloc(int64_t bytes, void** dptr, void* ipc_handle) {
+  KGP_REQUIRE(bytes > 0 && dptr != nullptr, KGP_ERR_INVALID, "bad peer buffer request");
+  void* p = nullptr;
+  KGP_CUDA(cudaMalloc(&p, (size_t)bytes));
+  KGP_CUDA(cudaMemset(p, 0, PEER_HDR));  // flags start at 0 (no epoch published or read)
+  if (ipc_handle) {
+    cudaIpcMemHandle_t h;
+    const cudaError_t rc = cudaIpcGetMemHandle(&h, p);
+    if (rc != cudaSuccess) {
+      cudaFree(p);
+      return cuda_check(rc, "cudaIpcGetMemHandle");
+    }
+    memcpy(ipc_handle, &h, sizeof(h));
+  }
+  *dptr = p;
+  return KGP_OK;
+}
+
+extern "C" int kgp_peer_open(const void* ipc_handle, void** dptr) {
+  KGP_REQUIRE(ipc_handle != nullptr && dptr != nullptr, KGP_ERR_INVALID, "NULL handle");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, ipc_handle, sizeof(h));
+  KGP_CUDA(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return KGP_OK;
+}
+
+extern "C" int kgp_peer_close(void* dptr) {
+  KGP_CUDA(cudaIpcCloseMemHandle(dptr));
+  return KGP_OK;
+}
+
+extern "C" int kgp_peer_free(void* dptr) {
+  KGP_CUDA(cudaFree(dptr));
+  return KGP_OK;
+}
+
+extern "C" int kgp_engine_peer_buffer_bytes(kgp_engine* e, int64_t k, int64_t own_rows, int64_t* bytes) {
+  CHECK_ENGINE(e);
+  KGP_REQUIRE(bytes != nullptr && k >= 1 && own_rows >= 0, KGP_ERR_INVALID, "bad peer buffer query");
+  const int split = (e->precision == KGP_FAST) ? 3 : 1;
+  const int64_t kp = (k + 15) / 16 * 16;
+  *bytes = PEER_HDR + (own_rows + 31) / 32 * (int64_t)tc_rhs_block_bytes(split, false, (int)kp);
+  return KGP_OK;
+}
+
+extern "C" int kgp_engine_set_peers(kgp_engine* e, int world, int rank, const int64_t* row_start,
+                                    void* const* bases) {
+  CHECK_ENGINE(e);
+  KGP_REQUIRE(e->precision != KGP_FP64, KGP_ERR_INVALID, "the fused all-gather operator needs the tensor-core "
+              "precision (fast or tf32)");
+  KGP_REQUIRE(world >= 1 && world <= KGP_MAX_PEERS && rank >= 0 && rank < world && row_start && bases,
+              KGP_ERR_INVALID, "bad peer configuration (world %d, rank %d; at most %d ranks)", world, rank,
+              KGP_MAX_PEERS);
+  KGP_REQUIRE(row_start[0] == 0 && row_start[world] == e->n, KGP_ERR_INVALID, "row blocks must cover [0, %lld)",
+              (long long)e->n);
+  for (int q = 0; q < world; ++q) {
+    KGP_REQUIRE(row_start[q + 1] >= row_start[q] && (q + 1 == world || row_start[q + 1] % 32 == 0),
+                KGP_ERR_INVALID, "row block boundaries must ascend on multiples of 32 (column blocks)");
+    KGP_REQUIRE(bases[q] != nullptr, KGP_ERR_INVALID, "NULL peer buffer for rank %d", q);
+  }
+  KGP_REQUIRE(e->row0 == row_start[rank] && e->nrows == row_start[rank + 1] - row_start[rank], KGP_ERR_INVALID,
+              "engine rows [%lld, %lld) are not rank %d's block [%lld, %lld) (kgp_engine_set_rows first)",
+              (long long)e->row0, (long long)(e->row0 + e->nrows), rank, (long long)row_start[rank],
+              (long long)row_start[rank + 1]);
+  e->pworld = world;
+  e->prank = rank;
+  for (int q = 0; q <= world; ++q) e->prow[q] = row_start[q];
+  for (int q = 0; q < world; ++q) e->pbase[q] = static_cast<uint8_t*>(bases[q]);
+  bump_graph_epoch();
+  return KGP_OK;
+}
+
+// Publish this rank's rows of B for product `epoch` (1, 2, ...): wait until every peer is
+// done reading epoch - 1, write the own tiles, then ready = epoch. b_loc must stay valid
+// until the matching kgp_engine_peer_matmul (its rows give the + s B term).
+extern "C" int kgp_engine_peer_publish(kgp_engine* e, int64_t k, const double* b_loc, int64_t b_rs, int64_t b_cs,
+                                       uint64_t epoch, void* stream) {
+  CHECK_ENGINE(e);
+  KGP_REQUIRE(e->pworld > 0, KGP_ERR_STATE, "no peer configuration (kgp_engine_set_peers)");
+  KGP_REQUIRE(epoch >= 1 && k >= 1 && b_loc != nullptr, KGP_ERR_INVALID, "bad publish arguments");
+  const int split = (e->precision == KGP_FAST) ? 3 : 1;
+  KGP_REQUIRE(k <= tc_max_kp(e->dpad, 2, split, 1), KGP_ERR_INVALID,
+              "the fused all-gather operator takes one launch's RHS block (k = %lld too wide)", (long long)k);
+  KGP_CUDA(cudaSetDevice(e->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned long long* f[KGP_MAX_PEERS] = {};
+  for (int q = 0; q < e->pworld; ++q) f[q] = reinterpret_cast<const unsigned long long*>(e->pbase[q] + 8);  // done
+  peer_wait_done_kernel<<<1, 32, 0, st>>>(e->pworld, e->prank, (unsigned long long)(epoch - 1), f[0], f[1],
+                                          f[2], f[3], f[4], f[5], f[6], f[7]);
+  KGP_LAUNCH("peer_wait_done_kernel");
+  const int kp = (int)((k + 15) / 16 * 16);
+  uint8_t* mine = e->pbase[e->prank];
+  int rc = prep_rhs(split, 0, e->nrows, k, 0, kp, b_loc, b_rs, b_cs, mine + PEER_HDR, st);
+  if (rc) return rc;
+  peer_flag_kernel<<<1, 1, 0, st>>>(reinterpret_cast<unsigned long long*>(mine), (unsigned long long)epoch);
+  KGP_LAUNCH("peer_flag_kernel");
+  e->pb = b_loc;
+  e->pb_rs = b_rs;
+  e->pb_cs = b_cs;
+  e->pk = k;
+  return KGP_OK;
+}
+
+// This rank's rows of Khat B (and dKhat/dl B, dKhat/df B) for product `epoch`, reading every
+// rank's published tiles as the column sweep reaches them; then done = epoch.
+extern "C" int kgp_engine_peer_matmul(kgp_engine* e, int64_t k, uint64_t epoch, double* out_k, double* out_dl,
+                                      double* out_df, int64_t o_rs, int64_t o_cs, void* stream) {
+  CHECK_ENGINE(e);
+  KGP_REQUIRE(e->pworld > 0, KGP_ERR_STATE, "no peer configuration (kgp_engine_set_peers)");
+  KGP_REQUIRE(e->pb != nullptr && k == e->pk, KGP_ERR_STATE, "kgp_engine_peer_publish(k = %lld) must precede",
+              (long long)k);
+  KGP_REQUIRE(out_k || out_dl || out_df, KGP_ERR_INVALID, "no output requested");
+  KGP_CUDA(cudaSetDevice(e->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = engine_prepare(e, st);
+  if (rc) return rc;
+  rc = tc_matmul(e, e->xrow.as<float>(), e->nrows, 0, k, e->pb, e->pb_rs, e->pb_cs, out_k, out_dl, out_df, o_rs,
+                 o_cs, st, false, epoch);
+  if (rc) return rc;
+  peer_flag_kernel<<<1, 1, 0, st>>>(reinterpret_cast<unsigned long long*>(e->pbase[e->prank] + 8),
+                                    (unsigned long long)epoch);
+  KGP_LAUNCH("peer_flag_kernel");
+  return KGP_OK;
 }

@@ -123,6 +123,30 @@ KGP_DEV void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, uint
       : "memory");
 }
 
+// ---------------------------------------------------------------- cross-GPU flags (fused all-gather)
+// Bounded wait for a peer's flag (system-scope acquire): a peer that never arrives traps the
+// kernel after `timeout_ns` (a CUDA error on the host) instead of hanging the device.
+KGP_DEV void peer_wait_flag(const unsigned long long* flag, unsigned long long want,
+                            unsigned long long timeout_ns = 20000000000ull) {
+  unsigned long long t0, now, v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+    if (v >= want) break;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    if (now - t0 > timeout_ns) {
+      printf("kgp: peer flag %p stuck at %llu (want %llu)\n", (const void*)flag, v, want);
+      __trap();
+    }
+    __nanosleep(128);
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");  // later bulk copies read what the flag released
+}
+KGP_DEV void peer_set_flag(unsigned long long* flag, unsigned long long v) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(v) : "memory");
+}
+
 // One lane of a converged warp (elect.sync): the single issuing thread for
 // tcgen05.mma / bulk copies, without a divergent `lane == 0` region that would
 // force the compiler to waterfall the (warp-uniform) operands into uniform registers.

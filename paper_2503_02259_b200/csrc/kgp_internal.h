@@ -9,6 +9,9 @@
 
 namespace kgp {
 
+constexpr int KGP_MAX_PEERS = 8;     // ranks of a fused all-gather operator (one node)
+constexpr int PEER_HDR = 1024;       // peer buffer: [ready u64 | done u64 | pad] then the tiles
+
 // ------------------------------------------------------------------ fast (tcgen05) operator
 struct TcParams {
   const float* xrow;      // (nrows, dpad+1): [q_i, u_i0 .. u_i(dpad-1)]
@@ -33,6 +36,14 @@ struct TcParams {
   double *out_k, *out_dl, *out_df;
   int64_t o_rs, o_cs;
   cudaEvent_t ev_start, ev_stop;  // host side: optional timing bracket around the main kernel
+  // fused all-gather (kgp_engine_peer_matmul): npeer > 0 -> the RHS tiles of column block g
+  // come from the owner rank q's published buffer ptile[q] (block g - pblk0[q]), read after
+  // that rank's ready flag reaches `epoch`
+  int npeer;
+  int pblk0[KGP_MAX_PEERS + 1];
+  const uint8_t* ptile[KGP_MAX_PEERS];
+  const unsigned long long* pready[KGP_MAX_PEERS];
+  unsigned long long epoch;
 };
 int tc_pad_dim(int d);
 int tc_max_kp(int dpad, int nout, int split, int nab);
@@ -130,6 +141,13 @@ struct kgp_engine_s {
   kgp::DevBuf bsplit;      // per-call RHS split
   kgp::DevBuf f64part;     // fp64 operator column-split partials
   kgp::DevBuf tcpart;      // fast operator column-split partials
+  // fused all-gather (kgp_engine_set_peers): rank `prank` of `pworld`, rows prow[q]..prow[q+1]
+  // of B owned by rank q, whose buffer (flags + tiles) is mapped at pbase[q]
+  int pworld = 0, prank = 0;
+  int64_t prow[kgp::KGP_MAX_PEERS + 1] = {};
+  uint8_t* pbase[kgp::KGP_MAX_PEERS] = {};
+  const double* pb = nullptr;  // own rows of B from the last publish (the + s B term)
+  int64_t pb_rs = 0, pb_cs = 0, pk = 0;
   bool prepared;
   // PCG workspace (grown on demand) and a pinned status word for the per-iteration readback
   kgp::DevBuf ws;

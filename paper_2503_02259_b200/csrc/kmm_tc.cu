@@ -332,13 +332,25 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
 
   if (warp == WPROD) {
     // ------------------------------------------------------------ producer (converged warp, one elected issuer)
-    int s = 0;
+    int s = 0, owner = -1;
     uint32_t ph = 0;
     for (int t = 0; t < nblk; ++t) {
       mbar_wait(&empty[s], ph ^ 1);
+      const uint8_t* bsrc = p.bsplit + (size_t)(t0 + t) * BBYTES;
+      if (p.npeer > 0) {  // fused all-gather: this block's RHS tile lives in its owner's buffer
+        const int tg = t0 + t;
+        int q = owner < 0 ? 0 : owner;
+        while (q + 1 < p.npeer && tg >= p.pblk0[q + 1]) ++q;
+        if (q != owner) {  // first block of this owner in the sweep: wait for its tiles
+          if (elect_one()) peer_wait_flag(p.pready[q], p.epoch);
+          __syncwarp();
+          owner = q;
+        }
+        bsrc = p.ptile[q] + (size_t)(tg - p.pblk0[q]) * BBYTES;
+      }
       if (elect_one()) {
         mbar_arrive_expect_tx(&full[s], BBYTES + VBYTES);
-        bulk_g2s(sB + s * BBYTES, p.bsplit + (size_t)(t0 + t) * BBYTES, BBYTES, &full[s]);
+        bulk_g2s(sB + s * BBYTES, bsrc, BBYTES, &full[s]);
         bulk_g2s(sV + s * VBYTES, reinterpret_cast<const uint8_t*>(p.xcol) + (size_t)(t0 + t) * VBYTES, VBYTES, &full[s]);
       }
       __syncwarp();

@@ -38,15 +38,18 @@ from paper_2503_02259_b200.errors import BreakdownError, NumericalError
 LOG_2PI = math.log(2.0 * math.pi)
 
 
-def row_range(n: int, world: int, rank: int):
-    """Balanced contiguous row block of `rank`."""
-    return rank * n // world, (rank + 1) * n // world
+def row_range(n: int, world: int, rank: int, align: int = 1):
+    """Balanced contiguous row block of `rank`; inner boundaries rounded down to multiples of
+    `align` (32 for the fused all-gather operator: its column blocks)."""
+    def edge(q):
+        return n if q >= world else (q * n // world) // align * align
+    return edge(rank), edge(rank + 1)
 
 
 class Comm:
     """The two collectives the solver needs, over torch.distributed (nccl or gloo)."""
 
-    def __init__(self, n: int, group=None):
+    def __init__(self, n: int, group=None, align: int = 1):
         import torch.distributed as dist
 
         self.dist = dist
@@ -54,7 +57,7 @@ class Comm:
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.n = n
-        self.ranges = [row_range(n, self.world, r) for r in range(self.world)]
+        self.ranges = [row_range(n, self.world, r, align) for r in range(self.world)]
         self.maxloc = max(r1 - r0 for r0, r1 in self.ranges)
         self.nccl = dist.get_backend(group) == "nccl"
 
@@ -148,8 +151,9 @@ def dist_pcg(ops, comm: Comm, y_loc, tol, max_iter: int, precondition, shift: fl
         z = minv(r)
         p = z.clone()
         rz = dots(r, z)
+        peer = getattr(ops, "matmul_local", None)  # fused all-gather operator (PeerTiles)
         for _ in range(stride):
-            ap = ops.matmul_rows(comm.allgather_rows(p))
+            ap = peer(p) if peer is not None else ops.matmul_rows(comm.allgather_rows(p))
             if diag_loc is not None:
                 ap = ap + diag_loc * p
             pap = dots(p, ap)
@@ -374,6 +378,20 @@ class CudaRowOps:
         torch = self._device.torch()
         return torch.empty((k, self.r1 - self.r0), dtype=torch.float64, device=self._device.device())
 
+    def _matmul_peer(self, p_loc):
+        """This rank's rows of Khat P from the local rows of P alone (kgp_engine_peer_publish +
+        kgp_engine_peer_matmul): the other ranks' rows are read from their published tiles
+        inside the operator kernel."""
+        k, nloc = p_loc.shape
+        p_loc = p_loc.contiguous()
+        out = self._out(k)
+        self._epoch = getattr(self, "_epoch", 0) + 1
+        st = self._device.stream_ptr()
+        self._call("kgp_engine_peer_publish", self.engine.handle, k, p_loc.data_ptr(), 1, nloc, self._epoch, st)
+        self._call("kgp_engine_peer_matmul", self.engine.handle, k, self._epoch, out.data_ptr(), None, None, 1, nloc,
+                   st)
+        return out
+
     def matmul_rows(self, p_full):
         k, n = p_full.shape
         out = self._out(k)
@@ -445,6 +463,65 @@ class CudaRowOps:
         return solver.slq_logdet_device(alphas.contiguous(), betas.contiguous(),
                                         torch.from_numpy(np.asarray(iters, dtype=np.int32)).to(dev),
                                         torch.from_numpy(np.asarray(norms_sq, dtype=np.float64)).to(dev))
+
+
+class PeerTiles:
+    """The fused all-gather operator's buffers for one rank (kgp_engine_set_peers): this rank's
+    published tile buffer plus every peer's, mapped through CUDA IPC (the 64-byte handles are
+    exchanged with all_gather_object, so any torch.distributed backend carries them).
+
+    ``bases`` (single-process use, e.g. ranks simulated on one device): the buffers of all
+    ranks, already allocated with kgp_peer_alloc; no IPC."""
+
+    def __init__(self, engine_handle, world: int, rank: int, row_start, k: int, comm=None, bases=None):
+        import ctypes
+
+        from paper_2503_02259_b200._lib import call
+
+        self._call = call
+        self.world, self.rank, self.k = world, rank, int(k)
+        self.row_start = np.asarray(row_start, dtype=np.int64)
+        self._opened, self._own = [], None
+        if bases is None:
+            nbytes = ctypes.c_int64()
+            own_rows = int(self.row_start[rank + 1] - self.row_start[rank])
+            call("kgp_engine_peer_buffer_bytes", engine_handle, self.k, own_rows, ctypes.byref(nbytes))
+            ptr, handle = ctypes.c_void_p(), ctypes.create_string_buffer(64)
+            call("kgp_peer_alloc", nbytes.value, ctypes.byref(ptr), handle)
+            self._own = ptr.value
+            handles = [None] * world
+            comm.dist.all_gather_object(handles, handle.raw, group=comm.group)
+            bases = []
+            for q in range(world):
+                if q == rank:
+                    bases.append(self._own)
+                    continue
+                mapped = ctypes.c_void_p()
+                call("kgp_peer_open", ctypes.create_string_buffer(handles[q], 64), ctypes.byref(mapped))
+                self._opened.append(mapped.value)
+                bases.append(mapped.value)
+        self.bases = list(bases)
+        arr = (ctypes.c_void_p * world)(*self.bases)
+        call("kgp_engine_set_peers", engine_handle, world, rank, self.row_start.ctypes.data, arr)
+        self._arr = arr
+
+    def close(self):
+        for p in self._opened:
+            self._call("kgp_peer_close", p)
+        self._opened = []
+        if self._own is not None:
+            self._call("kgp_peer_free", self._own)
+            self._own = None
+
+
+def enable_peer_exchange(ops, comm, k: int):
+    """Switch ``ops`` (CudaRowOps) to the fused all-gather operator for RHS blocks of k
+    columns: dist_pcg then calls ``ops.matmul_local(p_loc)`` instead of all_gather + product.
+    ``comm`` must split rows on multiples of 32 (``Comm(n, align=32)``)."""
+    starts = [r0 for r0, _ in comm.ranges] + [comm.n]
+    ops.peer = PeerTiles(ops.engine.handle, comm.world, comm.rank, starts, k, comm=comm)
+    ops.matmul_local = ops._matmul_peer
+    return ops
 
 
 def build_precond_factor(engine, m):

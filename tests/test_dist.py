@@ -272,3 +272,66 @@ def test_row_partitioned_fit_gloo(tmp_path):
     errfile = str(tmp_path / "err.txt")
     mp.spawn(_fit_worker, args=(2, _free_port(), errfile), nprocs=2, join=True)
     assert not os.path.exists(errfile), open(errfile).read()
+
+
+class PeerExchangeOps(OracleRowOps):
+    """dist_pcg's fused all-gather branch (``matmul_local``): the operator gets only the local
+    rows of P. The device path reads the peers' published tiles inside its kernel
+    (kgp_engine_peer_matmul); here the peers' rows arrive through a gloo all_gather."""
+
+    def __init__(self, x, r0, r1, ny, comm):
+        super().__init__(x, r0, r1, ny)
+        self.comm = comm
+        self.local_calls = 0
+
+    def matmul_local(self, p_loc):
+        self.local_calls += 1
+        # stand-in for the peers' published tiles (the base-class gather is not counted)
+        return self.matmul_rows(kdist.Comm.allgather_rows(self.comm, p_loc))
+
+
+class CountingComm(kdist.Comm):
+    def __init__(self, *a, **kw):
+        super().__init__(*a, **kw)
+        self.gathers = 0
+
+    def allgather_rows(self, x_loc, ranges=None):
+        self.gathers += 1
+        return super().allgather_rows(x_loc, ranges)
+
+
+def _peer_worker(rank, world, port, errfile):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        x, y, z = _problem()
+        n = len(y)
+        ny = orc.Nystrom(KT, x, L, F, S, 30)
+        comm = CountingComm(n, align=32)  # the fused operator's row blocks: 32-row boundaries
+        r0, r1 = comm.ranges[rank]
+        assert r0 % 32 == 0
+        ops = PeerExchangeOps(x, r0, r1, ny, comm)
+        res = kdist.dist_pcg(ops, comm, torch.from_numpy(np.ascontiguousarray(z.T[:, r0:r1])), 1e-10, 500, True,
+                             shift=S)
+        sol, al, be, rel, conv = orc.pcg(lambda b: orc.khat_matmul(KT, x, L, F, S, b), ny.apply_inverse, z, 1e-10,
+                                         500)
+        assert comm.gathers == 0 and ops.local_calls == int(res.iters.max())  # no separate operator all-gather
+        full = comm.allgather_rows(res.x).numpy().T
+        assert np.max(np.abs(full - sol)) <= 1e-6 * np.max(np.abs(sol)), "solution"
+        assert list(res.converged) == list(conv)
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as exc:
+        with open(errfile, "a") as fh:
+            fh.write(f"rank {rank}: {type(exc).__name__}: {exc}\n")
+        raise
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_partitioned_pcg_fused_exchange_gloo(tmp_path, world):
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    errfile = str(tmp_path / "err.txt")
+    mp.spawn(_peer_worker, args=(world, port, errfile), nprocs=world, join=True)
+    assert not os.path.exists(errfile), open(errfile).read()

@@ -806,3 +806,91 @@ def test_dense_mode_products_match_on_the_fly(pkg, n, k):
     got, ref = run(dense), run(otf)
     assert rel_max(got, ref) <= 1e-13
     assert np.array_equal(got, run(dense))  # fixed-order partial sums: run-to-run identical
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,n,k,nout", [(3, 3000, 16, 1), (2, 4100, 33, 2), (4, 8192, 32, 2)])
+def test_fused_allgather_operator_simulated_ranks(pkg, world, n, k, nout):
+    """The fused all-gather operator (kgp_engine_set_peers / peer_publish / peer_matmul): every
+    rank reads the other ranks' published RHS tiles inside its kernel. Ranks simulated on one
+    device (all buffers local, published before any rank multiplies): each rank's rows equal
+    its row block of the ordinary product -- bitwise when both use the same tile layout (same
+    kernel, same column split) -- over several epochs (the ready/done flag protocol). No kernel
+    here waits for a launch that has not run yet: all ranks publish before any multiplies."""
+    import ctypes
+
+    import torch
+
+    from paper_2503_02259_b200 import _lib, dist as kdist
+
+    rng = np.random.default_rng(world * 100 + k)
+    x = rng.standard_normal((n, 8))
+    hp = _hp(pkg, 1.1, 1.3, 0.05)
+    starts = [kdist.row_range(n, world, q, 32)[0] for q in range(world)] + [n]
+    engines, bases = [], []
+    for q in range(world):
+        e = pkg.KernelEngine(pkg.KernelType.GAUSSIAN, x, hp, precision="fast")
+        _lib.call("kgp_engine_set_rows", e.handle, starts[q], starts[q + 1] - starts[q])
+        nb, ptr = ctypes.c_int64(), ctypes.c_void_p()
+        _lib.call("kgp_engine_peer_buffer_bytes", e.handle, k, starts[q + 1] - starts[q], ctypes.byref(nb))
+        _lib.call("kgp_peer_alloc", nb.value, ctypes.byref(ptr), None)
+        engines.append(e)
+        bases.append(ptr.value)
+    tiles = [kdist.PeerTiles(engines[q].handle, world, q, starts, k, bases=bases) for q in range(world)]
+    st = torch.cuda.current_stream().cuda_stream
+    try:
+        for epoch in (1, 2, 3):
+            b = torch.randn(k, n, dtype=torch.float64, device="cuda")  # (k, n): column-major blocks
+            locs = [b[:, starts[q]:starts[q + 1]].contiguous() for q in range(world)]
+            for q in range(world):
+                nl = starts[q + 1] - starts[q]
+                _lib.call("kgp_engine_peer_publish", engines[q].handle, k, locs[q].data_ptr(), 1, nl, epoch, st)
+            for q in range(world):
+                nl = starts[q + 1] - starts[q]
+                outk = torch.empty((k, nl), dtype=torch.float64, device="cuda")
+                outl = torch.empty_like(outk) if nout == 2 else None
+                _lib.call("kgp_engine_peer_matmul", engines[q].handle, k, epoch, outk.data_ptr(),
+                          outl.data_ptr() if outl is not None else None, None, 1, nl, st)
+                ref_k = torch.empty_like(outk)
+                ref_l = torch.empty_like(outk) if nout == 2 else None
+                _lib.call("kgp_engine_matmul", engines[q].handle, k, b.data_ptr(), 1, n, ref_k.data_ptr(),
+                          ref_l.data_ptr() if ref_l is not None else None, None, 1, nl, st)
+                torch.cuda.synchronize()
+                if nout == 2 and k > 32:
+                    # the ordinary two-output product uses the LB layout here (bf16 lo parts);
+                    # published tiles are all-tf32: same precision class, not the same bits
+                    assert rel_max(outk.cpu().numpy(), ref_k.cpu().numpy()) <= 2e-5, (epoch, q)
+                    assert rel_max(outl.cpu().numpy(), ref_l.cpu().numpy()) <= 2e-4, (epoch, q)
+                else:
+                    assert torch.equal(outk, ref_k), (epoch, q)
+                    if nout == 2:
+                        assert torch.equal(outl, ref_l), (epoch, q)
+    finally:
+        for t in tiles:
+            t.close()
+        for p in bases:
+            _lib.call("kgp_peer_free", p)
+
+
+@pytest.mark.gpu
+def test_fused_allgather_operator_errors(pkg):
+    import ctypes
+
+    from paper_2503_02259_b200 import _lib
+    from paper_2503_02259_b200.errors import KernelGpError
+
+    x = np.random.default_rng(0).standard_normal((256, 3))
+    e64 = pkg.KernelEngine(pkg.KernelType.GAUSSIAN, x, _hp(pkg, 1, 1, 0.1), precision="fp64")
+    starts = (ctypes.c_int64 * 3)(0, 128, 256)
+    ptrs = (ctypes.c_void_p * 2)(1, 1)
+    with pytest.raises(ValueError, match="tensor-core"):
+        _lib.call("kgp_engine_set_peers", e64.handle, 2, 0, starts, ptrs)
+    ef = pkg.KernelEngine(pkg.KernelType.GAUSSIAN, x, _hp(pkg, 1, 1, 0.1), precision="fast")
+    with pytest.raises(KernelGpError, match="no peer configuration"):
+        _lib.call("kgp_engine_peer_publish", ef.handle, 4, 1, 1, 256, 1, None)
+    _lib.call("kgp_engine_set_rows", ef.handle, 0, 128)
+    bad = (ctypes.c_int64 * 3)(0, 100, 256)
+    with pytest.raises(ValueError, match="multiples of 32"):
+        _lib.call("kgp_engine_set_peers", ef.handle, 2, 0, bad, ptrs)
+    with pytest.raises(ValueError, match="not rank 1"):
+        _lib.call("kgp_engine_set_peers", ef.handle, 2, 1, starts, ptrs)

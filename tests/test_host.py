@@ -126,3 +126,17 @@ def test_build_tridiag_and_bands():
         solver.build_tridiag(solver.CgTrace(np.array([-1.0]), np.array([0.1]), 1, 0.0))
     with pytest.raises(ValueError):
         solver.slq_logdet([], [])
+
+
+def test_row_range_alignment():
+    """Row blocks of the fused all-gather operator start on column-block (32-row) boundaries
+    and still cover [0, n) in order; align=1 is the plain balanced split."""
+    from paper_2503_02259_b200 import dist as kdist
+
+    for n, world in ((3000, 3), (4100, 2), (65536, 8), (100, 8)):
+        rs = [kdist.row_range(n, world, q, 32) for q in range(world)]
+        assert rs[0][0] == 0 and rs[-1][1] == n
+        assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+        assert all(r0 % 32 == 0 for r0, _ in rs)
+        assert [kdist.row_range(n, world, q) for q in range(world)] == [
+            (q * n // world, (q + 1) * n // world) for q in range(world)]
