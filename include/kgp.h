@@ -119,8 +119,10 @@ int kgp_peer_open(const void* ipc_handle, void** dptr); /* map a peer's buffer (
 int kgp_peer_close(void* dptr);                         /* unmap an opened peer buffer */
 int kgp_peer_free(void* dptr);                          /* free an own kgp_peer_alloc buffer */
 int kgp_engine_peer_buffer_bytes(kgp_engine* e, int64_t k, int64_t own_rows, int64_t* bytes);
-/* engine rows must already be rank's block (kgp_engine_set_rows); bases[q] = rank q's buffer */
-int kgp_engine_set_peers(kgp_engine* e, int world, int rank, const int64_t* row_start, void* const* bases);
+/* engine rows must already be rank's block (kgp_engine_set_rows); bases[q] = rank q's buffer,
+ * sized by kgp_engine_peer_buffer_bytes for RHS blocks of up to k_cap columns */
+int kgp_engine_set_peers(kgp_engine* e, int world, int rank, const int64_t* row_start, void* const* bases,
+                         int64_t k_cap);
 /* b_loc: this rank's rows (nrows x k, strides b_rs / b_cs), valid until the matching peer_matmul */
 int kgp_engine_peer_publish(kgp_engine* e, int64_t k, const double* b_loc, int64_t b_rs, int64_t b_cs,
                             uint64_t epoch, void* stream);

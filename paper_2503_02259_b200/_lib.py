@@ -93,7 +93,7 @@ _SIGNATURES = {
     "kgp_peer_close": [c_vp],
     "kgp_peer_free": [c_vp],
     "kgp_engine_peer_buffer_bytes": [c_vp, c_i64, c_i64, _P(c_i64)],
-    "kgp_engine_set_peers": [c_vp, ctypes.c_int, ctypes.c_int, c_vp, c_vp],
+    "kgp_engine_set_peers": [c_vp, ctypes.c_int, ctypes.c_int, c_vp, c_vp, c_i64],
     "kgp_engine_peer_publish": [c_vp, c_i64, c_vp, c_i64, c_i64, ctypes.c_uint64, c_vp],
     "kgp_engine_peer_matmul": [c_vp, c_i64, ctypes.c_uint64, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp],
 }

@@ -887,7 +887,7 @@ extern "C" int kgp_engine_peer_buffer_bytes(kgp_engine* e, int64_t k, int64_t ow
 }
 
 extern "C" int kgp_engine_set_peers(kgp_engine* e, int world, int rank, const int64_t* row_start,
-                                    void* const* bases) {
+                                    void* const* bases, int64_t k_cap) {
   CHECK_ENGINE(e);
   KGP_REQUIRE(e->precision != KGP_FP64, KGP_ERR_INVALID, "the fused all-gather operator needs the tensor-core "
               "precision (fast or tf32)");
@@ -905,8 +905,10 @@ extern "C" int kgp_engine_set_peers(kgp_engine* e, int world, int rank, const in
               "engine rows [%lld, %lld) are not rank %d's block [%lld, %lld) (kgp_engine_set_rows first)",
               (long long)e->row0, (long long)(e->row0 + e->nrows), rank, (long long)row_start[rank],
               (long long)row_start[rank + 1]);
+  KGP_REQUIRE(k_cap >= 1, KGP_ERR_INVALID, "k_cap must be >= 1");
   e->pworld = world;
   e->prank = rank;
+  e->pkcap = k_cap;
   for (int q = 0; q <= world; ++q) e->prow[q] = row_start[q];
   for (int q = 0; q < world; ++q) e->pbase[q] = static_cast<uint8_t*>(bases[q]);
   bump_graph_epoch();
@@ -921,6 +923,9 @@ extern "C" int kgp_engine_peer_publish(kgp_engine* e, int64_t k, const double* b
   CHECK_ENGINE(e);
   KGP_REQUIRE(e->pworld > 0, KGP_ERR_STATE, "no peer configuration (kgp_engine_set_peers)");
   KGP_REQUIRE(epoch >= 1 && k >= 1 && b_loc != nullptr, KGP_ERR_INVALID, "bad publish arguments");
+  KGP_REQUIRE((k + 15) / 16 <= (e->pkcap + 15) / 16, KGP_ERR_INVALID,
+              "RHS block of %lld columns exceeds the peer buffers' capacity (%lld)", (long long)k,
+              (long long)e->pkcap);
   const int split = (e->precision == KGP_FAST) ? 3 : 1;
   KGP_REQUIRE(k <= tc_max_kp(e->dpad, 2, split, 1), KGP_ERR_INVALID,
               "the fused all-gather operator takes one launch's RHS block (k = %lld too wide)", (long long)k);

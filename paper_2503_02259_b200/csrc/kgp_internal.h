@@ -147,7 +147,7 @@ struct kgp_engine_s {
   int64_t prow[kgp::KGP_MAX_PEERS + 1] = {};
   uint8_t* pbase[kgp::KGP_MAX_PEERS] = {};
   const double* pb = nullptr;  // own rows of B from the last publish (the + s B term)
-  int64_t pb_rs = 0, pb_cs = 0, pk = 0;
+  int64_t pb_rs = 0, pb_cs = 0, pk = 0, pkcap = 0;
   bool prepared;
   // PCG workspace (grown on demand) and a pinned status word for the per-iteration readback
   kgp::DevBuf ws;

@@ -502,7 +502,7 @@ class PeerTiles:
                 bases.append(mapped.value)
         self.bases = list(bases)
         arr = (ctypes.c_void_p * world)(*self.bases)
-        call("kgp_engine_set_peers", engine_handle, world, rank, self.row_start.ctypes.data, arr)
+        call("kgp_engine_set_peers", engine_handle, world, rank, self.row_start.ctypes.data, arr, self.k)
         self._arr = arr
 
     def close(self):

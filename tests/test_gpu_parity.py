@@ -884,13 +884,13 @@ def test_fused_allgather_operator_errors(pkg):
     starts = (ctypes.c_int64 * 3)(0, 128, 256)
     ptrs = (ctypes.c_void_p * 2)(1, 1)
     with pytest.raises(ValueError, match="tensor-core"):
-        _lib.call("kgp_engine_set_peers", e64.handle, 2, 0, starts, ptrs)
+        _lib.call("kgp_engine_set_peers", e64.handle, 2, 0, starts, ptrs, 4)
     ef = pkg.KernelEngine(pkg.KernelType.GAUSSIAN, x, _hp(pkg, 1, 1, 0.1), precision="fast")
     with pytest.raises(KernelGpError, match="no peer configuration"):
         _lib.call("kgp_engine_peer_publish", ef.handle, 4, 1, 1, 256, 1, None)
     _lib.call("kgp_engine_set_rows", ef.handle, 0, 128)
     bad = (ctypes.c_int64 * 3)(0, 100, 256)
     with pytest.raises(ValueError, match="multiples of 32"):
-        _lib.call("kgp_engine_set_peers", ef.handle, 2, 0, bad, ptrs)
+        _lib.call("kgp_engine_set_peers", ef.handle, 2, 0, bad, ptrs, 4)
     with pytest.raises(ValueError, match="not rank 1"):
-        _lib.call("kgp_engine_set_peers", ef.handle, 2, 1, starts, ptrs)
+        _lib.call("kgp_engine_set_peers", ef.handle, 2, 1, starts, ptrs, 4)
