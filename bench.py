@@ -45,6 +45,10 @@ def parse():
     ap.add_argument("--ref-rows", type=int, default=2048, help="rows per step of the --impl reference arm")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--skip-nlml", action="store_true")
+    ap.add_argument("--exchange", default="replicated", choices=["replicated", "peer"],
+                    help="replicated: every rank holds all of Z (no exchange in the step); peer: each rank "
+                         "publishes its rows of Z and the fused all-gather operator reads the others' "
+                         "(kgp_engine_peer_*, DESIGN.md section 6)")
     return ap.parse_args()
 
 
@@ -160,7 +164,8 @@ def bench_config(args, w, world):
     return {"workload": "cfg2 standalone fused MatMul (BASELINE.json configs[1])", "n": w.n, "d": w.d,
             "k": w.z.shape[1], "kernel": "gaussian", "l": w.l, "f": w.f, "s": w.s,
             "outputs": ["Khat.Z", "dKhat/dl.Z"], "precision": args.precision,
-            "l2": "flushed (256 MB write) between timed iterations", "parallelism": f"rows{world}"}
+            "l2": "flushed (256 MB write) between timed iterations", "parallelism": f"rows{world}",
+            "exchange": args.exchange}
 
 
 def run_reference(args):
@@ -366,10 +371,13 @@ def run_gpu(args):
 
     w = workloads.cfg2(n=args.n, k=args.k)
     n, k = w.n, w.z.shape[1]
-    r0, r1 = rank * n // world, (rank + 1) * n // world
+    from paper_2503_02259_b200 import dist as kdist
+
+    peer = args.exchange == "peer"
+    r0, r1 = kdist.row_range(n, world, rank, 32 if peer else 1)
     hp = Hyperparams(w.l, w.f, w.s)
     eng = KernelEngine(KernelType.GAUSSIAN, w.x, hp, precision=args.precision)
-    if world > 1:
+    if world > 1 or peer:
         _lib.call("kgp_engine_set_rows", eng.handle, r0, r1 - r0)
     rows = r1 - r0
     zd = torch.from_numpy(w.z).cuda()
@@ -377,8 +385,30 @@ def run_gpu(args):
     out_l = torch.empty_like(out_k)
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # 256 MB > 126 MB L2
+    tiles = None
+    if peer:
+        starts = [kdist.row_range(n, world, q, 32)[0] for q in range(world)] + [n]
+        if world == 1:  # the fused path on one GPU: the rank reads its own published tiles
+            import ctypes
+
+            nb, ptr = ctypes.c_int64(), ctypes.c_void_p()
+            _lib.call("kgp_engine_peer_buffer_bytes", eng.handle, k, rows, ctypes.byref(nb))
+            _lib.call("kgp_peer_alloc", nb.value, ctypes.byref(ptr), None)
+            tiles = kdist.PeerTiles(eng.handle, 1, 0, starts, k, bases=[ptr.value])
+            tiles._own = ptr.value
+        else:
+            tiles = kdist.PeerTiles(eng.handle, world, rank, starts, k, comm=kdist.Comm(n, align=32))
+    zloc = zd[r0:r1]
+    epoch = [0]
 
     def step():
+        if peer:  # publish own rows of Z, then the operator pulls every rank's tiles
+            epoch[0] += 1
+            _lib.call("kgp_engine_peer_publish", eng.handle, k, zloc.data_ptr(), zloc.stride(0), zloc.stride(1),
+                      epoch[0], stream.cuda_stream)
+            _lib.call("kgp_engine_peer_matmul", eng.handle, k, epoch[0], out_k.data_ptr(), out_l.data_ptr(), None,
+                      out_k.stride(0), out_k.stride(1), stream.cuda_stream)
+            return
         _lib.call("kgp_engine_matmul", eng.handle, k, zd.data_ptr(), zd.stride(0), zd.stride(1),
                   out_k.data_ptr(), out_l.data_ptr(), None, out_k.stride(0), out_k.stride(1), stream.cuda_stream)
 
@@ -480,6 +510,11 @@ def run_gpu(args):
             line["nlml"] = nlml_metric(cpu=not args.no_cpu_baseline)
             line["nlml_cfg3"] = nlml_cfg3_metric()
         print(json.dumps(line))
+    if tiles is not None:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()  # no rank unmaps a buffer another may still read
+        tiles.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
