@@ -190,6 +190,15 @@ def dist_pcg(ops, comm: Comm, y_loc, tol, max_iter: int, precondition, shift: fl
     return DistSolve(x, alphas, betas, iters, rel, rel <= tol)
 
 
+def _grads(ops, comm, v_loc):
+    """This rank's rows of dKhat/dl V and dKhat/df V: through the fused all-gather operator
+    when ``ops`` has one (``grads_local``), else all_gather + row-block product."""
+    local = getattr(ops, "grads_local", None)
+    if local is not None:
+        return local(v_loc)
+    return ops.grads_rows(comm.allgather_rows(v_loc))
+
+
 def dist_nlml_grad(ops, comm: Comm, y_loc, probes_loc, norms_sq, tol, max_iter, probe_tol=None,
                    precondition=True, shift=1.0, probe_max_iter=None):
     """nlml_grad_iterative (gp.py:133-179) over row-sharded vectors.
@@ -215,7 +224,7 @@ def dist_nlml_grad(ops, comm: Comm, y_loc, probes_loc, norms_sq, tol, max_iter, 
     loss = 0.5 * (yw + logdet + comm.n * LOG_2PI)
     v_loc = torch.cat([w[None, :], probes_loc], dim=0)
     u_loc = torch.cat([w[None, :], us.x], dim=0)
-    dl, df = ops.grads_rows(comm.allgather_rows(v_loc))
+    dl, df = _grads(ops, comm, v_loc)
     part = torch.stack([(u_loc * dl).sum(dim=1), (u_loc * df).sum(dim=1), (u_loc * v_loc).sum(dim=1)])
     part = comm.allreduce(part).cpu().numpy()
     grads = [0.5 * (-part[t, 0] + part[t, 1:].sum() / kz) for t in range(3)]
@@ -253,7 +262,7 @@ def dist_gpc_nlml_grad(ops, comm: Comm, targets_loc, noise_loc, probes_loc, norm
     yw = comm.allreduce((targets_loc * w).sum(dim=1)).cpu().numpy()
     v_loc = torch.cat([w, probes_loc], dim=0)
     u_loc = torch.cat([w, sol.x[c:]], dim=0)
-    dl, df = ops.grads_rows(comm.allgather_rows(v_loc))
+    dl, df = _grads(ops, comm, v_loc)
     part = torch.stack([(u_loc * dl).sum(dim=1), (u_loc * df).sum(dim=1), (u_loc * v_loc).sum(dim=1)])
     part = comm.allreduce(part).cpu().numpy()
     for k in range(c):
@@ -392,6 +401,18 @@ class CudaRowOps:
                    st)
         return out
 
+    def _grads_peer(self, v_loc):
+        """dKhat/dl and dKhat/df on this rank's rows from the local rows of V (fused all-gather)."""
+        k, nloc = v_loc.shape
+        v_loc = v_loc.contiguous()
+        dl, df = self._out(k), self._out(k)
+        self._epoch = getattr(self, "_epoch", 0) + 1
+        st = self._device.stream_ptr()
+        self._call("kgp_engine_peer_publish", self.engine.handle, k, v_loc.data_ptr(), 1, nloc, self._epoch, st)
+        self._call("kgp_engine_peer_matmul", self.engine.handle, k, self._epoch, None, dl.data_ptr(), df.data_ptr(), 1,
+                   nloc, st)
+        return dl, df
+
     def matmul_rows(self, p_full):
         k, n = p_full.shape
         out = self._out(k)
@@ -521,6 +542,7 @@ def enable_peer_exchange(ops, comm, k: int):
     starts = [r0 for r0, _ in comm.ranges] + [comm.n]
     ops.peer = PeerTiles(ops.engine.handle, comm.world, comm.rank, starts, k, comm=comm)
     ops.matmul_local = ops._matmul_peer
+    ops.grads_local = ops._grads_peer
     return ops
 
 

@@ -289,6 +289,10 @@ class PeerExchangeOps(OracleRowOps):
         # stand-in for the peers' published tiles (the base-class gather is not counted)
         return self.matmul_rows(kdist.Comm.allgather_rows(self.comm, p_loc))
 
+    def grads_local(self, v_loc):
+        self.local_calls += 1
+        return self.grads_rows(kdist.Comm.allgather_rows(self.comm, v_loc))
+
 
 class CountingComm(kdist.Comm):
     def __init__(self, *a, **kw):
@@ -319,6 +323,14 @@ def _peer_worker(rank, world, port, errfile):
         full = comm.allgather_rows(res.x).numpy().T
         assert np.max(np.abs(full - sol)) <= 1e-6 * np.max(np.abs(sol)), "solution"
         assert list(res.converged) == list(conv)
+        # NLML + gradient: the solves and the derivative products all go through the fused path
+        g0 = comm.gathers
+        got = kdist.dist_nlml_grad(ops, comm, torch.from_numpy(y[r0:r1].copy()),
+                                   torch.from_numpy(np.ascontiguousarray(z.T[:, r0:r1])),
+                                   np.einsum("ij,ij->j", z, z), 1e-10, 3000, precondition=True, shift=S)
+        ref = orc.nlml_grad(KT, x, y, L, F, S, z, ny, tol=1e-10, max_iter=3000)
+        assert np.all(np.abs(np.array(got[:4]) - np.array(ref[:4])) <= 1e-8 * np.abs(np.array(ref[:4]))), (got, ref)
+        assert comm.gathers == g0  # no operator all-gather anywhere in the evaluation
         dist.barrier()
         dist.destroy_process_group()
     except Exception as exc:
