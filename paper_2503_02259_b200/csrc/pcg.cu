@@ -717,12 +717,25 @@ int pcg_grouped_impl(kgp_engine_s* e, const PcSet& pcs, int64_t k, int64_t kpc, 
       // iterations run a graph over the group-1 prefix [0, kpc) only: the state is column-major
       // with group 1 first, so the same buffers serve both graphs
       bool narrow = !(kpc > 0 && kpc < k);
+      auto go_narrow = [&]() -> int {
+        PcgGroups gn = g;
+        gn.kz = g.kz < g.kpc ? g.kz : g.kpc;
+        int rc2 = pcg_graph(e, pcs, kpc, gn, B, &exec, &gk);
+        narrow = true;
+        return rc2;
+      };
       int launched = 1, checked = 1;
       while (launched < max_iter && !done) {
         KGP_CUDA(cudaGraphLaunch(exec, st));
         count_launches(gk);
         KGP_CUDA(cudaEventRecord(e->events[launched % kLookahead], st));
         ++launched;
+        // every group-2 column stops by its cap it2 at the latest: after it2 iterations the
+        // narrow graph is exact without waiting for the (look-ahead delayed) history
+        if (!narrow && launched >= g.it2) {
+          rc = go_narrow();
+          if (rc) return rc;
+        }
         if (launched - checked >= kLookahead) {
           KGP_CUDA(cudaEventSynchronize(e->events[checked % kLookahead]));
           if (H[HIST * checked + 1]) {
@@ -732,11 +745,8 @@ int pcg_grouped_impl(kgp_engine_s* e, const PcSet& pcs, int64_t k, int64_t kpc, 
           }
           done = (H[HIST * checked] == 0);
           if (!done && !narrow && H[HIST * checked] == H[HIST * checked + 2]) {
-            PcgGroups gn = g;
-            gn.kz = g.kz < g.kpc ? g.kz : g.kpc;
-            rc = pcg_graph(e, pcs, kpc, gn, B, &exec, &gk);
+            rc = go_narrow();
             if (rc) return rc;
-            narrow = true;
           }
           ++checked;
         }
