@@ -195,6 +195,7 @@ static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t 
     p.out_df = out_df ? out_df + c0 * o_cs : nullptr;
     p.o_rs = o_rs;
     p.o_cs = o_cs;
+    p.gate = e->gate;
     if (peer_epoch) {
       p.npeer = e->pworld;
       for (int q = 0; q < e->pworld; ++q) {
@@ -321,6 +322,7 @@ static int engine_matmul_core(kgp_engine_s* e, int64_t k, const double* b, int64
   }
   if (e->precision == KGP_FP64) {
     F64Params p{};
+    p.gate = e->gate;
     p.xr = e->x64.as<double>() + e->row0 * e->d;
     p.xc = e->x64.as<double>();
     p.nrows = e->nrows;

@@ -39,6 +39,7 @@ struct TcParams {
   // fused all-gather (kgp_engine_peer_matmul): npeer > 0 -> the RHS tiles of column block g
   // come from the owner rank q's published buffer ptile[q] (block g - pblk0[q]), read after
   // that rank's ready flag reaches `epoch`
+  const int32_t* gate;    // non-NULL: skip the launch when *gate == 0 (PCG: no active column left)
   int npeer;
   int pblk0[KGP_MAX_PEERS + 1];
   const uint8_t* ptile[KGP_MAX_PEERS];
@@ -70,6 +71,7 @@ struct F64Params {
   double *out_k, *out_dl, *out_df;
   int64_t o_rs, o_cs;
   int64_t jchunk;          // columns per grid.z split (set by launch_kmm_f64)
+  const int32_t* gate;     // non-NULL: skip the launch when *gate == 0 (PCG: no active column left)
   double* part;            // split partials (set by launch_kmm_f64)
   int64_t part_stride;
 };
@@ -148,6 +150,9 @@ struct kgp_engine_s {
   uint8_t* pbase[kgp::KGP_MAX_PEERS] = {};
   const double* pb = nullptr;  // own rows of B from the last publish (the + s B term)
   int64_t pb_rs = 0, pb_cs = 0, pk = 0, pkcap = 0;
+  // set by the PCG driver while it captures its iteration graph: the active-column count the
+  // operator launches check first, so iterations replayed past convergence skip the product
+  const int32_t* gate = nullptr;
   bool prepared;
   // PCG workspace (grown on demand) and a pinned status word for the per-iteration readback
   kgp::DevBuf ws;

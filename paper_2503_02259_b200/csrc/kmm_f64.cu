@@ -25,6 +25,7 @@ constexpr int MAXD = 16;
 
 template <int KT, int NOUT, int KS, int DB>
 __global__ void __launch_bounds__(NT) kmm_f64_kernel(const F64Params p) {
+  if (p.gate != nullptr && *p.gate == 0) return;  // PCG iteration past convergence
   __shared__ double sXj[TJ][DB + 1];
   __shared__ __align__(16) double sB[TJ][KS];
 
@@ -104,6 +105,7 @@ __global__ void __launch_bounds__(NT) kmm_f64_kernel(const F64Params p) {
 
 // sum the column-split partials in split order, then the epilogue
 __global__ void f64_reduce_kernel(const F64Params p, int nsplit) {
+  if (p.gate != nullptr && *p.gate == 0) return;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= p.nrows * p.k) return;
   const int64_t r = e / p.k;

@@ -245,6 +245,7 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
   static_assert(!LB || (NOUT == 2 && SPLIT == 3), "LB layout: fused two-output 3xTF32");
   constexpr uint32_t VBYTES = G::VBYTES;
   constexpr bool NEED_G = (NOUT == 2);
+  if (p.gate != nullptr && *p.gate == 0) return;  // PCG iteration past convergence: nothing to do
 
   extern __shared__ __align__(1024) uint8_t smem[];
   const int KP = p.kp;
@@ -677,6 +678,7 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
 
 // sum the grid.y column-split partials in split order, then the epilogue of kmm_tc_kernel
 __global__ void tc_reduce_kernel(const TcParams p, int nsplit, int nacc) {
+  if (p.gate != nullptr && *p.gate == 0) return;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= p.nrows * p.k) return;
   const int64_t r = e / p.k;

@@ -542,7 +542,9 @@ int pcg_graph(kgp_engine_s* e, const PcSet& pcs, int64_t k, const PcgGroups& g, 
   cudaGraph_t graph = nullptr;
   const int64_t counted = kgp_launch_count();
   KGP_CUDA(cudaStreamBeginCapture(e->cstream, cudaStreamCaptureModeRelaxed));
+  e->gate = B.S.status;  // status[0]: active columns after the previous iteration's beta
   int rc = enqueue_iteration(e, pcs, k, g, B, e->cstream);
+  e->gate = nullptr;
   cudaError_t ce = cudaStreamEndCapture(e->cstream, &graph);
   count_launches(counted - kgp_launch_count());  // captured, not launched
   if (rc) {
