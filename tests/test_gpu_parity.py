@@ -865,6 +865,25 @@ def test_fused_allgather_operator_simulated_ranks(pkg, world, n, k, nout):
                     assert torch.equal(outk, ref_k), (epoch, q)
                     if nout == 2:
                         assert torch.equal(outl, ref_l), (epoch, q)
+        # derivative-only outputs (dist_nlml_grad's grads_local: out_k NULL, dL and dF)
+        epoch = 4
+        b = torch.randn(k, n, dtype=torch.float64, device="cuda")
+        locs = [b[:, starts[q]:starts[q + 1]].contiguous() for q in range(world)]
+        for q in range(world):
+            nl = starts[q + 1] - starts[q]
+            _lib.call("kgp_engine_peer_publish", engines[q].handle, k, locs[q].data_ptr(), 1, nl, epoch, st)
+        for q in range(world):
+            nl = starts[q + 1] - starts[q]
+            dl, df = (torch.empty((k, nl), dtype=torch.float64, device="cuda") for _ in range(2))
+            _lib.call("kgp_engine_peer_matmul", engines[q].handle, k, epoch, None, dl.data_ptr(), df.data_ptr(), 1,
+                      nl, st)
+            rl, rf = torch.empty_like(dl), torch.empty_like(df)
+            _lib.call("kgp_engine_matmul", engines[q].handle, k, b.data_ptr(), 1, n, None, rl.data_ptr(),
+                      rf.data_ptr(), 1, nl, st)
+            torch.cuda.synchronize()
+            tol_l = 2e-4 if k > 32 else 0.0  # LB layout in the ordinary two-output product for k > 32
+            assert rel_max(dl.cpu().numpy(), rl.cpu().numpy()) <= tol_l, q
+            assert rel_max(df.cpu().numpy(), rf.cpu().numpy()) <= (2e-5 if k > 32 else 0.0), q
     finally:
         for t in tiles:
             t.close()
