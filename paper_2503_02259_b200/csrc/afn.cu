@@ -736,11 +736,7 @@ extern "C" int kgp_local_variance(int kernel, int64_t nq, int d, const double* x
   switch (kernel) {
 #define KGP_LV_CASE(K)                                                                                          \
   case K: {                                                                                                     \
-    static bool configured = false;                                                                             \
-    if (!configured) {                                                                                          \
-      KGP_CUDA(cudaFuncSetAttribute(local_var_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-      configured = true;                                                                                        \
-    }                                                                                                           \
+    KGP_SMEM_ATTR(local_var_kernel<K>, smem);                                                            \
     local_var_kernel<K><<<(unsigned)nq, FS_T, smem, st>>>(nq, d, xq, x, l, f * f, s, npt, nbr, var,            \
                                                           status.as<int32_t>());                                \
     break;                                                                                                      \
@@ -775,11 +771,7 @@ extern "C" int kgp_afn_fsai(int kernel, int64_t n2, int d, const double* x2, dou
   switch (kernel) {
 #define KGP_FSAI_CASE(K)                                                                                   \
   case K: {                                                                                                \
-    static bool configured = false;                                                                        \
-    if (!configured) {                                                                                     \
-      KGP_CUDA(cudaFuncSetAttribute(fsai_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-      configured = true;                                                                                   \
-    }                                                                                                      \
+    KGP_SMEM_ATTR(fsai_kernel<K>, smem);                                                            \
     fsai_kernel<K><<<(unsigned)n2, FS_T, smem, st>>>(n2, d, x2, l, f2, s, m, w, npt, nbr, dshift, gval,    \
                                                     gcol, status.as<int32_t>());                           \
     break;                                                                                                 \

@@ -205,6 +205,7 @@ static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t 
       }
       p.pblk0[e->pworld] = nblk;
       p.epoch = peer_epoch;
+      p.ptimeout_ns = e->ptimeout_ns;
     }
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if (e->timing && cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusNone) {
@@ -829,14 +830,14 @@ extern "C" int kgp_slq_logdet(int64_t k, int32_t max_iter, const double* alphas,
 // ------------------------------------------------------------------ fused all-gather + operator
 namespace {
 
-__global__ void peer_wait_done_kernel(int world, int rank, unsigned long long want,
+__global__ void peer_wait_done_kernel(int world, int rank, unsigned long long want, unsigned long long timeout_ns,
                                       const unsigned long long* f0, const unsigned long long* f1,
                                       const unsigned long long* f2, const unsigned long long* f3,
                                       const unsigned long long* f4, const unsigned long long* f5,
                                       const unsigned long long* f6, const unsigned long long* f7) {
   const unsigned long long* f[8] = {f0, f1, f2, f3, f4, f5, f6, f7};
   const int q = threadIdx.x;
-  if (q < world && q != rank) kgp::peer_wait_flag(f[q], want);
+  if (q < world && q != rank) kgp::peer_wait_flag(f[q], want, timeout_ns);
 }
 
 __global__ void peer_flag_kernel(unsigned long long* flag, unsigned long long v) { kgp::peer_set_flag(flag, v); }
@@ -888,6 +889,18 @@ extern "C" int kgp_engine_peer_buffer_bytes(kgp_engine* e, int64_t k, int64_t ow
   return KGP_OK;
 }
 
+// A peer configuration is valid only for the precision and row block it was set up with
+// (tile sizes and block ownership depend on both); later set_precision / set_rows calls
+// invalidate it, and publish / peer_matmul re-check before touching the shared buffers.
+static int peer_check(const kgp_engine* e) {
+  KGP_REQUIRE(e->pworld > 0, KGP_ERR_STATE, "no peer configuration (kgp_engine_set_peers)");
+  KGP_REQUIRE(e->precision == e->pprec && e->precision != KGP_FP64, KGP_ERR_STATE,
+              "engine precision changed since kgp_engine_set_peers (call it again)");
+  KGP_REQUIRE(e->row0 == e->prow[e->prank] && e->nrows == e->prow[e->prank + 1] - e->prow[e->prank], KGP_ERR_STATE,
+              "engine rows changed since kgp_engine_set_peers (call it again)");
+  return KGP_OK;
+}
+
 extern "C" int kgp_engine_set_peers(kgp_engine* e, int world, int rank, const int64_t* row_start,
                                     void* const* bases, int64_t k_cap) {
   CHECK_ENGINE(e);
@@ -910,7 +923,18 @@ extern "C" int kgp_engine_set_peers(kgp_engine* e, int world, int rank, const in
   KGP_REQUIRE(k_cap >= 1, KGP_ERR_INVALID, "k_cap must be >= 1");
   e->pworld = world;
   e->prank = rank;
+  e->pprec = e->precision;
   e->pkcap = k_cap;
+  {
+    // Peer waits trap after this long (a trapped context is lost for the process: size it
+    // well above any host-side skew between ranks). KGP_PEER_TIMEOUT_S overrides.
+    double sec = 600.0;
+    if (const char* v = getenv("KGP_PEER_TIMEOUT_S")) {
+      const double t = atof(v);
+      if (t > 0) sec = t;
+    }
+    e->ptimeout_ns = (unsigned long long)(sec * 1e9);
+  }
   for (int q = 0; q <= world; ++q) e->prow[q] = row_start[q];
   for (int q = 0; q < world; ++q) e->pbase[q] = static_cast<uint8_t*>(bases[q]);
   bump_graph_epoch();
@@ -923,7 +947,8 @@ extern "C" int kgp_engine_set_peers(kgp_engine* e, int world, int rank, const in
 extern "C" int kgp_engine_peer_publish(kgp_engine* e, int64_t k, const double* b_loc, int64_t b_rs, int64_t b_cs,
                                        uint64_t epoch, void* stream) {
   CHECK_ENGINE(e);
-  KGP_REQUIRE(e->pworld > 0, KGP_ERR_STATE, "no peer configuration (kgp_engine_set_peers)");
+  int prc = peer_check(e);
+  if (prc) return prc;
   KGP_REQUIRE(epoch >= 1 && k >= 1 && b_loc != nullptr, KGP_ERR_INVALID, "bad publish arguments");
   KGP_REQUIRE((k + 15) / 16 <= (e->pkcap + 15) / 16, KGP_ERR_INVALID,
               "RHS block of %lld columns exceeds the peer buffers' capacity (%lld)", (long long)k,
@@ -935,7 +960,8 @@ extern "C" int kgp_engine_peer_publish(kgp_engine* e, int64_t k, const double* b
   cudaStream_t st = (cudaStream_t)stream;
   const unsigned long long* f[KGP_MAX_PEERS] = {};
   for (int q = 0; q < e->pworld; ++q) f[q] = reinterpret_cast<const unsigned long long*>(e->pbase[q] + 8);  // done
-  peer_wait_done_kernel<<<1, 32, 0, st>>>(e->pworld, e->prank, (unsigned long long)(epoch - 1), f[0], f[1],
+  peer_wait_done_kernel<<<1, 32, 0, st>>>(e->pworld, e->prank, (unsigned long long)(epoch - 1), e->ptimeout_ns,
+                                          f[0], f[1],
                                           f[2], f[3], f[4], f[5], f[6], f[7]);
   KGP_LAUNCH("peer_wait_done_kernel");
   const int kp = (int)((k + 15) / 16 * 16);
@@ -956,7 +982,8 @@ extern "C" int kgp_engine_peer_publish(kgp_engine* e, int64_t k, const double* b
 extern "C" int kgp_engine_peer_matmul(kgp_engine* e, int64_t k, uint64_t epoch, double* out_k, double* out_dl,
                                       double* out_df, int64_t o_rs, int64_t o_cs, void* stream) {
   CHECK_ENGINE(e);
-  KGP_REQUIRE(e->pworld > 0, KGP_ERR_STATE, "no peer configuration (kgp_engine_set_peers)");
+  int prc = peer_check(e);
+  if (prc) return prc;
   KGP_REQUIRE(e->pb != nullptr && k == e->pk, KGP_ERR_STATE, "kgp_engine_peer_publish(k = %lld) must precede",
               (long long)k);
   KGP_REQUIRE(out_k || out_dl || out_df, KGP_ERR_INVALID, "no output requested");

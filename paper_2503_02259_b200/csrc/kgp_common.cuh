@@ -1,6 +1,7 @@
 // Shared device helpers for libkgp (sm_100a only).
 #pragma once
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdio>
 #include <stdint.h>
 
@@ -24,6 +25,19 @@ void count_launches(int64_t n);
     ::kgp::count_launches(1);                                  \
     int _rc = ::kgp::cuda_check(cudaGetLastError(), what);     \
     if (_rc != KGP_OK) return _rc;                             \
+  } while (0)
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device context: raise it once per
+// (kernel, device), tracked in a per-call-site bitmask (devices 0..63), thread-safe.
+#define KGP_SMEM_ATTR(kern, bytes)                                                                   \
+  do {                                                                                               \
+    static std::atomic<uint64_t> _kgp_smem_mask{0};                                                  \
+    int _dev = 0;                                                                                    \
+    KGP_CUDA(cudaGetDevice(&_dev));                                                                  \
+    const uint64_t _bit = 1ull << (_dev & 63);                                                       \
+    if (!(_kgp_smem_mask.load(std::memory_order_acquire) & _bit)) {                                  \
+      KGP_CUDA(cudaFuncSetAttribute((kern), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(bytes))); \
+      _kgp_smem_mask.fetch_or(_bit, std::memory_order_acq_rel);                                      \
+    }                                                                                                \
   } while (0)
 #define KGP_REQUIRE(cond, code, ...)                           \
   do {                                                         \
@@ -125,9 +139,12 @@ KGP_DEV void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, uint
 
 // ---------------------------------------------------------------- cross-GPU flags (fused all-gather)
 // Bounded wait for a peer's flag (system-scope acquire): a peer that never arrives traps the
-// kernel after `timeout_ns` (a CUDA error on the host) instead of hanging the device.
+// kernel after `timeout_ns` instead of hanging the device. A trap is a sticky CUDA error:
+// the process's context is lost, so the bound (KGP_PEER_TIMEOUT_S, default 600 s) must sit
+// far above any host-side skew between ranks; dist.py barriers at set_peers and before the
+// first publish so only device progress is ever waited on.
 KGP_DEV void peer_wait_flag(const unsigned long long* flag, unsigned long long want,
-                            unsigned long long timeout_ns = 20000000000ull) {
+                            unsigned long long timeout_ns) {
   unsigned long long t0, now, v;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   for (;;) {

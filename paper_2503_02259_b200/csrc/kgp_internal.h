@@ -45,6 +45,7 @@ struct TcParams {
   const uint8_t* ptile[KGP_MAX_PEERS];
   const unsigned long long* pready[KGP_MAX_PEERS];
   unsigned long long epoch;
+  unsigned long long ptimeout_ns;  // bounded peer-flag wait (KGP_PEER_TIMEOUT_S, default 600 s)
 };
 int tc_pad_dim(int d);
 int tc_max_kp(int dpad, int nout, int split, int nab);
@@ -145,7 +146,8 @@ struct kgp_engine_s {
   kgp::DevBuf tcpart;      // fast operator column-split partials
   // fused all-gather (kgp_engine_set_peers): rank `prank` of `pworld`, rows prow[q]..prow[q+1]
   // of B owned by rank q, whose buffer (flags + tiles) is mapped at pbase[q]
-  int pworld = 0, prank = 0;
+  int pworld = 0, prank = 0, pprec = 0;
+  unsigned long long ptimeout_ns = 0;
   int64_t prow[kgp::KGP_MAX_PEERS + 1] = {};
   uint8_t* pbase[kgp::KGP_MAX_PEERS] = {};
   const double* pb = nullptr;  // own rows of B from the last publish (the + s B term)

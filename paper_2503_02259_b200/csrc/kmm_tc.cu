@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
         int q = owner < 0 ? 0 : owner;
         while (q + 1 < p.npeer && tg >= p.pblk0[q + 1]) ++q;
         if (q != owner) {  // first block of this owner in the sweep: wait for its tiles
-          if (elect_one()) peer_wait_flag(p.pready[q], p.epoch);
+          if (elect_one()) peer_wait_flag(p.pready[q], p.epoch, p.ptimeout_ns);
           __syncwarp();
           owner = q;
         }
@@ -710,11 +710,7 @@ int launch_one(const TcParams& p_in, cudaStream_t st) {
   p.nsb = (fixed + 8 * stage <= limit) ? 8 : 4;  // deeper prefetch when shared memory allows
   const size_t smem = fixed + p.nsb * stage;
   KGP_REQUIRE(smem <= limit, KGP_ERR_INVALID, "fast operator tile config needs %zu B of shared memory", smem);
-  static bool configured = false;  // one attribute call per instantiation
-  if (!configured) {
-    KGP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)limit));
-    configured = true;
-  }
+  KGP_SMEM_ATTR(kern, limit);
   const int nsplit = (p.nblk + p.nper - 1) / p.nper;
   dim3 grid((unsigned)((p.nrows + 127) / 128), (unsigned)nsplit);
   if (p.ev_start) KGP_CUDA(cudaEventRecord(p.ev_start, st));

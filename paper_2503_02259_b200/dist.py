@@ -500,6 +500,7 @@ class PeerTiles:
         from paper_2503_02259_b200._lib import call
 
         self._call = call
+        self.comm = comm
         self.world, self.rank, self.k = world, rank, int(k)
         self.row_start = np.asarray(row_start, dtype=np.int64)
         self._opened, self._own = [], None
@@ -525,14 +526,30 @@ class PeerTiles:
         arr = (ctypes.c_void_p * world)(*self.bases)
         call("kgp_engine_set_peers", engine_handle, world, rank, self.row_start.ctypes.data, arr, self.k)
         self._arr = arr
+        # every rank is configured before any rank publishes: the only waits the device ever
+        # does on a peer flag are then for device progress, never for a peer's host setup
+        if comm is not None:
+            comm.dist.barrier(group=comm.group)
 
     def close(self):
+        """Tear down safely: this rank's kernels finish (sync), then every rank's (barrier),
+        before any mapping is closed or the exported buffer freed -- a peer's operator may
+        still be reading this rank's tiles over NVLink until it has passed the barrier."""
+        if self._opened or self._own is not None:
+            import torch
+
+            if torch.cuda.is_available():
+                torch.cuda.synchronize()
+            if self.comm is not None:
+                self.comm.dist.barrier(group=self.comm.group)
         for p in self._opened:
             self._call("kgp_peer_close", p)
         self._opened = []
         if self._own is not None:
             self._call("kgp_peer_free", self._own)
             self._own = None
+        if self.comm is not None:  # nobody frees its buffer while a peer still maps it
+            self.comm.dist.barrier(group=self.comm.group)
 
 
 def enable_peer_exchange(ops, comm, k: int):
