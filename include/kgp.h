@@ -42,6 +42,8 @@ extern "C" {
 #define KGP_FP64 0  /* fp64 tile, fp64 contraction (parity anchor)                        */
 #define KGP_FAST 1  /* fp32 centred tile + 3xTF32 tcgen05 contraction, fp32 TMEM accumulation */
 #define KGP_TF32 2  /* fp32 centred tile + 1xTF32 tcgen05 contraction (throughput mode)     */
+#define KGP_BF16X3 3 /* fp32 centred tile split into two bf16 terms, contraction A0B0 + A0B1 + A1B0
+                        (kind::f16, K=16), fp32 TMEM accumulation (MatMul throughput mode)     */
 
 /* preconditioner kinds (kgp_precond_kind) */
 #define KGP_PRECOND_NYSTROM 0

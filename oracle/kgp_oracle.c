@@ -113,3 +113,32 @@ int kgpo_matmul(int kt, int64_t n, int d, const double* x, double l, double f, d
   }
   return 0;
 }
+
+/* Materialised rectangular panel (kernels.py:79-94 via the numba panels, _panels_numba.py:37-131,
+ * prange over rows): out[i,j] = scale * kappa(x_i, y_j) (which = 0) or scale * dkappa/dl (which = 1),
+ * plus `diag` on i == j when add_diag (Khat = f^2 kappa + s I, kmat.py:107-120). Row-major (nx, ny).
+ * The reference's DENSE mode (auto for n <= 20000) builds these with every host core; the CPU
+ * baseline of the NLML metric does the same here. */
+int kgpo_panel(int kt, int which, int64_t nx, int64_t ny, int d, const double* x, const double* y, double l,
+               double scale, double diag, int add_diag, double* out, int nthreads) {
+  if (kt < 0 || kt > 2 || which < 0 || which > 1 || nx < 0 || ny < 0 || d < 1) return 1;
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < nx; ++i) {
+    const double* xi = x + i * d;
+    double* o = out + i * ny;
+    for (int64_t j = 0; j < ny; ++j) {
+      const double* yj = y + j * d;
+      double acc = 0.0;
+      for (int q = 0; q < d; ++q) {
+        double diff = xi[q] - yj[q];
+        acc += diff * diff;
+      }
+      o[j] = scale * (which == 0 ? kappa(kt, acc, l) : dkappa(kt, acc, l));
+    }
+    if (add_diag && i < ny) o[i] += diag;
+  }
+  return 0;
+}

@@ -30,6 +30,11 @@ def lib():
             ctypes.c_double, ctypes.c_double, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
         _lib.kgpo_max_threads.restype = ctypes.c_int
+        _lib.kgpo_panel.restype = ctypes.c_int
+        _lib.kgpo_panel.argtypes = [
+            ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
+            ctypes.c_void_p, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_void_p,
+            ctypes.c_int]
     return _lib
 
 
@@ -54,3 +59,18 @@ def matmul(kt, x, l, f, s, b, row0=0, nrows=None, want_k=True, want_dl=False, nt
     if rc != 0:
         raise ValueError("kgpo_matmul: bad arguments")
     return ok, od
+
+
+def panel(kt, x, y, l, which="k", scale=1.0, diag=0.0, nthreads=0):
+    """scale * kappa(x, y) (which "k") or scale * dkappa/dl (which "l"), plus ``diag`` on the
+    diagonal when diag != 0 (Khat = f^2 kappa + s I): the materialised panels of kernels.py:79-94
+    / kmat.py:107-141, OpenMP over rows like the numba prange panels."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    out = np.empty((x.shape[0], y.shape[0]))
+    rc = lib().kgpo_panel(KERNEL_IDS[kt], 0 if which == "k" else 1, x.shape[0], y.shape[0], x.shape[1],
+                          x.ctypes.data, y.ctypes.data, l, scale, diag, int(diag != 0.0), out.ctypes.data,
+                          nthreads)
+    if rc != 0:
+        raise ValueError("kgpo_panel: bad arguments")
+    return out

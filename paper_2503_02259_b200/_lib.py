@@ -24,7 +24,7 @@ LIB_PATH = os.environ.get("KGP_LIB") or os.path.join(HERE, "libkgp.so")  # KGP_L
 
 OK, ERR_INVALID, ERR_RESOURCE, ERR_BREAKDOWN, ERR_NUMERICAL, ERR_CUDA, ERR_STATE = range(7)
 KERNEL_IDS = {"gaussian": 0, "matern32": 1, "matern52": 2}
-PRECISIONS = {"fp64": 0, "fast": 1, "tf32": 2}
+PRECISIONS = {"fp64": 0, "fast": 1, "tf32": 2, "bf16x3": 3}
 
 _EXC = {
     ERR_INVALID: ValueError,

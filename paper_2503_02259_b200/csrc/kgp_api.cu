@@ -87,17 +87,19 @@ static int tc_env_int(const char* name, int dflt) {
   return s ? atoi(s) : dflt;
 }
 
-// blocks (x32 columns) accumulated in TMEM before promotion: 8 with two accumulator buffers
-// (the drain overlaps the MMA), 16 with one (each promotion stalls the MMA: k = 64 two
-// outputs 4.93 -> 4.62 ms; error 2.7e-6 -> 3.9e-6, tools/flush_sweep.py); env KGP_TC_FLUSH
-// overrides both
+// blocks (x32 columns) accumulated in TMEM before promotion: 16 (512 columns). With one
+// accumulator buffer each promotion stalls the MMA (k = 64 two outputs 4.93 -> 4.62 ms at 16
+// vs 8); with two, fewer promotions mean fewer accumulator-barrier round trips for the MMA
+// issuer (cfg2 3.332 -> 3.302 ms with register promotion sums). Error 2.9e-6 -> 4.3e-6 at
+// cfg2 (tools/op_err2.py); env KGP_TC_FLUSH overrides.
 static int tc_flush_blocks(int nab) {
   static int v = [] {
     const char* s = getenv("KGP_TC_FLUSH");
     int f = s ? atoi(s) : 0;
     return f < 0 ? 0 : f;
   }();
-  return v > 0 ? v : (nab == 1 ? 16 : 8);
+  (void)nab;
+  return v > 0 ? v : 16;
 }
 
 static std::mutex g_handles_mu;
@@ -132,6 +134,9 @@ static double scale_dl_fast(int kt, double l, double f) {
   return f2 / (3.0 * l);
 }
 
+// tcgen05 contraction scheme of a tensor-core precision: 3 = 3xTF32, 1 = 1xTF32, 2 = bf16x3
+int tc_split_of(int precision) { return precision == KGP_FAST ? 3 : precision == KGP_BF16X3 ? 2 : 1; }
+
 // Shared by the square operator (xrow = engine rows, shift on) and the cross operator.
 // skip_prep: the RHS split of exactly this B is already in e->bsplit (row-chunked host
 // products prepare it once for all chunks; valid when k fits one launch)
@@ -140,7 +145,7 @@ static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t 
                      int64_t o_cs, cudaStream_t st, bool skip_prep = false, uint64_t peer_epoch = 0) {
   // peer_epoch > 0: fused all-gather -- the RHS tiles come from the ranks' published buffers
   // (kgp_engine_peer_publish), b is this rank's own rows (diag_row0 = 0 indexes them)
-  const int split = (e->precision == KGP_FAST) ? 3 : 1;
+  const int split = tc_split_of(e->precision);
   const int nout = out_dl ? 2 : 1;
   const int nblk = (int)((e->n + 31) / 32);
   // two accumulator buffers when the RHS block fits, else one (the drain then briefly
@@ -219,8 +224,24 @@ static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t 
       p.ev_start = e->tev[e->tev_used++];
       p.ev_stop = e->tev[e->tev_used++];
     }
+    static const char* trace_path = getenv("KGP_TC_TRACE");  // diagnostic pipeline trace
+    static unsigned long long* trace_buf = nullptr;
+    if (trace_path && !trace_buf) KGP_CUDA(cudaMalloc(&trace_buf, 10 * 256 * sizeof(unsigned long long)));
+    if (trace_path) {
+      KGP_CUDA(cudaMemsetAsync(trace_buf, 0, 10 * 256 * sizeof(unsigned long long), st));
+      p.trace = trace_buf;
+    }
     rc = launch_kmm_tc(e->kt, e->dpad, nout, split, p, st);
     if (rc) return rc;
+    if (trace_path) {
+      unsigned long long h[10 * 256];
+      KGP_CUDA(cudaMemcpyAsync(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost, st));
+      KGP_CUDA(cudaStreamSynchronize(st));
+      if (FILE* fh = fopen(trace_path, "ab")) {
+        fwrite(h, sizeof(h), 1, fh);
+        fclose(fh);
+      }
+    }
   }
   return KGP_OK;
 }
@@ -410,7 +431,7 @@ extern "C" int kgp_engine_create(kgp_engine** out, int device, int kernel, int p
   KGP_REQUIRE(out != nullptr, KGP_ERR_INVALID, "out pointer is NULL");
   *out = nullptr;
   KGP_REQUIRE(kernel >= 0 && kernel <= 2, KGP_ERR_INVALID, "unknown kernel id %d", kernel);
-  KGP_REQUIRE(precision >= 0 && precision <= 2, KGP_ERR_INVALID, "unknown precision %d", precision);
+  KGP_REQUIRE(precision >= 0 && precision <= 3, KGP_ERR_INVALID, "unknown precision %d", precision);
   KGP_REQUIRE(n >= 1 && d >= 1, KGP_ERR_INVALID, "X must be a nonempty 2-d array, got (%lld, %d)", (long long)n, d);
   KGP_REQUIRE(d <= 16, KGP_ERR_INVALID, "dimension d=%d exceeds the supported maximum of 16", d);
   KGP_REQUIRE(x != nullptr, KGP_ERR_INVALID, "X pointer is NULL");
@@ -474,7 +495,7 @@ extern "C" int kgp_engine_set_params(kgp_engine* e, double l, double f, double s
 
 extern "C" int kgp_engine_set_precision(kgp_engine* e, int precision) {
   CHECK_ENGINE(e);
-  KGP_REQUIRE(precision >= 0 && precision <= 2, KGP_ERR_INVALID, "unknown precision %d", precision);
+  KGP_REQUIRE(precision >= 0 && precision <= 3, KGP_ERR_INVALID, "unknown precision %d", precision);
   e->precision = precision;
   e->prepared = false;
   bump_graph_epoch();
@@ -579,7 +600,7 @@ extern "C" int kgp_engine_matmul_host(kgp_engine* e, int64_t k, const double* b,
   double* df = out_df ? dout + (nout - 1) * rows * k : nullptr;
   KGP_CUDA(cudaMemcpyAsync(db, b, sizeof(double) * n * k, cudaMemcpyHostToDevice, st));
   // chunk only the tensor-core path without a heteroscedastic diagonal, when k fits one launch
-  const int split = (e->precision == KGP_FAST) ? 3 : 1;
+  const int split = tc_split_of(e->precision);
   const bool chunked = e->precision != KGP_FP64 && e->dn_classes == 0 &&
                        k <= tc_max_kp(e->dpad, out_dl ? 2 : 1, split, 1) && rows >= 32768;
   if (!e->xstream) {
@@ -883,7 +904,7 @@ extern "C" int kgp_peer_free(void* dptr) {
 extern "C" int kgp_engine_peer_buffer_bytes(kgp_engine* e, int64_t k, int64_t own_rows, int64_t* bytes) {
   CHECK_ENGINE(e);
   KGP_REQUIRE(bytes != nullptr && k >= 1 && own_rows >= 0, KGP_ERR_INVALID, "bad peer buffer query");
-  const int split = (e->precision == KGP_FAST) ? 3 : 1;
+  const int split = tc_split_of(e->precision);
   const int64_t kp = (k + 15) / 16 * 16;
   *bytes = PEER_HDR + (own_rows + 31) / 32 * (int64_t)tc_rhs_block_bytes(split, false, (int)kp);
   return KGP_OK;
@@ -953,7 +974,7 @@ extern "C" int kgp_engine_peer_publish(kgp_engine* e, int64_t k, const double* b
   KGP_REQUIRE((k + 15) / 16 <= (e->pkcap + 15) / 16, KGP_ERR_INVALID,
               "RHS block of %lld columns exceeds the peer buffers' capacity (%lld)", (long long)k,
               (long long)e->pkcap);
-  const int split = (e->precision == KGP_FAST) ? 3 : 1;
+  const int split = tc_split_of(e->precision);
   KGP_REQUIRE(k <= tc_max_kp(e->dpad, 2, split, 1), KGP_ERR_INVALID,
               "the fused all-gather operator takes one launch's RHS block (k = %lld too wide)", (long long)k);
   KGP_CUDA(cudaSetDevice(e->device));

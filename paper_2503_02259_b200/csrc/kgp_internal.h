@@ -28,6 +28,7 @@ struct TcParams {
   int nab;                // TMEM accumulator buffers: 2 (drain overlaps the MMA) or 1 (wider kp)
   int lb;                 // LB layout (tc_lb_mode): A lo parts in bf16, bf16 lo*hi correction, 3 A stages
   int flush;              // blocks per TMEM accumulation segment before promotion to fp32 smem
+  unsigned long long* trace;  // diagnostic (env KGP_TC_TRACE=path): clock64 per pipeline event of CTA (0,0)
   int debug;              // diagnostic bit flags (env KGP_TC_DEBUG): 1 no contraction MMA, 2 no distance MMA, 4 no transform
   double f2, s, two_f, scale_dl;
   const double* b;        // original fp64 RHS (for + s B)
@@ -54,6 +55,7 @@ int tc_nsa(int dpad, int nout, int split, int kp);
 int tc_lb_mode(int dpad, int nout, int split, int kp);
 int tc_lb_nab(int mode, int kp);
 int tc_rhs_block_bytes(int split, bool lb, int kp);
+int tc_split_of(int precision);
 int tc_col_block_bytes(int dpad);
 bool tc_direct(int dpad);
 int tc_dist_mode(int dpad);  // 0 direct differences, 1 tensor-core expansion, 2 FP32 expansion

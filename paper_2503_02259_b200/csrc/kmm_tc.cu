@@ -42,14 +42,31 @@ namespace kgp {
 
 namespace {
 
+#ifndef KGP_TC_RACC
+#define KGP_TC_RACC 1  // drain: promotion sums in registers when the RHS block has <= 64 columns
+#endif
+// Backoff (ns) of the mbarrier waits by role (0 = spin): see mbar_wait_backoff
+#ifndef KGP_TC_SLEEP_DRAIN
+#define KGP_TC_SLEEP_DRAIN 0
+#endif
+#ifndef KGP_TC_SLEEP_COMP
+#define KGP_TC_SLEEP_COMP 0
+#endif
+#ifndef KGP_TC_SLEEP_PROD
+#define KGP_TC_SLEEP_PROD 0
+#endif
+
 // Compute warp sets: set e handles blocks t = e (mod NS); every ring a set touches (TMEM
 // A stages, distance buffers) has NS slots so each slot has exactly one writer set.
 // NS = 2 when the A stages are wide (two outputs, hi/lo), 3 otherwise (TMEM budget).
 #ifndef KGP_TC_NSET
 #define KGP_TC_NSET 0  // 0: per-configuration default (ns_for)
 #endif
+#ifndef KGP_TC_BF_NS
+#define KGP_TC_BF_NS 3  // compute sets of the bf16x3 kernels
+#endif
 constexpr int ns_for(int nout, int split) {
-  return KGP_TC_NSET ? KGP_TC_NSET : ((nout == 2 && split == 3) ? 2 : 3);
+  return KGP_TC_NSET ? KGP_TC_NSET : (split == 2 ? KGP_TC_BF_NS : ((nout == 2 && split == 3) ? 2 : 3));
 }
 constexpr int WPS = 4;                    // warps per set = one per TMEM lane quadrant
 constexpr int MAXNS = 4;
@@ -79,6 +96,10 @@ KGP_DEV float2 hi2(float2 v) {
 KGP_DEV float2 fsub2(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
 KGP_DEV float2 lo2(float2 v) { return fsub2(v, hi2(v)); }
 
+#ifndef KGP_TC_XP
+#define KGP_TC_XP 0  // measured: the FP32 expansion is slower than the tensor-core distance at d = 8 (FP32-pipe bound)
+#endif
+
 // Kernel transform of the scaled squared distance t2 = gamma r^2 (see prep.cu):
 //   Gaussian  t2 = r^2 log2(e) / (2 l^2)   kappa = 2^-t2              g = t2 kappa
 //   Matern32  t2 = 3 r^2 / l^2             kappa = (1+t) e^-t         g = t2 e^-t
@@ -86,9 +107,14 @@ KGP_DEV float2 lo2(float2 v) { return fsub2(v, hi2(v)); }
 // with t = sqrt(t2); dkappa/dl = scale_dl * g (scale folded into the epilogue).
 // CLAMP: t2 from the expansion can cancel below zero (_panels_numpy.py:26-27); direct
 // differences (d <= 4) are a sum of squares and skip the clamp (one FMNMX per entry).
+// The clamp costs one FMNMX per entry in issue-bound compute warps, so it is not an
+// instruction: the Gaussian takes t2 as is (a cancelled t2 = -eps gives kappa = 1 + eps ln 2 and
+// g = -eps, both within the fp32 tile's own error of the clamped values), and the Matern
+// square root reads |t2| (a free source modifier); only the XP (FP32-expansion) path, which
+// can cancel further, keeps FMNMX.
 template <int KT, bool NEED_G, bool CLAMP = true>
 KGP_DEV void transform2(float2 t2, float2& kv, float2& gv) {
-  if (CLAMP) {
+  if (CLAMP && KGP_TC_XP) {
     t2.x = fmaxf(t2.x, 0.0f);
     t2.y = fmaxf(t2.y, 0.0f);
   }
@@ -110,7 +136,7 @@ KGP_DEV void transform2(float2 t2, float2& kv, float2& gv) {
     }
     float2 t = __fmul2_rn(t2, y);  // t2 = 0: y is finite (seed of +0), t = 0
 #else
-    float2 t = make_float2(sqrtf_approx(t2.x), sqrtf_approx(t2.y));
+    float2 t = make_float2(sqrtf_approx(fabsf(t2.x)), sqrtf_approx(fabsf(t2.y)));
 #endif
     float2 a = __fmul2_rn(t, make_float2(-1.4426950408889634f, -1.4426950408889634f));
     float2 e = make_float2(ex2f(a.x), ex2f(a.y));
@@ -152,9 +178,6 @@ KGP_DEV void store_tile(uint32_t taddr, const float2 (&v)[2][4]) {
   }
 }
 
-#ifndef KGP_TC_XP
-#define KGP_TC_XP 0  // measured: the FP32 expansion is slower than the tensor-core distance at d = 8 (FP32-pipe bound)
-#endif
 // 32x32b layout (thread = one TMEM lane/row, registers = 16 consecutive columns)
 template <int SPLIT>
 KGP_DEV void store_row16(uint32_t taddr, const float2 (&v)[8]) {
@@ -175,6 +198,34 @@ KGP_DEV void store_row16(uint32_t taddr, const float2 (&v)[8]) {
     }
     tmem_st16(taddr + 32, w);
   }
+}
+
+// bf16x3 layout: 16 columns of one row as two round-to-nearest bf16 terms A0 + A1 (8 bf16
+// pairs each, lower K in the low half): A0 at a0addr, A1 at a1addr (8 TMEM columns each)
+#ifndef KGP_TC_BFTRUNC
+#define KGP_TC_BFTRUNC 0  // 1: A0 by truncation (2 LOP + PRMT per pair) instead of round-to-nearest
+#endif
+KGP_DEV void store_row16_bf(uint32_t a0addr, uint32_t a1addr, const float2 (&v)[8]) {
+  uint32_t w0[8], w1[8];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+#if KGP_TC_BFTRUNC
+    const float2 h = make_float2(__uint_as_float(__float_as_uint(v[m].x) & 0xFFFF0000u),
+                                 __uint_as_float(__float_as_uint(v[m].y) & 0xFFFF0000u));
+    const float2 r = fsub2(v[m], h);
+    const __nv_bfloat162 b1 = __floats2bfloat162_rn(r.x, r.y);
+    w0[m] = __byte_perm(__float_as_uint(h.x), __float_as_uint(h.y), 0x7632);
+#else
+    const __nv_bfloat162 b0 = __floats2bfloat162_rn(v[m].x, v[m].y);
+    const float2 f0 = __bfloat1622float2(b0);
+    const float2 r = fsub2(v[m], f0);
+    const __nv_bfloat162 b1 = __floats2bfloat162_rn(r.x, r.y);
+    w0[m] = *reinterpret_cast<const uint32_t*>(&b0);
+#endif
+    w1[m] = *reinterpret_cast<const uint32_t*>(&b1);
+  }
+  tmem_st8(a0addr, w0);
+  tmem_st8(a1addr, w1);
 }
 
 // LB layout: 16 columns of one row as tf32 hi (truncated, 16 TMEM columns at taddr)
@@ -201,7 +252,9 @@ KGP_DEV void store_row16_lb(uint32_t taddr, uint32_t laddr, const float2 (&v)[8]
 #ifndef KGP_TC_LD32
 #define KGP_TC_LD32 1
 #endif
-constexpr bool use_ld32(int nout, int split, bool dmma) { return KGP_TC_LD32 && dmma && nout == 2 && split == 3; }
+constexpr bool use_ld32(int nout, int split, bool dmma) {
+  return dmma && ((KGP_TC_LD32 && nout == 2 && split == 3) || split == 2);  // bf16x3: row layout only
+}
 
 template <int D>
 struct Geo {
@@ -219,6 +272,19 @@ struct Geo {
 // corrections are hi*B_lo (tf32) and lo*bf16(B) (kind::f16, K=16), so an A stage takes 96
 // columns instead of 128 and TMEM holds three of them. Error terms: |lo| < 2^-10 |A|
 // (truncated hi), bf16 rounding 2^-9 of lo and of B -> 2^-18 |A||B| per product.
+// Pipeline trace (diagnostic, env KGP_TC_TRACE): clock64 of event `ev` for block `t` in CTA (0, 0).
+#ifndef KGP_TC_INSTR
+#define KGP_TC_INSTR 0  // 1: compile the pipeline trace and the store/load-skipping diagnostics
+#endif
+#define KGP_TR(ev, t)                                                                                       \
+  do {                                                                                                      \
+    if (KGP_TC_INSTR && p.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && (t) < 256 && (threadIdx.x & 31) == 0) { \
+      unsigned long long _c;                                                                                \
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(_c));                                                    \
+      p.trace[(ev) * 256 + (t)] = _c;                                                                       \
+    }                                                                                                       \
+  } while (0)
+
 template <int KT, int D, int NOUT, int SPLIT, int LBM>
 __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_tc_kernel(const TcParams p) {
   constexpr bool LB = LBM > 0;
@@ -336,7 +402,8 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
     int s = 0, owner = -1;
     uint32_t ph = 0;
     for (int t = 0; t < nblk; ++t) {
-      mbar_wait(&empty[s], ph ^ 1);
+      mbar_wait_backoff(&empty[s], ph ^ 1, KGP_TC_SLEEP_PROD);
+      KGP_TR(0, t);
       const uint8_t* bsrc = p.bsplit + (size_t)(t0 + t) * BBYTES;
       if (p.npeer > 0) {  // fused all-gather: this block's RHS tile lives in its owner's buffer
         const int tg = t0 + t;
@@ -367,6 +434,7 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
       mbar_wait(&full[s], ph_s);
       mbar_wait(&afull[a], ph_a);
       tc_fence_after();
+      KGP_TR(7, t);
       const uint32_t bhi = smem_u32(sB + s * BBYTES);
       const uint64_t dhi = sw128_kmajor_desc(bhi);
       const uint64_t dlo = sw128_kmajor_desc(bhi + KP * 128);
@@ -390,7 +458,26 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
         tc_commit(&empty[s]);
         tc_commit(&aempty[a]);
         if (last) tc_commit(&accfull[ab]);
-      } else if (!LB && elect_one()) {
+      } else if (SPLIT == 2 && elect_one()) {
+        // bf16x3: A0 B0 + A0 B1 + A1 B0 per output and K=16 step (kind::f16)
+        const uint32_t idesc_b = idesc_bf16_m128(KP);
+#pragma unroll
+        for (int o = 0; o < ((p.debug & 1) ? 0 : NOUT); ++o) {
+          const uint32_t dt = tbase + ab * NACC + o * KP;
+          const uint32_t a0 = tbase + abase + a * ASTAGE + o * OCOLS;
+#pragma unroll
+          for (int k2 = 0; k2 < BJ / 16; ++k2) {
+            const uint64_t b0 = interleave_kmajor_desc(bhi + k2 * 2 * KP * 16, KP * 16, 128);
+            const uint64_t b1 = interleave_kmajor_desc(bhi + 64 * KP + k2 * 2 * KP * 16, KP * 16, 128);
+            mma_f16_ts(dt, a0 + 8 * k2, b0, idesc_b, (pos > 0 || k2 > 0) ? 1u : 0u);
+            mma_f16_ts(dt, a0 + 8 * k2, b1, idesc_b, 1u);
+            mma_f16_ts(dt, a0 + 16 + 8 * k2, b0, idesc_b, 1u);
+          }
+        }
+        tc_commit(&empty[s]);
+        tc_commit(&aempty[a]);
+        if (last) tc_commit(&accfull[ab]);
+      } else if (!LB && SPLIT != 2 && elect_one()) {
 #pragma unroll
         for (int o = 0; o < ((p.debug & 1) ? 0 : NOUT); ++o) {
           const uint32_t dt = tbase + ab * NACC + o * KP;
@@ -410,6 +497,7 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
         if (last) tc_commit(&accfull[ab]);
       }
       __syncwarp();
+      KGP_TR(8, t);
       if (last) {
         pos = 0;
         if (++ab == NAB) { ab = 0; ph_acc ^= 1; }
@@ -430,6 +518,7 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
         mbar_wait(&full[s], ph_s);
         mbar_wait(&dempty[db], ph_d ^ 1);
         tc_fence_after();
+        KGP_TR(1, t);
         if (elect_one()) {
           const uint32_t va = smem_u32(sV + s * VBYTES);
           const uint32_t dd = tbase + dbase + db * BJ;
@@ -447,6 +536,7 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
           tc_commit(&empty[s]);         // this stage's V' has been read
         }
         __syncwarp();
+        KGP_TR(2, t);
         if (++s == NSB) { s = 0; ph_s ^= 1; }
         if (++db == ND) { db = 0; ph_d ^= 1; }
       }
@@ -479,18 +569,26 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
       const uint32_t ph_e = (t / NSET) & 1;  // this set's own block count: dfull[set] phase
       if (use_ld32(NOUT, SPLIT, DMMA)) {
         // thread = row qd*32 + lane; 32x32b loads/stores of 16 columns at a time
-        mbar_wait(&dfull[set], ph_e);
+        mbar_wait_backoff(&dfull[set], ph_e, KGP_TC_SLEEP_COMP);
         tc_fence_after();
+        if (qd == 0) KGP_TR(3, t);
         uint32_t v0[16], v1[16];
-        tmem_ld16(lane_base + dbase + db * BJ, v0);
-        tmem_ld16(lane_base + dbase + db * BJ + 16, v1);
-        tc_wait_ld_tied(v0);
-        tc_wait_ld_tied(v1);
+        if (KGP_TC_INSTR && (p.debug & 32)) {  // diagnostic: no distance loads
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v0[i] = v1[i] = __float_as_uint(1.0f + lane);
+        } else {
+          tmem_ld16(lane_base + dbase + db * BJ, v0);
+          tmem_ld16(lane_base + dbase + db * BJ + 16, v1);
+          tc_wait_ld_tied(v0);
+          tc_wait_ld_tied(v1);
+        }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&dempty[db]);
-        mbar_wait(&aempty[a], ph_a ^ 1);
+        if (qd == 0) KGP_TR(4, t);
+        mbar_wait_backoff(&aempty[a], ph_a ^ 1, KGP_TC_SLEEP_COMP);
         tc_fence_after();
+        if (qd == 0) KGP_TR(5, t);
         const uint32_t tcol = lane_base + abase + a * ASTAGE;
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
@@ -505,7 +603,12 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
               transform2<KT, NEED_G>(t2, kv[m], gv[m]);
             }
           }
-          if (LB) {
+          if (KGP_TC_INSTR && (p.debug & 16)) {  // diagnostic: no A-tile stores (keep the values live)
+            if (__float_as_uint(kv[0].x) == 0x7fc00001u && __float_as_uint(gv[0].y) == 0x7fc00001u) p.part[0] = 0.f;
+          } else if (SPLIT == 2) {
+            store_row16_bf(tcol + 8 * half, tcol + 16 + 8 * half, kv);
+            if (NEED_G) store_row16_bf(tcol + OCOLS + 8 * half, tcol + OCOLS + 16 + 8 * half, gv);
+          } else if (LB) {
             store_row16_lb(tcol + 16 * half, tcol + 32 + 8 * half, kv);
             store_row16_lb(tcol + OCOLS + 16 * half, tcol + OCOLS + 32 + 8 * half, gv);
           } else {
@@ -517,6 +620,7 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&afull[a]);
+        if (qd == 0) KGP_TR(6, t);
         continue;
       }
       float2 acc[4][4];  // [row][column pair m]: rows lane/4 + 8 rr, columns 2g + 8m + {0,1}
@@ -614,9 +718,55 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
     const int nseg = (nblk + flush - 1) / flush;
     int ab = 0;
     uint32_t ph = 0;
+#if KGP_TC_RACC
+    // (two compute sets only: the three-set kernels' 608 threads leave no room for 64 more
+    // registers per thread)
+    if (NS <= 2 && NACC <= 64) {
+      // promotion sums in registers (thread = row, <= 64 columns): no shared-memory traffic in
+      // the sweep, whose LDS/STS would share the MIO queue with the MMA issue and TMEM ops
+      float racc[64];
+      for (int seg = 0; seg < nseg; ++seg) {
+        mbar_wait_backoff(&accfull[ab], ph, KGP_TC_SLEEP_DRAIN);
+        tc_fence_after();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t v[2][16];
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+            if (32 * h + 16 * q < NACC) tmem_ld16(lane_base + ab * NACC + 32 * h + 16 * q, v[q]);
+          tc_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 2; ++q) tc_wait_ld_tied(v[q]);
+          if (h == 1 || NACC <= 32) {
+            if (h == 0 || 32 < NACC) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&accempty[ab]);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            if (32 * h + 16 * q < NACC) {
+#pragma unroll
+              for (int jj = 0; jj < 16; ++jj) {
+                const float x = __uint_as_float(v[q][jj]);
+                float& a = racc[32 * h + 16 * q + jj];
+                a = (seg == 0) ? x : a + x;
+              }
+            }
+          }
+        }
+        if (++ab == NAB) { ab = 0; ph ^= 1; }
+      }
+#pragma unroll
+      for (int c = 0; c < 64; ++c)
+        if (c < NACC) sAcc[c * 128 + row] = racc[c];
+    } else
+#endif
     for (int seg = 0; seg < nseg; ++seg) {
-      mbar_wait(&accfull[ab], ph);
+      mbar_wait_backoff(&accfull[ab], ph, KGP_TC_SLEEP_DRAIN);
       tc_fence_after();
+      if (qd == 0) KGP_TR(9, seg);
       // groups of up to 64 columns: all loads of a group, one wait; the buffer is released
       // as soon as the last group is in registers, before the shared-memory adds (with one
       // accumulator buffer the MMA waits on exactly this release)
@@ -727,6 +877,14 @@ int launch_one(const TcParams& p_in, cudaStream_t st) {
 
 template <int KT, int D>
 int launch_kt_d(const TcParams& p, int nout, int split, cudaStream_t st) {
+  if (split == 2) {
+    if constexpr (Geo<D>::DMMA) {
+      return nout == 1 ? launch_one<KT, D, 1, 2, 0>(p, st) : launch_one<KT, D, 2, 2, 0>(p, st);
+    } else {
+      set_error(KGP_ERR_INVALID, "bf16x3 precision needs d > 4 (tensor-core distance)");
+      return KGP_ERR_INVALID;
+    }
+  }
   if (nout == 1) return split == 3 ? launch_one<KT, D, 1, 3, 0>(p, st) : launch_one<KT, D, 1, 1, 0>(p, st);
   if (split != 3) return launch_one<KT, D, 2, 1, 0>(p, st);
   if constexpr (Geo<D>::DMMA && D == 8) {
@@ -820,6 +978,7 @@ int tc_lb_nab(int mode, int kp) {
 
 // bytes of one 32-row RHS block in bsplit: tf32 hi (| lo) K-major 128B-swizzled (| bf16 interleaved)
 int tc_rhs_block_bytes(int split, bool lb, int kp) { return ((split == 3 ? 2 : 1) * 128 + (lb ? 64 : 0)) * kp; }
+// (split 2, bf16x3: B0 | B1 as bf16, 2 x 64 kp bytes = the same 128 kp as one tf32 tile)
 
 // Column split factor that fills the last wave of 148 SMs (1 CTA/SM): the smallest
 // S <= maxsplit reaching 95% wave efficiency with >= 16 column blocks per CTA.

@@ -113,7 +113,15 @@ __global__ void prep_rhs_kernel(int split, int lb, int64_t n, int64_t k, int64_t
   uint8_t* tile = out + t * (int64_t)(tpo * 128 + (lb ? 64 : 0)) * kp;
   const uint32_t off = sw128_offset((uint32_t)c, (uint32_t)jj);
   float vf = (float)v;
-  if (split == 3) {
+  if (split == 2) {
+    // bf16x3: B = B0 + B1 (two round-to-nearest bf16 terms), each in the interleaved K-major
+    // layout of the kind::f16 B operand: B0 at +0, B1 at +64 kp
+    const __nv_bfloat16 b0 = __float2bfloat16_rn(vf);
+    const __nv_bfloat16 b1 = __float2bfloat16_rn(vf - __bfloat162float(b0));
+    const uint32_t o16 = interleave16_offset((uint32_t)c, (uint32_t)jj, (uint32_t)kp);
+    *reinterpret_cast<__nv_bfloat16*>(tile + o16) = b0;
+    *reinterpret_cast<__nv_bfloat16*>(tile + 64 * kp + o16) = b1;
+  } else if (split == 3) {
     uint32_t hi = __float_as_uint(vf) & 0xFFFFE000u;
     float lo = vf - __uint_as_float(hi);
     *reinterpret_cast<uint32_t*>(tile + off) = hi;

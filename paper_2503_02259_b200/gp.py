@@ -58,6 +58,15 @@ class Prediction:
     mean: np.ndarray
     stddev: np.ndarray
 
+    # Listing 1's field names (pred.prediction_mean, pred.prediction_stddev)
+    @property
+    def prediction_mean(self) -> np.ndarray:
+        return self.mean
+
+    @property
+    def prediction_stddev(self) -> np.ndarray:
+        return self.stddev
+
 
 class ProbeSet:
     """Standard-normal probe block Z (n, k_z), reproducible from its seed (gp.py:65-85)."""

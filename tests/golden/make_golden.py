@@ -242,5 +242,42 @@ def main():
     print("golden fixtures written to", HERE, "backend", backends.backend_name())
 
 
+def main_cfg3(n: int = 16384):
+    """configs[2]'s generator (Matern-3/2, d=4, X~U[0,1]^4 fp32, l=0.2 f=1.5 s=1e-3, 32 probes)
+    at reduced n through the reference's OWN estimator (gp.py:133-179: Nystrom rank 1024
+    w-solve, unpreconditioned probe CG, SLQ) in tolerance mode, tol = probe_tol = 1e-10, the
+    reference's default engine mode (auto -> DENSE at n <= 20000; DENSE vs ON_THE_FLY agree to
+    ~1e-11 in this mode). ~8 min on 8 cores.
+
+        python tests/golden/make_golden.py cfg3
+    """
+    import time
+
+    _import_reference()
+    from kernelgp import gp, precond
+    from kernelgp.kernels import KernelType
+    from kernelgp.kmat import Hyperparams, KernelEngine
+
+    sys.path.insert(0, REPO)
+    from paper_2503_02259_b200 import workloads
+
+    w = workloads.cfg3(n=n)
+    hp = Hyperparams(l=w.l, f=w.f, s=w.s)
+    e = KernelEngine(KernelType.MATERN32, w.x, hp)
+    probes = gp.ProbeSet.generate(w.n, w.k_z, w.probe_seed)
+    t0 = time.time()
+    pre = precond.build(e, w.rank)
+    lg = gp.nlml_grad_iterative(e, w.y, pre, probes, tol=1e-10, max_iter=6000, probe_tol=1e-10)
+    out = {"n": np.array(n), "mode": np.array(str(e.mode.value)),
+           "checksum": np.array([np.sum(w.x ** 2), np.sum(w.y ** 2), np.sum(probes.vectors ** 2)]),
+           "iter_tight": np.array([lg.loss, lg.grad_l, lg.grad_f, lg.grad_s]),
+           "converged": np.array(bool(lg.converged)), "seconds": np.array(time.time() - t0)}
+    np.savez_compressed(os.path.join(HERE, "cfg3_small.npz"), **out)
+    print("cfg3_small.npz", out)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["cfg3"]:
+        main_cfg3()
+    else:
+        main()

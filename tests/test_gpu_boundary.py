@@ -1,0 +1,261 @@
+"""The drop-in boundary beyond the operator: the reference's duck-typed operator seam
+(IdentityOperator, tests/test_gp.py:13-30, 93-102), single-vector CG (solver.py:68-119 with
+the checks of tests/test_solver.py:13-66), and HiGP's Listing-1 GPR problem API
+(PAPER.md:126-134). Tolerances are written next to each check."""
+
+import numpy as np
+import pytest
+
+from conftest import golden, rel_max
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2503_02259_b200 as p
+
+    return p
+
+
+class IdentityOperator:
+    """Khat = I: matmul is a copy, dK/ds = I, the others 0 (restates tests/test_gp.py:13-30)."""
+
+    def __init__(self, n, theta_s):
+        self.n = n
+        self._s = theta_s
+
+    def matmul(self, b):
+        return np.array(b, dtype=np.float64)
+
+    def grad_matmul(self, theta, b):
+        b = np.asarray(b, dtype=np.float64)
+        return b.copy() if theta is self._s else np.zeros_like(b)
+
+    def materialize(self):
+        return np.eye(self.n)
+
+    def materialize_grad(self, theta):
+        return np.eye(self.n) if theta is self._s else np.zeros((self.n, self.n))
+
+
+class DuckEngine:
+    """This package's device engine seen ONLY through the duck-typed protocol (what an
+    unmodified kernelgp sees after the INTEGRATION.md §2 injection): nlml_grad_iterative
+    then runs its generic host-driven branch over the device products."""
+
+    def __init__(self, engine):
+        self._e = engine
+        self.n = engine.n
+
+    def matmul(self, b):
+        return self._e.matmul(b)
+
+    def grad_matmul(self, theta, b):
+        return self._e.grad_matmul(theta, b)
+
+
+# ---------------------------------------------------------------------------- operator seam
+def test_identity_operator_exact_values(pkg, rng):
+    """tests/test_gp.py:93-102: exact loss, exact zero l/f gradients, s gradient to 1e-14."""
+    from paper_2503_02259_b200 import gp
+
+    n, k_z = 15, 8
+    y = rng.standard_normal(n)
+    probes = gp.ProbeSet.generate(n, k_z, 11)
+    lg = gp.nlml_grad_iterative(IdentityOperator(n, pkg.Theta.S), y, None, probes, tol=1e-12)
+    assert lg.loss == 0.5 * (y @ y + n * gp.LOG_2PI)
+    trace_term = float(np.mean(probes.norms_sq))
+    np.testing.assert_allclose(lg.grad_s, 0.5 * (-(y @ y) + trace_term), rtol=1e-14)
+    assert lg.grad_l == 0.0 and lg.grad_f == 0.0
+    assert lg.converged
+
+
+def test_identity_operator_exact_path(pkg, rng):
+    """grad_exact / nlml_exact over the duck-typed dense protocol: loss = (|y|^2 + n log 2pi)/2,
+    grad_s = (n - |y|^2)/2 (Khat = I, dK/ds = I), grad_l = grad_f = 0."""
+    from paper_2503_02259_b200 import gp
+
+    n = 12
+    y = rng.standard_normal(n)
+    op = IdentityOperator(n, pkg.Theta.S)
+    lg = gp.grad_exact(op, y)
+    np.testing.assert_allclose(lg.loss, 0.5 * (y @ y + n * gp.LOG_2PI), rtol=1e-14)
+    np.testing.assert_allclose(gp.nlml_exact(op, y), lg.loss, rtol=1e-15)
+    np.testing.assert_allclose(lg.grad_s, 0.5 * (n - y @ y), rtol=1e-13)
+    assert lg.grad_l == 0.0 and lg.grad_f == 0.0
+
+
+def test_duck_typed_device_engine_matches_reference(pkg):
+    """The injected-engine route: the reference's estimator driven through
+    the duck-typed protocol over the device operator gives the reference's golden values
+    (nlml.npz iter_tight: n=1024 Gaussian, tol = probe_tol = 1e-10), <= 1e-6 relative."""
+    from paper_2503_02259_b200 import gp, precond
+
+    g = golden("nlml.npz")
+    l, f, s = g["hp"]
+    e = pkg.KernelEngine(pkg.KernelType.GAUSSIAN, g["x"], pkg.Hyperparams(l, f, s), precision="fp64")
+    pre = precond.build(e, int(g["rank"]))
+    probes = gp.ProbeSet(g["probes"])
+    lg = gp.nlml_grad_iterative(DuckEngine(e), g["y"], pre, probes, tol=1e-10, max_iter=3000, probe_tol=1e-10)
+    ref = g["iter_tight"][:4]
+    got = np.array([lg.loss, lg.grad_l, lg.grad_f, lg.grad_s])
+    assert np.all(np.abs(got - ref) <= 1e-6 * np.abs(ref)), (got, ref)
+    assert lg.converged
+
+
+# ---------------------------------------------------------------------------- cg_solve
+def _spd(n, rng, shift=1.0):
+    g = rng.standard_normal((n, n))
+    return g @ g.T + shift * np.eye(n)
+
+
+def test_cg_solve_reference_checks(pkg, rng):
+    """tests/test_solver.py:13-66 restated on this package's cg_solve (device vector state)."""
+    from paper_2503_02259_b200 import solver
+    from paper_2503_02259_b200.errors import BreakdownError
+
+    # identity converges in one iteration, bitwise x = y, alpha = 1, T = [[1]]
+    y = rng.standard_normal(8)
+    x, tr = solver.cg_solve(lambda v: v, y, tol=1e-12)
+    np.testing.assert_array_equal(x, y)
+    assert tr.iterations == 1
+    np.testing.assert_allclose(tr.alphas, [1.0], rtol=1e-14)
+    np.testing.assert_allclose(solver.build_tridiag(tr), [[1.0]], rtol=1e-14)
+    # diagonal: finite termination
+    a = np.diag([1.0, 2.0])
+    x, tr = solver.cg_solve(lambda v: a @ v, np.array([1.0, 1.0]), tol=1e-14)
+    assert tr.iterations <= 2
+    np.testing.assert_allclose(x, [1.0, 0.5], rtol=1e-12)
+    # random SPD vs dense solve
+    a = _spd(50, rng)
+    y = rng.standard_normal(50)
+    x, tr = solver.cg_solve(lambda v: a @ v, y, tol=1e-10, max_iter=200)
+    exact = np.linalg.solve(a, y)
+    assert np.linalg.norm(x - exact) / np.linalg.norm(exact) <= 1e-9
+    assert tr.final_rel_residual <= 1e-10
+    # breakdown on an indefinite operator
+    a2 = np.diag([1.0, -1.0])
+    with pytest.raises(BreakdownError):
+        solver.cg_solve(lambda v: a2 @ v, np.array([0.0, 1.0]))
+    # zero right-hand side: no iteration
+    x, tr = solver.cg_solve(lambda v: v, np.zeros(4))
+    np.testing.assert_array_equal(x, np.zeros(4))
+    assert tr.iterations == 0
+    # A-norm error is monotone in the iteration count
+    a = _spd(30, rng, shift=0.5)
+    y = rng.standard_normal(30)
+    exact = np.linalg.solve(a, y)
+    errs = []
+    for it in range(1, 31):
+        x, _ = solver.cg_solve(lambda v: a @ v, y, tol=0.0, max_iter=it)
+        d = x - exact
+        errs.append(np.sqrt(d @ a @ d))
+    assert np.all(np.diff(errs) <= 1e-8 * errs[0])
+    # fixed-iteration mode (tol = 0)
+    a = _spd(20, rng)
+    _, tr = solver.cg_solve(lambda v: a @ v, rng.standard_normal(20), tol=0.0, max_iter=7)
+    assert tr.iterations == 7
+    with pytest.raises(ValueError):
+        solver.cg_solve(lambda v: v, y, tol=-1.0)
+
+
+def test_cg_solve_x0(pkg, rng):
+    """solver.py:86-96: x0 starts the iteration at r = y - A x0; an exact x0 returns at once
+    with an empty trace; a partial x0 converges to the same solution."""
+    from paper_2503_02259_b200 import solver
+
+    a = _spd(40, rng)
+    y = rng.standard_normal(40)
+    exact = np.linalg.solve(a, y)
+    x, tr = solver.cg_solve(lambda v: a @ v, y, x0=exact, tol=1e-8)
+    assert tr.iterations == 0 and tr.final_rel_residual <= 1e-8
+    np.testing.assert_array_equal(x, exact)
+    x0 = exact + 0.1 * rng.standard_normal(40)
+    x, tr = solver.cg_solve(lambda v: a @ v, y, x0=x0, tol=1e-12, max_iter=500)
+    assert np.linalg.norm(x - exact) <= 1e-10 * np.linalg.norm(exact)
+    assert 0 < tr.iterations <= 200
+
+
+def test_cg_solve_device_engine_matches_reference_pcg(pkg):
+    """cg_solve over this package's engine (the device driver) on column 0 of the reference's
+    solver.npz plain PCG (tol 1e-8, M = I). CG counts at tol 1e-8 are chaotic under rounding
+    changes even inside the reference (test_pcg_matches_reference): count within 15 %, the
+    first 8 alphas/betas to 1e-9, the solution to 1e-6 of max|ref| (100 x tol)."""
+    from paper_2503_02259_b200 import solver
+
+    g = golden("solver.npz")
+    l, f, s = g["hp"]
+    e = pkg.KernelEngine(pkg.KernelType.GAUSSIAN, g["x"], pkg.Hyperparams(l, f, s), precision="fp64")
+    x, tr = solver.cg_solve(e.matmul, g["y"][:, 0], tol=1e-8, max_iter=500)
+    it = int(g["plain_iters"][0])
+    assert abs(tr.iterations - it) <= max(1, int(np.ceil(0.15 * it)))
+    m = min(tr.iterations, it, 8)
+    np.testing.assert_allclose(tr.alphas[:m], g["plain_alphas"][0, :m], rtol=1e-9)
+    np.testing.assert_allclose(tr.betas[:m], g["plain_betas"][0, :m], rtol=1e-9)
+    assert rel_max(x, g["plain_sol"][:, 0]) <= 1e-6 and tr.final_rel_residual <= 1e-8
+
+
+# ---------------------------------------------------------------------------- GPR problem API
+def test_gpr_calc_loss_grad_matches_core(pkg, rng):
+    """calc_loss_grad equals the core grad_exact with the softplus chain rule
+    (n=100, 1e-12), two handles used alternately give independent results, and an injected
+    Khat = I operator gives loss = (|y|^2 + n log 2pi)/2."""
+    from paper_2503_02259_b200 import gp, gpr, train
+
+    x, y = rng.uniform(-1, 1, (100, 2)), rng.standard_normal(100)
+    x2, y2 = rng.uniform(-1, 1, (80, 3)), rng.standard_normal(80)
+    p1 = gpr.setup(data=x, label=y, kernel_type=pkg.KernelType.MATERN52, mode="exact", precision="fp64")
+    p2 = gpr.setup(data=x2, label=y2, kernel_type="gaussian", mode="exact", precision="fp64")
+    raw = train.RawParams.from_hyperparams(pkg.Hyperparams(0.7, 1.2, 0.05))
+    ref1 = gp.grad_exact(pkg.KernelEngine(pkg.KernelType.MATERN52, x, raw.to_hyperparams(), precision="fp64"), y)
+    ref2 = gp.grad_exact(pkg.KernelEngine(pkg.KernelType.GAUSSIAN, x2, raw.to_hyperparams(), precision="fp64"), y2)
+    for _ in range(2):
+        for prob, ref in ((p1, ref1), (p2, ref2), (p1, ref1)):
+            loss, g = prob.calc_loss_grad(raw)
+            np.testing.assert_allclose(loss, ref.loss, rtol=1e-12)
+            np.testing.assert_allclose(g, train.chain_grads(raw, ref.grads()), rtol=1e-12)
+    p1.release()
+    with pytest.raises(Exception, match="released"):
+        p1.calc_loss_grad(raw)
+    n = 20
+    yi = rng.standard_normal(n)
+    pid = gpr.setup(data=rng.standard_normal((n, 2)), label=yi, mode="iterative", k_z=4,
+                    operator=IdentityOperator(n, pkg.Theta.S))
+    lg = pid.loss_grad(pkg.Hyperparams(1.0, 1.0, 1.0))
+    assert lg.loss == 0.5 * (yi @ yi + n * gp.LOG_2PI)
+
+
+def test_gpr_listing1_training_matches_fit(pkg):
+    """Listing 1: GPRModel + torch.optim.Adam reproduces train.fit's exact-mode
+    trajectory -- loss history of the reference (train.npz, Matern-5/2, 15 Adam steps) to 1e-9
+    -- and gpr_prediction is exactly gp.predict."""
+    import torch
+
+    from paper_2503_02259_b200 import gp, gpr
+
+    g = golden("train.npz")
+    prob = gpr.setup(data=g["x"], label=g["y"], kernel_type="matern52", mode="exact", rng_seed=3,
+                     precision="fp64")
+    model = gpr.GPRModel(prob)
+    np.testing.assert_allclose(model.get_params().as_array(), g["init"], rtol=1e-12)
+    opt = torch.optim.Adam(model.parameters(), lr=0.1)
+    losses = []
+    for _ in range(len(g["exact_loss"])):
+        losses.append(model.calc_loss_grad())
+        opt.step()
+    np.testing.assert_allclose(losses, g["exact_loss"], rtol=1e-9)
+    np.testing.assert_allclose(model.get_params().as_array(), g["exact_params"], rtol=1e-8)
+    params = model.get_params()
+    xs = np.random.default_rng(1).uniform(-2, 2, (25, 2))
+    pred = gpr.gpr_prediction(g["x"], g["y"], xs, "matern52", params)
+    core = gp.predict(pkg.KernelType.MATERN52, g["x"], g["y"], xs, params, mode="exact")
+    np.testing.assert_array_equal(pred.prediction_mean, core.mean)
+    np.testing.assert_array_equal(pred.prediction_stddev, core.stddev)
+    # test_x = train_x with a tiny noise: the posterior mean interpolates the labels
+    tiny = pkg.Hyperparams(params.l, params.f, 1e-8)
+    p2 = gpr.gpr_prediction(g["x"][:40], g["y"][:40], g["x"][:40], "matern52", tiny)
+    assert np.abs(p2.prediction_mean - g["y"][:40]).max() <= 1e-4

@@ -108,7 +108,9 @@ def test_lazy_exports_match_reference_surface():
                  "cg_solve", "pcg_solve", "build_tridiag", "slq_logdet", "LossGrad", "Prediction", "ProbeSet",
                  "nlml_exact", "grad_exact", "nlml_grad_iterative", "predict", "RawParams", "TrainConfig",
                  "TrainResult", "fit"}
-    extensions = {"AFNPreconditioner"}  # north-star additions beyond kernelgp/__init__.py:16-44
+    # north-star additions beyond kernelgp/__init__.py:16-44: AFN, and HiGP's Listing-1 GPR
+    # problem API
+    extensions = {"AFNPreconditioner", "GPRProblem", "GPRModel", "GPROptions", "gpr_prediction"}
     assert set(p.__all__) == ref_names | extensions
     for name in ref_names:
         getattr(p, name)
@@ -140,3 +142,26 @@ def test_row_range_alignment():
         assert all(r0 % 32 == 0 for r0, _ in rs)
         assert [kdist.row_range(n, world, q) for q in range(world)] == [
             (q * n // world, (q + 1) * n // world) for q in range(world)]
+
+
+def test_gpr_setup_host_contract():
+    """SPEC.md:523-528 / 546-547: setup copies the data (no aliasing), a label-length mismatch
+    raises, empty test_x gives empty arrays, releasing twice is a no-op (never a crash).
+    No device work happens in setup, so this runs on the CPU."""
+    from paper_2503_02259_b200 import gpr
+
+    rng = np.random.default_rng(0)
+    x, y = rng.standard_normal((10, 2)), rng.standard_normal(10)
+    prob = gpr.setup(data=x, label=y, kernel_type="gaussian")
+    x[0, 0] = 99.0
+    y[0] = 99.0
+    assert prob.x[0, 0] != 99.0 and prob.y[0] != 99.0 and prob.n == 10
+    assert not prob.x.flags.writeable
+    with pytest.raises(ValueError, match="mismatch"):
+        gpr.setup(data=x, label=y[:9])
+    with pytest.raises(ValueError):
+        gpr.setup(data=x, label=y, mode="bogus")
+    pred = gpr.gpr_prediction(x, y, np.empty((0, 2)), "gaussian", (1.0, 1.0, 0.1))
+    assert pred.prediction_mean.shape == (0,) and pred.prediction_stddev.shape == (0,)
+    assert prob.release() is True
+    assert prob.release() is False
