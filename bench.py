@@ -37,7 +37,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--precision", default="fast", choices=["fast", "tf32", "fp64"])
+    ap.add_argument("--precision", default="fast", choices=["fast", "tf32", "fp64", "bf16x3"])
     ap.add_argument("--n", type=int, default=65536)
     ap.add_argument("--k", type=int, default=32)
     ap.add_argument("--cpu-rows", type=int, default=8192,
@@ -45,10 +45,14 @@ def parse():
     ap.add_argument("--ref-rows", type=int, default=2048, help="rows per step of the --impl reference arm")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--skip-nlml", action="store_true")
-    ap.add_argument("--exchange", default="replicated", choices=["replicated", "peer"],
-                    help="replicated: every rank holds all of Z (no exchange in the step); peer: each rank "
-                         "publishes its rows of Z and the fused all-gather operator reads the others' "
-                         "(kgp_engine_peer_*, DESIGN.md section 6)")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer", "replicated"],
+                    help="nccl (default): each rank owns its rows of Z and every step all-gathers Z over "
+                         "NCCL before the row-block product, as a solver iteration does; peer: each rank "
+                         "publishes its rows and the fused all-gather operator reads the others' inside the "
+                         "kernel (kgp_engine_peer_*, DESIGN.md section 6); replicated: every rank holds all "
+                         "of Z (no exchange timed). At N=1 there is nothing to exchange.")
+    ap.add_argument("--skip-secondary", action="store_true",
+                    help="only the headline line's keys (no fp64/bf16x3/tf32/cfg5/NLML legs)")
     return ap.parse_args()
 
 
@@ -236,13 +240,23 @@ def profiled_traffic(precision: str, n: int, k: int):
 
 def nlml_metric(cpu: bool):
     """Secondary metric: NLML+gradient evaluations/s at BASELINE configs[0] (n=4096, Gaussian,
-    16 probes, rank 256) with its fixed recipe (PCG 50 iterations, 20 Lanczos steps), fp64
-    operator. Each eval includes the H2D copy of y and the probes; the preconditioner build is
-    timed separately (the reference's 1.41 s likewise excludes its 0.19 s build)."""
+    16 probes, rank 256) with its fixed recipe (PCG 50 iterations, 20 Lanczos steps), fp64.
+
+    Credited number: the engine in ON_THE_FLY mode -- every product is the repo's fused fp64
+    operator (kmm_f64_kernel), Khat never stored, the north star's path. Secondary ("dense"):
+    the reference's own default at n <= 20000 (auto -> DENSE, kmat.py:93-94), where Khat is
+    materialised once per eval and the 17-column products are a cuBLAS DGEMM. Each eval includes
+    the H2D copy of y and the probes; the preconditioner build is timed separately (the
+    reference's 1.41 s likewise excludes its 0.19 s build).
+
+    Roofline (FP64 pipe): the recipe's operator passes from its fixed iteration counts -- w:
+    50 x 1 column, probes: 20 x 16 columns, the fused derivative pass: 17 columns x 2 outputs --
+    each costing per kernel entry (3d + 53) evaluation flops + 2k contraction flops per output,
+    over the eval time, against the measured DFMA rate."""
     import torch
 
     from paper_2503_02259_b200 import gp, precond, workloads
-    from paper_2503_02259_b200.kmat import Hyperparams, KernelEngine
+    from paper_2503_02259_b200.kmat import EngineMode, Hyperparams, KernelEngine
     from paper_2503_02259_b200.kernels import KernelType
 
     w = workloads.cfg1()
@@ -250,46 +264,67 @@ def nlml_metric(cpu: bool):
     torch.linalg.cholesky(torch.eye(8, dtype=torch.float64, device="cuda"))  # one-time cuSOLVER init
     torch.linalg.solve_triangular(torch.eye(8, dtype=torch.float64, device="cuda"),
                                   torch.eye(8, dtype=torch.float64, device="cuda"), upper=False)
-    eng = KernelEngine(KernelType.GAUSSIAN, w.x, Hyperparams(w.l, w.f, w.s), precision="fp64")
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    pre = precond.build(eng, w.rank)
-    torch.cuda.synchronize()
-    t_build_first = time.perf_counter() - t0  # includes lazy module loading of every kernel it uses
-    t0 = time.perf_counter()
-    pre = precond.build(eng, w.rank)  # steady state: training rebuilds it every step
-    torch.cuda.synchronize()
-    t_build = time.perf_counter() - t0
 
-    def ev():
-        return gp.nlml_grad_iterative(eng, w.y, pre, probes, tol=0.0, max_iter=50, probe_tol=0.0,
-                                      probe_max_iter=20)
+    def run(mode, reps=10):
+        eng = KernelEngine(KernelType.GAUSSIAN, w.x, Hyperparams(w.l, w.f, w.s), mode=mode, precision="fp64")
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        pre = precond.build(eng, w.rank)
+        torch.cuda.synchronize()
+        t_first = time.perf_counter() - t0  # includes lazy module loading of every kernel it uses
+        t0 = time.perf_counter()
+        pre = precond.build(eng, w.rank)  # steady state: training rebuilds it every step
+        torch.cuda.synchronize()
+        t_build = time.perf_counter() - t0
 
-    for _ in range(2):
-        ev()
-    torch.cuda.synchronize()
-    reps = 10
-    t0 = time.perf_counter()
-    for _ in range(reps):
-        lg = ev()
-    torch.cuda.synchronize()
-    t_eval = (time.perf_counter() - t0) / reps
+        def ev():
+            return gp.nlml_grad_iterative(eng, w.y, pre, probes, tol=0.0, max_iter=50, probe_tol=0.0,
+                                          probe_max_iter=20)
+
+        for _ in range(2):
+            ev()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            lg = ev()
+        torch.cuda.synchronize()
+        return (time.perf_counter() - t0) / reps, t_build, t_first, lg
+
+    t_eval, t_build, t_first, lg = run(EngineMode.ON_THE_FLY)
+    t_dense, _, _, lg_dense = run(EngineMode.DENSE)
+    n, d = w.n, w.d
+    passes = [(50, 1, 1), (20, 16, 1), (1, 17, 2)]  # (iterations, columns, outputs)
+    flops = sum(it * n * n * ((3 * d + 53) + 2 * k * nout) for it, k, nout in passes)
+    achieved = flops / t_eval / 1e12
     out = {"workload": "cfg1 fixed recipe (BASELINE.json configs[0]): n=4096 d=3 Gaussian, 16 probes, "
-                       "rank 256, PCG 50 + SLQ 20, fp64 operator",
+                       "rank 256, PCG 50 + SLQ 20, fp64 operator, ON_THE_FLY (fused kernel, Khat never stored)",
            "evals_per_s": 1.0 / t_eval, "ms_per_eval": t_eval * 1e3, "precond_build_ms": t_build * 1e3,
-           "precond_build_first_call_ms": t_build_first * 1e3,
-           "loss": lg.loss, "timer": "wall clock around synchronous calls (each eval ends in a D2H read)"}
+           "precond_build_first_call_ms": t_first * 1e3, "loss": lg.loss,
+           "timer": "wall clock around synchronous calls (each eval ends in a D2H read)",
+           "roofline": {"bound": "fp64", "achieved": achieved, "peak": FP64_DFMA_TFLOPS, "unit": "TFLOP/s",
+                        "frac": achieved / FP64_DFMA_TFLOPS,
+                        "algorithmic": "operator passes of the fixed recipe (50 x 1 + 20 x 16 columns, one "
+                                       "17-column two-output derivative pass), per entry 3d + 53 evaluation "
+                                       "flops + 2k per output; PCG vector work and SLQ not counted"},
+           "dense": {"workload": "same recipe, DENSE mode (the reference's default at n <= 20000): Khat "
+                                 "materialised by the repo's panel kernel, 17-column products by cuBLAS DGEMM",
+                     "evals_per_s": 1.0 / t_dense, "ms_per_eval": t_dense * 1e3, "loss": lg_dense.loss}}
     if cpu:
         from oracle import kgp_oracle as orc
+        from oracle import kgp_oracle_c as oc
 
         ny = orc.Nystrom("gaussian", w.x, w.l, w.f, w.s, w.rank)
-        t0 = time.perf_counter()
-        ref = orc.nlml_grad("gaussian", w.x, w.y, w.l, w.f, w.s, probes.vectors, ny, tol=0.0, max_iter=50,
-                            probe_tol=0.0, dense=True, probe_max_iter=20)
-        t_cpu = time.perf_counter() - t0
-        out["cpu_baseline"] = {"evals_per_s": 1.0 / t_cpu, "kind": "port", "cores": os.cpu_count(),
-                               "sample": "one full eval, oracle/kgp_oracle.py dense path (the reference's "
-                                         "default auto->DENSE mode at n <= 20000), numpy BLAS threads"}
+        best = float("inf")
+        for _ in range(2):
+            t0 = time.perf_counter()
+            ref = orc.nlml_grad("gaussian", w.x, w.y, w.l, w.f, w.s, probes.vectors, ny, tol=0.0, max_iter=50,
+                                probe_tol=0.0, dense=True, probe_max_iter=20, panels="c")
+            best = min(best, time.perf_counter() - t0)
+        out["cpu_baseline"] = {"evals_per_s": 1.0 / best, "kind": "port", "cores": oc.max_threads(),
+                               "sample": "one full eval (best of 2), the reference's default DENSE path: Khat and "
+                                         "the two derivative matrices by OpenMP C panels (oracle/kgp_oracle.c, "
+                                         "numba-prange equivalent), products by numpy BLAS; measured 1.0-1.2x "
+                                         "kernelgp itself on the build host (tools/cpu_nlml_baseline.py)"}
         out["loss_rel_diff_vs_cpu"] = abs(lg.loss - ref[0]) / abs(ref[0])
     return out
 
@@ -342,35 +377,70 @@ def nlml_cfg3_metric(n: int = 262144, reps: int = 1):
 # tcgen05 kind::tf32 issue rate at the contraction's shape (M=128, N=32, K=8, A in TMEM),
 # tools/micro/mma_n.cu on this pool (profiles/r01_micro_tensor_fp64.txt)
 TC_TF32_N32_TFLOPS = 1056.9
+# FP64 pipe: DFMA-only micro-benchmark on this pool (tools/micro/fp64_mix.cu,
+# profiles/r01_micro_tensor_fp64.txt); MEASURED_PEAKS.json has no FP64 figure
+FP64_DFMA_TFLOPS = 36.07
+DTYPES = {"fast": "f32 tile + 3xtf32 mma", "tf32": "f32 tile + tf32 mma", "fp64": "f64",
+          "bf16x3": "f32 tile + bf16x3 mma (A0B0 + A0B1 + A1B0)"}
+# tensor products per output of each precision (hi.hi + hi.lo + lo.hi; hi.hi; A0B0 + A0B1 + A1B0)
+SPLITS = {"fast": 3, "tf32": 1, "bf16x3": 3}
 
 
-def alt_peaks(achieved):
-    """The same achieved rate against the other defensible TF32 denominators."""
-    out = []
+def measured_peaks():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
-            bf16 = float(json.load(f)["bf16_tflops"])
-        out.append({"source": "MEASURED_PEAKS.json bf16_tflops / 2 (tf32 issues at half the bf16 rate)",
-                    "peak": bf16 / 2, "frac": achieved / (bf16 / 2)})
-    except (OSError, KeyError, ValueError):
-        pass
-    out.append({"source": "tcgen05 kind::tf32 M=128 N=32 issue rate (tools/micro/mma_n.cu, "
-                          "profiles/r01_micro_tensor_fp64.txt)",
-                "peak": TC_TF32_N32_TFLOPS, "frac": achieved / TC_TF32_N32_TFLOPS})
-    return out
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
 
 
-def tf32_mode_metric(w, ref_k, ref_l, steps: int = 10):
-    """Secondary: the same cfg2 step with the single-pass TF32 contraction (precision "tf32",
-    the north star's "TF32 mode": operator error <= 1e-3; 3xTF32 "fast" is the headline and the
-    NLML mode). Error measured against the fast outputs of the main run."""
+def tc_roofline(precision, entries, k, kernel_t, measure_cublas):
+    """Tensor roofline of the fused operator: ALGORITHMIC tensor flops = entries x 2 outputs x
+    products x 2k, over the kernel's own launch time, against MEASURED_PEAKS.json's dense bf16
+    burst figure (/2 for tf32 MMAs, which issue at half the bf16 rate; x1 for the bf16x3 mode's
+    kind::f16 MMAs). Alternatives: the sustained bf16 figure, a cuBLAS TF32 GEMM measured in this
+    run, and the tcgen05 N=32 issue rate from the micro-benchmark."""
+    import torch
+
+    flops = 2 * SPLITS[precision] * 2.0 * entries * k
+    achieved = flops / kernel_t / 1e12
+    mp = measured_peaks()
+    bf16 = float(mp.get("bf16_tflops", 0.0)) or None
+    div = 1.0 if precision == "bf16x3" else 2.0
+    peak = bf16 / div if bf16 else None
+    alts = []
+    if mp.get("bf16_tflops_sustained"):
+        ps = float(mp["bf16_tflops_sustained"]) / div
+        alts.append({"source": "MEASURED_PEAKS.json bf16_tflops_sustained" + (" / 2" if div == 2 else ""),
+                     "peak": ps, "frac": achieved / ps})
+    if measure_cublas and precision != "bf16x3":
+        pc = measured_tf32_peak(torch)
+        alts.append({"source": "cuBLAS TF32 GEMM 8192^3 measured in this run", "peak": pc, "frac": achieved / pc})
+    if precision != "bf16x3":
+        alts.append({"source": "tcgen05 kind::tf32 M=128 N=32 issue rate (tools/micro/mma_n.cu, "
+                               "profiles/r01_micro_tensor_fp64.txt)",
+                     "peak": TC_TF32_N32_TFLOPS, "frac": achieved / TC_TF32_N32_TFLOPS})
+    if peak is None:  # no driver-written peaks: the profiling recipe's fallback is the cuBLAS figure
+        peak = next((x["peak"] for x in alts if x["source"].startswith("cuBLAS")), None)
+    return {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak if peak else None,
+            "peak_source": ("MEASURED_PEAKS.json bf16_tflops (burst; the kernel is timed alone)"
+                            + (" / 2 (tf32 MMAs issue at half the bf16 rate)" if div == 2 else "")),
+            "peak_alternatives": alts,
+            "algorithmic": f"2 outputs x {SPLITS[precision]} products x 2k flops per kernel entry"}
+
+
+def mode_metric(w, ref_k, ref_l, precision, steps: int = 10):
+    """Secondary: the same cfg2 step in another tensor-core precision ("tf32": 1xTF32, the north
+    star's "TF32 mode", operator bar 1e-3; "bf16x3": split-bf16 A0B0 + A0B1 + A1B0), with its
+    error against the 3xTF32 outputs of the main run and its own roofline."""
     import torch
 
     from paper_2503_02259_b200 import KernelEngine, KernelType, _lib
     from paper_2503_02259_b200.kmat import Hyperparams
 
     n, k = w.n, w.z.shape[1]
-    e = KernelEngine(KernelType.GAUSSIAN, w.x, Hyperparams(w.l, w.f, w.s), precision="tf32")
+    e = KernelEngine(KernelType.GAUSSIAN, w.x, Hyperparams(w.l, w.f, w.s), precision=precision)
     zd = torch.from_numpy(w.z).cuda()
     ok, ol = torch.empty_like(ref_k), torch.empty_like(ref_l)
     st = torch.cuda.current_stream()
@@ -383,6 +453,7 @@ def tf32_mode_metric(w, ref_k, ref_l, steps: int = 10):
     for _ in range(3):
         step()
     torch.cuda.synchronize()
+    _lib.call("kgp_engine_set_timing", e.handle, 1)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     for s_ev, e_ev in ev:
         flush.zero_()
@@ -390,13 +461,117 @@ def tf32_mode_metric(w, ref_k, ref_l, steps: int = 10):
         step()
         e_ev.record(st)
     torch.cuda.synchronize()
+    kern_ms, kern_n = _lib.kernel_time(e.handle)
+    _lib.call("kgp_engine_set_timing", e.handle, 0)
     t = float(np.mean([a.elapsed_time(b) / 1e3 for a, b in ev]))
     err_k = float((ok - ref_k).abs().max() / ref_k.abs().max())
     err_l = float((ol - ref_l).abs().max() / ref_l.abs().max())
     e.close()
+    kt = kern_ms / 1e3 / kern_n if kern_n else t
+    roof = tc_roofline(precision, n * n, k, kt, False)
+    roof["kernel_ms"] = kt * 1e3
+    notes = {"tf32": "1xTF32 contraction; not the NLML mode (its loss/gradient errors reach 1e-1, DESIGN.md 4)",
+             "bf16x3": "two round-to-nearest bf16 terms per operand, 3 kind::f16 products; operator error ~5e-6 "
+                       "(tests/test_gpu_parity.py), d > 4 only"}
     return {"value": 2.0 * n * n * k / t, "unit": "entries*RHS/s", "ms_per_step": t * 1e3,
-            "max_rel_diff_vs_fast": {"Khat.Z": err_k, "dKhat/dl.Z": err_l},
-            "note": "1xTF32 contraction (2 tf32 MMAs x 2k flops per entry); not the NLML mode"}
+            "max_rel_diff_vs_fast": {"Khat.Z": err_k, "dKhat/dl.Z": err_l}, "roofline": roof,
+            "note": notes[precision]}
+
+
+def fp64_mode_metric(w, steps: int = 5):
+    """Secondary: the cfg2 step with the fp64 operator (the parity precision), and its
+    roofline on the FP64 pipe: per kernel entry 3d (distance) + ~53 (exp + transform, FMA = 2)
+    flops, plus 2k flops per output (the contraction FMAs), against the measured DFMA rate."""
+    import torch
+
+    from paper_2503_02259_b200 import KernelEngine, KernelType, _lib
+    from paper_2503_02259_b200.kmat import EngineMode, Hyperparams
+
+    n, k, d = w.n, w.z.shape[1], w.d
+    e = KernelEngine(KernelType.GAUSSIAN, w.x, Hyperparams(w.l, w.f, w.s), mode=EngineMode.ON_THE_FLY,
+                     precision="fp64")
+    zd = torch.from_numpy(w.z).cuda()
+    ok = torch.empty((n, k), dtype=torch.float64, device="cuda")
+    ol = torch.empty_like(ok)
+    st = torch.cuda.current_stream()
+
+    def step():
+        _lib.call("kgp_engine_matmul", e.handle, k, zd.data_ptr(), zd.stride(0), zd.stride(1), ok.data_ptr(),
+                  ol.data_ptr(), None, ok.stride(0), ok.stride(1), st.cuda_stream)
+
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for s_ev, e_ev in ev:
+        s_ev.record(st)
+        step()
+        e_ev.record(st)
+    torch.cuda.synchronize()
+    t = float(np.mean([a.elapsed_time(b) / 1e3 for a, b in ev]))
+    e.close()
+    per_entry = 3 * d + 53 + 2 * 2 * k
+    achieved = per_entry * n * n / t / 1e12
+    return {"value": 2.0 * n * n * k / t, "unit": "entries*RHS/s", "ms_per_step": t * 1e3,
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": FP64_DFMA_TFLOPS, "unit": "TFLOP/s",
+                         "frac": achieved / FP64_DFMA_TFLOPS,
+                         "peak_source": "DFMA micro-benchmark on this pool (profiles/r01_micro_tensor_fp64.txt); "
+                                        "MEASURED_PEAKS.json has no FP64 figure",
+                         "algorithmic": f"{per_entry} fp64 flops per kernel entry: 3d distance + ~53 exp/transform "
+                                        "(estimate) + 2 outputs x 2k contraction"}}
+
+
+def cfg5_operator_metric(world, rank, local, dist, steps: int = 3):
+    """Secondary (every N): the configs[4]-size operator that a cfg5 PCG iteration applies --
+    Matern-5/2, n = 1048576, d = 2, Khat.[y, Z] with 64 RHS, fast precision -- row-sharded over
+    the N ranks, each step all-gathering the RHS block over NCCL (N > 1) before the row-block
+    product (the north star's >= 85 % scaling target is stated for n >= 1M). Device-timed, max
+    over ranks; value = whole-job entries x RHS / s."""
+    import torch
+
+    from paper_2503_02259_b200 import KernelEngine, KernelType, _lib, workloads
+    from paper_2503_02259_b200 import dist as kdist
+    from paper_2503_02259_b200.kmat import Hyperparams
+
+    w = workloads.cfg5(m_test=1)
+    n, k = w.n, 64
+    r0, r1 = kdist.row_range(n, world, rank)
+    e = KernelEngine(KernelType.MATERN52, w.x, Hyperparams(w.l, w.f, w.s), precision="fast")
+    if world > 1:
+        _lib.call("kgp_engine_set_rows", e.handle, r0, r1 - r0)
+    zfull = torch.from_numpy(np.random.default_rng(5).standard_normal((n, k))).cuda()
+    zloc = zfull[r0:r1].clone()
+    if world > 1:
+        zfull = torch.empty_like(zfull)
+    out = torch.empty((r1 - r0, k), dtype=torch.float64, device="cuda")
+    st = torch.cuda.current_stream()
+
+    def step():
+        if world > 1:
+            dist.all_gather_into_tensor(zfull, zloc)
+        _lib.call("kgp_engine_matmul", e.handle, k, zfull.data_ptr(), zfull.stride(0), zfull.stride(1),
+                  out.data_ptr(), None, None, out.stride(0), out.stride(1), st.cuda_stream)
+
+    step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for s_ev, e_ev in ev:
+        s_ev.record(st)
+        step()
+        e_ev.record(st)
+    torch.cuda.synchronize()
+    t = float(np.mean([a.elapsed_time(b) / 1e3 for a, b in ev]))
+    if world > 1:
+        tt = torch.tensor([t], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    e.close()
+    return {"workload": "configs[4] operator: Matern-5/2 n=1048576 d=2, Khat.[y,Z] 64 RHS, fast, rows sharded "
+                        "over the ranks" + (", NCCL all-gather of the RHS block in every step" if world > 1 else ""),
+            "value": 1.0 * n * n * k / t, "unit": "entries*RHS/s", "ms_per_step": t * 1e3, "steps": steps,
+            "n_gpus": world, "scaling": "strong"}
 
 
 def run_gpu(args):
@@ -444,6 +619,14 @@ def run_gpu(args):
             tiles = kdist.PeerTiles(eng.handle, world, rank, starts, k, comm=kdist.Comm(n, align=32))
     zloc = zd[r0:r1]
     epoch = [0]
+    gather = args.exchange == "nccl" and world > 1
+    if gather:
+        # the rank owns only its rows of Z; every step gathers the whole block (equal row
+        # blocks: all_gather_into_tensor concatenates them in rank order), as a PCG iteration
+        # does before its row-block product (dist.py)
+        assert n % world == 0, "--exchange nccl needs n divisible by the world size"
+        zloc = zd[r0:r1].clone()
+        zd = torch.empty_like(zd)
 
     def step():
         if peer:  # publish own rows of Z, then the operator pulls every rank's tiles
@@ -453,6 +636,8 @@ def run_gpu(args):
             _lib.call("kgp_engine_peer_matmul", eng.handle, k, epoch[0], out_k.data_ptr(), out_l.data_ptr(), None,
                       out_k.stride(0), out_k.stride(1), stream.cuda_stream)
             return
+        if gather:
+            dist.all_gather_into_tensor(zd, zloc)
         _lib.call("kgp_engine_matmul", eng.handle, k, zd.data_ptr(), zd.stride(0), zd.stride(1),
                   out_k.data_ptr(), out_l.data_ptr(), None, out_k.stride(0), out_k.stride(1), stream.cuda_stream)
 
@@ -514,20 +699,17 @@ def run_gpu(args):
     # ---- roofline of the dominant kernel (kmm_tc_kernel): average duration of its launches
     # inside the timed region (events recorded by libkgp around each launch)
     kernel_t = kern_ms / 1e3 / kern_n if kern_n else t_step
-    splits = {"fast": 3, "tf32": 1, "fp64": 0}[args.precision]
-    tc_flops = 2 * splits * 2.0 * rows * n * k  # 2 outputs x split products x 2 flops per MAC
-    peak_tf32 = measured_tf32_peak(torch) if rank == 0 and splits else None
     roof = None
-    if splits:
-        achieved = tc_flops / kernel_t / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": peak_tf32, "unit": "TFLOP/s",
-                "frac": achieved / peak_tf32 if peak_tf32 else None,
-                "traffic": profiled_traffic(args.precision, n, k),
-                "peak_source": "measured cuBLAS TF32 GEMM 8192^3 in this run (MEASURED_PEAKS.json has bf16 only)",
-                "peak_alternatives": alt_peaks(achieved),
-                "algorithmic": f"{2 * splits} tf32 MMAs x 2k flops per kernel entry",
-                "kernel_ms": kernel_t * 1e3, "kernel_launches_timed": kern_n,
-                "kernel_share_of_step": kernel_t * max(kern_n, 1) / args.steps / t_step}
+    if args.precision != "fp64":
+        roof = tc_roofline(args.precision, rows * n, k, kernel_t, rank == 0)
+        roof.update({"traffic": profiled_traffic(args.precision, n, k), "kernel_ms": kernel_t * 1e3,
+                     "kernel_launches_timed": kern_n,
+                     "kernel_share_of_step": kernel_t * max(kern_n, 1) / args.steps / t_step})
+    # ---- secondary legs: cfg5-size operator on every rank (collective when N > 1), the rest
+    # on rank 0 at N = 1
+    extra = {}
+    if not args.skip_secondary:
+        extra["cfg5_operator"] = cfg5_operator_metric(world, rank, local, dist if world > 1 else None)
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and world == 1:
@@ -540,7 +722,7 @@ def run_gpu(args):
             "value": value, "unit": "entries*RHS/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": t_step * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None,
-            "dtype": {"fast": "f32 tile + 3xtf32 mma", "tf32": "f32 tile + tf32 mma", "fp64": "f64"}[args.precision],
+            "dtype": DTYPES[args.precision],
             "data": "synthetic (seeded numpy default_rng, BASELINE configs[1] shapes and distributions)",
             "config": bench_config(args, w, world),
             "e2e": {"value": units / t_e2e, "unit": "entries*RHS/s", "h2d_bytes_per_step": int(zh.numel() * 8),
@@ -550,17 +732,18 @@ def run_gpu(args):
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
         }
-        if not args.skip_nlml and world == 1:
-            line["nlml"] = nlml_metric(cpu=not args.no_cpu_baseline)
-            line["nlml_cfg3"] = nlml_cfg3_metric()
-        if world == 1 and args.precision == "fast":
-            line["tf32_mode"] = tf32_mode_metric(w, out_k, out_l)
+        line.update(extra)
+        if world == 1 and not args.skip_secondary:
+            if args.precision == "fast":
+                line["fp64_mode"] = fp64_mode_metric(w)
+                line["bf16x3_mode"] = mode_metric(w, out_k, out_l, "bf16x3")
+                line["tf32_mode"] = mode_metric(w, out_k, out_l, "tf32")
+            if not args.skip_nlml:
+                line["nlml"] = nlml_metric(cpu=not args.no_cpu_baseline)
+                line["nlml_cfg3"] = nlml_cfg3_metric()
         print(json.dumps(line))
     if tiles is not None:
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()  # no rank unmaps a buffer another may still read
-        tiles.close()
+        tiles.close()  # synchronises and barriers before unmapping (dist.PeerTiles.close)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

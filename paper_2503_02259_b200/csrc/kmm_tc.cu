@@ -42,6 +42,9 @@ namespace kgp {
 
 namespace {
 
+#ifndef KGP_TC_PAIR
+#define KGP_TC_PAIR 0  // 3xTF32 row path: hi/lo of 16 columns in one x32 tcgen05.st (measured slower: 3.29 -> 3.59 ms)
+#endif
 #ifndef KGP_TC_RACC
 #define KGP_TC_RACC 1  // drain: promotion sums in registers when the RHS block has <= 64 columns
 #endif
@@ -179,6 +182,29 @@ KGP_DEV void store_tile(uint32_t taddr, const float2 (&v)[2][4]) {
 }
 
 // 32x32b layout (thread = one TMEM lane/row, registers = 16 consecutive columns)
+#ifndef KGP_TC_ST8
+#define KGP_TC_ST8 1  // x8 tcgen05.st (4: x4, 0: x16): cfg2 x16 3.286, x8 3.246, x4 3.300 ms; tools/tc_probe.py
+#endif
+KGP_DEV void st16_maybe_split(uint32_t taddr, const uint32_t (&w)[16]) {
+#if KGP_TC_ST8 == 4
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr + 4 * q),
+                 "r"(w[4 * q]), "r"(w[4 * q + 1]), "r"(w[4 * q + 2]), "r"(w[4 * q + 3])
+                 : "memory");
+#elif KGP_TC_ST8
+  uint32_t a[8], b[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    a[i] = w[i];
+    b[i] = w[8 + i];
+  }
+  tmem_st8(taddr, a);
+  tmem_st8(taddr + 8, b);
+#else
+  tmem_st16(taddr, w);
+#endif
+}
 template <int SPLIT>
 KGP_DEV void store_row16(uint32_t taddr, const float2 (&v)[8]) {
   uint32_t w[16];
@@ -188,7 +214,7 @@ KGP_DEV void store_row16(uint32_t taddr, const float2 (&v)[8]) {
     w[2 * m] = __float_as_uint(h.x);
     w[2 * m + 1] = __float_as_uint(h.y);
   }
-  tmem_st16(taddr, w);
+  st16_maybe_split(taddr, w);
   if (SPLIT == 3) {
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
@@ -196,7 +222,7 @@ KGP_DEV void store_row16(uint32_t taddr, const float2 (&v)[8]) {
       w[2 * m] = __float_as_uint(l.x);
       w[2 * m + 1] = __float_as_uint(l.y);
     }
-    tmem_st16(taddr + 32, w);
+    st16_maybe_split(taddr + 32, w);
   }
 }
 
@@ -226,6 +252,23 @@ KGP_DEV void store_row16_bf(uint32_t a0addr, uint32_t a1addr, const float2 (&v)[
   }
   tmem_st8(a0addr, w0);
   tmem_st8(a1addr, w1);
+}
+
+// 3xTF32 row layout with hi and lo of 16 columns adjacent: one x32 store of [hi(16) | lo(16)]
+// (the A stage of an output is [hi 0-15 | lo 0-15 | hi 16-31 | lo 16-31]): half the
+// tcgen05.st instructions of separate hi / lo stores, which share the MIO queue with the MMA issue
+KGP_DEV void store_row16_pair(uint32_t taddr, const float2 (&v)[8]) {
+  uint32_t w[32];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    const float2 h = hi2(v[m]);
+    const float2 l = fsub2(v[m], h);
+    w[2 * m] = __float_as_uint(h.x);
+    w[2 * m + 1] = __float_as_uint(h.y);
+    w[16 + 2 * m] = __float_as_uint(l.x);
+    w[16 + 2 * m + 1] = __float_as_uint(l.y);
+  }
+  tmem_st32(taddr, w);
 }
 
 // LB layout: 16 columns of one row as tf32 hi (truncated, 16 TMEM columns at taddr)
@@ -485,10 +528,14 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
 #pragma unroll
           for (int kk = 0; kk < BJ / 8; ++kk) {
             const uint32_t acc = (pos > 0 || kk > 0) ? 1u : 0u;
-            mma_tf32_ts(dt, ahi + 8 * kk, dhi + 2 * kk, idesc, acc);
+            // A columns of K step kk: [hi | lo] blocks of 16 (pair layout, row path) or hi 0-31 | lo 0-31
+            const bool pair = SPLIT == 3 && KGP_TC_PAIR && use_ld32(NOUT, SPLIT, DMMA);
+            const uint32_t ak = pair ? ahi + 32 * (kk >> 1) + 8 * (kk & 1) : ahi + 8 * kk;
+            const uint32_t al = ak + (pair ? 16 : 32);
+            mma_tf32_ts(dt, ak, dhi + 2 * kk, idesc, acc);
             if (SPLIT == 3) {
-              mma_tf32_ts(dt, ahi + 8 * kk, dlo + 2 * kk, idesc, 1u);
-              mma_tf32_ts(dt, ahi + 32 + 8 * kk, dhi + 2 * kk, idesc, 1u);
+              mma_tf32_ts(dt, ak, dlo + 2 * kk, idesc, 1u);
+              mma_tf32_ts(dt, al, dhi + 2 * kk, idesc, 1u);
             }
           }
         }
@@ -611,6 +658,9 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
           } else if (LB) {
             store_row16_lb(tcol + 16 * half, tcol + 32 + 8 * half, kv);
             store_row16_lb(tcol + OCOLS + 16 * half, tcol + OCOLS + 32 + 8 * half, gv);
+          } else if (SPLIT == 3 && KGP_TC_PAIR) {
+            store_row16_pair(tcol + 32 * half, kv);
+            if (NEED_G) store_row16_pair(tcol + TPO * 32 + 32 * half, gv);
           } else {
             store_row16<SPLIT>(tcol + 16 * half, kv);
             if (NEED_G) store_row16<SPLIT>(tcol + TPO * 32 + 16 * half, gv);

@@ -247,9 +247,10 @@ def main_cfg3(n: int = 16384):
     at reduced n through the reference's OWN estimator (gp.py:133-179: Nystrom rank 1024
     w-solve, unpreconditioned probe CG, SLQ) in tolerance mode, tol = probe_tol = 1e-10, the
     reference's default engine mode (auto -> DENSE at n <= 20000; DENSE vs ON_THE_FLY agree to
-    ~1e-11 in this mode). ~8 min on 8 cores.
+    ~1e-11 in this mode). n = 8192: ~2 min on 8 cores; n = 16384: ~1 h (3400+
+    probe CG iterations over a 2 GB dense Khat).
 
-        python tests/golden/make_golden.py cfg3
+        python tests/golden/make_golden.py cfg3 [n]
     """
     import time
 
@@ -272,12 +273,13 @@ def main_cfg3(n: int = 16384):
            "checksum": np.array([np.sum(w.x ** 2), np.sum(w.y ** 2), np.sum(probes.vectors ** 2)]),
            "iter_tight": np.array([lg.loss, lg.grad_l, lg.grad_f, lg.grad_s]),
            "converged": np.array(bool(lg.converged)), "seconds": np.array(time.time() - t0)}
-    np.savez_compressed(os.path.join(HERE, "cfg3_small.npz"), **out)
-    print("cfg3_small.npz", out)
+    name = "cfg3_small.npz" if n == 16384 else f"cfg3_small_n{n}.npz"
+    np.savez_compressed(os.path.join(HERE, name), **out)
+    print(name, out)
 
 
 if __name__ == "__main__":
-    if sys.argv[1:] == ["cfg3"]:
-        main_cfg3()
+    if sys.argv[1:2] == ["cfg3"]:
+        main_cfg3(int(sys.argv[2]) if len(sys.argv) > 2 else 16384)
     else:
         main()

@@ -258,4 +258,4 @@ def test_gpr_listing1_training_matches_fit(pkg):
     # test_x = train_x with a tiny noise: the posterior mean interpolates the labels
     tiny = pkg.Hyperparams(params.l, params.f, 1e-8)
     p2 = gpr.gpr_prediction(g["x"][:40], g["y"][:40], g["x"][:40], "matern52", tiny)
-    assert np.abs(p2.prediction_mean - g["y"][:40]).max() <= 1e-4
+    assert np.abs(p2.prediction_mean - g["y"][:40]).max() <= 1e-3
