@@ -87,19 +87,19 @@ static int tc_env_int(const char* name, int dflt) {
   return s ? atoi(s) : dflt;
 }
 
-// blocks (x32 columns) accumulated in TMEM before promotion: 16 (512 columns). With one
-// accumulator buffer each promotion stalls the MMA (k = 64 two outputs 4.93 -> 4.62 ms at 16
-// vs 8); with two, fewer promotions mean fewer accumulator-barrier round trips for the MMA
-// issuer (cfg2 3.332 -> 3.302 ms with register promotion sums). Error 2.9e-6 -> 4.3e-6 at
-// cfg2 (tools/op_err2.py); env KGP_TC_FLUSH overrides.
+// blocks (x32 columns) accumulated in TMEM before promotion: 8 with two accumulator buffers
+// (the drain overlaps the MMA), 16 with one (each promotion stalls the MMA: k = 64 two
+// outputs 4.93 -> 4.62 ms; error 2.7e-6 -> 3.9e-6, tools/flush_sweep.py). 16 with two buffers
+// is 0.6 % faster at cfg2 but its operator error (4.3e-6) put the fast-mode configs[0] NLML
+// grad_f at 2.7e-3, over the 1e-3 bar (8: 4.2e-4; tools/nlml_precision.py), so 8 stays.
+// Env KGP_TC_FLUSH overrides both.
 static int tc_flush_blocks(int nab) {
   static int v = [] {
     const char* s = getenv("KGP_TC_FLUSH");
     int f = s ? atoi(s) : 0;
     return f < 0 ? 0 : f;
   }();
-  (void)nab;
-  return v > 0 ? v : 16;
+  return v > 0 ? v : (nab == 1 ? 16 : 8);
 }
 
 static std::mutex g_handles_mu;

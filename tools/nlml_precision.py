@@ -12,7 +12,7 @@ g = golden("cfg1_full.npz")
 ref = g["iter_tight"][:4]
 w = workloads.cfg1()
 probes = gp.ProbeSet.generate(w.n, w.k_z, w.probe_seed)
-for prec in ("fp64", "fast", "tf32"):
+for prec in (sys.argv[1:] or ["fp64", "fast", "tf32"]):
     e = kgp.KernelEngine(kgp.KernelType.GAUSSIAN, w.x, kgp.Hyperparams(w.l, w.f, w.s), precision=prec)
     try:
         lg = gp.nlml_grad_iterative(e, w.y, precond.build(e, w.rank), probes, tol=1e-10, max_iter=3000,
