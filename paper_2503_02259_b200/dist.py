@@ -98,7 +98,7 @@ class DistSolve:
 
 
 def dist_pcg(ops, comm: Comm, y_loc, tol, max_iter: int, precondition, shift: float = 1.0, diag_loc=None,
-             minv_fn=None):
+             minv_fn=None, check_every: int = 8):
     """Batched PCG over row-sharded state (solver.py:122-192). y_loc: (k, n_loc).
 
     Column groups as the device driver's (pcg.cu pcg_grouped_impl): ``tol`` and the
@@ -109,19 +109,31 @@ def dist_pcg(ops, comm: Comm, y_loc, tol, max_iter: int, precondition, shift: fl
     ``diag_loc`` (k, n_loc): a per-column diagonal added to the operator on the local rows
     (column j solves (Khat + diag(d_j)) x = y_j -- the Dirichlet GPC classes, the device
     path's kgp_engine_set_diag). ``minv_fn(head_loc) -> z_loc`` replaces the built-in
-    preconditioner on the leading columns (e.g. one replicated handle per GPC class)."""
+    preconditioner on the leading columns (e.g. one replicated handle per GPC class).
+
+    Device-resident: every per-column scalar (alpha, beta, rz, rel, the active mask, the
+    iteration counts, the breakdown flags) lives in device tensors, the dot products are
+    all-reduced in-stream (NCCL on GPUs: two all-reduces of k or 2k values per iteration, no
+    host synchronisation), and the host reads the active count only every ``check_every``
+    iterations -- iterations issued past a column's stop are masked no-ops (alpha = 0,
+    p unchanged), the pcg.cu driver's look-ahead. Per column the recurrence is the
+    reference's, so results equal a per-iteration host loop's."""
     torch = __import__("torch")
     k = y_loc.shape[0]
-    tol = np.broadcast_to(np.asarray(tol, dtype=np.float64), (k,)).copy()
-    cap = np.broadcast_to(np.asarray(max_iter, dtype=np.int64), (k,)).copy()
-    if np.any(tol < 0) or np.any(cap < 1):
+    tol_h = np.broadcast_to(np.asarray(tol, dtype=np.float64), (k,)).copy()
+    cap_h = np.broadcast_to(np.asarray(max_iter, dtype=np.int64), (k,)).copy()
+    if np.any(tol_h < 0) or np.any(cap_h < 1):
         raise ValueError("need tol >= 0 and max_iter >= 1")
     kp = k if precondition is True else (0 if precondition is False else int(precondition))
-    stride = int(cap.max())
+    stride = int(cap_h.max())
     dev, f64 = y_loc.device, torch.float64
+    tol_d = torch.from_numpy(tol_h).to(dev)
+    cap_d = torch.from_numpy(cap_h).to(dev)
 
-    def dots(a, b):
-        return comm.allreduce((a * b).sum(dim=1)).cpu().numpy()
+    def rowdots(*pairs):
+        """all-reduced per-column dots of each (a, b) pair, one collective: (len(pairs), k)."""
+        part = torch.stack([(a * b).sum(dim=1) for a, b in pairs])
+        return comm.allreduce(part)
 
     full_minv = getattr(ops, "replicated_minv", None)
     r0, r1 = comm.ranges[comm.rank]
@@ -141,53 +153,69 @@ def dist_pcg(ops, comm: Comm, y_loc, tol, max_iter: int, precondition, shift: fl
 
     x = torch.zeros_like(y_loc)
     r = y_loc.clone()
-    ynorm = np.sqrt(dots(r, r))
-    rel = np.where(ynorm > 0, 1.0, 0.0)
-    active = rel > tol
+    ynorm = torch.sqrt(rowdots((r, r))[0])
+    rel = torch.where(ynorm > 0, torch.ones_like(ynorm), torch.zeros_like(ynorm))
+    active = rel > tol_d
     alphas = torch.zeros((k, stride), dtype=f64, device=dev)
     betas = torch.zeros((k, stride), dtype=f64, device=dev)
-    iters = np.zeros(k, dtype=np.int64)
-    if active.any():
+    iters = torch.zeros(k, dtype=torch.int64, device=dev)
+    colbase = torch.arange(k, device=dev) * stride
+    brk_col = torch.full((), -1, dtype=torch.int64, device=dev)     # first column that broke down
+    brk_val = torch.zeros((), dtype=f64, device=dev)
+    nonfinite = torch.zeros((), dtype=torch.bool, device=dev)
+    safe_ynorm = torch.where(ynorm > 0, ynorm, torch.ones_like(ynorm))
+
+    def check():
+        c = int(brk_col.item())
+        if c >= 0:
+            raise BreakdownError(f"p^T A p = {float(brk_val.item())} in column {c}; operator is not SPD")
+        if bool(nonfinite.item()):
+            raise NumericalError("residual became non-finite during PCG")
+
+    if bool(active.any().item()):
         z = minv(r)
         p = z.clone()
-        rz = dots(r, z)
+        rz = rowdots((r, z))[0]
         peer = getattr(ops, "matmul_local", None)  # fused all-gather operator (PeerTiles)
-        for _ in range(stride):
+        for it in range(stride):
             ap = peer(p) if peer is not None else ops.matmul_rows(comm.allgather_rows(p))
             if diag_loc is not None:
                 ap = ap + diag_loc * p
-            pap = dots(p, ap)
-            act = np.flatnonzero(active)
-            bad = [j for j in act if not np.isfinite(pap[j]) or pap[j] <= 0.0]
-            if bad:
-                raise BreakdownError(f"p^T A p = {pap[bad[0]]} in column {bad[0]}; operator is not SPD")
-            alpha = np.zeros(k)
-            alpha[act] = rz[act] / pap[act]
-            at = torch.from_numpy(alpha).to(dev)[:, None]
-            x += at * p
-            r -= at * ap
-            idx = torch.from_numpy(act).to(dev)
-            alphas[idx, torch.from_numpy(iters[act]).to(dev)] = torch.from_numpy(alpha[act]).to(dev)
+            pap = rowdots((p, ap))[0]
+            bad = active & (~torch.isfinite(pap) | (pap <= 0.0))
+            first = torch.where(bad, torch.arange(k, device=dev), torch.full_like(iters, k)).min()
+            newbrk = (brk_col < 0) & (first < k)
+            brk_val = torch.where(newbrk, pap[first.clamp(max=k - 1)], brk_val)
+            brk_col = torch.where(newbrk, first, brk_col)
+            alpha = torch.where(active, rz / torch.where(active, pap, torch.ones_like(pap)), torch.zeros_like(pap))
+            x += alpha[:, None] * p
+            r -= alpha[:, None] * ap
+            slot = colbase + iters.clamp(max=stride - 1)
+            flat_a = alphas.view(-1)
+            flat_a[slot] = torch.where(active, alpha, flat_a[slot])
             z = minv(r)
-            rr = dots(r, r)
-            rzn = rr.copy()
-            if kp:
-                rzn[:kp] = dots(r[:kp], z[:kp])
-            if not np.all(np.isfinite(rr[act])):
-                raise NumericalError("residual became non-finite during PCG")
-            beta = np.zeros(k)
-            beta[act] = rzn[act] / rz[act]
-            betas[idx, torch.from_numpy(iters[act]).to(dev)] = torch.from_numpy(beta[act]).to(dev)
-            iters[act] += 1
-            rz[act] = rzn[act]
-            rel[act] = np.sqrt(rr[act]) / ynorm[act]
-            active[act] = (rel[act] > tol[act]) & (iters[act] < cap[act])
-            keep = np.flatnonzero(active)
-            if keep.size == 0:
-                break
-            kt = torch.from_numpy(keep).to(dev)
-            p[kt] = z[kt] + torch.from_numpy(beta[keep]).to(dev)[:, None] * p[kt]
-    return DistSolve(x, alphas, betas, iters, rel, rel <= tol)
+            if kp > 0:  # unpreconditioned columns have z = r, so r.z is their r.r bit for bit
+                d = rowdots((r, r), (r, z))
+                rr, rzn = d[0], d[1]
+            else:
+                rr = rowdots((r, r))[0]
+                rzn = rr
+            nonfinite = nonfinite | (active & ~torch.isfinite(rr)).any()
+            beta = torch.where(active, rzn / torch.where(active, rz, torch.ones_like(rz)), torch.zeros_like(rz))
+            flat_b = betas.view(-1)
+            flat_b[slot] = torch.where(active, beta, flat_b[slot])
+            iters = iters + active.to(torch.int64)
+            rz = torch.where(active, rzn, rz)
+            rel = torch.where(active, torch.sqrt(rr) / safe_ynorm, rel)
+            active = active & (rel > tol_d) & (iters < cap_d)
+            p = torch.where(active[:, None], z + beta[:, None] * p, p)
+            if (it + 1) % check_every == 0 or it + 1 == stride:
+                check()
+                if not bool(active.any().item()):
+                    break
+        check()
+    rel_h = rel.cpu().numpy()
+    return DistSolve(x, alphas, betas, iters.cpu().numpy(), rel_h, rel_h <= tol_h)
 
 
 def _grads(ops, comm, v_loc):

@@ -319,7 +319,9 @@ def _peer_worker(rank, world, port, errfile):
                              shift=S)
         sol, al, be, rel, conv = orc.pcg(lambda b: orc.khat_matmul(KT, x, L, F, S, b), ny.apply_inverse, z, 1e-10,
                                          500)
-        assert comm.gathers == 0 and ops.local_calls == int(res.iters.max())  # no separate operator all-gather
+        # no separate operator all-gather; one operator call per iteration, plus at most the
+        # look-ahead of dist_pcg's device-resident loop (host checks every 8 iterations)
+        assert comm.gathers == 0 and int(res.iters.max()) <= ops.local_calls <= int(res.iters.max()) + 8
         full = comm.allgather_rows(res.x).numpy().T
         assert np.max(np.abs(full - sol)) <= 1e-6 * np.max(np.abs(sol)), "solution"
         assert list(res.converged) == list(conv)
