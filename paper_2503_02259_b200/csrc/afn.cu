@@ -35,11 +35,12 @@ namespace {
 
 // ------------------------------------------------------------------ k nearest earlier points
 constexpr int KNN_T = 128;
-constexpr int KNN_MAX = 64;
+constexpr int KNN_MAX = 64;         // FSAI pattern (earlier points)
+constexpr int KNN_MAX_CROSS = 128;  // local predictive variance neighbourhoods
 
 // PREV: queries are the candidates themselves (xq == x) and only j < i count (FSAI pattern);
 // otherwise every candidate counts (nearest training points of test points).
-template <int D, bool PREV>
+template <int D, bool PREV, int MAXK = KNN_MAX>
 __global__ void __launch_bounds__(KNN_T) knn_kernel(int64_t nq, const double* __restrict__ xq, int64_t nx,
                                                     const double* __restrict__ x, int npt, int64_t* __restrict__ out) {
   __shared__ double xs[KNN_T * D];
@@ -47,8 +48,8 @@ __global__ void __launch_bounds__(KNN_T) knn_kernel(int64_t nq, const double* __
   double q[D];
 #pragma unroll
   for (int c = 0; c < D; ++c) q[c] = i < nq ? xq[i * D + c] : 0.0;
-  double bd[KNN_MAX];
-  int64_t bj[KNN_MAX];
+  double bd[MAXK];
+  int64_t bj[MAXK];
   int cnt = 0;
   int64_t last = nx;
   if (PREV) last = (int64_t)(blockIdx.x + 1) * KNN_T < nx ? (int64_t)(blockIdx.x + 1) * KNN_T : nx;
@@ -411,12 +412,13 @@ __global__ void afn_gather_tail_kernel(int64_t n2, int64_t m, const double* __re
 // var(x*) ~= f^2 - c^T (Khat_NN)^-1 c over the K nearest training points N of x* (local
 // kriging): one CTA per test point, S_NN = f^2 kappa + s I and c = f^2 kappa(x*, x_N) in
 // shared memory, Cholesky, var = f^2 - |L^-1 c|^2.
+constexpr int LV_MAXM = KNN_MAX_CROSS;  // 128 x 128 fp64 block: 128 KB of shared memory
 struct LvSmem {
-  double S[FS_MAXM * FS_MAXM];
-  double xs[FS_MAXM * 16];
-  double c[FS_MAXM];
+  double S[LV_MAXM * LV_MAXM];
+  double xs[LV_MAXM * 16];
+  double c[LV_MAXM];
   double q[16];
-  int idx[FS_MAXM];
+  int idx[LV_MAXM];
   int m;
   int fail;
 };
@@ -701,7 +703,7 @@ extern "C" int kgp_knn_prev(int64_t n, int d, const double* x, int npt, int64_t*
 extern "C" int kgp_knn_cross(int64_t nq, const double* xq, int64_t nx, const double* x, int d, int npt,
                              int64_t* idx_out, void* stream) {
   KGP_REQUIRE(nq >= 0 && nx >= 1 && d >= 1 && d <= 16, KGP_ERR_INVALID, "bad kNN shapes (d=%d)", d);
-  KGP_REQUIRE(npt >= 1 && npt <= KNN_MAX, KGP_ERR_INVALID, "npt=%d outside [1, %d]", npt, KNN_MAX);
+  KGP_REQUIRE(npt >= 1 && npt <= KNN_MAX_CROSS, KGP_ERR_INVALID, "npt=%d outside [1, %d]", npt, KNN_MAX_CROSS);
   KGP_REQUIRE(nq == 0 || (xq != nullptr && x != nullptr && idx_out != nullptr), KGP_ERR_INVALID, "NULL pointer");
   if (nq == 0) return KGP_OK;
   cudaStream_t st = (cudaStream_t)stream;
@@ -709,7 +711,10 @@ extern "C" int kgp_knn_cross(int64_t nq, const double* xq, int64_t nx, const dou
   switch (d) {
 #define KGP_KNNX_CASE(D)                                                        \
   case D:                                                                       \
-    knn_kernel<D, false><<<grid, KNN_T, 0, st>>>(nq, xq, nx, x, npt, idx_out);  \
+    if (npt <= KNN_MAX)                                                         \
+      knn_kernel<D, false><<<grid, KNN_T, 0, st>>>(nq, xq, nx, x, npt, idx_out); \
+    else                                                                        \
+      knn_kernel<D, false, KNN_MAX_CROSS><<<grid, KNN_T, 0, st>>>(nq, xq, nx, x, npt, idx_out); \
     break;
     KGP_KNNX_CASE(1) KGP_KNNX_CASE(2) KGP_KNNX_CASE(3) KGP_KNNX_CASE(4) KGP_KNNX_CASE(5) KGP_KNNX_CASE(6)
     KGP_KNNX_CASE(7) KGP_KNNX_CASE(8) KGP_KNNX_CASE(9) KGP_KNNX_CASE(10) KGP_KNNX_CASE(11) KGP_KNNX_CASE(12)
@@ -723,8 +728,8 @@ extern "C" int kgp_knn_cross(int64_t nq, const double* xq, int64_t nx, const dou
 extern "C" int kgp_local_variance(int kernel, int64_t nq, int d, const double* xq, const double* x, double l,
                                   double f, double s, int npt, const int64_t* nbr, double* var, void* stream) {
   KGP_REQUIRE(kernel >= 0 && kernel <= 2, KGP_ERR_INVALID, "unknown kernel id %d", kernel);
-  KGP_REQUIRE(d >= 1 && d <= 16 && npt >= 1 && npt <= KNN_MAX && nq >= 0 && nq < ((int64_t)1 << 31),
-              KGP_ERR_INVALID, "bad local-variance shapes");
+  KGP_REQUIRE(d >= 1 && d <= 16 && npt >= 1 && npt <= KNN_MAX_CROSS && nq >= 0 && nq < ((int64_t)1 << 31),
+              KGP_ERR_INVALID, "bad local-variance shapes (npt <= %d)", KNN_MAX_CROSS);
   KGP_REQUIRE(l > 0.0 && s > 0.0, KGP_ERR_INVALID, "length scale and noise must be positive");
   if (nq == 0) return KGP_OK;
   cudaStream_t st = (cudaStream_t)stream;
