@@ -1,1 +1,2 @@
-for fl in 4 8 12 16; do echo "flush $fl"; KGP_TC_FLUSH=$fl timeout 200 python tools/nlml_precision.py fast bf16x3 2>&1 | grep -E "fast|bf16"; KGP_TC_FLUSH=$fl timeout 100 python tools/tc_probe.py 65536 32 2 fast; done
+for v in default one1 one2 one3; do L=paper_2503_02259_b200/libkgp.so; [ $v != default ] && L=tools/variants/$v/libkgp.so; for i in 1 2; do echo -n "$v "; KGP_LIB=$L timeout 100 python tools/tc_probe.py 65536 32 2 fast; done; done
+for v in one1 one2; do KGP_LIB=tools/variants/$v/libkgp.so timeout 100 python tools/op_err2.py 65536 32 fast; done
