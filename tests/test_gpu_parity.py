@@ -71,11 +71,13 @@ def test_engine_fp64_matches_reference(pkg, tag):
     assert rel_max(df, g[f"{tag}_df"]) <= 1e-12
 
 
-@pytest.mark.parametrize("precision,bar", [("fast", 2e-5), ("tf32", 1e-3)])
+@pytest.mark.parametrize("precision,bar", [("fast", 2e-5), ("tf32", 1e-3), ("bf16x3", 5e-5)])
 @pytest.mark.parametrize("tag", list("abcdefg"))
 def test_engine_tensorcore_matches_reference(pkg, tag, precision, bar):
     g = golden("engine.npz")
     n, d, k, l, f, s, bs = g[f"{tag}_meta"]
+    if precision == "bf16x3" and d <= 4:
+        pytest.skip("bf16x3 runs with the tensor-core distance only (d > 4)")
     e = pkg.KernelEngine(pkg.KernelType(str(g[f"{tag}_kt"])), g[f"{tag}_x"], _hp(pkg, l, f, s),
                          precision=precision)
     b = g[f"{tag}_b"]
@@ -103,6 +105,33 @@ def test_fast_operator_shapes(pkg, kt, d, k):
     assert rel_max(got[2], ref[2]) <= 2e-5
 
 
+@pytest.mark.parametrize("kt", KTS)
+@pytest.mark.parametrize("d", [5, 8, 11, 16])
+@pytest.mark.parametrize("k", [1, 16, 17, 33, 64, 130])
+def test_bf16x3_operator_shapes(pkg, kt, d, k):
+    """The bf16x3 contraction (two round-to-nearest bf16 terms per operand, A0B0 + A0B1 + A1B0)
+    against the fp64 engine: 5e-5 (2.5x the 3xTF32 bar: its two-term bf16 splits keep 16
+    mantissa bits, the tf32 hi/lo ones 22; single-column products reach 2.4e-5) and 5e-4 for
+    dKhat/dl."""
+    rng = np.random.default_rng(d * 1000 + k + 7)
+    n = 300 + 7 * d
+    x = rng.standard_normal((n, d))
+    b = rng.standard_normal((n, k))
+    hp = _hp(pkg, 0.9 * np.sqrt(d), 1.3, 0.2)
+    ref = pkg.KernelEngine(pkg.KernelType(kt), x, hp, precision="fp64").matmul_with_grads(b)
+    got = pkg.KernelEngine(pkg.KernelType(kt), x, hp, precision="bf16x3").matmul_with_grads(b)
+    assert rel_max(got[0], ref[0]) <= 5e-5
+    assert rel_max(got[1], ref[1]) <= 5e-4
+    assert rel_max(got[2], ref[2]) <= 5e-5
+
+
+def test_bf16x3_rejects_direct_distance(pkg):
+    x = np.random.default_rng(0).standard_normal((100, 3))
+    e = pkg.KernelEngine(pkg.KernelType.GAUSSIAN, x, _hp(pkg, 1, 1, 0.1), precision="bf16x3")
+    with pytest.raises(ValueError, match="d > 4"):
+        e.matmul(np.ones((100, 2)))
+
+
 def test_cfg2_row_subsample(pkg):
     """configs[1] at full size: fast K.Z and dK/dl.Z against the C oracle on 512 rows."""
     import torch
@@ -111,19 +140,21 @@ def test_cfg2_row_subsample(pkg):
     from paper_2503_02259_b200 import workloads
 
     w = workloads.cfg2()
-    e = pkg.KernelEngine(pkg.KernelType.GAUSSIAN, w.x, _hp(pkg, w.l, w.f, w.s), precision="fast")
     zd = torch.from_numpy(w.z).cuda()
-    kk, dl, _ = e.apply(zd, True, True, False)
     rows = np.random.default_rng(7).choice(w.n, 512, replace=False)
     rows.sort()
-    kk, dl = kk.cpu().numpy()[rows], dl.cpu().numpy()[rows]
     refk = np.empty((512, w.z.shape[1]))
     refd = np.empty_like(refk)
     for i, gi in enumerate(rows):
         a, bb = oc.matmul("gaussian", w.x, w.l, w.f, w.s, w.z, row0=int(gi), nrows=1, want_dl=True)
         refk[i], refd[i] = a[0], bb[0]
-    assert rel_max(kk, refk) <= 2e-5
-    assert rel_max(dl, refd) <= 2e-4
+    for precision in ("fast", "bf16x3"):
+        e = pkg.KernelEngine(pkg.KernelType.GAUSSIAN, w.x, _hp(pkg, w.l, w.f, w.s), precision=precision)
+        kk, dl, _ = e.apply(zd, True, True, False)
+        kk, dl = kk.cpu().numpy()[rows], dl.cpu().numpy()[rows]
+        assert rel_max(kk, refk) <= 2e-5, precision
+        assert rel_max(dl, refd) <= 2e-4, precision
+        e.close()
 
 
 def test_cross_matmul_matches_panel(pkg):
