@@ -12,6 +12,8 @@
 // columns (grid.y); when the row blocks cannot fill the GPU the column range is split
 // over grid.z and the partial sums are reduced in a fixed order (deterministic).
 // Bound: the FP64 pipe (distance 3d + exp ~25 + KS FMA per entry and output).
+#include <stdlib.h>
+
 #include "kgp_common.cuh"
 #include "kgp_internal.h"
 
@@ -103,6 +105,167 @@ __global__ void __launch_bounds__(NT) kmm_f64_kernel(const F64Params p) {
   }
 }
 
+// ------------------------------------------------------------------ symmetric small-k path
+// Khat is symmetric, so for the SQUARE operator with few right-hand sides (the PCG w-solve's
+// single column, where evaluating kernel entries is nearly all the work) every entry is
+// evaluated once: a CTA takes a pair of 128-point blocks (I, J >= I) and uses each kappa_ij for
+// both y_I += K_IJ B_J (thread = row i, register accumulators) and y_J += K_IJ^T B_I (each
+// warp's 32 row contributions per column j summed by a transpose-butterfly: 31 shuffles per
+// 32 columns, lane l ending with column l; the warps combined in shared memory). Every
+// row receives exactly one partial per partner block; P[partner][row][c] is summed in
+// partner order by f64_sym_reduce_kernel (run-to-run deterministic). 64-point blocks: the
+// kernel is FP64-latency-bound (ncu: fp64 pipe 49 %, stall_wait dominant at 128-point blocks
+// and ~14 warps per SM), so twice the CTAs matter more than the larger tiles' reuse.
+#ifndef KGP_F64_SB
+#define KGP_F64_SB 64
+#endif
+constexpr int SB = KGP_F64_SB;  // points per block (64: twice the CTAs of 128, the kernel is latency-bound)
+constexpr int SNW = SB / 32;    // warps per CTA
+
+template <int KT, int KS, int DB>
+__global__ void __launch_bounds__(SB) kmm_f64_sym_kernel(const F64Params p, int nb, double* __restrict__ part) {
+  if (p.gate != nullptr && *p.gate == 0) return;
+  __shared__ double sX[SB][DB + 1];
+  __shared__ double sB[SB][KS];
+  __shared__ double sCol[SNW][SB][KS];
+  // tile pair (I, J), I <= J, from the linear index
+  const int64_t tix = blockIdx.x;
+  int I = (int)((sqrt(8.0 * (double)tix + 1.0) - 1.0) * 0.5);  // row of the packed upper triangle
+  while ((int64_t)I * (I + 1) / 2 > tix) --I;
+  while ((int64_t)(I + 1) * (I + 2) / 2 <= tix) ++I;
+  // packed order by J: tix = J (J + 1) / 2 + I' with I' <= J
+  const int J = I;
+  const int Ip = (int)(tix - (int64_t)J * (J + 1) / 2);
+  const int rowblk = Ip, colblk = J;  // rowblk <= colblk
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = (int)p.ncols, d = p.d;
+  const int64_t r = (int64_t)rowblk * SB + tid;
+  const bool live = r < n;
+  double xi[DB];
+#pragma unroll
+  for (int q = 0; q < DB; ++q) xi[q] = (live && q < d) ? p.xr[r * d + q] : 0.0;
+  double bi[KS];
+#pragma unroll
+  for (int c = 0; c < KS; ++c) bi[c] = (live && c < p.k) ? p.b[r * p.b_rs + (int64_t)c * p.b_cs] : 0.0;
+  const int64_t j0 = (int64_t)colblk * SB;
+  const int nj = (int)(n - j0 < SB ? n - j0 : SB);
+  for (int e = tid; e < nj * d; e += SB) sX[e / d][e % d] = p.xc[(j0 + e / d) * d + e % d];
+  for (int e = tid; e < SB * KS; e += SB) {  // rows past the last point stay zero
+    const int jj = e / KS, c = e % KS;
+    sB[jj][c] = (jj < nj && c < p.k) ? p.b[(j0 + jj) * p.b_rs + (int64_t)c * p.b_cs] : 0.0;
+  }
+  __syncthreads();
+  const bool offdiag = rowblk != colblk;
+  double acc[KS];
+#pragma unroll
+  for (int c = 0; c < KS; ++c) acc[c] = 0.0;
+  constexpr int Q = 32 / KS;  // columns per butterfly chunk: Q x KS = 32 values per lane
+  for (int jc = 0; jc < SB; jc += Q) {
+    double v[Q][KS];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int jj = jc + q;
+      double kv = 0.0;
+      if (live && jj < nj) {
+        double r2 = 0.0;
+#pragma unroll
+        for (int t = 0; t < DB; ++t) {
+          if (t < d) {
+            const double df = xi[t] - sX[jj][t];
+            r2 = __dadd_rn(r2, __dmul_rn(df, df));  // numba's rounding (no FMA contraction)
+          }
+        }
+        kv = kappa64<KT>(r2, p.l);
+      }
+#pragma unroll
+      for (int c = 0; c < KS; ++c) {
+        acc[c] = fma(kv, sB[jj < SB ? jj : 0][c], acc[c]);
+        v[q][c] = kv * bi[c];
+      }
+    }
+    if (offdiag) {
+      // transpose-butterfly over the Q columns (log2 Q halving steps), then a plain xor-sum
+      // over the lanes sharing lane % Q: lane l ends with the warp's sum for column l % Q
+#pragma unroll
+      for (int c = 0; c < KS; ++c) {
+#pragma unroll
+        for (int off = Q / 2; off >= 1; off >>= 1) {
+#pragma unroll
+          for (int q = 0; q < off; ++q) {
+            const bool up = (lane & off) != 0;
+            const double send = up ? v[q][c] : v[q + off][c];
+            const double keep = up ? v[q + off][c] : v[q][c];
+            v[q][c] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+          }
+        }
+#pragma unroll
+        for (int off = Q; off < 32; off <<= 1) v[0][c] += __shfl_xor_sync(0xffffffffu, v[0][c], off);
+        if (lane < Q) sCol[warp][jc + lane][c] = v[0][c];
+      }
+    }
+  }
+  // row direction: this block pair's contribution to rows of rowblk, partner = colblk
+  if (live) {
+#pragma unroll
+    for (int c = 0; c < KS; ++c)
+      if (c < p.k) part[((int64_t)colblk * n + r) * p.k + c] = acc[c];
+  }
+  if (offdiag) {  // column direction: contribution to rows of colblk, partner = rowblk
+    __syncthreads();
+    if (tid < nj) {
+#pragma unroll
+      for (int c = 0; c < KS; ++c) {
+        if (c >= p.k) continue;
+        double t = sCol[0][tid][c];
+#pragma unroll
+        for (int w = 1; w < SNW; ++w) t += sCol[w][tid][c];
+        part[((int64_t)rowblk * n + j0 + tid) * p.k + c] = t;
+      }
+    }
+  }
+}
+
+__global__ void f64_sym_reduce_kernel(const F64Params p, int nb, const double* __restrict__ part) {
+  if (p.gate != nullptr && *p.gate == 0) return;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = p.ncols;
+  if (e >= n * p.k) return;
+  const int64_t r = e / p.k;
+  const int c = (int)(e % p.k);
+  // eight independent loads in flight, added in partner order (deterministic)
+  const int64_t stride = n * p.k;
+  double a = 0.0;
+  int q = 0;
+  for (; q + 8 <= nb; q += 8) {
+    double t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t[u] = part[(int64_t)(q + u) * stride + e];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a += t[u];
+  }
+  for (; q < nb; ++q) a += part[(int64_t)q * stride + e];
+  const int64_t o = r * p.o_rs + (int64_t)c * p.o_cs;
+  if (p.out_k) p.out_k[o] = p.f2 * a + p.s * p.b[r * p.b_rs + (int64_t)c * p.b_cs];
+  if (p.out_df) p.out_df[o] = p.two_f * a;
+}
+
+template <int KT, int KS>
+int launch_sym_ks(const F64Params& p, int nb, double* part, cudaStream_t st) {
+  const unsigned pairs = (unsigned)((int64_t)nb * (nb + 1) / 2);
+  if (p.d <= 4) kmm_f64_sym_kernel<KT, KS, 4><<<pairs, SB, 0, st>>>(p, nb, part);
+  else if (p.d <= 8) kmm_f64_sym_kernel<KT, KS, 8><<<pairs, SB, 0, st>>>(p, nb, part);
+  else kmm_f64_sym_kernel<KT, KS, 16><<<pairs, SB, 0, st>>>(p, nb, part);
+  KGP_LAUNCH("kmm_f64_sym_kernel");
+  return KGP_OK;
+}
+
+template <int KT>
+int launch_sym(const F64Params& p, int nb, double* part, cudaStream_t st) {
+  if (p.k == 1) return launch_sym_ks<KT, 1>(p, nb, part, st);
+  if (p.k == 2) return launch_sym_ks<KT, 2>(p, nb, part, st);
+  return launch_sym_ks<KT, 4>(p, nb, part, st);
+}
+
 // sum the column-split partials in split order, then the epilogue
 __global__ void f64_reduce_kernel(const F64Params p, int nsplit) {
   if (p.gate != nullptr && *p.gate == 0) return;
@@ -171,6 +334,26 @@ int launch_kmm_f64(int kt, const F64Params& p_in, DevBuf& ws, cudaStream_t st) {
   KGP_REQUIRE(kt >= 0 && kt <= 2, KGP_ERR_INVALID, "unknown kernel id %d", kt);
   if (p_in.nrows <= 0) return KGP_OK;
   F64Params p = p_in;
+  // symmetric path: the square operator (rows = columns = all points, the + s B shift on
+  // the diagonal), K-type outputs only, k <= 4, n <= 16384 (partials: n / SB x n x k fp64)
+  static const bool sym_on = [] {
+    const char* e = getenv("KGP_F64_SYM");
+    return !(e && atoi(e) == 0);
+  }();
+  if (sym_on && p.xr == p.xc && p.nrows == p.ncols && p.diag_row0 == 0 && p.out_dl == nullptr && p.k >= 1 &&
+      p.k <= 4 && p.ncols <= 16384) {
+    const int nb = (int)((p.ncols + SB - 1) / SB);
+    int rc = ws.ensure(sizeof(double) * (size_t)nb * p.ncols * p.k);
+    if (rc) return rc;
+    double* part = ws.as<double>();
+    rc = (kt == GAUSS) ? launch_sym<GAUSS>(p, nb, part, st)
+                       : (kt == MAT32) ? launch_sym<MAT32>(p, nb, part, st) : launch_sym<MAT52>(p, nb, part, st);
+    if (rc) return rc;
+    const int64_t cnt = p.ncols * p.k;
+    f64_sym_reduce_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(p, nb, part);
+    KGP_LAUNCH("f64_sym_reduce_kernel");
+    return KGP_OK;
+  }
   const int nout = p.out_dl ? 2 : 1;
   const int ks = slice_for(p.k, nout);
   const int64_t rblk = (p.nrows + NT - 1) / NT, kslc = (p.k + ks - 1) / ks;

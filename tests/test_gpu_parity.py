@@ -132,6 +132,27 @@ def test_bf16x3_rejects_direct_distance(pkg):
         e.matmul(np.ones((100, 2)))
 
 
+@pytest.mark.parametrize("kt", KTS)
+@pytest.mark.parametrize("n,k", [(1, 1), (127, 1), (129, 2), (1000, 3), (2049, 4), (300, 5)])
+def test_fp64_symmetric_small_k(pkg, kt, n, k):
+    """The fp64 square operator with k <= 4 evaluates each entry once for both row blocks
+    (kmm_f64_sym_kernel, transpose-butterfly column sums, partner-ordered partials): equal to
+    the oracle's streamed operator to the fp64 bar, including ragged last blocks; k = 5 takes
+    the ordinary path. ON_THE_FLY so the products are not the DENSE-mode DGEMM."""
+    from oracle import kgp_oracle as orc
+
+    rng = np.random.default_rng(n + 31 * k)
+    x = rng.uniform(0, 1, (n, 3))
+    b = rng.standard_normal((n, k))
+    hp = _hp(pkg, 0.4, 1.3, 0.05)
+    e = pkg.KernelEngine(pkg.KernelType(kt), x, hp, mode=pkg.EngineMode.ON_THE_FLY, precision="fp64")
+    ref = orc.khat_matmul(kt, x, hp.l, hp.f, hp.s, b)
+    assert rel_max(e.matmul(b), ref) <= 1e-12
+    assert rel_max(e.grad_matmul(pkg.Theta.F, b), orc.khat_matmul(kt, x, hp.l, hp.f, hp.s, b, theta="f")) <= 1e-12
+    got = e.matmul(b)
+    assert np.array_equal(got, e.matmul(b))  # run-to-run identical
+
+
 def test_cfg2_row_subsample(pkg):
     """configs[1] at full size: fast K.Z and dK/dl.Z against the C oracle on 512 rows."""
     import torch
