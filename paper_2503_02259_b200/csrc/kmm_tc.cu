@@ -42,9 +42,6 @@ namespace kgp {
 
 namespace {
 
-#ifndef KGP_TC_PAIR
-#define KGP_TC_PAIR 0  // 3xTF32 row path: hi/lo of 16 columns in one x32 tcgen05.st (measured slower: 3.29 -> 3.59 ms)
-#endif
 #ifndef KGP_TC_RACC
 #define KGP_TC_RACC 1  // drain: promotion sums in registers when the RHS block has <= 64 columns
 #endif
@@ -228,47 +225,19 @@ KGP_DEV void store_row16(uint32_t taddr, const float2 (&v)[8]) {
 
 // bf16x3 layout: 16 columns of one row as two round-to-nearest bf16 terms A0 + A1 (8 bf16
 // pairs each, lower K in the low half): A0 at a0addr, A1 at a1addr (8 TMEM columns each)
-#ifndef KGP_TC_BFTRUNC
-#define KGP_TC_BFTRUNC 0  // 1: A0 by truncation (2 LOP + PRMT per pair) instead of round-to-nearest
-#endif
 KGP_DEV void store_row16_bf(uint32_t a0addr, uint32_t a1addr, const float2 (&v)[8]) {
   uint32_t w0[8], w1[8];
 #pragma unroll
   for (int m = 0; m < 8; ++m) {
-#if KGP_TC_BFTRUNC
-    const float2 h = make_float2(__uint_as_float(__float_as_uint(v[m].x) & 0xFFFF0000u),
-                                 __uint_as_float(__float_as_uint(v[m].y) & 0xFFFF0000u));
-    const float2 r = fsub2(v[m], h);
-    const __nv_bfloat162 b1 = __floats2bfloat162_rn(r.x, r.y);
-    w0[m] = __byte_perm(__float_as_uint(h.x), __float_as_uint(h.y), 0x7632);
-#else
     const __nv_bfloat162 b0 = __floats2bfloat162_rn(v[m].x, v[m].y);
     const float2 f0 = __bfloat1622float2(b0);
     const float2 r = fsub2(v[m], f0);
     const __nv_bfloat162 b1 = __floats2bfloat162_rn(r.x, r.y);
     w0[m] = *reinterpret_cast<const uint32_t*>(&b0);
-#endif
     w1[m] = *reinterpret_cast<const uint32_t*>(&b1);
   }
   tmem_st8(a0addr, w0);
   tmem_st8(a1addr, w1);
-}
-
-// 3xTF32 row layout with hi and lo of 16 columns adjacent: one x32 store of [hi(16) | lo(16)]
-// (the A stage of an output is [hi 0-15 | lo 0-15 | hi 16-31 | lo 16-31]): half the
-// tcgen05.st instructions of separate hi / lo stores, which share the MIO queue with the MMA issue
-KGP_DEV void store_row16_pair(uint32_t taddr, const float2 (&v)[8]) {
-  uint32_t w[32];
-#pragma unroll
-  for (int m = 0; m < 8; ++m) {
-    const float2 h = hi2(v[m]);
-    const float2 l = fsub2(v[m], h);
-    w[2 * m] = __float_as_uint(h.x);
-    w[2 * m + 1] = __float_as_uint(h.y);
-    w[16 + 2 * m] = __float_as_uint(l.x);
-    w[16 + 2 * m + 1] = __float_as_uint(l.y);
-  }
-  tmem_st32(taddr, w);
 }
 
 // LB layout: 16 columns of one row as tf32 hi (truncated, 16 TMEM columns at taddr)
@@ -528,14 +497,10 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
 #pragma unroll
           for (int kk = 0; kk < BJ / 8; ++kk) {
             const uint32_t acc = (pos > 0 || kk > 0) ? 1u : 0u;
-            // A columns of K step kk: [hi | lo] blocks of 16 (pair layout, row path) or hi 0-31 | lo 0-31
-            const bool pair = SPLIT == 3 && KGP_TC_PAIR && use_ld32(NOUT, SPLIT, DMMA);
-            const uint32_t ak = pair ? ahi + 32 * (kk >> 1) + 8 * (kk & 1) : ahi + 8 * kk;
-            const uint32_t al = ak + (pair ? 16 : 32);
-            mma_tf32_ts(dt, ak, dhi + 2 * kk, idesc, acc);
+            mma_tf32_ts(dt, ahi + 8 * kk, dhi + 2 * kk, idesc, acc);
             if (SPLIT == 3) {
-              mma_tf32_ts(dt, ak, dlo + 2 * kk, idesc, 1u);
-              mma_tf32_ts(dt, al, dhi + 2 * kk, idesc, 1u);
+              mma_tf32_ts(dt, ahi + 8 * kk, dlo + 2 * kk, idesc, 1u);
+              mma_tf32_ts(dt, ahi + 32 + 8 * kk, dhi + 2 * kk, idesc, 1u);
             }
           }
         }
@@ -658,9 +623,6 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
           } else if (LB) {
             store_row16_lb(tcol + 16 * half, tcol + 32 + 8 * half, kv);
             store_row16_lb(tcol + OCOLS + 16 * half, tcol + OCOLS + 32 + 8 * half, gv);
-          } else if (SPLIT == 3 && KGP_TC_PAIR) {
-            store_row16_pair(tcol + 32 * half, kv);
-            if (NEED_G) store_row16_pair(tcol + TPO * 32 + 32 * half, gv);
           } else {
             store_row16<SPLIT>(tcol + 16 * half, kv);
             if (NEED_G) store_row16<SPLIT>(tcol + TPO * 32 + 16 * half, gv);

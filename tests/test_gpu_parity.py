@@ -965,3 +965,23 @@ def test_fused_allgather_operator_errors(pkg):
         _lib.call("kgp_engine_set_peers", ef.handle, 2, 0, bad, ptrs, 4)
     with pytest.raises(ValueError, match="not rank 1"):
         _lib.call("kgp_engine_set_peers", ef.handle, 2, 1, starts, ptrs, 4)
+    # a peer configuration is valid only for the precision and row block it was made with
+    # (ADVICE r1): a later set_precision / set_rows makes publish and peer_matmul refuse
+    import ctypes as ct
+
+    nb, ptr = ct.c_int64(), ct.c_void_p()
+    one = (ct.c_int64 * 2)(0, 256)
+    _lib.call("kgp_engine_set_rows", ef.handle, 0, 256)
+    _lib.call("kgp_engine_peer_buffer_bytes", ef.handle, 4, 256, ct.byref(nb))
+    _lib.call("kgp_peer_alloc", nb.value, ct.byref(ptr), None)
+    try:
+        _lib.call("kgp_engine_set_peers", ef.handle, 1, 0, one, (ct.c_void_p * 1)(ptr.value), 4)
+        _lib.call("kgp_engine_set_precision", ef.handle, 2)  # tf32
+        with pytest.raises(KernelGpError, match="precision changed"):
+            _lib.call("kgp_engine_peer_publish", ef.handle, 4, 1, 1, 256, 1, None)
+        _lib.call("kgp_engine_set_precision", ef.handle, 1)
+        _lib.call("kgp_engine_set_rows", ef.handle, 0, 128)
+        with pytest.raises(KernelGpError, match="rows changed"):
+            _lib.call("kgp_engine_peer_matmul", ef.handle, 4, 1, 1, None, None, 1, 128, None)
+    finally:
+        _lib.call("kgp_peer_free", ptr.value)
