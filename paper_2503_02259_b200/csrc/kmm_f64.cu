@@ -17,6 +17,17 @@
 #include "kgp_common.cuh"
 #include "kgp_internal.h"
 
+#ifndef KGP_F64_FASTEXP
+#define KGP_F64_FASTEXP 1  // the operator's entries through exp_neg64 (kgp_common.cuh)
+#endif
+#if KGP_F64_FASTEXP
+#define KGP_KAPPA kappa64f
+#define KGP_DKAPPA dkappa64f
+#else
+#define KGP_KAPPA kappa64
+#define KGP_DKAPPA dkappa64
+#endif
+
 namespace kgp {
 
 namespace {
@@ -68,8 +79,8 @@ __global__ void __launch_bounds__(NT) kmm_f64_kernel(const F64Params p) {
           r2 = __dadd_rn(r2, __dmul_rn(df, df));  // numba's rounding (no FMA contraction)
         }
       }
-      const double kv = kappa64<KT>(r2, p.l);
-      const double gv = NOUT == 2 ? dkappa64<KT>(r2, p.l) : 0.0;
+      const double kv = KGP_KAPPA<KT>(r2, p.l);
+      const double gv = NOUT == 2 ? KGP_DKAPPA<KT>(r2, p.l) : 0.0;
 #pragma unroll
       for (int c = 0; c < KS; c += 2) {
         const double2 bv = *reinterpret_cast<const double2*>(&sB[jj][c]);
@@ -175,7 +186,7 @@ __global__ void __launch_bounds__(SB) kmm_f64_sym_kernel(const F64Params p, int 
             r2 = __dadd_rn(r2, __dmul_rn(df, df));  // numba's rounding (no FMA contraction)
           }
         }
-        kv = kappa64<KT>(r2, p.l);
+        kv = KGP_KAPPA<KT>(r2, p.l);
       }
 #pragma unroll
       for (int c = 0; c < KS; ++c) {
