@@ -265,8 +265,8 @@ def nlml_metric(cpu: bool):
     torch.linalg.solve_triangular(torch.eye(8, dtype=torch.float64, device="cuda"),
                                   torch.eye(8, dtype=torch.float64, device="cuda"), upper=False)
 
-    def run(mode, reps=10):
-        eng = KernelEngine(KernelType.GAUSSIAN, w.x, Hyperparams(w.l, w.f, w.s), mode=mode, precision="fp64")
+    def run(mode, reps=10, precision="fp64"):
+        eng = KernelEngine(KernelType.GAUSSIAN, w.x, Hyperparams(w.l, w.f, w.s), mode=mode, precision=precision)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         pre = precond.build(eng, w.rank)
@@ -295,6 +295,7 @@ def nlml_metric(cpu: bool):
 
     t_eval, t_build, t_first, lg = run(EngineMode.ON_THE_FLY)
     t_dense, _, _, lg_dense = run(EngineMode.DENSE)
+    t_fast, _, _, lg_fast = run(EngineMode.ON_THE_FLY, precision="fast")
     n, d = w.n, w.d
     passes = [(50, 1, 1), (20, 16, 1), (1, 17, 2)]  # (iterations, columns, outputs)
     flops = sum(it * n * n * ((3 * d + 53) + 2 * k * nout) for it, k, nout in passes)
@@ -312,7 +313,12 @@ def nlml_metric(cpu: bool):
                                        "flops + 2k per output; PCG vector work and SLQ not counted"},
            "dense": {"workload": "same recipe, DENSE mode (the reference's default at n <= 20000): Khat "
                                  "materialised by the repo's panel kernel, 17-column products by cuBLAS DGEMM",
-                     "evals_per_s": 1.0 / t_dense, "ms_per_eval": t_dense * 1e3, "loss": lg_dense.loss}}
+                     "evals_per_s": 1.0 / t_dense, "ms_per_eval": t_dense * 1e3, "loss": lg_dense.loss},
+           "fast_mode": {"workload": "same recipe, ON_THE_FLY with the 3xTF32 fused tcgen05 operator (the north "
+                                     "star's tensor-core NLML mode, <= 1e-3: tests/test_gpu_parity.py "
+                                     "test_cfg1_fast_mode_within_tf32_bar)",
+                         "evals_per_s": 1.0 / t_fast, "ms_per_eval": t_fast * 1e3, "loss": lg_fast.loss,
+                         "loss_rel_diff_vs_fp64": abs(lg_fast.loss - lg.loss) / abs(lg.loss)}}
     if cpu:
         from oracle import kgp_oracle as orc
         from oracle import kgp_oracle_c as oc

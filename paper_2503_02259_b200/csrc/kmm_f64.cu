@@ -369,7 +369,12 @@ int launch_kmm_f64(int kt, const F64Params& p_in, DevBuf& ws, cudaStream_t st) {
   const int ks = slice_for(p.k, nout);
   const int64_t rblk = (p.nrows + NT - 1) / NT, kslc = (p.k + ks - 1) / ks;
   // split the columns until ~8 CTAs per SM are in flight (148 SMs), at >= 128 columns per split
-  int64_t nsplit = (8 * 148 + rblk * kslc - 1) / (rblk * kslc);
+  static const int ctas_per_sm = [] {
+    const char* e = getenv("KGP_F64_CTAS");
+    const int v = e ? atoi(e) : 8;
+    return v > 0 ? v : 8;
+  }();
+  int64_t nsplit = (ctas_per_sm * 148 + rblk * kslc - 1) / (rblk * kslc);
   const int64_t maxsplit = p.ncols / 128 > 0 ? p.ncols / 128 : 1;
   if (nsplit > maxsplit) nsplit = maxsplit;
   if (nsplit > 65535) nsplit = 65535;
