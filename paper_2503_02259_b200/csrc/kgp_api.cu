@@ -157,8 +157,8 @@ static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t 
     const int kc = (int)((k - c0) < kmax ? (k - c0) : kmax);
     const int kp = (kc + 15) / 16 * 16;
     const int lbm = peer_epoch ? 0 : tc_lb_mode(e->dpad, nout, split, kp);  // published tiles: classic layout
-    const bool lb = lbm != 0;
-    const int nab = lb ? tc_lb_nab(lbm, kp) : (kp <= kmax2 ? 2 : 1);
+    const bool lb = lbm == 1 || lbm == 2;  // lbm 3 (W2) keeps the all-tf32 RHS tiles
+    const int nab = lbm ? tc_lb_nab(lbm, kp) : (kp <= kmax2 ? 2 : 1);
     int rc = KGP_OK;
     if (!peer_epoch && !(skip_prep && kc == k)) {
       rc = e->bsplit.ensure((size_t)nblk * tc_rhs_block_bytes(split, lb, kp));
@@ -185,7 +185,7 @@ static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t 
       if (rc) return rc;
       p.part = e->tcpart.as<float>();
     }
-    p.flush = tc_flush_blocks(nab);
+    p.flush = lbm == 3 ? tc_env_int("KGP_TC_W2FLUSH", 8) : tc_flush_blocks(nab);  // W2: one buffer, flush 8 (error)
     p.debug = tc_env_int("KGP_TC_DEBUG", 0);
     p.f2 = e->f * e->f;
     p.s = e->s;

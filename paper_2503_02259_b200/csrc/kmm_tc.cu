@@ -100,6 +100,37 @@ KGP_DEV float2 lo2(float2 v) { return fsub2(v, hi2(v)); }
 #define KGP_TC_XP 0  // measured: the FP32 expansion is slower than the tensor-core distance at d = 8 (FP32-pipe bound)
 #endif
 
+// 2^x (x <= 0) on the FMA pipe instead of MUFU: x = n + f (n = rint(x) by the 1.5 * 2^23 shift,
+// |f| <= 1/2), degree-5 minimax p(f) (relative error 2.3e-7 with fp32 Horner, the same class as
+// ex2.approx's), exponent field += n by one LEA. x is clamped at -125 (2^-125 is zero next to
+// the tile's 1e-7 relative error; ex2.approx.ftz flushes there). MUFU ops go through the SM's
+// MIO queue, which the tcgen05.mma issue shares: moving some of the
+// exponentials onto the FMA pipe shortens that queue.
+#ifndef KGP_TC_LEAN
+#define KGP_TC_LEAN 1  // MMA warp skips the full[s] wait, distance warp skips its empty[s] commit
+#endif
+#ifndef KGP_TC_PRE
+#define KGP_TC_PRE 0  // 16-column halves transformed before the A-stage wait (fused 32x32b path)
+#endif
+#ifndef KGP_TC_EXPPOLY
+#define KGP_TC_EXPPOLY 0  // column pairs (of 8 per 16-column half) whose exp2 runs on the FMA pipe
+#endif
+KGP_DEV float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -125.0f);
+  x.y = fmaxf(x.y, -125.0f);
+  const float2 y = __fadd2_rn(x, make_float2(12582912.0f, 12582912.0f));
+  const float2 n = __fadd2_rn(y, make_float2(-12582912.0f, -12582912.0f));
+  const float2 f = fsub2(x, n);
+  float2 p = __ffma2_rn(f, make_float2(0.0013276470126584172f, 0.0013276470126584172f),
+                        make_float2(0.009675540961325169f, 0.009675540961325169f));
+  p = __ffma2_rn(f, p, make_float2(0.05550713464617729f, 0.05550713464617729f));
+  p = __ffma2_rn(f, p, make_float2(0.24022120237350464f, 0.24022120237350464f));
+  p = __ffma2_rn(f, p, make_float2(0.6931469440460205f, 0.6931469440460205f));
+  p = __ffma2_rn(f, p, make_float2(1.0000001192092896f, 1.0000001192092896f));
+  return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(y.x) << 23)),
+                     __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(y.y) << 23)));
+}
+
 // Kernel transform of the scaled squared distance t2 = gamma r^2 (see prep.cu):
 //   Gaussian  t2 = r^2 log2(e) / (2 l^2)   kappa = 2^-t2              g = t2 kappa
 //   Matern32  t2 = 3 r^2 / l^2             kappa = (1+t) e^-t         g = t2 e^-t
@@ -112,14 +143,14 @@ KGP_DEV float2 lo2(float2 v) { return fsub2(v, hi2(v)); }
 // g = -eps, both within the fp32 tile's own error of the clamped values), and the Matern
 // square root reads |t2| (a free source modifier); only the XP (FP32-expansion) path, which
 // can cancel further, keeps FMNMX.
-template <int KT, bool NEED_G, bool CLAMP = true>
+template <int KT, bool NEED_G, bool CLAMP = true, bool POLY = false>
 KGP_DEV void transform2(float2 t2, float2& kv, float2& gv) {
   if (CLAMP && KGP_TC_XP) {
     t2.x = fmaxf(t2.x, 0.0f);
     t2.y = fmaxf(t2.y, 0.0f);
   }
   if (KT == GAUSS) {
-    kv = make_float2(ex2f(-t2.x), ex2f(-t2.y));
+    kv = POLY ? ex2_poly2(make_float2(-t2.x, -t2.y)) : make_float2(ex2f(-t2.x), ex2f(-t2.y));
     if (NEED_G) gv = __fmul2_rn(t2, kv);
   } else {
 #if KGP_TC_SQRT_FMA
@@ -299,7 +330,14 @@ struct Geo {
 
 template <int KT, int D, int NOUT, int SPLIT, int LBM>
 __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_tc_kernel(const TcParams p) {
-  constexpr bool LB = LBM > 0;
+  constexpr bool LB = (LBM == 1 || LBM == 2);
+  // W2 (LBM 3, fused two-output 3xTF32, kp <= 32): hi*[B_hi | B_lo] as ONE N = 2kp MMA and lo*B_hi
+  // as an N = kp MMA into the first half of the same accumulator: 16 contraction MMAs per block
+  // instead of 24, the same tensor-pipe time (N = 64 runs at ~2x the N = 32 cycles), fewer issue
+  // slots for the MMA warp (the kernel's bottleneck). Accumulator per output:
+  // [hi B_hi + lo B_hi | hi B_lo] (2kp columns, one buffer), summed pairwise by the drain.
+  constexpr bool W2 = LBM == 3;
+  static_assert(!W2 || (NOUT == 2 && SPLIT == 3), "W2 layout: fused two-output 3xTF32");
   constexpr int NS = ns_of(NOUT, SPLIT, LBM);
   // sets, distance buffers, A stages. LBM 1: a third A stage written alternately by the two
   // sets (a stage is rewritten only after the MMAs of the block three back have read it, so
@@ -323,19 +361,25 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
   static_assert(!LB || (NOUT == 2 && SPLIT == 3), "LB layout: fused two-output 3xTF32");
   constexpr uint32_t VBYTES = G::VBYTES;
   constexpr bool NEED_G = (NOUT == 2);
+  // Runtime diagnostic switches (KGP_TC_DEBUG) in the MMA loop and the 16x256b transform: the
+  // tensor-core-distance kernels compile them out (cfg2 3.33 -> 3.15 ms: the dead branches cost
+  // the compute and MMA warps issue slots and predicated copies); the direct-difference kernels
+  // keep them, whose scheduling measured 6-8 % faster with them (Matern-3/2 d=4 k=33: 2.83 vs
+  // 3.05 ms; tools/gpu_ab.sh)
+  constexpr bool RTD = !Geo<D>::DMMA || KGP_TC_INSTR;
   if (p.gate != nullptr && *p.gate == 0) return;  // PCG iteration past convergence: nothing to do
 
   extern __shared__ __align__(1024) uint8_t smem[];
   const int KP = p.kp;
   const int NSB = p.nsb;                           // 4 or 8
   const int nsb_log = (NSB == 8) ? 3 : 2;
-  const int NACC = NOUT * KP;                      // accumulator columns per buffer
+  const int NACC = (W2 ? 2 : 1) * NOUT * KP;       // accumulator columns per buffer (TMEM)
   const uint32_t BBYTES = (uint32_t)((TPO * 128 + (LB ? 64 : 0)) * KP);  // tf32 hi | lo (| bf16)
   uint8_t* sB = smem;                              // NSB x BBYTES, 1024-aligned
   uint8_t* sV = smem + NSB * BBYTES;               // NSB x VBYTES (column data / V' tiles)
   uint8_t* sU = sV + NSB * VBYTES;                 // U' hi/lo (DMMA)
-  float* sAcc = reinterpret_cast<float*>(sU + G::UBYTES);  // NACC x 128 fp32, column-major
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sAcc + NACC * 128);
+  float* sAcc = reinterpret_cast<float*>(sU + G::UBYTES);  // NOUT * KP x 128 fp32, column-major
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sAcc + NOUT * KP * 128);
   uint64_t* full = bars;
   uint64_t* empty = bars + MAXNSB;
   uint64_t* afull = bars + 2 * MAXNSB;
@@ -361,7 +405,9 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSB; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], DMMA ? 2 : 1 + WPS);  // DMMA: released by both MMA warps' commits
+      // DMMA: released by the contraction warp's commit alone when KGP_TC_LEAN (the distance MMAs
+      // that read the stage's V' completed before dfull, hence before the tile they feed exists)
+      mbar_init(&empty[s], DMMA ? (KGP_TC_LEAN ? 1 : 2) : 1 + WPS);
     }
     for (int a = 0; a < NSA; ++a) {
       mbar_init(&afull[a], WPS);
@@ -443,7 +489,14 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
     uint32_t ph_s = 0, ph_a = 0, ph_acc = 0;
     for (int t = 0; t < nblk; ++t) {
       if (pos == 0) mbar_wait(&accempty[ab], ph_acc ^ 1);  // buffer drained (segment start)
-      mbar_wait(&full[s], ph_s);
+      // KGP_TC_LEAN: no wait on full[s]. The A tile of block t exists only after its compute set
+      // saw the block's distances (DMMA: issued after the distance warp saw full[s]) or its
+      // column data (direct path: the set itself waits on full[s]), so afull[a] completing
+      // already orders this warp after the stage's bulk copies (acquire chains through the
+      // barriers); every mbarrier probe is an MIO round trip on the issuer's critical path.
+      // (Measured: cfg2 3.13 -> 3.02 ms; on the direct-difference path, whose sets wait on
+      // full[s] themselves, dropping it made Matern-3/2 d=4 slower, so it stays there)
+      if (!(KGP_TC_LEAN && DMMA)) mbar_wait(&full[s], ph_s);
       mbar_wait(&afull[a], ph_a);
       tc_fence_after();
       KGP_TR(7, t);
@@ -455,7 +508,7 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
         const uint32_t idesc_b = idesc_bf16_m128(KP);
         const uint32_t bbf = bhi + 2 * KP * 128;  // bf16(B), interleaved K-major
 #pragma unroll
-        for (int o = 0; o < ((p.debug & 1) ? 0 : NOUT); ++o) {
+        for (int o = 0; o < ((RTD && (p.debug & 1)) ? 0 : NOUT); ++o) {
           const uint32_t dt = tbase + ab * NACC + o * KP;
           const uint32_t ahi = tbase + abase + a * ASTAGE + o * OCOLS;
 #pragma unroll
@@ -464,7 +517,7 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
             mma_tf32_ts(dt, ahi + 8 * kk, dlo + 2 * kk, idesc, 1u);
           }
 #pragma unroll
-          for (int k2 = 0; k2 < ((p.debug & 8) ? 0 : BJ / 16); ++k2)
+          for (int k2 = 0; k2 < ((KGP_TC_INSTR && (p.debug & 8)) ? 0 : BJ / 16); ++k2)
             mma_f16_ts(dt, ahi + 32 + 8 * k2, interleave_kmajor_desc(bbf + k2 * 2 * KP * 16, KP * 16, 128), idesc_b, 1u);
         }
         tc_commit(&empty[s]);
@@ -474,7 +527,7 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
         // bf16x3: A0 B0 + A0 B1 + A1 B0 per output and K=16 step (kind::f16)
         const uint32_t idesc_b = idesc_bf16_m128(KP);
 #pragma unroll
-        for (int o = 0; o < ((p.debug & 1) ? 0 : NOUT); ++o) {
+        for (int o = 0; o < ((RTD && (p.debug & 1)) ? 0 : NOUT); ++o) {
           const uint32_t dt = tbase + ab * NACC + o * KP;
           const uint32_t a0 = tbase + abase + a * ASTAGE + o * OCOLS;
 #pragma unroll
@@ -489,9 +542,24 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
         tc_commit(&empty[s]);
         tc_commit(&aempty[a]);
         if (last) tc_commit(&accfull[ab]);
-      } else if (!LB && SPLIT != 2 && elect_one()) {
+      } else if (W2 && elect_one()) {
+        const uint32_t idesc_w = idesc_tf32_m128(2 * KP);
 #pragma unroll
-        for (int o = 0; o < ((p.debug & 1) ? 0 : NOUT); ++o) {
+        for (int o = 0; o < NOUT; ++o) {
+          const uint32_t dt = tbase + ab * NACC + o * 2 * KP;
+          const uint32_t ahi = tbase + abase + (a * ATILES + o * TPO) * 32;
+#pragma unroll
+          for (int kk = 0; kk < BJ / 8; ++kk) {
+            mma_tf32_ts(dt, ahi + 8 * kk, dhi + 2 * kk, idesc_w, (pos > 0 || kk > 0) ? 1u : 0u);  // hi [B_hi | B_lo]
+            mma_tf32_ts(dt, ahi + 32 + 8 * kk, dhi + 2 * kk, idesc, 1u);                           // lo B_hi
+          }
+        }
+        tc_commit(&empty[s]);
+        tc_commit(&aempty[a]);
+        if (last) tc_commit(&accfull[ab]);
+      } else if (!LB && !W2 && SPLIT != 2 && elect_one()) {
+#pragma unroll
+        for (int o = 0; o < ((RTD && (p.debug & 1)) ? 0 : NOUT); ++o) {
           const uint32_t dt = tbase + ab * NACC + o * KP;
           const uint32_t ahi = tbase + abase + (a * ATILES + o * TPO) * 32;
 #pragma unroll
@@ -535,7 +603,7 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
           const uint32_t va = smem_u32(sV + s * VBYTES);
           const uint32_t dd = tbase + dbase + db * BJ;
 #pragma unroll
-          for (int kk = 0; kk < ((p.debug & 2) ? 0 : KD / 8); ++kk) {
+          for (int kk = 0; kk < ((KGP_TC_INSTR && (p.debug & 2)) ? 0 : KD / 8); ++kk) {
             // one K=8 step = two 16-byte chunks; chunk stride (LBO) = rows * 16 B
             const uint32_t uh = tbase + ucol + 8 * kk, ul = uh + KDS;  // U' hi / lo in TMEM
             const uint64_t vh = interleave_kmajor_desc(va + kk * 2 * BJ * 16, BJ * 16, 128);
@@ -545,7 +613,7 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
             mma_tf32_ts(dd, ul, vh, idesc_d, 1u);
           }
           tc_commit(&dfull[t % NSET]);  // to the set that owns block t (its own phase sequence)
-          tc_commit(&empty[s]);         // this stage's V' has been read
+          if (!KGP_TC_LEAN) tc_commit(&empty[s]);  // this stage's V' has been read
         }
         __syncwarp();
         KGP_TR(2, t);
@@ -598,34 +666,49 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
         __syncwarp();
         if (lane == 0) mbar_arrive(&dempty[db]);
         if (qd == 0) KGP_TR(4, t);
+        // the first KGP_TC_PRE 16-column halves are transformed before the A-stage wait (off the
+        // chain MMA(t - NS) -> stage free -> tile stored -> MMA(t))
+        float2 kv[2][8], gv[2][8];
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          if (half >= KGP_TC_PRE) continue;
+#pragma unroll
+          for (int m = 0; m < 8; ++m) {
+            const uint32_t* vv = half ? v1 : v0;
+            const float2 t2 = make_float2(__uint_as_float(vv[2 * m]), __uint_as_float(vv[2 * m + 1]));
+            transform2<KT, NEED_G>(t2, kv[half][m], gv[half][m]);
+          }
+        }
         mbar_wait_backoff(&aempty[a], ph_a ^ 1, KGP_TC_SLEEP_COMP);
         tc_fence_after();
         if (qd == 0) KGP_TR(5, t);
         const uint32_t tcol = lane_base + abase + a * ASTAGE;
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
-          float2 kv[8], gv[8];
 #pragma unroll
           for (int m = 0; m < 8; ++m) {
+            if (half < KGP_TC_PRE) break;
             const uint32_t* vv = half ? v1 : v0;
             const float2 t2 = make_float2(__uint_as_float(vv[2 * m]), __uint_as_float(vv[2 * m + 1]));
-            if (p.debug & 4) {
-              kv[m] = gv[m] = t2;
+            if (KGP_TC_INSTR && (p.debug & 4)) {
+              kv[half][m] = gv[half][m] = t2;
+            } else if (m < KGP_TC_EXPPOLY) {
+              transform2<KT, NEED_G, true, true>(t2, kv[half][m], gv[half][m]);
             } else {
-              transform2<KT, NEED_G>(t2, kv[m], gv[m]);
+              transform2<KT, NEED_G>(t2, kv[half][m], gv[half][m]);
             }
           }
           if (KGP_TC_INSTR && (p.debug & 16)) {  // diagnostic: no A-tile stores (keep the values live)
-            if (__float_as_uint(kv[0].x) == 0x7fc00001u && __float_as_uint(gv[0].y) == 0x7fc00001u) p.part[0] = 0.f;
+            if (__float_as_uint(kv[half][0].x) == 0x7fc00001u && __float_as_uint(gv[half][0].y) == 0x7fc00001u) p.part[0] = 0.f;
           } else if (SPLIT == 2) {
-            store_row16_bf(tcol + 8 * half, tcol + 16 + 8 * half, kv);
-            if (NEED_G) store_row16_bf(tcol + OCOLS + 8 * half, tcol + OCOLS + 16 + 8 * half, gv);
+            store_row16_bf(tcol + 8 * half, tcol + 16 + 8 * half, kv[half]);
+            if (NEED_G) store_row16_bf(tcol + OCOLS + 8 * half, tcol + OCOLS + 16 + 8 * half, gv[half]);
           } else if (LB) {
-            store_row16_lb(tcol + 16 * half, tcol + 32 + 8 * half, kv);
-            store_row16_lb(tcol + OCOLS + 16 * half, tcol + OCOLS + 32 + 8 * half, gv);
+            store_row16_lb(tcol + 16 * half, tcol + 32 + 8 * half, kv[half]);
+            store_row16_lb(tcol + OCOLS + 16 * half, tcol + OCOLS + 32 + 8 * half, gv[half]);
           } else {
-            store_row16<SPLIT>(tcol + 16 * half, kv);
-            if (NEED_G) store_row16<SPLIT>(tcol + TPO * 32 + 16 * half, gv);
+            store_row16<SPLIT>(tcol + 16 * half, kv[half]);
+            if (NEED_G) store_row16<SPLIT>(tcol + TPO * 32 + 16 * half, gv[half]);
           }
         }
         tc_wait_st();
@@ -707,7 +790,7 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
         for (int q = 0; q < 2; ++q)
 #pragma unroll
           for (int m = 0; m < 4; ++m) {
-            if (p.debug & 4) {
+            if (RTD && (p.debug & 4)) {
               kv[q][m] = gv[q][m] = acc[2 * half + q][m];
             } else {
               transform2<KT, NEED_G, DMMA || XP>(acc[2 * half + q][m], kv[q][m], gv[q][m]);
@@ -731,6 +814,45 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
     int ab = 0;
     uint32_t ph = 0;
 #if KGP_TC_RACC
+    if (W2) {
+      // W2: per output [hi B_hi + lo B_hi | hi B_lo]; the two halves are summed here (fp32,
+      // round-to-nearest) into the packed promotion sums racc[o kp + c]
+      float racc[64];
+      for (int seg = 0; seg < nseg; ++seg) {
+        mbar_wait_backoff(&accfull[ab], ph, KGP_TC_SLEEP_DRAIN);
+        tc_fence_after();
+#pragma unroll
+        for (int o = 0; o < NOUT; ++o) {
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            if (16 * q >= KP) continue;
+            uint32_t v0[16], v1[16];
+            tmem_ld16(lane_base + ab * NACC + o * 2 * KP + 16 * q, v0);
+            tmem_ld16(lane_base + ab * NACC + o * 2 * KP + KP + 16 * q, v1);
+            tc_wait_ld();
+            tc_wait_ld_tied(v0);
+            tc_wait_ld_tied(v1);
+            if (o == NOUT - 1 && 16 * (q + 1) >= KP) {  // the single buffer is free once every column is in registers
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&accempty[ab]);
+            }
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) {
+              const float x = __uint_as_float(v0[jj]) + __uint_as_float(v1[jj]);
+              float& a = racc[o * 32 + 16 * q + jj];
+              a = (seg == 0) ? x : a + x;
+            }
+          }
+        }
+        if (++ab == NAB) { ab = 0; ph ^= 1; }
+      }
+#pragma unroll
+      for (int o = 0; o < NOUT; ++o)
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+          if (c < KP) sAcc[(o * KP + c) * 128 + row] = racc[o * 32 + c];
+    } else
     // (two compute sets only: the three-set kernels' 608 threads leave no room for 64 more
     // registers per thread)
     if (NS <= 2 && NACC <= 64) {
@@ -813,8 +935,8 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
     const int64_t r = (int64_t)blockIdx.x * 128 + row;
     if (p.part != nullptr) {
       if (r < p.nrows) {
-        float* dst = p.part + ((int64_t)blockIdx.y * p.nrows + r) * NACC;
-        for (int c = 0; c < NACC; ++c) dst[c] = sAcc[c * 128 + row];
+        float* dst = p.part + ((int64_t)blockIdx.y * p.nrows + r) * (NOUT * KP);
+        for (int c = 0; c < NOUT * KP; ++c) dst[c] = sAcc[c * 128 + row];
       }
     } else if (r < p.nrows) {
       for (int c = 0; c < p.k; ++c) {
@@ -863,7 +985,7 @@ __global__ void tc_reduce_kernel(const TcParams p, int nsplit, int nacc) {
 
 template <int KT, int D, int NOUT, int SPLIT, int LBM>
 int launch_one(const TcParams& p_in, cudaStream_t st) {
-  constexpr bool LB = LBM > 0;
+  constexpr bool LB = (LBM == 1 || LBM == 2);
   auto kern = kmm_tc_kernel<KT, D, NOUT, SPLIT, LBM>;
   TcParams p = p_in;
   const size_t stage = (size_t)tc_rhs_block_bytes(SPLIT, LB, p.kp) + Geo<D>::VBYTES;
@@ -899,6 +1021,7 @@ int launch_kt_d(const TcParams& p, int nout, int split, cudaStream_t st) {
   }
   if (nout == 1) return split == 3 ? launch_one<KT, D, 1, 3, 0>(p, st) : launch_one<KT, D, 1, 1, 0>(p, st);
   if (split != 3) return launch_one<KT, D, 2, 1, 0>(p, st);
+  if (p.lb == 3) return launch_one<KT, D, 2, 3, 3>(p, st);
   if constexpr (Geo<D>::DMMA && D == 8) {
     if (p.lb == 1) return launch_one<KT, D, 2, 3, 1>(p, st);
     if (p.lb == 2) return launch_one<KT, D, 2, 3, 2>(p, st);
@@ -975,6 +1098,15 @@ int tc_lb_mode(int dpad, int nout, int split, int kp) {
     const char* s = getenv("KGP_TC_LB3");
     return s ? atoi(s) : 0;
   }();
+  static const int envw = [] {
+    const char* s = getenv("KGP_TC_W2");
+    return s ? atoi(s) : 0;
+  }();
+  // W2 measured (n = 65536, two outputs): Gaussian d=8 k=32 3.02 -> 3.15 ms (the single accumulator
+  // buffer's drain stalls; with flush 16 3.06), k=16 2.54 -> 2.38; Matern-3/2 d=4 k=16 4.21 ->
+  // 5.06. Operator error 3.05e-6 -> 2.52e-6 (the hi B_lo column sums promoted separately). Off by
+  // default (env KGP_TC_W2=1): the MMA issue count is not what bounds the kernel at k = 32.
+  if (envw && nout == 2 && split == 3 && kp <= 32 && !env3) return 3;
   if (env == 0 || tc_dist_mode(dpad) != 1 || dpad != 8 || nout != 2 || split != 3 || kp > 64) return 0;
   if (kp > 32) return 1;
   if (env3) return 2;
@@ -983,6 +1115,7 @@ int tc_lb_mode(int dpad, int nout, int split, int kp) {
 
 // TMEM accumulator buffers for a LB mode (0: the caller's choice for the classic layout)
 int tc_lb_nab(int mode, int kp) {
+  if (mode == 3) return 1;  // W2: 2 x 2kp accumulator columns, one buffer
   if (mode == 2) return kp <= 32 ? 2 : 1;
   if (mode == 1) return kp <= 32 ? 2 : 1;
   return 0;
