@@ -102,12 +102,38 @@ KGP_DEV double exp_neg64(double x) {
 
 // (the Gaussian keeps the library exp: measured faster there -- cfg2-shape fp64 step 52 vs
 // 63 ms -- while the Matern kernels gain 25 %: 2.75 -> 2.05 ms at n = 16384, k = 33)
-template <int KT>
+// FG: the Gaussian's exponential by the branch-free exp_neg64 as well (the library exp's
+// slow-path branch splits every entry's evaluation into its own basic block): measured at the
+// cfg2 shape (d = 8, k = 32, two outputs) 94.8 -> 55.9 ms; at d = 3 (configs[0]) the library exp
+// is 3 % faster, so the operators select it by dimension
+template <int KT, bool FG = false>
 KGP_DEV double kappa64f(double r2, double l) {
-  if (KT == GAUSS) return exp(-r2 * (1.0 / (2.0 * l * l)));
+  if (KT == GAUSS) return FG ? exp_neg64(-r2 * (1.0 / (2.0 * l * l))) : exp(-r2 * (1.0 / (2.0 * l * l)));
   double t = (KT == MAT32 ? SQRT3 : SQRT5) / l * sqrt(r2);
   if (KT == MAT32) return (1.0 + t) * exp_neg64(-t);
   return (1.0 + t + (5.0 / (3.0 * l * l)) * r2) * exp_neg64(-t);
+}
+
+// kappa and dkappa/dl of one entry from ONE exponential: the same values, bit for bit, as
+// kappa64f / dkappa64f (the same expressions, the exponential's argument rounded the same way)
+template <int KT, bool FG = false>
+KGP_DEV void kd64f(double r2, double l, double& kv, double& gv) {
+  if (KT == GAUSS) {
+    const double x = -r2 * (1.0 / (2.0 * l * l));
+    const double e = FG ? exp_neg64(x) : exp(x);
+    kv = e;
+    gv = r2 * (1.0 / (l * l * l)) * e;
+    return;
+  }
+  const double t = (KT == MAT32 ? SQRT3 : SQRT5) / l * sqrt(r2);
+  const double e = exp_neg64(-t);
+  if (KT == MAT32) {
+    kv = (1.0 + t) * e;
+    gv = (3.0 / (l * l * l)) * r2 * e;
+  } else {
+    kv = (1.0 + t + (5.0 / (3.0 * l * l)) * r2) * e;
+    gv = (5.0 / (3.0 * l * l * l)) * r2 * (1.0 + t) * e;
+  }
 }
 
 template <int KT>

@@ -79,8 +79,17 @@ __global__ void __launch_bounds__(NT) kmm_f64_kernel(const F64Params p) {
           r2 = __dadd_rn(r2, __dmul_rn(df, df));  // numba's rounding (no FMA contraction)
         }
       }
-      const double kv = KGP_KAPPA<KT>(r2, p.l);
-      const double gv = NOUT == 2 ? KGP_DKAPPA<KT>(r2, p.l) : 0.0;
+      double kv, gv = 0.0;
+#if KGP_F64_FASTEXP
+      if (NOUT == 2) {
+        kd64f<KT, (DB >= 8)>(r2, p.l, kv, gv);  // one exponential for both outputs
+      } else {
+        kv = kappa64f<KT, (DB >= 8)>(r2, p.l);
+      }
+#else
+      kv = KGP_KAPPA<KT>(r2, p.l);
+      if (NOUT == 2) gv = KGP_DKAPPA<KT>(r2, p.l);
+#endif
 #pragma unroll
       for (int c = 0; c < KS; c += 2) {
         const double2 bv = *reinterpret_cast<const double2*>(&sB[jj][c]);

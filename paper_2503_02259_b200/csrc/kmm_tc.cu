@@ -557,7 +557,7 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
         tc_commit(&empty[s]);
         tc_commit(&aempty[a]);
         if (last) tc_commit(&accfull[ab]);
-      } else if (!LB && !W2 && SPLIT != 2 && elect_one()) {
+      } else if (!LB && !W2 && SPLIT != 2 && elect_one()) {  // (exactly one elect_one() per branch chain)
 #pragma unroll
         for (int o = 0; o < ((RTD && (p.debug & 1)) ? 0 : NOUT); ++o) {
           const uint32_t dt = tbase + ab * NACC + o * KP;
