@@ -452,6 +452,16 @@ KGP_DEV uint64_t interleave_kmajor_desc(uint32_t smem_addr, uint32_t lbo, uint32
 }
 
 // Byte offset of element (row r, k) in a K-major no-swizzle tf32 tile with `rows` rows.
+// Tensor-core distance operands (d > 4): U'_i = [-2 gamma c_i (dpad) | q_i hi, q_i lo, 1, 1 | 0..]
+// and V'_j = [c_j (dpad) | 1, 1, q_j hi, q_j lo | 0..], q = gamma |c|^2 split into an exact tf32
+// head and its remainder. t2 = U'.V' then needs the tf32 lo parts of the coordinates only, so
+// the 3xTF32 product is hi.hi over all K plus hi.lo and lo.hi over the first dpad columns: 4
+// MMAs per block at dpad = 8 instead of 6 with [u, q, 1] . [c, 1, q] (KGP_TC_DIST4 0)
+#ifndef KGP_TC_DIST4
+#define KGP_TC_DIST4 1
+#endif
+__host__ __device__ constexpr int tc_dist_kd(int dpad) { return ((dpad + (KGP_TC_DIST4 ? 4 : 2)) + 7) / 8 * 8; }
+
 __host__ __device__ inline uint32_t interleave_offset(uint32_t r, uint32_t k, uint32_t rows) {
   return (k >> 2) * (rows * 16u) + (r >> 3) * 128u + (r & 7u) * 16u + (k & 3u) * 4u;
 }

@@ -109,6 +109,9 @@ KGP_DEV float2 lo2(float2 v) { return fsub2(v, hi2(v)); }
 #ifndef KGP_TC_LEAN
 #define KGP_TC_LEAN 1  // MMA warp skips the full[s] wait, distance warp skips its empty[s] commit
 #endif
+#ifndef KGP_TC_LRX
+#define KGP_TC_LRX 1  // lean form for the direct-difference kernels where it measured faster (LRX)
+#endif
 #ifndef KGP_TC_PRE
 #define KGP_TC_PRE 0  // 16-column halves transformed before the A-stage wait (fused 32x32b path)
 #endif
@@ -305,7 +308,7 @@ struct Geo {
   // MMA into TMEM (DMMA); d <= 4: direct differences on the FP32 pipe
   static constexpr bool XP = (D > 4) && KGP_TC_XP;
   static constexpr bool DMMA = (D > 4) && !KGP_TC_XP;
-  static constexpr int KD = ((D + 2) + 7) / 8 * 8;           // augmented K of the distance MMA
+  static constexpr int KD = tc_dist_kd(D);                   // augmented K of the distance MMA
   static constexpr uint32_t VBYTES = DMMA ? 2u * BJ * KD * 4u : (uint32_t)(D + 1) * BJ * 4u;  // per block
   static constexpr uint32_t UBYTES = 0u;  // U' lives in TMEM
 };
@@ -363,10 +366,16 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
   constexpr bool NEED_G = (NOUT == 2);
   // Runtime diagnostic switches (KGP_TC_DEBUG) in the MMA loop and the 16x256b transform: the
   // tensor-core-distance kernels compile them out (cfg2 3.33 -> 3.15 ms: the dead branches cost
-  // the compute and MMA warps issue slots and predicated copies); the direct-difference kernels
-  // keep them, whose scheduling measured 6-8 % faster with them (Matern-3/2 d=4 k=33: 2.83 vs
-  // 3.05 ms; tools/gpu_ab.sh)
-  constexpr bool RTD = !Geo<D>::DMMA || KGP_TC_INSTR;
+  // the compute and MMA warps issue slots and predicated copies); of the direct-difference
+  // kernels only the LRX ones do (Matern-3/2 d=4 k=33 one output: 2.83 ms with them, 3.05
+  // without; tools/gpu_ab.sh)
+  // LRX: the direct-difference kernels that measured faster with the lean variants too
+  // (compiled-out switches, no full-stage wait in the MMA warp; tools/gpu_direct2.sh, n = 65536):
+  // two outputs (k = 1-33: 10-20 % faster, k = 64: 2-5 % slower), d <= 2 and the Gaussian (k >= 33:
+  // 7-10 % faster, k <= 16: within 3 %). Matern with d = 3..4 and one output (the configs[2]
+  // PCG product) measured up to 20 % slower lean and keeps the original form
+  constexpr bool LRX = KGP_TC_LRX && (NOUT == 2 || D <= 2 || KT == GAUSS);
+  constexpr bool RTD = (!Geo<D>::DMMA && !LRX) || KGP_TC_INSTR;
   if (p.gate != nullptr && *p.gate == 0) return;  // PCG iteration past convergence: nothing to do
 
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -441,10 +450,24 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
       for (int kk = 0; kk < 16; ++kk) {
         const int k = k0 + kk;
         float v = 0.f;
-        if (ok && k < KD) v = (k < D) ? xr[1 + k] : (k == D ? xr[0] : (k == D + 1 ? 1.0f : 0.0f));
-        const float hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+        float hi, lo;
+        if (KGP_TC_DIST4) {
+          // [u (D) | q hi, q lo, 1, 1]: only the coordinates carry a lo part
+          const float q = ok ? xr[0] : 0.0f;
+          const float qh = __uint_as_float(__float_as_uint(q) & 0xFFFFE000u);
+          if (ok && k < D) v = xr[1 + k];
+          else if (ok && k == D) v = qh;
+          else if (ok && k == D + 1) v = q - qh;
+          else if (ok && (k == D + 2 || k == D + 3)) v = 1.0f;
+          hi = (k < D) ? __uint_as_float(__float_as_uint(v) & 0xFFFFE000u) : v;
+          lo = (k < D) ? v - hi : 0.0f;
+        } else {
+          if (ok && k < KD) v = (k < D) ? xr[1 + k] : (k == D ? xr[0] : (k == D + 1 ? 1.0f : 0.0f));
+          hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+          lo = v - hi;
+        }
         hv[kk] = __float_as_uint(hi);
-        lv[kk] = __float_as_uint(v - hi);
+        lv[kk] = __float_as_uint(lo);
       }
       tmem_st16(uaddr + k0, hv);
       tmem_st16(uaddr + KDS + k0, lv);
@@ -496,7 +519,7 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
       // barriers); every mbarrier probe is an MIO round trip on the issuer's critical path.
       // (Measured: cfg2 3.13 -> 3.02 ms; on the direct-difference path, whose sets wait on
       // full[s] themselves, dropping it made Matern-3/2 d=4 slower, so it stays there)
-      if (!(KGP_TC_LEAN && DMMA)) mbar_wait(&full[s], ph_s);
+      if (!(KGP_TC_LEAN && (DMMA || LRX))) mbar_wait(&full[s], ph_s);
       mbar_wait(&afull[a], ph_a);
       tc_fence_after();
       KGP_TR(7, t);
@@ -609,8 +632,10 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
             const uint64_t vh = interleave_kmajor_desc(va + kk * 2 * BJ * 16, BJ * 16, 128);
             const uint64_t vl = interleave_kmajor_desc(va + vlo_off + kk * 2 * BJ * 16, BJ * 16, 128);
             mma_tf32_ts(dd, uh, vh, idesc_d, kk > 0 ? 1u : 0u);
-            mma_tf32_ts(dd, uh, vl, idesc_d, 1u);
-            mma_tf32_ts(dd, ul, vh, idesc_d, 1u);
+            if (!KGP_TC_DIST4 || kk < D / 8) {  // DIST4: lo parts only in the coordinate columns
+              mma_tf32_ts(dd, uh, vl, idesc_d, 1u);
+              mma_tf32_ts(dd, ul, vh, idesc_d, 1u);
+            }
           }
           tc_commit(&dfull[t % NSET]);  // to the set that owns block t (its own phase sequence)
           if (!KGP_TC_LEAN) tc_commit(&empty[s]);  // this stage's V' has been read
@@ -739,6 +764,7 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
         if (lane == 0) mbar_arrive(&dempty[db]);
       } else {
         mbar_wait(&full[s], ph_s);
+        if (qd == 0) KGP_TR(3, t);
         // this thread's 8 columns, permuted by prep_cols into two float4 at 8g
         const float* xs = reinterpret_cast<const float*>(sV + s * VBYTES) + 8 * g;
         if (XP) {  // t2 = q_i + q_j + sum_k u_ik v_jk   (u = -2 gamma c_i, v = c_j, q = gamma |c|^2)
@@ -779,8 +805,10 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
       }
+      if (qd == 0) KGP_TR(4, t);
       mbar_wait(&aempty[a], ph_a ^ 1);
       tc_fence_after();
+      if (qd == 0) KGP_TR(5, t);
       const uint32_t tcol = lane_base + abase + a * ATILES * 32;
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
@@ -804,6 +832,7 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&afull[a]);
+      if (qd == 0) KGP_TR(6, t);
     }
   } else {
     // ------------------------------------------------------------ drain + epilogue warps
@@ -1049,13 +1078,13 @@ int tc_dist_mode(int dpad) { return dpad <= 4 ? 0 : (KGP_TC_XP ? 2 : 1); }
 
 int tc_col_block_bytes(int dpad) {
   if (tc_dist_mode(dpad) != 1) return (dpad + 1) * BJ * 4;
-  const int kd = ((dpad + 2) + 7) / 8 * 8;
+  const int kd = tc_dist_kd(dpad);
   return 2 * BJ * kd * 4;
 }
 
 static int tc_fixed_cols(int dpad, int ns) {
   if (tc_dist_mode(dpad) != 1) return 0;
-  const int kd = ((dpad + 2) + 7) / 8 * 8;
+  const int kd = tc_dist_kd(dpad);
   return ns * BJ + 2 * ((kd + 15) / 16 * 16);  // distance buffers + U' hi/lo
 }
 

@@ -77,17 +77,27 @@ __global__ void prep_cols_kernel(int kt, int d, int dpad, int mode, int64_t n, i
     o[pos] = mode == 0 ? 0.0f : (float)(gamma * nrm);
     return;
   }
-  // tensor-core distance: V'_j = [c_j (dpad), 1, q_j, 0 ...] as tf32 hi / lo tiles
-  // (K-major, no swizzle, 32 rows), block t at byte t * 2 * 32 * kd * 4
-  const int kd = ((dpad + 2) + 7) / 8 * 8;
+  // tensor-core distance (kgp_common.cuh tc_dist_kd): V'_j = [c_j (dpad), 1, 1, q_j hi, q_j lo, 0 ...]
+  // (KGP_TC_DIST4; else [c_j, 1, q_j, 0 ...]) as tf32 hi / lo tiles (K-major, no swizzle, 32 rows),
+  // block t at byte t * 2 * 32 * kd * 4
+  const int kd = tc_dist_kd(dpad);
   uint8_t* base = reinterpret_cast<uint8_t*>(out) + t * (int64_t)(2 * 32 * kd * 4);
+  const double q = gamma * nrm;
+  const float qf = (float)q;
+  const float qh = __uint_as_float(__float_as_uint(qf) & 0xFFFFE000u);
+  const float ql = (float)(q - (double)qh);
   for (int k = 0; k < kd; ++k) {
     float v = 0.0f;
-    if (j < n) v = (k < dpad) ? (float)c[k] : (k == dpad ? 1.0f : (k == dpad + 1 ? (float)(gamma * nrm) : 0.0f));
-    const float hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+    if (KGP_TC_DIST4) {
+      if (j < n) v = (k < dpad) ? (float)c[k] : (k == dpad || k == dpad + 1) ? 1.0f : k == dpad + 2 ? qh : k == dpad + 3 ? ql : 0.0f;
+    } else {
+      if (j < n) v = (k < dpad) ? (float)c[k] : (k == dpad ? 1.0f : (k == dpad + 1 ? qf : 0.0f));
+    }
+    const bool split = !KGP_TC_DIST4 || k < dpad;
+    const float hi = split ? __uint_as_float(__float_as_uint(v) & 0xFFFFE000u) : v;
     const uint32_t off = interleave_offset((uint32_t)jj, (uint32_t)k, 32);
     *reinterpret_cast<float*>(base + off) = hi;
-    *reinterpret_cast<float*>(base + 32 * kd * 4 + off) = v - hi;
+    *reinterpret_cast<float*>(base + 32 * kd * 4 + off) = split ? v - hi : 0.0f;
   }
 }
 

@@ -10,7 +10,8 @@ from paper_2503_02259_b200 import _lib
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
 prec = sys.argv[2] if len(sys.argv) > 2 else "fast"
 rng = np.random.default_rng(0)
-for kt, d in (("gaussian", 8), ("matern32", 4), ("matern52", 2), ("gaussian", 3)):
+KD = [tuple(x.split(":")) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else [("gaussian", "8"), ("matern32", "4"), ("matern52", "2"), ("gaussian", "3")]
+for kt, d in ((a, int(b)) for a, b in KD):
     x = rng.uniform(0, 1, (n, d))
     e = kgp.KernelEngine(kgp.KernelType(kt), x, kgp.Hyperparams(0.2, 1.0, 1e-3), precision=prec)
     for k in (1, 16, 33, 64):
