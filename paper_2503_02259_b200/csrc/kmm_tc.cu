@@ -96,6 +96,9 @@ KGP_DEV float2 hi2(float2 v) {
 KGP_DEV float2 fsub2(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
 KGP_DEV float2 lo2(float2 v) { return fsub2(v, hi2(v)); }
 
+#ifndef KGP_TC_DMIN
+#define KGP_TC_DMIN 4  // padded dimensions <= DMIN use direct differences, larger the tensor-core distance
+#endif
 #ifndef KGP_TC_XP
 #define KGP_TC_XP 0  // measured: the FP32 expansion is slower than the tensor-core distance at d = 8 (FP32-pipe bound)
 #endif
@@ -306,8 +309,8 @@ template <int D>
 struct Geo {
   // d > 4: t2 by the expansion q_i + q_j + u_i.v_j, on the FP32 pipe (XP) or as a tensor-core
   // MMA into TMEM (DMMA); d <= 4: direct differences on the FP32 pipe
-  static constexpr bool XP = (D > 4) && KGP_TC_XP;
-  static constexpr bool DMMA = (D > 4) && !KGP_TC_XP;
+  static constexpr bool XP = (D > KGP_TC_DMIN) && KGP_TC_XP;
+  static constexpr bool DMMA = (D > KGP_TC_DMIN) && !KGP_TC_XP;
   static constexpr int KD = tc_dist_kd(D);                   // augmented K of the distance MMA
   static constexpr uint32_t VBYTES = DMMA ? 2u * BJ * KD * 4u : (uint32_t)(D + 1) * BJ * 4u;  // per block
   static constexpr uint32_t UBYTES = 0u;  // U' lives in TMEM
@@ -632,7 +635,7 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
             const uint64_t vh = interleave_kmajor_desc(va + kk * 2 * BJ * 16, BJ * 16, 128);
             const uint64_t vl = interleave_kmajor_desc(va + vlo_off + kk * 2 * BJ * 16, BJ * 16, 128);
             mma_tf32_ts(dd, uh, vh, idesc_d, kk > 0 ? 1u : 0u);
-            if (!KGP_TC_DIST4 || kk < D / 8) {  // DIST4: lo parts only in the coordinate columns
+            if (!KGP_TC_DIST4 || 8 * kk < D) {  // DIST4: lo parts only in the coordinate columns
               mma_tf32_ts(dd, uh, vl, idesc_d, 1u);
               mma_tf32_ts(dd, ul, vh, idesc_d, 1u);
             }
@@ -1073,8 +1076,8 @@ int launch_kt(const TcParams& p, int dpad, int nout, int split, cudaStream_t st)
 }  // namespace
 
 int tc_pad_dim(int d) { return d <= 2 ? 2 : d <= 4 ? 4 : d <= 8 ? 8 : 16; }
-bool tc_direct(int dpad) { return dpad <= 4; }
-int tc_dist_mode(int dpad) { return dpad <= 4 ? 0 : (KGP_TC_XP ? 2 : 1); }
+bool tc_direct(int dpad) { return dpad <= KGP_TC_DMIN; }
+int tc_dist_mode(int dpad) { return dpad <= KGP_TC_DMIN ? 0 : (KGP_TC_XP ? 2 : 1); }
 
 int tc_col_block_bytes(int dpad) {
   if (tc_dist_mode(dpad) != 1) return (dpad + 1) * BJ * 4;
