@@ -20,6 +20,13 @@
 #ifndef KGP_F64_FASTEXP
 #define KGP_F64_FASTEXP 1  // the operator's entries through exp_neg64 (kgp_common.cuh)
 #endif
+#ifndef KGP_F64_CAP2
+// RHS columns per slice with two outputs (register budget): 28 -> 168 registers, 3 CTAs per SM;
+// measured against 24 (n = 16384): Gaussian d=8 k=51 9.67 -> 5.03 ms (two slices of 28 instead of
+// three of 20: each slice re-evaluates every kernel entry), Matern-5/2 d=2 k=28 3.89 -> 2.53 ms;
+// 32 (211 registers, 2 CTAs per SM) made cfg2's k = 32 55.9 -> 93.6 ms, so 32 runs as 2 x 16
+#define KGP_F64_CAP2 28
+#endif
 #if KGP_F64_FASTEXP
 #define KGP_KAPPA kappa64f
 #define KGP_DKAPPA dkappa64f
@@ -308,11 +315,11 @@ __global__ void f64_reduce_kernel(const F64Params p, int nsplit) {
   if (p.out_dl) p.out_dl[o] = p.f2_dl * g;
 }
 
-// RHS slice width: the fewest slices within the register budget (24 columns with two
-// outputs, 48 with one), each rounded up to a multiple of 4 -- every slice re-evaluates
+// RHS slice width: the fewest slices within the register budget (KGP_F64_CAP2 = 28 columns with
+// two outputs, 48 with one), each rounded up to a multiple of 4 -- every slice re-evaluates
 // the kernel entries, so k = 33 runs as one slice of 36, not 32 + 4
 inline int slice_for(int k, int nout) {
-  const int cap = nout == 2 ? 24 : 48;
+  const int cap = nout == 2 ? KGP_F64_CAP2 : 48;
   const int nsl = (k + cap - 1) / cap;
   return ((k + nsl - 1) / nsl + 3) / 4 * 4;
 }
@@ -322,7 +329,7 @@ int launch_ks(const F64Params& p, int ks, dim3 grid, cudaStream_t st) {
   switch (ks) {
 #define KGP_F64_KS(K)                                                      \
   case K:                                                                  \
-    if constexpr (NOUT == 1 || K <= 24) {                                  \
+    if constexpr (NOUT == 1 || K <= KGP_F64_CAP2) {                        \
       kmm_f64_kernel<KT, NOUT, K, DB><<<grid, NT, 0, st>>>(p);             \
       break;                                                               \
     }                                                                      \
