@@ -318,8 +318,8 @@ __global__ void f64_reduce_kernel(const F64Params p, int nsplit) {
 // RHS slice width: the fewest slices within the register budget (KGP_F64_CAP2 = 28 columns with
 // two outputs, 48 with one), each rounded up to a multiple of 4 -- every slice re-evaluates
 // the kernel entries, so k = 33 runs as one slice of 36, not 32 + 4
-inline int slice_for(int k, int nout) {
-  const int cap = nout == 2 ? KGP_F64_CAP2 : 48;
+inline int slice_for(int k, int nout, int d) {
+  const int cap = nout == 2 ? (d > 8 ? 24 : KGP_F64_CAP2) : 48;  // d > 8: 16 more coordinate registers
   const int nsl = (k + cap - 1) / cap;
   return ((k + nsl - 1) / nsl + 3) / 4 * 4;
 }
@@ -382,7 +382,7 @@ int launch_kmm_f64(int kt, const F64Params& p_in, DevBuf& ws, cudaStream_t st) {
     return KGP_OK;
   }
   const int nout = p.out_dl ? 2 : 1;
-  const int ks = slice_for(p.k, nout);
+  const int ks = slice_for(p.k, nout, p.d);
   const int64_t rblk = (p.nrows + NT - 1) / NT, kslc = (p.k + ks - 1) / ks;
   // split the columns until ~8 CTAs per SM are in flight (148 SMs), at >= 128 columns per split
   static const int ctas_per_sm = [] {
