@@ -1,5 +1,5 @@
 # round 2 (second session): full GPU tests, bench, smoke; then ncu launch list + full capture of the headline kernel
-O=gpurun_out/r02d; mkdir -p $O
+O=gpurun_out/${R02:-r02d}; mkdir -p $O
 timeout 2400 python -m pytest tests -m gpu -q -x -p no:cacheprovider > $O/gpu_tests.log 2>&1; echo tests rc=$?; tail -2 $O/gpu_tests.log
 timeout 900 python bench.py > $O/bench.log 2>&1; echo bench rc=$?
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo smoke rc=$?; tail -1 $O/smoke.log
