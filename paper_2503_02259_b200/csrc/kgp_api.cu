@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <mutex>
 #include <set>
 
@@ -79,6 +80,8 @@ static void engine_free_host_state(kgp_engine_s* e) {
   if (e->cublas) cublasDestroy((cublasHandle_t)e->cublas);
   for (auto ev : e->xev)
     if (ev) cudaEventDestroy(ev);
+  for (auto ev : e->zev)
+    if (ev) cudaEventDestroy(ev);
   for (auto ev : e->tev) cudaEventDestroy(ev);
 }
 
@@ -140,9 +143,22 @@ int tc_split_of(int precision) { return precision == KGP_FAST ? 3 : precision ==
 // Shared by the square operator (xrow = engine rows, shift on) and the cross operator.
 // skip_prep: the RHS split of exactly this B is already in e->bsplit (row-chunked host
 // products prepare it once for all chunks; valid when k fits one launch)
+// Column chunk of a pipelined product (kgp_engine_matmul_host): this launch sweeps column blocks
+// [blk0, blk1) only, writing fp32 partials into slots [slot0, slot0 + used) of a buffer sized for
+// `slots_total`; the last chunk (reduce) sums every slot in order.
+struct ColChunk {
+  int blk0, blk1, slot0, slots_total;
+  bool reduce;
+  int used;  // out: slots this chunk wrote
+};
+static int tc_col_chunk_splits(int64_t nrows, int nblocks) {
+  return tc_col_split(nrows, nblocks, tc_env_int("KGP_TC_MAXSPLIT", 16));
+}
+
 static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t diag_row0, int64_t k, const double* b,
                      int64_t b_rs, int64_t b_cs, double* out_k, double* out_dl, double* out_df, int64_t o_rs,
-                     int64_t o_cs, cudaStream_t st, bool skip_prep = false, uint64_t peer_epoch = 0) {
+                     int64_t o_cs, cudaStream_t st, bool skip_prep = false, uint64_t peer_epoch = 0,
+                     ColChunk* cc = nullptr) {
   // peer_epoch > 0: fused all-gather -- the RHS tiles come from the ranks' published buffers
   // (kgp_engine_peer_publish), b is this rank's own rows (diag_row0 = 0 indexes them)
   const int split = tc_split_of(e->precision);
@@ -163,7 +179,8 @@ static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t 
     if (!peer_epoch && !(skip_prep && kc == k)) {
       rc = e->bsplit.ensure((size_t)nblk * tc_rhs_block_bytes(split, lb, kp));
       if (rc) return rc;
-      rc = prep_rhs(split, lb ? 1 : 0, e->n, k, c0, kp, b, b_rs, b_cs, e->bsplit.as<uint8_t>(), st);
+      rc = prep_rhs(split, lb ? 1 : 0, e->n, k, c0, kp, b, b_rs, b_cs, e->bsplit.as<uint8_t>(), st,
+                    cc ? cc->blk0 : 0, cc ? cc->blk1 : -1);
       if (rc) return rc;
     }
     TcParams p{};
@@ -177,10 +194,24 @@ static int tc_matmul(kgp_engine_s* e, const float* xrow, int64_t nrows, int64_t 
     p.nsa = tc_nsa(e->dpad, nout, split, kp);
     p.nab = nab;
     p.lb = lbm;
-    const int nsplit = tc_col_split(nrows, nblk, tc_env_int("KGP_TC_MAXSPLIT", 16));
+    const int nsplit = tc_col_chunk_splits(nrows, nblk);
     p.nper = (nblk + nsplit - 1) / nsplit;
     p.part = nullptr;
-    if (nsplit > 1) {
+    if (cc) {  // one column chunk: its own split of [blk0, blk1), partials kept for the chunks after it
+      KGP_REQUIRE(kc == k && !peer_epoch, KGP_ERR_STATE, "column-chunked product needs k in one launch");
+      const int nb = cc->blk1 - cc->blk0;
+      const int ns = tc_col_chunk_splits(nrows, nb);
+      p.tbeg = cc->blk0;
+      p.nblk = cc->blk1;
+      p.nper = (nb + ns - 1) / ns;
+      cc->used = (nb + p.nper - 1) / p.nper;
+      KGP_REQUIRE(cc->slot0 + cc->used <= cc->slots_total, KGP_ERR_STATE, "column-chunk slots overrun");
+      rc = e->tcpart.ensure(sizeof(float) * (size_t)cc->slots_total * nrows * nout * kp);
+      if (rc) return rc;
+      p.part = e->tcpart.as<float>();
+      p.slot0 = cc->slot0;
+      p.noreduce = cc->reduce ? 0 : 1;
+    } else if (nsplit > 1) {
       rc = e->tcpart.ensure(sizeof(float) * (size_t)nsplit * nrows * nout * kp);
       if (rc) return rc;
       p.part = e->tcpart.as<float>();
@@ -598,7 +629,6 @@ extern "C" int kgp_engine_matmul_host(kgp_engine* e, int64_t k, const double* b,
   double* dk = out_k ? dout : nullptr;
   double* dl = out_dl ? dout + (out_k ? 1 : 0) * rows * k : nullptr;
   double* df = out_df ? dout + (nout - 1) * rows * k : nullptr;
-  KGP_CUDA(cudaMemcpyAsync(db, b, sizeof(double) * n * k, cudaMemcpyHostToDevice, st));
   // chunk only the tensor-core path without a heteroscedastic diagonal, when k fits one launch
   const int split = tc_split_of(e->precision);
   const bool chunked = e->precision != KGP_FP64 && e->dn_classes == 0 &&
@@ -606,6 +636,37 @@ extern "C" int kgp_engine_matmul_host(kgp_engine* e, int64_t k, const double* b,
   if (!e->xstream) {
     KGP_CUDA(cudaStreamCreateWithFlags(&e->xstream, cudaStreamNonBlocking));
     for (auto& ev : e->xev) KGP_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    for (auto& ev : e->zev) KGP_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  }
+  // input pipelining (chunked path): B's rows are the operator's COLUMNS, so the first row chunk
+  // runs as nz column-chunked launches, launch c needing only B's rows of column chunk c -- the
+  // host->device copy of chunk c + 1 (copy stream) overlaps launch c; every later row chunk
+  // finds all of B resident (KGP_HOST_ZCHUNKS, default 4; 1 = one copy before any compute)
+  const int64_t nblk_all = (n + 31) / 32;
+  // Chunk sizes grow geometrically (ratio KGP_HOST_ZRATIO, default 4; 3 chunks: 1/21, 4/21, 16/21 of B): only the first, small
+  // copy is exposed, and launch c (over chunk c's columns for ~40 % of the rows) outlasts the copy
+  // of chunk c + 1
+  int nz = chunked ? tc_env_int("KGP_HOST_ZCHUNKS", 3) : 1;
+  nz = nz < 1 ? 1 : (nz > 8 ? 8 : nz);
+  if (nz > nblk_all) nz = (int)nblk_all;
+  const double zr = std::max(1.0, tc_env_int("KGP_HOST_ZRATIO", 4) / 1.0);
+  auto zblk = [&](int c) -> int {
+    if (c <= 0) return 0;
+    if (c >= nz) return (int)nblk_all;
+    const double f = zr == 1.0 ? (double)c / nz : (std::pow(zr, c) - 1.0) / (std::pow(zr, nz) - 1.0);
+    return (int)std::max<int64_t>(c, std::min<int64_t>(nblk_all - (nz - c), (int64_t)(f * nblk_all + 0.5)));
+  };
+  if (nz > 1) {
+    KGP_CUDA(cudaEventRecord(e->zev[8], st));  // the copy stream starts after earlier work on st
+    KGP_CUDA(cudaStreamWaitEvent(e->xstream, e->zev[8], 0));
+    for (int c = 0; c < nz; ++c) {
+      const int64_t j0 = (int64_t)zblk(c) * 32, j1 = std::min<int64_t>(n, (int64_t)zblk(c + 1) * 32);
+      KGP_CUDA(cudaMemcpyAsync(db + j0 * k, b + j0 * k, sizeof(double) * (j1 - j0) * k, cudaMemcpyHostToDevice,
+                               e->xstream));
+      KGP_CUDA(cudaEventRecord(e->zev[c], e->xstream));
+    }
+  } else {
+    KGP_CUDA(cudaMemcpyAsync(db, b, sizeof(double) * n * k, cudaMemcpyHostToDevice, st));
   }
   // 3 row chunks, the last one a third of an even share (KGP_HOST_CHUNKS / KGP_HOST_TAIL;
   // tools/e2e_tail.sh): cfg2 e2e 3.97 ms (one chunk 4.39; 2 even 4.13; 4 even 4.17) -- the
@@ -634,7 +695,23 @@ extern "C" int kgp_engine_matmul_host(kgp_engine* e, int64_t k, const double* b,
     };
     const int64_t r0 = edge(c), r1 = edge(c + 1);
     if (r1 <= r0) continue;
-    if (chunked) {
+    if (chunked && c == 0 && nz > 1) {
+      int total = 0;  // partial slots over all column chunks (tc_matmul's split of each chunk)
+      for (int z = 0; z < nz; ++z) {
+        const int nb = zblk(z + 1) - zblk(z);
+        const int ns = tc_col_chunk_splits(r1 - r0, nb), nper = (nb + ns - 1) / ns;
+        total += (nb + nper - 1) / nper;
+      }
+      int slot = 0;
+      for (int z = 0; z < nz && !rc; ++z) {
+        KGP_CUDA(cudaStreamWaitEvent(st, e->zev[z], 0));
+        ColChunk cc{zblk(z), zblk(z + 1), slot, total, z == nz - 1, 0};
+        rc = tc_matmul(e, e->xrow.as<float>() + r0 * (e->dpad + 1), r1 - r0, e->row0 + r0, k, db, k, 1,
+                       dk ? dk + r0 * k : nullptr, dl ? dl + r0 * k : nullptr, df ? df + r0 * k : nullptr, k, 1,
+                       st, false, 0, &cc);
+        slot += cc.used;
+      }
+    } else if (chunked) {
       rc = tc_matmul(e, e->xrow.as<float>() + r0 * (e->dpad + 1), r1 - r0, e->row0 + r0, k, db, k, 1,
                      dk ? dk + r0 * k : nullptr, dl ? dl + r0 * k : nullptr, df ? df + r0 * k : nullptr, k, 1, st,
                      c > 0);

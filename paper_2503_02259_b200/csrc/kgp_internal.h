@@ -20,6 +20,9 @@ struct TcParams {
   int64_t nrows;
   int nblk;
   int nper;               // column blocks per CTA along grid.y (column split)
+  int tbeg;               // first column block of this launch (grid.y sweeps [tbeg, nblk)); 0 normally
+  int slot0;              // partial-sum slot of grid.y = 0 (column-chunked launches share one part buffer)
+  int noreduce;           // 1: leave the partials for a later launch's tc_reduce (more column chunks follow)
   float* part;            // split partial sums (nsplit x nrows x nout*kp); nullptr: no split
   int kp;                 // padded RHS count (multiple of 16, <= 128)
   int k;                  // true RHS count in this launch
@@ -87,7 +90,7 @@ int prep_rows(int kt, int precision_split, int d, int dpad, int64_t nrows, const
 int prep_cols(int kt, int d, int dpad, int64_t n, const double* x, const double* mean, double l, float* out,
               cudaStream_t st);
 int prep_rhs(int split, int lb, int64_t n, int64_t k, int64_t c0, int kp, const double* b, int64_t b_rs, int64_t b_cs,
-             uint8_t* out, cudaStream_t st);
+             uint8_t* out, cudaStream_t st, int blk0 = 0, int blk1 = -1);
 int col_mean(int64_t n, int d, const double* x, double* mean, cudaStream_t st);
 
 // ------------------------------------------------------------------ symmetric DENSE product (symv.cu)
@@ -174,6 +177,7 @@ struct kgp_engine_s {
   kgp::DevBuf hostbuf;
   cudaStream_t xstream = nullptr;
   cudaEvent_t xev[4] = {};
+  cudaEvent_t zev[9] = {};   // host entry: H2D chunks of the RHS (8) + "stream ready" (1)
   // optional heteroscedastic diagonal (kgp_engine_set_diag): Khat column c gets + diag(dn[:, dmap[c]])
   int dn_classes = 0;
   int64_t dn_ncols = 0;

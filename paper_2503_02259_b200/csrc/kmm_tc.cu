@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
   const int ucol = dbase + (DMMA ? ND * BJ : 0);   // then U' hi | lo (KD columns each)
   const int abase = ucol + (DMMA ? 2 * KDS : 0);   // then the A stages
   // column split (grid.y): this CTA sweeps column blocks [t0, t0 + nblk)
-  const int t0 = blockIdx.y * p.nper;
+  const int t0 = p.tbeg + blockIdx.y * p.nper;
   const int nblk = (p.nblk - t0) < p.nper ? (p.nblk - t0) : p.nper;
   const int flush = p.flush;
 
@@ -967,7 +967,7 @@ __global__ void __launch_bounds__(nthreads_for(ns_of(NOUT, SPLIT, LBM)), 1) kmm_
     const int64_t r = (int64_t)blockIdx.x * 128 + row;
     if (p.part != nullptr) {
       if (r < p.nrows) {
-        float* dst = p.part + ((int64_t)blockIdx.y * p.nrows + r) * (NOUT * KP);
+        float* dst = p.part + ((int64_t)(p.slot0 + blockIdx.y) * p.nrows + r) * (NOUT * KP);
         for (int c = 0; c < NOUT * KP; ++c) dst[c] = sAcc[c * 128 + row];
       }
     } else if (r < p.nrows) {
@@ -1027,15 +1027,15 @@ int launch_one(const TcParams& p_in, cudaStream_t st) {
   const size_t smem = fixed + p.nsb * stage;
   KGP_REQUIRE(smem <= limit, KGP_ERR_INVALID, "fast operator tile config needs %zu B of shared memory", smem);
   KGP_SMEM_ATTR(kern, limit);
-  const int nsplit = (p.nblk + p.nper - 1) / p.nper;
+  const int nsplit = (p.nblk - p.tbeg + p.nper - 1) / p.nper;
   dim3 grid((unsigned)((p.nrows + 127) / 128), (unsigned)nsplit);
   if (p.ev_start) KGP_CUDA(cudaEventRecord(p.ev_start, st));
   kern<<<grid, nthreads_for(ns_of(NOUT, SPLIT, LBM)), smem, st>>>(p);
   KGP_LAUNCH("kmm_tc_kernel");
   if (p.ev_stop) KGP_CUDA(cudaEventRecord(p.ev_stop, st));
-  if (nsplit > 1) {
+  if (p.part != nullptr && !p.noreduce) {  // the partials of every slot so far, in slot order
     const int64_t cnt = p.nrows * p.k;
-    tc_reduce_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(p, nsplit, NOUT * p.kp);
+    tc_reduce_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(p, p.slot0 + nsplit, NOUT * p.kp);
     KGP_LAUNCH("tc_reduce_kernel");
   }
   return KGP_OK;

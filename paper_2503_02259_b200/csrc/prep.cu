@@ -107,15 +107,16 @@ __device__ inline uint32_t tf32_rna_bits(float v) {
   return r;
 }
 
-__global__ void prep_rhs_kernel(int split, int lb, int64_t n, int64_t k, int64_t c0, int kp, int nblk,
+__global__ void prep_rhs_kernel(int split, int lb, int64_t n, int64_t k, int64_t c0, int kp, int blk0, int nblk,
                                 const double* __restrict__ b, int64_t b_rs, int64_t b_cs, uint8_t* __restrict__ out) {
-  // one thread per (block t, rhs column c, in-block row jj); jj fastest for coalesced column-major reads
+  // one thread per (block t, rhs column c, in-block row jj); jj fastest for coalesced column-major reads;
+  // blocks [blk0, blk0 + nblk)
   int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t total = (int64_t)nblk * kp * 32;
   if (g >= total) return;
   const int jj = (int)(g & 31);
   const int c = (int)((g >> 5) % kp);
-  const int64_t t = (g >> 5) / kp;
+  const int64_t t = blk0 + (g >> 5) / kp;
   const int64_t j = t * 32 + jj;
   const int64_t cc = c0 + c;
   double v = (j < n && cc < k) ? b[j * b_rs + cc * b_cs] : 0.0;
@@ -171,10 +172,14 @@ int prep_cols(int kt, int d, int dpad, int64_t n, const double* x, const double*
 }
 
 int prep_rhs(int split, int lb, int64_t n, int64_t k, int64_t c0, int kp, const double* b, int64_t b_rs, int64_t b_cs,
-             uint8_t* out, cudaStream_t st) {
-  int nblk = (int)((n + 31) / 32);
+             uint8_t* out, cudaStream_t st, int blk0, int blk1) {
+  const int nall = (int)((n + 31) / 32);
+  if (blk1 < 0 || blk1 > nall) blk1 = nall;
+  const int nblk = blk1 - blk0;
+  if (nblk <= 0) return KGP_OK;
   int64_t total = (int64_t)nblk * kp * 32;
-  prep_rhs_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(split, lb, n, k, c0, kp, nblk, b, b_rs, b_cs, out);
+  prep_rhs_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(split, lb, n, k, c0, kp, blk0, nblk, b, b_rs, b_cs,
+                                                                    out);
   KGP_LAUNCH("prep_rhs_kernel");
   return KGP_OK;
 }
