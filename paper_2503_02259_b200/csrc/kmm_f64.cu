@@ -252,25 +252,47 @@ __global__ void __launch_bounds__(SB) kmm_f64_sym_kernel(const F64Params p, int 
   }
 }
 
-__global__ void f64_sym_reduce_kernel(const F64Params p, int nb, const double* __restrict__ part) {
+// Partial-sum reduction, RW warps per 32 consecutive elements: warp w sums the slots q = w (mod
+// RW) in slot order (four loads in flight), then the RW warp sums are added in warp order --
+// a fixed tree, so run-to-run identical. (One thread per element serialised 64 dependent adds
+// over 16 CTAs at configs[0]: 10.6 us per product; latency, not bandwidth.)
+constexpr int RW = 8;
+KGP_DEV double reduce_slots(const double* __restrict__ part, int nslot, int64_t stride, int64_t e, bool live,
+                            double (*red)[32]) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double a = 0.0;
+  if (live) {
+    int q = w;
+    for (; q + 3 * RW < nslot; q += 4 * RW) {
+      const double t0 = part[(int64_t)q * stride + e], t1 = part[(int64_t)(q + RW) * stride + e];
+      const double t2 = part[(int64_t)(q + 2 * RW) * stride + e], t3 = part[(int64_t)(q + 3 * RW) * stride + e];
+      a += t0;
+      a += t1;
+      a += t2;
+      a += t3;
+    }
+    for (; q < nslot; q += RW) a += part[(int64_t)q * stride + e];
+  }
+  red[w][lane] = a;
+  __syncthreads();
+  double t = 0.0;
+  if (w == 0) {
+#pragma unroll
+    for (int u = 0; u < RW; ++u) t += red[u][lane];
+  }
+  return t;
+}
+
+__global__ void __launch_bounds__(RW * 32) f64_sym_reduce_kernel(const F64Params p, int nb, const double* __restrict__ part) {
   if (p.gate != nullptr && *p.gate == 0) return;
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ double red[RW][32];
+  const int64_t e = (int64_t)blockIdx.x * 32 + (threadIdx.x & 31);
   const int64_t n = p.ncols;
-  if (e >= n * p.k) return;
+  const bool live = e < n * p.k;
+  const double a = reduce_slots(part, nb, n * p.k, e, live, red);
+  if (!live || threadIdx.x >= 32) return;
   const int64_t r = e / p.k;
   const int c = (int)(e % p.k);
-  // eight independent loads in flight, added in partner order (deterministic)
-  const int64_t stride = n * p.k;
-  double a = 0.0;
-  int q = 0;
-  for (; q + 8 <= nb; q += 8) {
-    double t[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) t[u] = part[(int64_t)(q + u) * stride + e];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) a += t[u];
-  }
-  for (; q < nb; ++q) a += part[(int64_t)q * stride + e];
   const int64_t o = r * p.o_rs + (int64_t)c * p.o_cs;
   if (p.out_k) p.out_k[o] = p.f2 * a + p.s * p.b[r * p.b_rs + (int64_t)c * p.b_cs];
   if (p.out_df) p.out_df[o] = p.two_f * a;
@@ -294,17 +316,20 @@ int launch_sym(const F64Params& p, int nb, double* part, cudaStream_t st) {
 }
 
 // sum the column-split partials in split order, then the epilogue
-__global__ void f64_reduce_kernel(const F64Params p, int nsplit) {
+__global__ void __launch_bounds__(RW * 32) f64_reduce_kernel(const F64Params p, int nsplit) {
   if (p.gate != nullptr && *p.gate == 0) return;
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= p.nrows * p.k) return;
+  __shared__ double red[RW][32];
+  const int64_t e = (int64_t)blockIdx.x * 32 + (threadIdx.x & 31);
+  const bool live = e < p.nrows * p.k;
+  const double a = reduce_slots(p.part, nsplit, p.nrows * p.k, e, live, red);
+  double g = 0.0;
+  if (p.out_dl) {
+    __syncthreads();
+    g = reduce_slots(p.part + p.part_stride, nsplit, p.nrows * p.k, e, live, red);
+  }
+  if (!live || threadIdx.x >= 32) return;
   const int64_t r = e / p.k;
   const int c = (int)(e % p.k);
-  double a = 0.0, g = 0.0;
-  for (int z = 0; z < nsplit; ++z) {
-    a += p.part[(int64_t)z * p.nrows * p.k + e];
-    if (p.out_dl) g += p.part[p.part_stride + (int64_t)z * p.nrows * p.k + e];
-  }
   const int64_t o = r * p.o_rs + (int64_t)c * p.o_cs;
   if (p.out_k) {
     double v = p.f2 * a;
@@ -321,7 +346,13 @@ __global__ void f64_reduce_kernel(const F64Params p, int nsplit) {
 inline int slice_for(int k, int nout, int d) {
   const int cap = nout == 2 ? (d > 8 ? 24 : KGP_F64_CAP2) : 48;  // d > 8: 16 more coordinate registers
   const int nsl = (k + cap - 1) / cap;
-  return ((k + nsl - 1) / nsl + 3) / 4 * 4;
+  const int w = (k + nsl - 1) / nsl;
+  // widths of 2, 18 and 34 are instantiated too (k = 1, 17 and 33: the w-solve, configs[0]'s
+  // w + 16 probes and configs[2]'s w + 32 probes), everything else rounds up to a multiple of 4
+  if (w <= 2) return 2;
+  if (w == 17 || w == 18) return 18;
+  if (w == 33 || w == 34) return 34;
+  return (w + 3) / 4 * 4;
 }
 
 template <int KT, int NOUT, int DB>
@@ -334,7 +365,8 @@ int launch_ks(const F64Params& p, int ks, dim3 grid, cudaStream_t st) {
       break;                                                               \
     }                                                                      \
     [[fallthrough]];
-    KGP_F64_KS(4) KGP_F64_KS(8) KGP_F64_KS(12) KGP_F64_KS(16) KGP_F64_KS(20) KGP_F64_KS(24) KGP_F64_KS(28)
+    KGP_F64_KS(2) KGP_F64_KS(4) KGP_F64_KS(8) KGP_F64_KS(12) KGP_F64_KS(16) KGP_F64_KS(18) KGP_F64_KS(20)
+    KGP_F64_KS(24) KGP_F64_KS(28) KGP_F64_KS(34)
     KGP_F64_KS(32) KGP_F64_KS(36) KGP_F64_KS(40) KGP_F64_KS(44) KGP_F64_KS(48)
 #undef KGP_F64_KS
     default:
@@ -377,7 +409,7 @@ int launch_kmm_f64(int kt, const F64Params& p_in, DevBuf& ws, cudaStream_t st) {
                        : (kt == MAT32) ? launch_sym<MAT32>(p, nb, part, st) : launch_sym<MAT52>(p, nb, part, st);
     if (rc) return rc;
     const int64_t cnt = p.ncols * p.k;
-    f64_sym_reduce_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(p, nb, part);
+    f64_sym_reduce_kernel<<<(unsigned)((cnt + 31) / 32), RW * 32, 0, st>>>(p, nb, part);
     KGP_LAUNCH("f64_sym_reduce_kernel");
     return KGP_OK;
   }
@@ -411,7 +443,7 @@ int launch_kmm_f64(int kt, const F64Params& p_in, DevBuf& ws, cudaStream_t st) {
                                                                                 : launch_kt<MAT52>(p, ks, grid, st);
   if (rc || nsplit == 1) return rc;
   const int64_t cnt = p.nrows * p.k;
-  f64_reduce_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(p, (int)nsplit);
+  f64_reduce_kernel<<<(unsigned)((cnt + 31) / 32), RW * 32, 0, st>>>(p, (int)nsplit);
   KGP_LAUNCH("f64_reduce_kernel");
   return KGP_OK;
 }
