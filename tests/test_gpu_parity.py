@@ -650,6 +650,33 @@ def test_matmul_host_matches_device(pkg, precision):
     assert rel_max(ok2, ref_k.cpu().numpy()) <= bar
 
 
+@pytest.mark.parametrize("zchunks,ratio", [(2, 1), (5, 3), (8, 4)])
+def test_matmul_host_input_chunks(pkg, zchunks, ratio, monkeypatch):
+    """The host entry's input pipelining: B copied in `zchunks` chunks (sizes growing by `ratio`)
+    while the first row chunk runs as column-chunked launches sharing one partial buffer; ragged n
+    (not a multiple of 32) and a k that needs the 16-column padding."""
+    import torch
+
+    from paper_2503_02259_b200 import _lib
+
+    n, k = 70001, 21
+    rng = np.random.default_rng(zchunks)
+    x = rng.standard_normal((n, 8))
+    b = rng.standard_normal((n, k))
+    e = pkg.KernelEngine(pkg.KernelType.GAUSSIAN, x, _hp(pkg, 1.0, 1.2, 0.1), precision="fast")
+    ref_k, ref_l, _ = e.apply(torch.from_numpy(b).cuda(), True, True, False)
+    monkeypatch.setenv("KGP_HOST_ZCHUNKS", str(zchunks))
+    monkeypatch.setenv("KGP_HOST_ZRATIO", str(ratio))
+    bh = torch.from_numpy(b).pin_memory()
+    ok = torch.empty((n, k), dtype=torch.float64).pin_memory()
+    ol = torch.empty_like(ok).pin_memory()
+    for _ in range(2):  # the second call reuses the engine's buffers and events
+        _lib.call("kgp_engine_matmul_host", e.handle, k, bh.data_ptr(), ok.data_ptr(), ol.data_ptr(), None,
+                  torch.cuda.current_stream().cuda_stream)
+        assert rel_max(ok.numpy(), ref_k.cpu().numpy()) <= 1e-5
+        assert rel_max(ol.numpy(), ref_l.cpu().numpy()) <= 1e-5
+
+
 def test_preconditioned_probes_estimator(pkg):
     """preconditioned_probes=True (extension): log|M| and the N(0, M) draws are exact, and the
     device estimator equals its dense same-probe formula (1e-6 at tight tolerances)."""
