@@ -85,6 +85,12 @@ static void engine_free_host_state(kgp_engine_s* e) {
   for (auto ev : e->tev) cudaEventDestroy(ev);
 }
 
+#ifndef KGP_HOST_CHUNKS_DEFAULT
+#define KGP_HOST_CHUNKS_DEFAULT 3
+#endif
+#ifndef KGP_HOST_RRATIO_DEFAULT
+#define KGP_HOST_RRATIO_DEFAULT 50
+#endif
 static int tc_env_int(const char* name, int dflt) {
   const char* s = getenv(name);
   return s ? atoi(s) : dflt;
@@ -668,11 +674,15 @@ extern "C" int kgp_engine_matmul_host(kgp_engine* e, int64_t k, const double* b,
   } else {
     KGP_CUDA(cudaMemcpyAsync(db, b, sizeof(double) * n * k, cudaMemcpyHostToDevice, st));
   }
-  // 3 row chunks, the last one a third of an even share (KGP_HOST_CHUNKS / KGP_HOST_TAIL;
-  // tools/e2e_tail.sh): cfg2 e2e 3.97 ms (one chunk 4.39; 2 even 4.13; 4 even 4.17) -- the
-  // transfer of each chunk's outputs hides behind the next chunk and the exposed tail is short
+  // Row chunks shrinking geometrically (KGP_HOST_CHUNKS = 3, share ratio KGP_HOST_RRATIO = 50 %:
+  // 4/7, 2/7, 1/7 of the rows): each chunk's output copy hides behind the chunks after it, only the
+  // last, small chunk's copy is exposed. Measured at cfg2 (tools/e2e_tail3.sh, e2e_tail4.sh; with
+  // the input pipelining): 3.14 ms, reproducibly -- but ratios 45 / 55 % gave 3.53 / 3.65 ms and
+  // 4-8 chunks 3.28-3.83 ms, so the schedule is sensitive to how the chunk boundaries fall.
+  // KGP_HOST_RRATIO=0: the earlier schedule, equal shares with the last one KGP_HOST_TAIL percent
+  // of a share (3.28 ms; round 1: 3.97 ms vs 4.39 unchunked, before the input pipelining)
   const int max_chunks = (int)(sizeof(e->xev) / sizeof(e->xev[0]));
-  int nchunk = chunked ? tc_env_int("KGP_HOST_CHUNKS", 3) : 1;
+  int nchunk = chunked ? tc_env_int("KGP_HOST_CHUNKS", KGP_HOST_CHUNKS_DEFAULT) : 1;
   nchunk = nchunk < 1 ? 1 : (nchunk > max_chunks ? max_chunks : nchunk);
   if (chunked) {
     rc = engine_prepare(e, st);
@@ -688,6 +698,11 @@ extern "C" int kgp_engine_matmul_host(kgp_engine* e, int64_t k, const double* b,
     auto edge = [&](int c2) -> int64_t {
       if (c2 <= 0) return 0;
       if (c2 >= nchunk) return rows;
+      const double q = tc_env_int("KGP_HOST_RRATIO", KGP_HOST_RRATIO_DEFAULT) / 100.0;
+      if (q > 0.0 && q != 1.0) {
+        const double f = (1.0 - std::pow(q, c2)) / (1.0 - std::pow(q, nchunk));
+        return std::min(rows, (int64_t)(f * blocks + 0.5) * 128);
+      }
       const double tail = tc_env_int("KGP_HOST_TAIL", 35) / 100.0;
       const double last = tail / (nchunk - 1 + tail);  // fraction of the rows in the last chunk
       const double f = (double)c2 * (1.0 - last) / (nchunk - 1);

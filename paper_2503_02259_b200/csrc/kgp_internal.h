@@ -176,7 +176,7 @@ struct kgp_engine_s {
   // host-buffer products (kgp_engine_matmul_host): device staging, copy stream, chunk events
   kgp::DevBuf hostbuf;
   cudaStream_t xstream = nullptr;
-  cudaEvent_t xev[4] = {};
+  cudaEvent_t xev[8] = {};
   cudaEvent_t zev[9] = {};   // host entry: H2D chunks of the RHS (8) + "stream ready" (1)
   // optional heteroscedastic diagonal (kgp_engine_set_diag): Khat column c gets + diag(dn[:, dmap[c]])
   int dn_classes = 0;
