@@ -9,6 +9,7 @@
 #include <cmath>
 #include <mutex>
 #include <set>
+#include <vector>
 
 #include <cublas_v2.h>
 
@@ -675,12 +676,12 @@ extern "C" int kgp_engine_matmul_host(kgp_engine* e, int64_t k, const double* b,
     KGP_CUDA(cudaMemcpyAsync(db, b, sizeof(double) * n * k, cudaMemcpyHostToDevice, st));
   }
   // Row chunks shrinking geometrically (KGP_HOST_CHUNKS = 3, share ratio KGP_HOST_RRATIO = 50 %:
-  // 4/7, 2/7, 1/7 of the rows): each chunk's output copy hides behind the chunks after it, only the
-  // last, small chunk's copy is exposed. Measured at cfg2 (tools/e2e_tail3.sh, e2e_tail4.sh; with
-  // the input pipelining): 3.14 ms, reproducibly -- but ratios 45 / 55 % gave 3.53 / 3.65 ms and
-  // 4-8 chunks 3.28-3.83 ms, so the schedule is sensitive to how the chunk boundaries fall.
-  // KGP_HOST_RRATIO=0: the earlier schedule, equal shares with the last one KGP_HOST_TAIL percent
-  // of a share (3.28 ms; round 1: 3.97 ms vs 4.39 unchunked, before the input pipelining)
+  // ~4/7, 2/7, 1/7 of the rows) with every boundary snapped to whole waves of 148 row tiles: each
+  // chunk's output copy hides behind the chunks after it, only the last, small chunk's copy is
+  // exposed. cfg2 (tools/e2e_tail4.sh, KGP_HOST_TRACE=1 timelines): 3.14 ms. Without the wave
+  // snapping the same ratios gave 3.14-3.65 ms -- a chunk of 276 or 310 row tiles runs 2 partial
+  // waves (the column split cannot refill them at the small input chunks). KGP_HOST_RRATIO=0: the
+  // earlier schedule, equal shares with the last one KGP_HOST_TAIL percent of a share (3.28 ms)
   const int max_chunks = (int)(sizeof(e->xev) / sizeof(e->xev[0]));
   int nchunk = chunked ? tc_env_int("KGP_HOST_CHUNKS", KGP_HOST_CHUNKS_DEFAULT) : 1;
   nchunk = nchunk < 1 ? 1 : (nchunk > max_chunks ? max_chunks : nchunk);
@@ -690,24 +691,38 @@ extern "C" int kgp_engine_matmul_host(kgp_engine* e, int64_t k, const double* b,
   }
   double* hosts[3] = {out_k, out_dl, out_df};
   double* devs[3] = {dk, dl, df};
-  for (int c = 0; c < nchunk; ++c) {
-    // chunk boundaries on 128-row CTA tiles
-    const int64_t blocks = (rows + 127) / 128;
-    // chunk c ends at fraction (c+1)/nchunk of the rows, the last chunk shrunk to `tail_frac` of an
-    // even share so the exposed device->host tail is short (KGP_HOST_TAIL, percent)
-    auto edge = [&](int c2) -> int64_t {
-      if (c2 <= 0) return 0;
-      if (c2 >= nchunk) return rows;
-      const double q = tc_env_int("KGP_HOST_RRATIO", KGP_HOST_RRATIO_DEFAULT) / 100.0;
+  const bool trace = tc_env_int("KGP_HOST_TRACE", 0) != 0;
+  cudaEvent_t tev[1 + 2 * 8] = {};
+  if (trace) {
+    for (auto& ev : tev) KGP_CUDA(cudaEventCreate(&ev));
+    KGP_CUDA(cudaEventRecord(tev[0], st));  // after the input copies were queued (they run on the copy stream)
+  }
+  // chunk boundaries on 128-row CTA tiles
+  const int64_t blocks = (rows + 127) / 128;
+  std::vector<int64_t> edges(nchunk + 1, 0);
+  {
+    const double q = tc_env_int("KGP_HOST_RRATIO", KGP_HOST_RRATIO_DEFAULT) / 100.0;
+    const bool waves = tc_env_int("KGP_HOST_WAVES", 1) != 0;
+    edges[nchunk] = blocks;
+    for (int c = 1; c < nchunk; ++c) {
+      int64_t t;
       if (q > 0.0 && q != 1.0) {
-        const double f = (1.0 - std::pow(q, c2)) / (1.0 - std::pow(q, nchunk));
-        return std::min(rows, (int64_t)(f * blocks + 0.5) * 128);
+        // geometric shares; each boundary snapped to whole waves of 148 row tiles past the previous
+        // one (a launch over whole waves needs no column split to fill the SMs)
+        const double target = (1.0 - std::pow(q, c)) / (1.0 - std::pow(q, nchunk)) * (double)blocks;
+        t = waves ? edges[c - 1] + std::max<int64_t>(1, (int64_t)((target - (double)edges[c - 1]) / 148.0 + 0.5)) * 148
+                  : (int64_t)(target + 0.5);
+      } else {
+        // equal shares, the last one KGP_HOST_TAIL percent of a share
+        const double tail = tc_env_int("KGP_HOST_TAIL", 35) / 100.0;
+        const double last = tail / (nchunk - 1 + tail);
+        t = (int64_t)((double)c * (1.0 - last) / (nchunk - 1) * (double)blocks + 0.5);
       }
-      const double tail = tc_env_int("KGP_HOST_TAIL", 35) / 100.0;
-      const double last = tail / (nchunk - 1 + tail);  // fraction of the rows in the last chunk
-      const double f = (double)c2 * (1.0 - last) / (nchunk - 1);
-      return std::min(rows, (int64_t)(f * blocks + 0.5) * 128);
-    };
+      edges[c] = std::max(edges[c - 1] + 1, std::min(t, blocks - (nchunk - c)));
+    }
+  }
+  for (int c = 0; c < nchunk; ++c) {
+    auto edge = [&](int c2) -> int64_t { return std::min(rows, edges[c2] * 128); };
     const int64_t r0 = edge(c), r1 = edge(c + 1);
     if (r1 <= r0) continue;
     if (chunked && c == 0 && nz > 1) {
@@ -735,13 +750,26 @@ extern "C" int kgp_engine_matmul_host(kgp_engine* e, int64_t k, const double* b,
     }
     if (rc) return rc;
     KGP_CUDA(cudaEventRecord(e->xev[c], st));
+    if (trace) KGP_CUDA(cudaEventRecord(tev[1 + 2 * c], st));
     KGP_CUDA(cudaStreamWaitEvent(e->xstream, e->xev[c], 0));
     for (int o = 0; o < 3; ++o)
       if (hosts[o])
         KGP_CUDA(cudaMemcpyAsync(hosts[o] + r0 * k, devs[o] + r0 * k, sizeof(double) * (r1 - r0) * k,
                                  cudaMemcpyDeviceToHost, e->xstream));
+    if (trace) KGP_CUDA(cudaEventRecord(tev[2 + 2 * c], e->xstream));
   }
   KGP_CUDA(cudaStreamSynchronize(e->xstream));
+  if (trace) {  // diagnostic timeline (KGP_HOST_TRACE=1): per row chunk, compute done / copy done (us)
+    fprintf(stderr, "kgp host trace (rows %lld, %d chunks, %d input chunks):", (long long)rows, nchunk, nz);
+    for (int c = 0; c < nchunk; ++c) {
+      float a = 0.f, b2 = 0.f;
+      cudaEventElapsedTime(&a, tev[0], tev[1 + 2 * c]);
+      cudaEventElapsedTime(&b2, tev[0], tev[2 + 2 * c]);
+      fprintf(stderr, " [%d: compute %.0f, copy %.0f]", c, a * 1e3f, b2 * 1e3f);
+    }
+    fprintf(stderr, "\n");
+    for (auto ev : tev) cudaEventDestroy(ev);
+  }
   return KGP_OK;
 }
 
