@@ -20,6 +20,9 @@
 #ifndef KGP_F64_FASTEXP
 #define KGP_F64_FASTEXP 1  // the operator's entries through exp_neg64 (kgp_common.cuh)
 #endif
+#ifndef KGP_F64_SYM_FG
+#define KGP_F64_SYM_FG 0  // symmetric small-k kernel: branch-free exp_neg64 for the Gaussian
+#endif
 #ifndef KGP_F64_CAP2
 // RHS columns per slice with two outputs (register budget): 28 -> 168 registers, 3 CTAs per SM;
 // measured against 24 (n = 16384): Gaussian d=8 k=51 9.67 -> 5.03 ms (two slices of 28 instead of
@@ -202,7 +205,7 @@ __global__ void __launch_bounds__(SB) kmm_f64_sym_kernel(const F64Params p, int 
             r2 = __dadd_rn(r2, __dmul_rn(df, df));  // numba's rounding (no FMA contraction)
           }
         }
-        kv = KGP_KAPPA<KT>(r2, p.l);
+        kv = kappa64f<KT, KGP_F64_SYM_FG>(r2, p.l);
       }
 #pragma unroll
       for (int c = 0; c < KS; ++c) {
