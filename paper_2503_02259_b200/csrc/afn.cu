@@ -533,8 +533,15 @@ static int afn_apply_pm(kgp_precond_s* p, int64_t k, const double* b, int64_t b_
   // y1 = L^-1 b1
   rc = gemm_f64(k, m, m, bp, 1, k, linv, 1, m, y1, 1, k, 1.0, 0.0, nullptr, 0, 0, p->tmp, st);
   if (rc) return rc;
+  // W products: the DMMA streams of wgemm.cu where they beat cuBLAS DGEMM -- 33..40 columns,
+  // which a 32-wide library tile pads to 64; env KGP_AFN_WGEMM=0 never,
+  // =2 for every k <= 64 (tests, measurements)
+  const char* wge = getenv("KGP_AFN_WGEMM");
+  const int wg_mode = wge ? atoi(wge) : 1;
+  const bool wg = wg_mode != 0 && wgemm_supported(m, k, w, m) && (wg_mode == 2 || (k >= 33 && k <= 40));
   // t2 = b2 - W y1
-  rc = gemm_f64(k, n2, m, y1, 1, k, w, 1, m, t2, 1, k, -1.0, 1.0, bp + m * k, 1, k, p->tmp, st);
+  rc = wg ? wy_product(n2, m, k, w, m, y1, k, 1, t2, k, 1, -1.0, 1.0, bp + m * k, k, 1, st)
+          : gemm_f64(k, n2, m, y1, 1, k, w, 1, m, t2, 1, k, -1.0, 1.0, bp + m * k, 1, k, p->tmp, st);
   if (rc) return rc;
   // u2 = G^T (G t2)
   const unsigned sgrid = (unsigned)((n2 * k + 255) / 256);
@@ -544,7 +551,8 @@ static int afn_apply_pm(kgp_precond_s* p, int64_t k, const double* b, int64_t b_
                                        v, u2);
   KGP_LAUNCH("pm_csr_kernel");
   // z1 = y1 - W^T u2
-  rc = gemm_f64(k, m, n2, u2, 1, k, w, m, 1, z1, 1, k, -1.0, 1.0, y1, 1, k, p->tmp, st);
+  rc = wg ? wtu_product(n2, m, k, w, m, u2, k, 1, z1, k, 1, -1.0, 1.0, y1, k, 1, p->tmp, st)
+          : gemm_f64(k, m, n2, u2, 1, k, w, m, 1, z1, 1, k, -1.0, 1.0, y1, 1, k, p->tmp, st);
   if (rc) return rc;
   // o1 = L^-T z1
   rc = gemm_f64(k, m, m, z1, 1, k, linv, m, 1, o1, 1, k, 1.0, 0.0, nullptr, 0, 0, p->tmp, st);

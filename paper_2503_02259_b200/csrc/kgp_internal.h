@@ -245,6 +245,17 @@ int gemm_f64(int64_t M, int64_t N, int64_t K, const double* a, int64_t a_is, int
              int64_t b_ks, int64_t b_ns, double* c, int64_t c_is, int64_t c_ns, double alpha, double beta,
              const double* src, int64_t s_is, int64_t s_ns, DevBuf& tmp, cudaStream_t st);
 
+// the AFN application's W products for point-major blocks (wgemm.cu, DMMA):
+//   wy:  C = alpha W Y + beta S      (W n2 x m row-major, C n2 x k)
+//   wtu: Z = alpha W^T U + beta SRC  (Z m x k), fixed-order row-split partials in tmp
+bool wgemm_supported(int64_t m, int64_t k, const double* w, int64_t ldw);
+int wy_product(int64_t n2, int64_t m, int64_t k, const double* w, int64_t ldw, const double* y, int64_t y_rs,
+               int64_t y_cs, double* c, int64_t c_rs, int64_t c_cs, double alpha, double beta, const double* s,
+               int64_t s_rs, int64_t s_cs, cudaStream_t st);
+int wtu_product(int64_t n2, int64_t m, int64_t k, const double* w, int64_t ldw, const double* u, int64_t u_rs,
+                int64_t u_cs, double* z, int64_t z_rs, int64_t z_cs, double alpha, double beta, const double* src,
+                int64_t s_rs, int64_t s_cs, DevBuf& tmp, cudaStream_t st);
+
 // column-wise reductions / updates used by the PCG driver (pcg.cu)
 int pcg_solve_impl(kgp_engine_s* e, kgp_precond_s* pc, int64_t k, const double* y, double tol, int max_iter,
                    double* x_out, double* alphas, double* betas, int32_t* iters, double* rel, int32_t* conv,

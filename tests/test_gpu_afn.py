@@ -10,6 +10,8 @@ AFN has no reference implementation, so:
 * its purpose is checked by iteration counts against Nystrom at equal rank.
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -79,6 +81,34 @@ def test_afn_apply_matches_numpy(pkg, kt):
     b12 = np.random.default_rng(2).standard_normal((900, 12))
     assert rel_max(pre.apply_inverse(b12), ref.apply_inverse(b12)) <= 1e-8
     np.testing.assert_array_equal(pre.apply_inverse(b12), pre.apply_inverse(b12))
+
+
+@pytest.mark.parametrize("n,m,k", [(900, 64, 9), (900, 130, 17), (900, 64, 33), (1337, 130, 40),
+                                   (900, 66, 51), (900, 64, 64), (6000, 512, 33), (900, 63, 33)])
+def test_afn_apply_wide_blocks(pkg, n, m, k):
+    """Point-major application with the DMMA W products (wgemm.cu): ragged row counts, landmark
+    counts off the 32/64-element tiles (odd m takes the cuBLAS path), every column-tile count
+    1..8, several row splits and staged chunks; against the numpy statement of the same
+    algebra, deterministic run to run."""
+    import afn_ref
+    from paper_2503_02259_b200 import precond
+
+    x, _ = _problem("matern32", n, 3, 0.2, 1e-3)
+    l, f, s = 0.2, 1.3, 1e-3
+    e = pkg.KernelEngine(pkg.KernelType.MATERN32, x, pkg.Hyperparams(l=l, f=f, s=s))
+    pre = precond.build_afn(e, m, fsai_npt=10)
+    ref = afn_ref.AFN("matern32", x, l, f, s, m, 10)
+    b = np.random.default_rng(k).standard_normal((n, k))
+    want = ref.apply_inverse(b)
+    # default dispatch (DMMA streams for 33..40 columns), then forced for every width
+    for mode in ("1", "2"):
+        os.environ["KGP_AFN_WGEMM"] = mode
+        try:
+            got = pre.apply_inverse(b)
+            assert rel_max(got, want) <= 1e-8, mode
+            np.testing.assert_array_equal(got, pre.apply_inverse(b))
+        finally:
+            del os.environ["KGP_AFN_WGEMM"]
 
 
 def test_afn_preconditioned_pcg(pkg):
