@@ -100,33 +100,94 @@ KGP_DEV double exp_neg64(double x) {
   return __hiloint2double(__double2hiint(pv) + (k << 20), __double2loint(pv));
 }
 
+// Table-driven exp(x) for x <= 0: x = (64 e + j) ln2/64 + r, |r| <= ln2/128, exp(x) =
+// 2^e * 2^(j/64) * exp(r) with 2^(j/64) from a 64-entry table in shared memory (`tab`, filled by
+// exp_tab_fill) and exp(r) - 1 by its degree-5 Taylor polynomial (truncation r^6/720 <= 3.5e-17):
+// 11 FP64 instructions and one LDS against the 19 of exp_neg64 -- the fused fp64 operators are
+// bound by the FP64 pipe, the integer/LSU work rides along. The table entries are correctly
+// rounded (0.5 ulp), the result is within ~1.5 ulp; below 2^-1021 (x < -708) it is 0.
+__device__ const double EXP_TAB64[64] = {
+    0x1.0000000000000p+0, 0x1.02c9a3e778061p+0, 0x1.059b0d3158574p+0, 0x1.0874518759bc8p+0,
+    0x1.0b5586cf9890fp+0, 0x1.0e3ec32d3d1a2p+0, 0x1.11301d0125b51p+0, 0x1.1429aaea92de0p+0,
+    0x1.172b83c7d517bp+0, 0x1.1a35beb6fcb75p+0, 0x1.1d4873168b9aap+0, 0x1.2063b88628cd6p+0,
+    0x1.2387a6e756238p+0, 0x1.26b4565e27cddp+0, 0x1.29e9df51fdee1p+0, 0x1.2d285a6e4030bp+0,
+    0x1.306fe0a31b715p+0, 0x1.33c08b26416ffp+0, 0x1.371a7373aa9cbp+0, 0x1.3a7db34e59ff7p+0,
+    0x1.3dea64c123422p+0, 0x1.4160a21f72e2ap+0, 0x1.44e086061892dp+0, 0x1.486a2b5c13cd0p+0,
+    0x1.4bfdad5362a27p+0, 0x1.4f9b2769d2ca7p+0, 0x1.5342b569d4f82p+0, 0x1.56f4736b527dap+0,
+    0x1.5ab07dd485429p+0, 0x1.5e76f15ad2148p+0, 0x1.6247eb03a5585p+0, 0x1.6623882552225p+0,
+    0x1.6a09e667f3bcdp+0, 0x1.6dfb23c651a2fp+0, 0x1.71f75e8ec5f74p+0, 0x1.75feb564267c9p+0,
+    0x1.7a11473eb0187p+0, 0x1.7e2f336cf4e62p+0, 0x1.82589994cce13p+0, 0x1.868d99b4492edp+0,
+    0x1.8ace5422aa0dbp+0, 0x1.8f1ae99157736p+0, 0x1.93737b0cdc5e5p+0, 0x1.97d829fde4e50p+0,
+    0x1.9c49182a3f090p+0, 0x1.a0c667b5de565p+0, 0x1.a5503b23e255dp+0, 0x1.a9e6b5579fdbfp+0,
+    0x1.ae89f995ad3adp+0, 0x1.b33a2b84f15fbp+0, 0x1.b7f76f2fb5e47p+0, 0x1.bcc1e904bc1d2p+0,
+    0x1.c199bdd85529cp+0, 0x1.c67f12e57d14bp+0, 0x1.cb720dcef9069p+0, 0x1.d072d4a07897cp+0,
+    0x1.d5818dcfba487p+0, 0x1.da9e603db3285p+0, 0x1.dfc97337b9b5fp+0, 0x1.e502ee78b3ff6p+0,
+    0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0};
+
+// every thread of the CTA calls this before the first exp_neg64t (the caller synchronises)
+KGP_DEV void exp_tab_fill(double* tab) {
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) tab[i] = EXP_TAB64[i];
+}
+
+KGP_DEV double exp_neg64t(double x, const double* __restrict__ tab) {
+  if (x < -708.0) return 0.0;
+  // m = round(64 x / ln 2) by the 1.5 * 2^52 shifter (m in the low word), m = 64 e + j
+  const double t = fma(x, 0x1.71547652b82fep+6, 6755399441055744.0);
+  const int m = __double2loint(t);
+  const double md = t - 6755399441055744.0;
+  // r = x - m ln2/64, ln2/64 split so that m * hi is exact (|m| < 2^17, hi has 33 bits)
+  const double r = fma(md, -0x1.a39ef35793c76p-39, fma(md, -0x1.62e42fee00000p-7, x));
+  const double tj = tab[m & 63];
+  const double r2 = r * r;
+  const double a = fma(r, 1.0 / 6.0, 0.5);
+  const double b = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+  const double c = fma(r2, b, a);
+  const double q = fma(r2, c, r);       // exp(r) - 1
+  const double pv = fma(tj, q, tj);     // 2^(j/64) exp(r), in [0.99, 2.01)
+  return __hiloint2double(__double2hiint(pv) + ((m >> 6) << 20), __double2loint(pv));
+}
+
 // (the Gaussian keeps the library exp: measured faster there -- cfg2-shape fp64 step 52 vs
 // 63 ms -- while the Matern kernels gain 25 %: 2.75 -> 2.05 ms at n = 16384, k = 33)
 // FG: the Gaussian's exponential by the branch-free exp_neg64 as well (the library exp's
 // slow-path branch splits every entry's evaluation into its own basic block): measured at the
 // cfg2 shape (d = 8, k = 32, two outputs) 94.8 -> 55.9 ms; at d = 3 (configs[0]) the library exp
 // is 3 % faster, so the operators select it by dimension
+// TAB: the exponential by exp_neg64t (table in shared memory) for every kernel type
+#ifndef KGP_F64_TABEXP
+#define KGP_F64_TABEXP 1
+#endif
+template <int KT, bool FG>
+KGP_DEV double exp_sel(double x, const double* __restrict__ tab) {
+#if KGP_F64_TABEXP
+  return exp_neg64t(x, tab);
+#else
+  if (KT == GAUSS && !FG) return exp(x);
+  return exp_neg64(x);
+#endif
+}
+
 template <int KT, bool FG = false>
-KGP_DEV double kappa64f(double r2, double l) {
-  if (KT == GAUSS) return FG ? exp_neg64(-r2 * (1.0 / (2.0 * l * l))) : exp(-r2 * (1.0 / (2.0 * l * l)));
+KGP_DEV double kappa64f(double r2, double l, const double* __restrict__ tab) {
+  if (KT == GAUSS) return exp_sel<KT, FG>(-r2 * (1.0 / (2.0 * l * l)), tab);
   double t = (KT == MAT32 ? SQRT3 : SQRT5) / l * sqrt(r2);
-  if (KT == MAT32) return (1.0 + t) * exp_neg64(-t);
-  return (1.0 + t + (5.0 / (3.0 * l * l)) * r2) * exp_neg64(-t);
+  if (KT == MAT32) return (1.0 + t) * exp_sel<KT, FG>(-t, tab);
+  return (1.0 + t + (5.0 / (3.0 * l * l)) * r2) * exp_sel<KT, FG>(-t, tab);
 }
 
 // kappa and dkappa/dl of one entry from ONE exponential: the same values, bit for bit, as
 // kappa64f / dkappa64f (the same expressions, the exponential's argument rounded the same way)
 template <int KT, bool FG = false>
-KGP_DEV void kd64f(double r2, double l, double& kv, double& gv) {
+KGP_DEV void kd64f(double r2, double l, double& kv, double& gv, const double* __restrict__ tab) {
   if (KT == GAUSS) {
     const double x = -r2 * (1.0 / (2.0 * l * l));
-    const double e = FG ? exp_neg64(x) : exp(x);
+    const double e = exp_sel<KT, FG>(x, tab);
     kv = e;
     gv = r2 * (1.0 / (l * l * l)) * e;
     return;
   }
   const double t = (KT == MAT32 ? SQRT3 : SQRT5) / l * sqrt(r2);
-  const double e = exp_neg64(-t);
+  const double e = exp_sel<KT, FG>(-t, tab);
   if (KT == MAT32) {
     kv = (1.0 + t) * e;
     gv = (3.0 / (l * l * l)) * r2 * e;

@@ -14,6 +14,10 @@
 // Bound: the FP64 pipe (distance 3d + exp ~25 + KS FMA per entry and output).
 #include <stdlib.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "kgp_common.cuh"
 #include "kgp_internal.h"
 
@@ -29,6 +33,14 @@
 // three of 20: each slice re-evaluates every kernel entry), Matern-5/2 d=2 k=28 3.89 -> 2.53 ms;
 // 32 (211 registers, 2 CTAs per SM) made cfg2's k = 32 55.9 -> 93.6 ms, so 32 runs as 2 x 16
 #define KGP_F64_CAP2 28
+#endif
+#ifndef KGP_F64_FMADIST
+#define KGP_F64_FMADIST 0  // 1: r^2 accumulated with FMA (one rounding per term fewer than numba's order)
+#endif
+#if KGP_F64_FMADIST
+#define KGP_R2ACC(r2, df) fma((df), (df), (r2))
+#else
+#define KGP_R2ACC(r2, df) __dadd_rn((r2), __dmul_rn((df), (df)))  // numba's rounding (no FMA contraction)
 #endif
 #if KGP_F64_FASTEXP
 #define KGP_KAPPA kappa64f
@@ -51,6 +63,8 @@ __global__ void __launch_bounds__(NT) kmm_f64_kernel(const F64Params p) {
   if (p.gate != nullptr && *p.gate == 0) return;  // PCG iteration past convergence
   __shared__ double sXj[TJ][DB + 1];
   __shared__ __align__(16) double sB[TJ][KS];
+  __shared__ double sTab[64];  // 2^(j/64) of exp_neg64t (visible after the first tile barrier)
+  exp_tab_fill(sTab);
 
   const int tid = threadIdx.x;
   const int64_t r = (int64_t)blockIdx.x * NT + tid;
@@ -70,44 +84,60 @@ __global__ void __launch_bounds__(NT) kmm_f64_kernel(const F64Params p) {
     if (NOUT == 2) accg[c] = 0.0;
   }
 
+  // EB entries per inner step (independent distance / exponential chains, the contraction after
+  // them in column order so every sum keeps its order). Measured at EB = 4 / 2 over k = 4..64,
+  // d = 3..8 (tools/f64_grid.py): 25-35 % faster for one output at d = 8, k = 16..18 and 32..34,
+  // but 15-60 % slower for two outputs and for k = 24..28 and 40..48 (the chains' registers cost
+  // a resident CTA); configs[0] eval 4.93 -> 5.10 ms. One entry per step stays.
+  constexpr int EB = 1;
+  static_assert(TJ % EB == 0, "entry batch");
   for (int64_t j0 = jb; j0 < je; j0 += TJ) {
     const int nj = (int)(je - j0 < TJ ? je - j0 : TJ);
+    const int nje = (nj + EB - 1) / EB * EB;  // rows past nj up to the batch boundary: zero RHS
     __syncthreads();
     for (int e = tid; e < nj * d; e += NT) sXj[e / d][e % d] = p.xc[(j0 + e / d) * d + e % d];
-    for (int e = tid; e < nj * KS; e += NT) {
+    for (int e = tid; e < nje * KS; e += NT) {
       const int jj = e / KS, c = e % KS;
       const int cc = c0 + c;
-      sB[jj][c] = cc < p.k ? p.b[(j0 + jj) * p.b_rs + (int64_t)cc * p.b_cs] : 0.0;
+      sB[jj][c] = (jj < nj && cc < p.k) ? p.b[(j0 + jj) * p.b_rs + (int64_t)cc * p.b_cs] : 0.0;
     }
     __syncthreads();
-    for (int jj = 0; jj < nj; ++jj) {
-      double r2 = 0.0;
+    for (int jj = 0; jj < nje; jj += EB) {
+      double kv[EB], gv[EB];
 #pragma unroll
-      for (int q = 0; q < DB; ++q) {
-        if (q < d) {
-          const double df = xi[q] - sXj[jj][q];
-          r2 = __dadd_rn(r2, __dmul_rn(df, df));  // numba's rounding (no FMA contraction)
+      for (int u = 0; u < EB; ++u) {
+        const int jm = jj + u < nj ? jj + u : nj - 1;  // past nj: any finite value (its RHS row is 0)
+        double r2 = 0.0;
+#pragma unroll
+        for (int q = 0; q < DB; ++q) {
+          if (q < d) {
+            const double df = xi[q] - sXj[jm][q];
+            r2 = KGP_R2ACC(r2, df);  // numba's rounding (no FMA contraction)
+          }
         }
-      }
-      double kv, gv = 0.0;
+        gv[u] = 0.0;
 #if KGP_F64_FASTEXP
-      if (NOUT == 2) {
-        kd64f<KT, (DB >= 8)>(r2, p.l, kv, gv);  // one exponential for both outputs
-      } else {
-        kv = kappa64f<KT, (DB >= 8)>(r2, p.l);
-      }
-#else
-      kv = KGP_KAPPA<KT>(r2, p.l);
-      if (NOUT == 2) gv = KGP_DKAPPA<KT>(r2, p.l);
-#endif
-#pragma unroll
-      for (int c = 0; c < KS; c += 2) {
-        const double2 bv = *reinterpret_cast<const double2*>(&sB[jj][c]);
-        acc[c] = fma(kv, bv.x, acc[c]);
-        acc[c + 1] = fma(kv, bv.y, acc[c + 1]);
         if (NOUT == 2) {
-          accg[c] = fma(gv, bv.x, accg[c]);
-          accg[c + 1] = fma(gv, bv.y, accg[c + 1]);
+          kd64f<KT, (DB >= 8)>(r2, p.l, kv[u], gv[u], sTab);  // one exponential for both outputs
+        } else {
+          kv[u] = kappa64f<KT, (DB >= 8)>(r2, p.l, sTab);
+        }
+#else
+        kv[u] = KGP_KAPPA<KT>(r2, p.l);
+        if (NOUT == 2) gv[u] = KGP_DKAPPA<KT>(r2, p.l);
+#endif
+      }
+#pragma unroll
+      for (int u = 0; u < EB; ++u) {
+#pragma unroll
+        for (int c = 0; c < KS; c += 2) {
+          const double2 bv = *reinterpret_cast<const double2*>(&sB[jj + u][c]);
+          acc[c] = fma(kv[u], bv.x, acc[c]);
+          acc[c + 1] = fma(kv[u], bv.y, acc[c + 1]);
+          if (NOUT == 2) {
+            accg[c] = fma(gv[u], bv.x, accg[c]);
+            accg[c + 1] = fma(gv[u], bv.y, accg[c + 1]);
+          }
         }
       }
     }
@@ -117,6 +147,134 @@ __global__ void __launch_bounds__(NT) kmm_f64_kernel(const F64Params p) {
 #pragma unroll
   for (int c = 0; c < KS; ++c) {
     const int cc = c0 + c;
+    if (cc >= p.k) continue;
+    if (p.part) {
+      const int64_t slot = ((int64_t)blockIdx.z * p.nrows + r) * p.k + cc;
+      p.part[slot] = acc[c];
+      if (NOUT == 2) p.part[p.part_stride + slot] = accg[c];
+      continue;
+    }
+    const int64_t o = r * p.o_rs + (int64_t)cc * p.o_cs;
+    if (p.out_k) {
+      double v = p.f2 * acc[c];
+      if (p.diag_row0 >= 0) v += p.s * p.b[(p.diag_row0 + r) * p.b_rs + (int64_t)cc * p.b_cs];
+      p.out_k[o] = v;
+    }
+    if (p.out_df) p.out_df[o] = p.two_f * acc[c];
+    if (NOUT == 2 && p.out_dl) p.out_dl[o] = p.f2_dl * accg[c];
+  }
+}
+
+// ------------------------------------------------------------------ lane-split wide-k path
+// Every RHS slice of kmm_f64_kernel re-evaluates the kernel entries (distance + exponential, ~40
+// of the ~70 FP64 instructions per entry and slice at 16 columns and two outputs), and the slice
+// width is capped by the accumulator registers. Here G = 2 or 4 adjacent lanes share a row: lane
+// h of the group evaluates every G-th entry of the row (one evaluation per entry in all), the
+// group exchanges kappa (and dkappa/dl) by width-G shuffles, and each lane contracts all the
+// entries against ITS KQ columns of the slice -- G x KQ columns per evaluation with KQ
+// accumulators per lane and output (k = 32 with two outputs: one pass instead of 2 x 16).
+// Each (row, column) sum runs over the entries in the same order as in kmm_f64_kernel with
+// the same kappa, so both kernels give the same bits.
+constexpr int NTS = 256;  // threads per CTA (NTS / G rows)
+constexpr int kqp_of(int kq, int g) {
+  // padded lane stride of a column tile row: the G sub-rows a warp reads at once (16-byte loads)
+  // must fall into different 16-byte bank groups of the 128-byte bank row
+  int q = kq;
+  for (;; q += 2) {
+    bool ok = true;
+    for (int a = 0; a < g; ++a)
+      for (int b = a + 1; b < g; ++b) ok = ok && ((q * 8 * (b - a)) % 128 >= 16) && ((q * 8 * (b - a)) % 128 <= 112);
+    if (ok) return q;
+  }
+}
+
+template <int KT, int NOUT, int KQ, int DB, int G>
+__global__ void __launch_bounds__(NTS, (NOUT * KQ <= 32) ? 2 : 1) kmm_f64_split_kernel(const F64Params p) {
+  static_assert(KQ % 2 == 0 && (G == 2 || G == 4), "lane-split layout");
+  if (p.gate != nullptr && *p.gate == 0) return;
+  constexpr int ROWS = NTS / G, KS = G * KQ, KQP = kqp_of(KQ, G);
+  constexpr int EBS = 1;  // evaluation chains per lane and step (2: within 2 % either way, small spills)
+  static_assert(TJ % (G * EBS) == 0, "entry batch");
+  __shared__ double sXj[TJ][DB + 1];
+  __shared__ __align__(16) double sB[TJ][G][KQP];
+  __shared__ double sTab[64];
+  exp_tab_fill(sTab);
+
+  const int tid = threadIdx.x, h = tid % G;
+  const int64_t r = (int64_t)blockIdx.x * ROWS + tid / G;
+  const int c0 = blockIdx.y * KS;
+  const int d = p.d;
+  const int64_t jb = (int64_t)blockIdx.z * p.jchunk;
+  const int64_t je = jb + p.jchunk < p.ncols ? jb + p.jchunk : p.ncols;
+  const bool live = r < p.nrows;
+
+  double xi[DB];
+#pragma unroll
+  for (int q = 0; q < DB; ++q) xi[q] = (live && q < d) ? p.xr[r * d + q] : 0.0;
+  double acc[KQ], accg[NOUT == 2 ? KQ : 1];
+#pragma unroll
+  for (int c = 0; c < KQ; ++c) {
+    acc[c] = 0.0;
+    if (NOUT == 2) accg[c] = 0.0;
+  }
+
+  for (int64_t j0 = jb; j0 < je; j0 += TJ) {
+    const int nj = (int)(je - j0 < TJ ? je - j0 : TJ);
+    const int njg = (nj + G * EBS - 1) / (G * EBS) * (G * EBS);  // rows past nj up to the batch boundary: zero RHS
+    __syncthreads();
+    for (int e = tid; e < nj * d; e += NTS) sXj[e / d][e % d] = p.xc[(j0 + e / d) * d + e % d];
+    for (int e = tid; e < njg * KS; e += NTS) {
+      const int jj = e / KS, c = e % KS;
+      const int cc = c0 + c;
+      sB[jj][c / KQ][c % KQ] = (jj < nj && cc < p.k) ? p.b[(j0 + jj) * p.b_rs + (int64_t)cc * p.b_cs] : 0.0;
+    }
+    __syncthreads();
+    for (int jj = 0; jj < njg; jj += G * EBS) {
+      // this lane's entries of the batch: columns jj + u G + h (past nj: any finite value, the
+      // RHS row is 0); EBS independent evaluation chains per lane
+      double kv[EBS], gv[EBS];
+#pragma unroll
+      for (int u = 0; u < EBS; ++u) {
+        const int jm = jj + u * G + h < nj ? jj + u * G + h : nj - 1;
+        double r2 = 0.0;
+#pragma unroll
+        for (int q = 0; q < DB; ++q) {
+          if (q < d) {
+            const double df = xi[q] - sXj[jm][q];
+            r2 = KGP_R2ACC(r2, df);  // numba's rounding (no FMA contraction)
+          }
+        }
+        gv[u] = 0.0;
+        if (NOUT == 2) {
+          kd64f<KT, (DB >= 8)>(r2, p.l, kv[u], gv[u], sTab);
+        } else {
+          kv[u] = kappa64f<KT, (DB >= 8)>(r2, p.l, sTab);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < EBS; ++u) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const double kg = __shfl_sync(0xffffffffu, kv[u], g, G);
+          const double gg = NOUT == 2 ? __shfl_sync(0xffffffffu, gv[u], g, G) : 0.0;
+#pragma unroll
+          for (int c = 0; c < KQ; c += 2) {
+            const double2 bv = *reinterpret_cast<const double2*>(&sB[jj + u * G + g][h][c]);
+            acc[c] = fma(kg, bv.x, acc[c]);
+            acc[c + 1] = fma(kg, bv.y, acc[c + 1]);
+            if (NOUT == 2) {
+              accg[c] = fma(gg, bv.x, accg[c]);
+              accg[c + 1] = fma(gg, bv.y, accg[c + 1]);
+            }
+          }
+        }
+      }
+    }
+  }
+  if (!live) return;
+#pragma unroll
+  for (int c = 0; c < KQ; ++c) {
+    const int cc = c0 + h * KQ + c;
     if (cc >= p.k) continue;
     if (p.part) {
       const int64_t slot = ((int64_t)blockIdx.z * p.nrows + r) * p.k + cc;
@@ -158,6 +316,8 @@ __global__ void __launch_bounds__(SB) kmm_f64_sym_kernel(const F64Params p, int 
   __shared__ double sX[SB][DB + 1];
   __shared__ double sB[SB][KS];
   __shared__ double sCol[SNW][SB][KS];
+  __shared__ double sTab[64];
+  exp_tab_fill(sTab);
   // tile pair (I, J), I <= J, from the linear index
   const int64_t tix = blockIdx.x;
   int I = (int)((sqrt(8.0 * (double)tix + 1.0) - 1.0) * 0.5);  // row of the packed upper triangle
@@ -202,10 +362,10 @@ __global__ void __launch_bounds__(SB) kmm_f64_sym_kernel(const F64Params p, int 
         for (int t = 0; t < DB; ++t) {
           if (t < d) {
             const double df = xi[t] - sX[jj][t];
-            r2 = __dadd_rn(r2, __dmul_rn(df, df));  // numba's rounding (no FMA contraction)
+            r2 = KGP_R2ACC(r2, df);  // numba's rounding (no FMA contraction)
           }
         }
-        kv = kappa64f<KT, KGP_F64_SYM_FG>(r2, p.l);
+        kv = kappa64f<KT, KGP_F64_SYM_FG>(r2, p.l, sTab);
       }
 #pragma unroll
       for (int c = 0; c < KS; ++c) {
@@ -358,34 +518,98 @@ inline int slice_for(int k, int nout, int d) {
   return (w + 3) / 4 * 4;
 }
 
+// lane-split dispatch (measured over k = 4..64, d = 2..8, tools/f64_grid.py). Two outputs: k in
+// the fewest slices of w <= 64 columns, w = wmin..32 -> 2 lanes x 16, 33..64 -> 4 lanes x {10, 12,
+// 14, 16}. One output: only where the one-lane kernel's slice is wmin..32 columns wide (2 x 16 at
+// the same slice count; four lanes lose to the 34..48-column one-lane slices there).
+inline void split_for(int k, int nout, int d, int wmin, int& g, int& kq) {
+  g = kq = 0;
+  if (nout == 1) {
+    const int ks = slice_for(k, 1, d);
+    if (ks >= wmin && ks <= 32) {
+      g = 2;
+      kq = 16;
+    }
+    return;
+  }
+  const int nsl = (k + 63) / 64;
+  const int w = (k + nsl - 1) / nsl;
+  if (w < wmin) return;
+  if (w <= 32) {
+    g = 2;
+    kq = 16;
+    return;
+  }
+  g = 4;
+  kq = ((w + 3) / 4 + 1) / 2 * 2;
+  if (kq < 10) kq = 10;
+}
+
+using F64Kernel = void (*)(const F64Params);
+
 template <int KT, int NOUT, int DB>
-int launch_ks(const F64Params& p, int ks, dim3 grid, cudaStream_t st) {
+F64Kernel pick_ks(int ks) {
   switch (ks) {
-#define KGP_F64_KS(K)                                                      \
-  case K:                                                                  \
-    if constexpr (NOUT == 1 || K <= KGP_F64_CAP2) {                        \
-      kmm_f64_kernel<KT, NOUT, K, DB><<<grid, NT, 0, st>>>(p);             \
-      break;                                                               \
-    }                                                                      \
+#define KGP_F64_KS(K)                                                                  \
+  case K:                                                                              \
+    if constexpr (NOUT == 1 || K <= KGP_F64_CAP2) return kmm_f64_kernel<KT, NOUT, K, DB>; \
     [[fallthrough]];
     KGP_F64_KS(2) KGP_F64_KS(4) KGP_F64_KS(8) KGP_F64_KS(12) KGP_F64_KS(16) KGP_F64_KS(18) KGP_F64_KS(20)
     KGP_F64_KS(24) KGP_F64_KS(28) KGP_F64_KS(34)
     KGP_F64_KS(32) KGP_F64_KS(36) KGP_F64_KS(40) KGP_F64_KS(44) KGP_F64_KS(48)
 #undef KGP_F64_KS
     default:
-      set_error(KGP_ERR_INVALID, "fp64 operator slice %d unsupported", ks);
-      return KGP_ERR_INVALID;
+      return nullptr;
   }
-  KGP_LAUNCH("kmm_f64_kernel");
-  return KGP_OK;
 }
 
+template <int KT, int NOUT, int DB>
+F64Kernel pick_split(int g, int kq) {
+#define KGP_F64_SPL(GG, KQ) \
+  if (g == GG && kq == KQ) return kmm_f64_split_kernel<KT, NOUT, KQ, DB, GG>;
+  KGP_F64_SPL(2, 16)
+  if constexpr (NOUT == 2) {
+    KGP_F64_SPL(4, 10) KGP_F64_SPL(4, 12) KGP_F64_SPL(4, 14) KGP_F64_SPL(4, 16)
+  }
+#undef KGP_F64_SPL
+  return nullptr;
+}
+
+// the kernel instantiation for (kernel type, outputs, dimension bucket) and either a slice
+// width (g = 0) or a lane-split layout (g lanes x kq columns)
 template <int KT>
-int launch_kt(const F64Params& p, int ks, dim3 grid, cudaStream_t st) {
+F64Kernel pick_kt(const F64Params& p, int ks, int g, int kq) {
   const bool two = p.out_dl != nullptr;
-  if (p.d <= 4) return two ? launch_ks<KT, 2, 4>(p, ks, grid, st) : launch_ks<KT, 1, 4>(p, ks, grid, st);
-  if (p.d <= 8) return two ? launch_ks<KT, 2, 8>(p, ks, grid, st) : launch_ks<KT, 1, 8>(p, ks, grid, st);
-  return two ? launch_ks<KT, 2, 16>(p, ks, grid, st) : launch_ks<KT, 1, 16>(p, ks, grid, st);
+#define KGP_F64_PICK(NOUT, DB) (g ? pick_split<KT, NOUT, DB>(g, kq) : pick_ks<KT, NOUT, DB>(ks))
+  if (p.d <= 4) return two ? KGP_F64_PICK(2, 4) : KGP_F64_PICK(1, 4);
+  if (p.d <= 8) return two ? KGP_F64_PICK(2, 8) : KGP_F64_PICK(1, 8);
+  return two ? KGP_F64_PICK(2, 16) : KGP_F64_PICK(1, 16);
+#undef KGP_F64_PICK
+}
+
+// CTAs of `fn` one GPU holds at once (occupancy x SM count), cached per (kernel, device)
+int resident_ctas(F64Kernel fn, int threads, int* out) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> cache;
+  int dev = 0;
+  KGP_CUDA(cudaGetDevice(&dev));
+  const std::pair<const void*, int> key(reinterpret_cast<const void*>(fn), dev);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      *out = it->second;
+      return KGP_OK;
+    }
+  }
+  int occ = 0, sms = 0;
+  KGP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, 0));
+  KGP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int w = (occ > 0 ? occ : 1) * (sms > 0 ? sms : 1);
+  std::lock_guard<std::mutex> lk(mu);
+  cache[key] = w;
+  *out = w;
+  return KGP_OK;
 }
 
 }  // namespace
@@ -417,34 +641,71 @@ int launch_kmm_f64(int kt, const F64Params& p_in, DevBuf& ws, cudaStream_t st) {
     return KGP_OK;
   }
   const int nout = p.out_dl ? 2 : 1;
-  const int ks = slice_for(p.k, nout, p.d);
-  const int64_t rblk = (p.nrows + NT - 1) / NT, kslc = (p.k + ks - 1) / ks;
-  // split the columns until ~8 CTAs per SM are in flight (148 SMs), at >= 128 columns per split
-  static const int ctas_per_sm = [] {
-    const char* e = getenv("KGP_F64_CTAS");
-    const int v = e ? atoi(e) : 8;
-    return v > 0 ? v : 8;
+  // wide RHS blocks: G lanes per row share every kernel-entry evaluation (kmm_f64_split_kernel)
+  static const bool split_on = [] {
+    const char* e = getenv("KGP_F64_SPLIT");
+    return !(e && atoi(e) == 0);
   }();
-  int64_t nsplit = (ctas_per_sm * 148 + rblk * kslc - 1) / (rblk * kslc);
-  const int64_t maxsplit = p.ncols / 128 > 0 ? p.ncols / 128 : 1;
-  if (nsplit > maxsplit) nsplit = maxsplit;
-  if (nsplit > 65535) nsplit = 65535;
-  if (nsplit < 1) nsplit = 1;
+  // narrowest slice that takes the lane-split kernel, per output count (tools/f64_grid.py)
+  static const int wmin1 = [] { const char* e = getenv("KGP_F64_SPLIT_MIN1"); return e ? atoi(e) : 29; }();
+  static const int wmin2 = [] { const char* e = getenv("KGP_F64_SPLIT_MIN2"); return e ? atoi(e) : 29; }();
+  int sg = 0, skq = 0;
+  if (split_on) split_for(p.k, nout, p.d, nout == 2 ? wmin2 : wmin1, sg, skq);
+  const int ks = sg ? sg * skq : slice_for(p.k, nout, p.d);
+  const int rows_cta = sg ? NTS / sg : NT, threads = sg ? NTS : NT;
+  const int64_t rblk = (p.nrows + rows_cta - 1) / rows_cta, kslc = (p.k + ks - 1) / ks;
+  const F64Kernel fn = (kt == GAUSS) ? pick_kt<GAUSS>(p, ks, sg, skq)
+                                     : (kt == MAT32) ? pick_kt<MAT32>(p, ks, sg, skq) : pick_kt<MAT52>(p, ks, sg, skq);
+  KGP_REQUIRE(fn != nullptr, KGP_ERR_INVALID, "fp64 operator slice %d (lanes %d x %d) unsupported", ks, sg, skq);
+  // Column split (grid.z): the CTAs run in waves of `wave` = occupancy x SMs, each CTA sweeping
+  // ncols / nsplit columns in 64-column tiles, so the time is ~ waves x tiles per CTA. Take the
+  // split that minimises that product (the first such; chunks of >= 128 columns): a grid that
+  // overflows the last wave by a few CTAs costs a whole extra wave (n = 16384, k = 16, 7 CTAs per
+  // SM: 1280 CTAs on 1036 slots ran 2 waves for 1.24 waves of work).
+  int wave = 0;
+  int rc = resident_ctas(fn, threads, &wave);
+  if (rc) return rc;
+  static const int nsplit_env = [] {
+    const char* e = getenv("KGP_F64_NSPLIT");
+    return e ? atoi(e) : 0;
+  }();
+  const int64_t tiles = (p.ncols + TJ - 1) / TJ;
+  int64_t maxsplit = p.ncols / 128 > 0 ? p.ncols / 128 : 1;
+  if (maxsplit > 4096) maxsplit = 4096;
+  {  // partial sums: at most ~1 GB of workspace
+    const int64_t per_split = (int64_t)sizeof(double) * p.nrows * p.k * nout;
+    const int64_t cap = ((int64_t)1 << 30) / (per_split > 0 ? per_split : 1);
+    if (maxsplit > cap) maxsplit = cap > 1 ? cap : 1;
+  }
+  int64_t nsplit = 1, best = -1;
+  for (int64_t ns = 1; ns <= maxsplit; ++ns) {
+    const int64_t ctas = rblk * kslc * ns;
+    const int64_t waves = (ctas + wave - 1) / wave;
+    const int64_t per = (tiles + ns - 1) / ns;  // tiles per CTA
+    // one extra tile-equivalent per CTA for its prologue / epilogue and partial-sum traffic
+    const int64_t cost = waves * (per + 1);
+    if (best < 0 || cost < best) {
+      best = cost;
+      nsplit = ns;
+    }
+    if (ctas >= 64 * (int64_t)wave) break;  // many waves: the tail no longer matters
+  }
+  if (nsplit_env > 0) nsplit = nsplit_env < maxsplit ? nsplit_env : maxsplit;
   p.jchunk = ((p.ncols + nsplit - 1) / nsplit + TJ - 1) / TJ * TJ;
   nsplit = (p.ncols + p.jchunk - 1) / p.jchunk;
   p.part = nullptr;
   p.part_stride = 0;
   if (nsplit > 1) {
     const int64_t per = nsplit * p.nrows * p.k;
-    int rc = ws.ensure(sizeof(double) * per * (p.out_dl ? 2 : 1));
+    rc = ws.ensure(sizeof(double) * per * (p.out_dl ? 2 : 1));
     if (rc) return rc;
     p.part = ws.as<double>();
     p.part_stride = per;
   }
   dim3 grid((unsigned)rblk, (unsigned)kslc, (unsigned)nsplit);
-  int rc = (kt == GAUSS) ? launch_kt<GAUSS>(p, ks, grid, st) : (kt == MAT32) ? launch_kt<MAT32>(p, ks, grid, st)
-                                                                                : launch_kt<MAT52>(p, ks, grid, st);
-  if (rc || nsplit == 1) return rc;
+  fn<<<grid, threads, 0, st>>>(p);
+  KGP_LAUNCH(sg ? "kmm_f64_split_kernel" : "kmm_f64_kernel");
+  if (nsplit == 1) return KGP_OK;
   const int64_t cnt = p.nrows * p.k;
   f64_reduce_kernel<<<(unsigned)((cnt + 31) / 32), RW * 32, 0, st>>>(p, (int)nsplit);
   KGP_LAUNCH("f64_reduce_kernel");

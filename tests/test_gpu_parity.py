@@ -153,6 +153,32 @@ def test_fp64_symmetric_small_k(pkg, kt, n, k):
     assert np.array_equal(got, e.matmul(b))  # run-to-run identical
 
 
+@pytest.mark.parametrize("kt", KTS)
+@pytest.mark.parametrize("n,d,k", [(301, 3, 29), (257, 8, 32), (300, 4, 33), (130, 2, 40), (259, 8, 51), (200, 3, 64),
+                                   (190, 9, 65), (150, 5, 100), (140, 2, 130)])
+def test_fp64_lane_split_wide_k(pkg, kt, n, d, k):
+    """The fp64 operator's wide-k passes (kmm_f64_split_kernel: 2 or 4 lanes share a row and every
+    kernel-entry evaluation, each lane contracting its own columns of the slice): one output
+    (k > 48) and two outputs (k > 28), every (G, KQ) layout, ragged rows / columns / tiles,
+    against the oracle's streamed operator (kmat.py:165-189) at the fp64 bar, run-to-run identical."""
+    from oracle import kgp_oracle as orc
+
+    rng = np.random.default_rng(n + 31 * k)
+    x = rng.uniform(0, 1, (n, d))
+    b = rng.standard_normal((n, k))
+    hp = _hp(pkg, 0.4, 1.3, 0.05)
+    e = pkg.KernelEngine(pkg.KernelType(kt), x, hp, mode=pkg.EngineMode.ON_THE_FLY, precision="fp64")
+    ref_k = orc.khat_matmul(kt, x, hp.l, hp.f, hp.s, b)
+    ref_l = orc.khat_matmul(kt, x, hp.l, hp.f, hp.s, b, theta="l")
+    ref_f = orc.khat_matmul(kt, x, hp.l, hp.f, hp.s, b, theta="f")
+    got_k, got_l, got_f = e.matmul_with_grads(b)
+    assert rel_max(got_k, ref_k) <= 1e-12 and rel_max(got_l, ref_l) <= 1e-12 and rel_max(got_f, ref_f) <= 1e-12
+    one = e.matmul(b)
+    assert rel_max(one, ref_k) <= 1e-12
+    assert np.array_equal(one, e.matmul(b))
+    assert rel_max(one, got_k) <= 1e-13  # different layouts and column splits, the same entries
+
+
 def test_cfg2_row_subsample(pkg):
     """configs[1] at full size: fast K.Z and dK/dl.Z against the C oracle on 512 rows."""
     import torch

@@ -8,7 +8,7 @@ cd "$(dirname "$0")/../paper_2503_02259_b200/csrc"
 out=../../tools/variants/$name
 mkdir -p $out
 NV="/usr/local/cuda/bin/nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC --expt-relaxed-constexpr $flags"
-for f in kgp_api kmm_tc kmm_f64 prep panels woodbury pcg afn symv; do
+for f in kgp_api kmm_tc kmm_f64 prep panels woodbury pcg afn symv wgemm; do
   $NV -c $f.cu -o $out/$f.o &
 done
 wait
