@@ -307,11 +307,24 @@ __global__ void __launch_bounds__(NTS, (NOUT * KQ <= 32) ? 2 : 1) kmm_f64_split_
 #ifndef KGP_F64_SB
 #define KGP_F64_SB 64
 #endif
+// Butterfly chunk (columns evaluated before each transpose-sum) and the resident CTAs per SM the
+// register allocation must allow. 32 columns per chunk held 32 kappa values per lane: 96 registers,
+// 10 CTAs per SM, so configs[0]'s 2080 block pairs ran 1.41 waves (ncu: the second wave 41 % full).
+// 4 columns and a 64-register cap (16 CTAs per SM: one wave): one-column product 61 -> 50 us at
+// n = 4096, 0.82 -> 0.53 ms at n = 16384, configs[0] eval 4.93 -> 4.73 ms. Measured around it
+// (tools/gpu_sym.sh): chunk 8 / 16 at 16 CTAs 50 / 56 us, chunk 8 at 20 / 24 CTAs 52 / 53 us (k = 4
+// at n = 16384 0.83 -> 1.14 / 1.32 ms), chunk 4 at 24 CTAs 56 us.
+#ifndef KGP_F64_SYM_Q
+#define KGP_F64_SYM_Q 4
+#endif
+#ifndef KGP_F64_SYM_MINB
+#define KGP_F64_SYM_MINB 16
+#endif
 constexpr int SB = KGP_F64_SB;  // points per block (64: twice the CTAs of 128, the kernel is latency-bound)
 constexpr int SNW = SB / 32;    // warps per CTA
 
 template <int KT, int KS, int DB>
-__global__ void __launch_bounds__(SB) kmm_f64_sym_kernel(const F64Params p, int nb, double* __restrict__ part) {
+__global__ void __launch_bounds__(SB, KGP_F64_SYM_MINB) kmm_f64_sym_kernel(const F64Params p, int nb, double* __restrict__ part) {
   if (p.gate != nullptr && *p.gate == 0) return;
   __shared__ double sX[SB][DB + 1];
   __shared__ double sB[SB][KS];
@@ -349,7 +362,9 @@ __global__ void __launch_bounds__(SB) kmm_f64_sym_kernel(const F64Params p, int 
   double acc[KS];
 #pragma unroll
   for (int c = 0; c < KS; ++c) acc[c] = 0.0;
-  constexpr int Q = 32 / KS;  // columns per butterfly chunk: Q x KS = 32 values per lane
+  // columns per butterfly chunk: Q x KS <= 32 values per lane (the halving steps cost Q - 1
+  // shuffle-adds per Q columns whatever Q is; a smaller chunk holds fewer values in registers)
+  constexpr int Q = (32 / KS < KGP_F64_SYM_Q) ? 32 / KS : KGP_F64_SYM_Q;
   for (int jc = 0; jc < SB; jc += Q) {
     double v[Q][KS];
 #pragma unroll
