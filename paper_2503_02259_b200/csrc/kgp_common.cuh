@@ -105,7 +105,7 @@ KGP_DEV double exp_neg64(double x) {
 // exp_tab_fill) and exp(r) - 1 by its degree-5 Taylor polynomial (truncation r^6/720 <= 3.5e-17):
 // 11 FP64 instructions and one LDS against the 19 of exp_neg64 -- the fused fp64 operators are
 // bound by the FP64 pipe, the integer/LSU work rides along. The table entries are correctly
-// rounded (0.5 ulp), the result is within ~1.5 ulp; below 2^-1021 (x < -708) it is 0.
+// rounded (0.5 ulp), the result is within ~1.5 ulp; x < -708 is clamped to -708 (3.3e-308).
 __device__ const double EXP_TAB64[64] = {
     0x1.0000000000000p+0, 0x1.02c9a3e778061p+0, 0x1.059b0d3158574p+0, 0x1.0874518759bc8p+0,
     0x1.0b5586cf9890fp+0, 0x1.0e3ec32d3d1a2p+0, 0x1.11301d0125b51p+0, 0x1.1429aaea92de0p+0,
@@ -130,7 +130,10 @@ KGP_DEV void exp_tab_fill(double* tab) {
 }
 
 KGP_DEV double exp_neg64t(double x, const double* __restrict__ tab) {
-  if (x < -708.0) return 0.0;
+  // branch-free: an early return would end the basic block, and the callers rely on the scheduler
+  // interleaving this chain with their independent FMA streams. Arguments below -708 evaluate as
+  // exp(-708) = 3.3e-308 (instead of a subnormal or 0): an absolute error of 3e-308
+  x = fmax(x, -708.0);
   // m = round(64 x / ln 2) by the 1.5 * 2^52 shifter (m in the low word), m = 64 e + j
   const double t = fma(x, 0x1.71547652b82fep+6, 6755399441055744.0);
   const int m = __double2loint(t);

@@ -34,6 +34,9 @@
 // 32 (211 registers, 2 CTAs per SM) made cfg2's k = 32 55.9 -> 93.6 ms, so 32 runs as 2 x 16
 #define KGP_F64_CAP2 28
 #endif
+#ifndef KGP_F64_SWP
+#define KGP_F64_SWP 0  // 1: one-lane kernel evaluates entry jj + 1 while contracting entry jj (measured, off)
+#endif
 #ifndef KGP_F64_FMADIST
 #define KGP_F64_FMADIST 0  // 1: r^2 accumulated with FMA (one rounding per term fewer than numba's order)
 #endif
@@ -102,6 +105,45 @@ __global__ void __launch_bounds__(NT) kmm_f64_kernel(const F64Params p) {
       sB[jj][c] = (jj < nj && cc < p.k) ? p.b[(j0 + jj) * p.b_rs + (int64_t)cc * p.b_cs] : 0.0;
     }
     __syncthreads();
+#if KGP_F64_SWP
+    // software pipeline: entry jj + 1 is evaluated in the same loop body that contracts entry jj,
+    // so the in-order warp has the independent FMA stream to issue while the distance /
+    // exponential chain waits on its latencies (two live values more, no extra accumulators)
+    auto eval = [&](int jm, double& kvo, double& gvo) {
+      double r2 = 0.0;
+#pragma unroll
+      for (int q = 0; q < DB; ++q) {
+        if (q < d) {
+          const double df = xi[q] - sXj[jm][q];
+          r2 = KGP_R2ACC(r2, df);  // numba's rounding (no FMA contraction)
+        }
+      }
+      gvo = 0.0;
+      if (NOUT == 2) {
+        kd64f<KT, (DB >= 8)>(r2, p.l, kvo, gvo, sTab);  // one exponential for both outputs
+      } else {
+        kvo = kappa64f<KT, (DB >= 8)>(r2, p.l, sTab);
+      }
+    };
+    double kc, gc;
+    eval(0, kc, gc);
+    for (int jj = 0; jj < nj; ++jj) {
+      double kn, gn;
+      eval(jj + 1 < nj ? jj + 1 : nj - 1, kn, gn);  // the last one is not used
+#pragma unroll
+      for (int c = 0; c < KS; c += 2) {
+        const double2 bv = *reinterpret_cast<const double2*>(&sB[jj][c]);
+        acc[c] = fma(kc, bv.x, acc[c]);
+        acc[c + 1] = fma(kc, bv.y, acc[c + 1]);
+        if (NOUT == 2) {
+          accg[c] = fma(gc, bv.x, accg[c]);
+          accg[c + 1] = fma(gc, bv.y, accg[c + 1]);
+        }
+      }
+      kc = kn;
+      gc = gn;
+    }
+#else
     for (int jj = 0; jj < nje; jj += EB) {
       double kv[EB], gv[EB];
 #pragma unroll
@@ -141,6 +183,7 @@ __global__ void __launch_bounds__(NT) kmm_f64_kernel(const F64Params p) {
         }
       }
     }
+#endif
   }
   if (!live) return;
   // epilogue (kmat.py:186-188): scale, + s B on the diagonal rows; raw partials when split

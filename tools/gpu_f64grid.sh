@@ -11,8 +11,4 @@ grid() {
   timeout 120 python tools/f64_grid.py 65536 gaussian 8 2 32 2>&1 | tail -1
   timeout 60 python tools/nlml_time.py fp64 otf 20 2>&1 | tail -1
 }
-(
-echo "== batched, default policy"; grid
-echo "== batched, nosplit"; KGP_F64_SPLIT=0 grid
-) 2>&1 | tee $O/grid3.log
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_guard.py -q -x -p no:cacheprovider -k "fp64 or f64 or cfg1 or symmetric or golden or lane_split or determ or guard" 2>&1 | tail -3 | tee $O/tests3.log
+( echo "== ${TAG:-default}"; grid ) 2>&1 | tee $O/grid_${TAG:-default}.log
