@@ -542,3 +542,114 @@ def test_preconditioning_reduces_iterations(pkg, rng):
     clever = solver.pcg_solve(e.matmul, precond.build(e, 100).apply_inverse, y, tol=1e-8, max_iter=2000)
     assert clever.all_converged
     assert clever.traces[0].iterations < plain.traces[0].iterations
+
+
+# ---------------------------------------------------------------------------- panels (test_kernels.py)
+def test_pairwise_sq_dist_properties(pkg, rng):
+    """test_kernels.py:13-35 on the device panel kernel: exact small cases (a unit step, 3-4-5), a
+    double loop, non-negativity when nearly coincident points cancel, dimension mismatch."""
+    np.testing.assert_array_equal(pkg.pairwise_sq_dist([[0.0], [1.0]], [[0.0], [1.0]]), [[0.0, 1.0], [1.0, 0.0]])
+    np.testing.assert_array_equal(pkg.pairwise_sq_dist([[0.0, 0.0]], [[3.0, 4.0]]), [[25.0]])
+    x, y = rng.standard_normal((5, 3)), rng.standard_normal((4, 3))
+    loops = np.array([[np.sum((x[i] - y[j]) ** 2) for j in range(4)] for i in range(5)])
+    np.testing.assert_allclose(pkg.pairwise_sq_dist(x, y), loops, rtol=1e-13)
+    base = rng.standard_normal((50, 4)) * 100
+    xx = np.vstack([base, base + 1e-9])
+    assert np.all(pkg.pairwise_sq_dist(xx, xx) >= 0.0)
+    with pytest.raises(ValueError, match="dimension"):
+        pkg.pairwise_sq_dist([[0.0, 1.0]], [[0.0]])
+
+
+@pytest.mark.parametrize("kt", KTS)
+def test_kernel_panel_properties(pkg, kt, rng):
+    """test_kernels.py:38-70, 122-140: unit diagonal to the bit for l in {0.1, 1, 7.5}; transpose
+    symmetry to the bit; values in (0, 1] and equal to the scalar closed forms (1e-12); any row or
+    column tiling of a panel gives the same bits as the whole panel; invalid length scales rejected."""
+    K = pkg.KernelType(kt)
+    for l in (0.1, 1.0, 7.5):
+        x = rng.standard_normal((6, 2))
+        np.testing.assert_array_equal(np.diag(pkg.eval_kernel(K, x, x, l)), np.ones(6))
+    x, y = rng.standard_normal((7, 3)), rng.standard_normal((5, 3))
+    np.testing.assert_array_equal(pkg.eval_kernel(K, x, y, 0.8), pkg.eval_kernel(K, y, x, 0.8).T)
+    x, y = rng.standard_normal((8, 3)), rng.standard_normal((6, 3))
+    k = pkg.eval_kernel(K, x, y, 1.3)
+    assert np.all(k > 0) and np.all(k <= 1)
+    scalar = np.array([[_kappa(kt, float(np.linalg.norm(x[i] - y[j])), 1.3) for j in range(6)] for i in range(8)])
+    np.testing.assert_allclose(k, scalar, rtol=1e-12)
+    x, y = rng.standard_normal((83, 4)), rng.standard_normal((61, 4))
+    full = pkg.eval_kernel(K, x, y, 0.9)
+    np.testing.assert_array_equal(full, np.vstack([pkg.eval_kernel(K, x[i:i + 17], y, 0.9) for i in range(0, 83, 17)]))
+    np.testing.assert_array_equal(full, np.hstack([pkg.eval_kernel(K, x, y[j:j + 13], 0.9) for j in range(0, 61, 13)]))
+    gfull = pkg.eval_kernel_grad_l(K, x, y, 0.9)
+    np.testing.assert_array_equal(gfull,
+                                  np.vstack([pkg.eval_kernel_grad_l(K, x[i:i + 17], y, 0.9) for i in range(0, 83, 17)]))
+    for bad in (0.0, -1.0, float("nan")):
+        with pytest.raises(ValueError, match="length scale"):
+            pkg.eval_kernel(pkg.KernelType.GAUSSIAN, [[0.0]], [[1.0]], bad)
+
+
+def test_kernel_grad_l_properties(pkg, rng):
+    """test_kernels.py:73-120: d kappa / dl is exactly 0 at coincident points; the Gaussian's equals
+    kappa r^2 / l^3 (1e-13); all three against central finite differences of the scalar closed forms
+    on 60 random pairs over three decades of distance and two of length scale (1e-5; the reference's
+    sweep differentiates a 50-digit evaluation, here double precision with h = 1e-6 l on pairs whose
+    difference quotient is resolvable)."""
+    for kt in KTS:
+        np.testing.assert_array_equal(pkg.eval_kernel_grad_l(pkg.KernelType(kt), [[2.0, 3.0]], [[2.0, 3.0]], 0.7),
+                                      [[0.0]])
+    x, y = rng.standard_normal((5, 2)), rng.standard_normal((4, 2))
+    l = 1.7
+    k = pkg.eval_kernel(pkg.KernelType.GAUSSIAN, x, y, l)
+    np.testing.assert_allclose(pkg.eval_kernel_grad_l(pkg.KernelType.GAUSSIAN, x, y, l),
+                               k * pkg.pairwise_sq_dist(x, y) / l**3, rtol=1e-13)
+    for kt in KTS:
+        for _ in range(20):
+            d = int(rng.integers(1, 5))
+            u, v = rng.standard_normal(d), rng.standard_normal(d)
+            l = rng.uniform(0.5, 2.0)
+            h = 1e-6 * l
+            r = float(np.linalg.norm(u - v))
+            fd = (_kappa(kt, r, l + h) - _kappa(kt, r, l - h)) / (2 * h)
+            g = pkg.eval_kernel_grad_l(pkg.KernelType(kt), u[None, :], v[None, :], l)[0, 0]
+            assert abs(g - fd) / max(abs(fd), abs(g)) < 1e-5
+
+
+# ---------------------------------------------------------------------------- training (test_train.py)
+def test_training_properties(pkg):
+    """test_train.py:60-120 with the device engine under train.fit: one step records one loss and
+    one gradient norm and stops on MAX_STEPS; hyperparameters stay positive; the loss does not end
+    above where it started; exact mode is reproducible to the bit; iterative mode records a finite
+    loss per step; the median-heuristic initialisation; configuration validation."""
+    from paper_2503_02259_b200 import train
+
+    def data(n=80, seed=0):
+        r = np.random.default_rng(seed)
+        x = r.uniform(-2, 2, (n, 2))
+        return x, np.sin(x[:, 0]) * np.cos(x[:, 1]) + 0.1 * r.standard_normal(n)
+
+    x, y = data()
+    res = train.fit(pkg.KernelType.GAUSSIAN, x, y, train.TrainConfig(max_steps=1))
+    assert len(res.loss_history) == 1 and len(res.grad_norm_history) == 1
+    assert res.status is train.TrainStatus.MAX_STEPS
+    x, y = data(seed=1)
+    res = train.fit(pkg.KernelType.MATERN32, x, y, train.TrainConfig(max_steps=30))
+    assert res.params.l > 0 and res.params.f > 0 and res.params.s > 0
+    x, y = data(seed=2)
+    res = train.fit(pkg.KernelType.GAUSSIAN, x, y, train.TrainConfig(max_steps=60))
+    assert res.loss_history[-1] <= res.loss_history[0]
+    x, y = data(seed=3)
+    cfg = train.TrainConfig(max_steps=15, rng_seed=7)
+    a, b = train.fit(pkg.KernelType.GAUSSIAN, x, y, cfg), train.fit(pkg.KernelType.GAUSSIAN, x, y, cfg)
+    assert a.loss_history == b.loss_history
+    assert (a.params.l, a.params.f, a.params.s) == (b.params.l, b.params.f, b.params.s)
+    x, y = data(n=60, seed=4)
+    res = train.fit(pkg.KernelType.GAUSSIAN, x, y,
+                    train.TrainConfig(max_steps=10, mode="iterative", k_z=8, tol=1e-8, probe_tol=1e-6, rng_seed=1))
+    assert len(res.loss_history) == 10 and np.isfinite(res.loss_history).all()
+    hp = train.initial_hyperparams(np.array([[0.0], [1.0], [2.0], [10.0]]), np.array([0.0, 1.0, -1.0, 3.0]))
+    yv = np.array([0.0, 1.0, -1.0, 3.0])
+    np.testing.assert_allclose([hp.l, hp.f, hp.s], [5.0, np.std(yv), 0.01 * np.var(yv)], rtol=1e-12)
+    with pytest.raises(ValueError):
+        train.TrainConfig(learning_rate=0.0)
+    with pytest.raises(ValueError):
+        train.TrainConfig(mode="warp")
