@@ -578,15 +578,15 @@ inline int slice_for(int k, int nout, int d) {
 
 // lane-split dispatch (measured over k = 4..64, d = 2..8, tools/f64_grid.py). Two outputs: k in
 // the fewest slices of w <= 64 columns, w = wmin..32 -> 2 lanes x 16, 33..64 -> 4 lanes x {10, 12,
-// 14, 16}. One output: only where the one-lane kernel's slice is wmin..32 columns wide (2 x 16 at
-// the same slice count; four lanes lose to the 34..48-column one-lane slices there).
+// 14, 16}. One output: only where the one-lane kernel's slice is wmin..36 columns wide (2 x 16 or
+// 2 x 18 at the same slice count; four lanes lose to the 40..48-column one-lane slices there).
 inline void split_for(int k, int nout, int d, int wmin, int& g, int& kq) {
   g = kq = 0;
   if (nout == 1) {
     const int ks = slice_for(k, 1, d);
-    if (ks >= wmin && ks <= 32) {
+    if (ks >= wmin && ks <= 36) {
       g = 2;
-      kq = 16;
+      kq = ks <= 32 ? 16 : 18;
     }
     return;
   }
@@ -626,6 +626,9 @@ F64Kernel pick_split(int g, int kq) {
 #define KGP_F64_SPL(GG, KQ) \
   if (g == GG && kq == KQ) return kmm_f64_split_kernel<KT, NOUT, KQ, DB, GG>;
   KGP_F64_SPL(2, 16)
+  if constexpr (NOUT == 1) {
+    KGP_F64_SPL(2, 18)
+  }
   if constexpr (NOUT == 2) {
     KGP_F64_SPL(4, 10) KGP_F64_SPL(4, 12) KGP_F64_SPL(4, 14) KGP_F64_SPL(4, 16)
   }
