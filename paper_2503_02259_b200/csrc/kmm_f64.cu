@@ -8,10 +8,18 @@
 // one thread = one row. A CTA of 128 threads stages a tile of TJ column points and the
 // matching RHS rows in shared memory; every thread evaluates kappa (and dkappa/dl) of its
 // row against each column and FMAs it straight into its KS register accumulators (the
-// column data are warp-broadcast reads). The RHS is processed in slices of KS <= 24/32
-// columns (grid.y); when the row blocks cannot fill the GPU the column range is split
-// over grid.z and the partial sums are reduced in a fixed order (deterministic).
-// Bound: the FP64 pipe (distance 3d + exp ~25 + KS FMA per entry and output).
+// column data are warp-broadcast reads). The RHS is processed in slices of KS <= 28/48
+// columns (grid.y); the column range is split over grid.z so that the CTAs fill whole waves
+// of the instantiation's real occupancy, and the partial sums are reduced in a fixed order
+// (deterministic). Three kernels share this contract:
+//   kmm_f64_kernel        one lane per row (narrow slices);
+//   kmm_f64_split_kernel  2 or 4 lanes per row share every kernel-entry evaluation and split the
+//                         slice's columns (wide slices: one evaluation per entry for up to 64
+//                         columns instead of one per 16..28-column slice);
+//   kmm_f64_sym_kernel    the square operator with <= 4 columns evaluates each entry once for
+//                         both triangles.
+// Bound: the FP64 pipe (distance 3d + exp 13 + KS FMA per entry and output; the exponential is
+// exp_neg64t, kgp_common.cuh).
 #include <stdlib.h>
 
 #include <map>
