@@ -238,6 +238,20 @@ def profiled_traffic(precision: str, n: int, k: int):
     return rec.get(key, {}).get("bytes_per_launch")
 
 
+def fp64_slots(d: int, k: int, nout: int) -> int:
+    """FP64 instruction slots per kernel entry of the Gaussian fp64 operator as shipped: 3d for the
+    distance (subtract, multiply, add per coordinate: the reference's rounding order takes no FMA),
+    13 for the kernel value (argument scale, clamp, exp_neg64t's 11), 2 more for dkappa/dl, and one
+    FMA per right-hand side and output. The FP64 pipe issues one instruction per lane slot whether
+    it is an FMA or not, so the roofline is counted in slots and reported as 2 flops per slot
+    against the DFMA micro-benchmark (exp timed at the software-exp rate)."""
+    return 3 * d + 13 + (2 if nout == 2 else 0) + k * nout
+
+
+FP64_SLOTS_NOTE = ("per entry 3d (distance) + 13 (kernel value, exp_neg64t) + 2 (dkappa/dl, two outputs) + k per "
+                   "output FP64 instruction slots, 2 flops per slot against the DFMA rate")
+
+
 def nlml_metric(cpu: bool):
     """Secondary metric: NLML+gradient evaluations/s at BASELINE configs[0] (n=4096, Gaussian,
     16 probes, rank 256) with its fixed recipe (PCG 50 iterations, 20 Lanczos steps), fp64.
@@ -251,8 +265,9 @@ def nlml_metric(cpu: bool):
 
     Roofline (FP64 pipe): the recipe's operator passes from its fixed iteration counts -- w:
     50 x 1 column, probes: 20 x 16 columns, the fused derivative pass: 17 columns x 2 outputs --
-    each costing per kernel entry (3d + 53) evaluation flops + 2k contraction flops per output,
-    over the eval time, against the measured DFMA rate."""
+    each costing per kernel entry fp64_slots(d, k, outputs) FP64 instruction slots (every entry of
+    every pass counted as the reference streams it), over the eval time, against the measured
+    DFMA rate."""
     import torch
 
     from paper_2503_02259_b200 import gp, precond, workloads
@@ -298,7 +313,7 @@ def nlml_metric(cpu: bool):
     t_fast, _, _, lg_fast = run(EngineMode.ON_THE_FLY, precision="fast")
     n, d = w.n, w.d
     passes = [(50, 1, 1), (20, 16, 1), (1, 17, 2)]  # (iterations, columns, outputs)
-    flops = sum(it * n * n * ((3 * d + 53) + 2 * k * nout) for it, k, nout in passes)
+    flops = sum(it * n * n * 2 * fp64_slots(d, k, nout) for it, k, nout in passes)
     achieved = flops / t_eval / 1e12
     out = {"workload": "cfg1 fixed recipe (BASELINE.json configs[0]): n=4096 d=3 Gaussian, 16 probes, "
                        "rank 256, PCG 50 + SLQ 20, fp64 operator, ON_THE_FLY (fused kernel, Khat never stored)",
@@ -309,8 +324,8 @@ def nlml_metric(cpu: bool):
            "roofline": {"bound": "fp64", "achieved": achieved, "peak": FP64_DFMA_TFLOPS, "unit": "TFLOP/s",
                         "frac": achieved / FP64_DFMA_TFLOPS,
                         "algorithmic": "operator passes of the fixed recipe (50 x 1 + 20 x 16 columns, one "
-                                       "17-column two-output derivative pass), per entry 3d + 53 evaluation "
-                                       "flops + 2k per output; PCG vector work and SLQ not counted"},
+                                       "17-column two-output derivative pass), " + FP64_SLOTS_NOTE +
+                                       "; PCG vector work and SLQ not counted"},
            "dense": {"workload": "same recipe, DENSE mode (the reference's default at n <= 20000): Khat "
                                  "materialised by the repo's panel kernel, 17-column products by cuBLAS DGEMM",
                      "evals_per_s": 1.0 / t_dense, "ms_per_eval": t_dense * 1e3, "loss": lg_dense.loss},
@@ -491,8 +506,8 @@ def mode_metric(w, ref_k, ref_l, precision, steps: int = 10):
 
 def fp64_mode_metric(w, steps: int = 5):
     """Secondary: the cfg2 step with the fp64 operator (the parity precision), and its
-    roofline on the FP64 pipe: per kernel entry 3d (distance) + ~53 (exp + transform, FMA = 2)
-    flops, plus 2k flops per output (the contraction FMAs), against the measured DFMA rate."""
+    roofline on the FP64 pipe: fp64_slots(d, k, 2) instruction slots per kernel entry against the
+    measured DFMA rate."""
     import torch
 
     from paper_2503_02259_b200 import KernelEngine, KernelType, _lib
@@ -521,15 +536,14 @@ def fp64_mode_metric(w, steps: int = 5):
     torch.cuda.synchronize()
     t = float(np.mean([a.elapsed_time(b) / 1e3 for a, b in ev]))
     e.close()
-    per_entry = 3 * d + 53 + 2 * 2 * k
+    per_entry = 2 * fp64_slots(d, k, 2)
     achieved = per_entry * n * n / t / 1e12
     return {"value": 2.0 * n * n * k / t, "unit": "entries*RHS/s", "ms_per_step": t * 1e3,
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": FP64_DFMA_TFLOPS, "unit": "TFLOP/s",
                          "frac": achieved / FP64_DFMA_TFLOPS,
                          "peak_source": "DFMA micro-benchmark on this pool (profiles/r01_micro_tensor_fp64.txt); "
                                         "MEASURED_PEAKS.json has no FP64 figure",
-                         "algorithmic": f"{per_entry} fp64 flops per kernel entry: 3d distance + ~53 exp/transform "
-                                        "(estimate) + 2 outputs x 2k contraction"}}
+                         "algorithmic": f"{per_entry} DFMA-equivalent flops per kernel entry: " + FP64_SLOTS_NOTE}}
 
 
 def cfg5_operator_metric(world, rank, local, dist, steps: int = 3):
