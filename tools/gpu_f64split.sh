@@ -1,3 +1,4 @@
+# Variants first: tools/build_variant.sh notab "-DKGP_F64_TABEXP=0" (the exponential before exp_neg64t)
 # A/B of the fp64 operator: table exp (exp_neg64t) and the lane-split wide-k kernels
 O=gpurun_out/f64split; mkdir -p $O
 run() {

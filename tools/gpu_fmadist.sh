@@ -1,3 +1,4 @@
+# Variant first: tools/build_variant.sh fmadist "-DKGP_F64_FMADIST=1"
 O=gpurun_out/f64split; mkdir -p $O
 run() {
   timeout 120 python tools/f64_grid.py 65536 gaussian 8 2 32 2>&1 | tail -1

@@ -1,3 +1,4 @@
+# Variants first: tools/build_variant.sh <name> "-DKGP_F64_SYM_Q=<chunk> -DKGP_F64_SYM_MINB=<CTAs per SM>" (sym8: 8/16, s4_16: 4/16, s8_20: 8/20, s8_24: 8/24, s4_24: 4/24)
 O=gpurun_out/f64split; mkdir -p $O
 run() {
   timeout 120 python tools/f64_grid.py 4096 gaussian 3 1 1,2,4 2>&1 | tail -1
