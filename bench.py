@@ -333,7 +333,11 @@ def nlml_metric(cpu: bool):
                                      "star's tensor-core NLML mode, <= 1e-3: tests/test_gpu_parity.py "
                                      "test_cfg1_fast_mode_within_tf32_bar)",
                          "evals_per_s": 1.0 / t_fast, "ms_per_eval": t_fast * 1e3, "loss": lg_fast.loss,
-                         "loss_rel_diff_vs_fp64": abs(lg_fast.loss - lg.loss) / abs(lg.loss)}}
+                         "loss_rel_diff_vs_fp64": abs(lg_fast.loss - lg.loss) / abs(lg.loss),
+                         "loss_note": "the fixed recipe stops the solves unconverged (PCG 50, probes 20 "
+                                      "iterations, SLQ 20 steps), so the two precisions end on different "
+                                      "partial CG trajectories; converged (tol 1e-10) the same evaluation is "
+                                      "within 1e-3 of the reference in every component (the cited test)"}}
     if cpu:
         from oracle import kgp_oracle as orc
         from oracle import kgp_oracle_c as oc
